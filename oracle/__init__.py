@@ -1,0 +1,131 @@
+"""CPU oracle for libtsm -- TEST INFRASTRUCTURE ONLY.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s ``cpu_baseline``
+/ ``--impl reference`` legs may import this package.  The product package
+``paper_1905_03136_b200`` never imports it, and the two share no code: the
+arithmetic lives in ``oracle/oracle.c`` (plain C + OpenMP, explicit ``fma``),
+this module only marshals numpy arrays into it.
+
+Definitions (PAPER.md is the authority):
+  * TSMTTSM ``C = A^T B``, ``C[m][n] = sum_k A[k][m] B[k][n]``
+    -- PAPER.md:64-68 (op definitions), PAPER.md:342-349 (Listing 1).
+  * TSMM ``B = A C``, ``B[k][n] = sum_m A[k][m] C[m][n]``
+    -- PAPER.md:64-68, PAPER.md:372-375 (reduction along the short M axis).
+  * Z = complex128, plain (non-conjugating) transpose -- DESIGN.md reading R1.
+
+Every function returns ``(result, bound)`` where ``bound`` is the north-star
+tolerance scale ``|A|^T |B|`` (TSMTTSM) or ``|A||C|`` (TSMM).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "oracle.c")
+_LIB_PATH = os.path.join(_HERE, "liboracle.so")
+_lib = None
+
+# -march=x86-64-v3: AVX2 + FMA so that fma() is one instruction; no fast-math,
+# no contraction beyond the explicit fma() calls, no FTZ/DAZ.
+CFLAGS = ["-O3", "-march=x86-64-v3", "-fno-fast-math", "-ffp-contract=off",
+          "-fopenmp", "-shared", "-fPIC", "-std=c99"]
+
+
+def build(force: bool = False) -> str:
+    """Compile oracle.c into liboracle.so (gcc).  Building the checker is not using it."""
+    if force or not os.path.exists(_LIB_PATH) or \
+            os.path.getmtime(_LIB_PATH) < os.path.getmtime(_SRC):
+        tmp = _LIB_PATH + f".tmp{os.getpid()}"
+        subprocess.check_call(["gcc", *CFLAGS, "-o", tmp, _SRC, "-lm"])
+        os.replace(tmp, _LIB_PATH)
+    return _LIB_PATH
+
+
+def _load():
+    global _lib
+    if _lib is None:
+        lib = ctypes.CDLL(build())
+        dp = ctypes.POINTER(ctypes.c_double)
+        for name in ("oracle_tsmttsm_d", "oracle_tsmttsm_z", "oracle_tsmm_d", "oracle_tsmm_z"):
+            f = getattr(lib, name)
+            f.argtypes = [ctypes.c_int64, ctypes.c_int, ctypes.c_int, dp, dp, dp, dp]
+            f.restype = None
+        lib.oracle_max_err_ratio.argtypes = [ctypes.c_int64, ctypes.c_int, dp, dp, dp,
+                                             ctypes.POINTER(ctypes.c_int64), dp]
+        lib.oracle_max_err_ratio.restype = ctypes.c_double
+        lib.oracle_num_threads.restype = ctypes.c_int
+        lib.oracle_set_num_threads.argtypes = [ctypes.c_int]
+        _lib = lib
+    return _lib
+
+
+def _ptr(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+
+
+def _prep(x: np.ndarray, is_complex: bool) -> np.ndarray:
+    dt = np.complex128 if is_complex else np.float64
+    if x.dtype != dt:
+        raise TypeError(f"oracle expects {dt}, got {x.dtype}")
+    return np.ascontiguousarray(x)
+
+
+def num_threads() -> int:
+    return _load().oracle_num_threads()
+
+
+def set_num_threads(n: int) -> None:
+    _load().oracle_set_num_threads(int(n))
+
+
+def tsmttsm(A: np.ndarray, B: np.ndarray):
+    """C = A^T B (plain transpose).  A: K x M, B: K x N -> (C M x N, bound M x N)."""
+    is_c = np.iscomplexobj(A)
+    A = _prep(A, is_c)
+    B = _prep(B, is_c)
+    K, M = A.shape
+    K2, N = B.shape
+    if K != K2:
+        raise ValueError("A and B must have the same row count K")
+    C = np.zeros((M, N), dtype=A.dtype)
+    bound = np.zeros((M, N), dtype=np.float64)
+    f = _load().oracle_tsmttsm_z if is_c else _load().oracle_tsmttsm_d
+    f(K, M, N, _ptr(A), _ptr(B), _ptr(C), _ptr(bound))
+    return C, bound
+
+
+def tsmm(A: np.ndarray, C: np.ndarray):
+    """B = A C.  A: K x M, C: M x N -> (B K x N, bound K x N)."""
+    is_c = np.iscomplexobj(A)
+    A = _prep(A, is_c)
+    C = _prep(C, is_c)
+    K, M = A.shape
+    M2, N = C.shape
+    if M != M2:
+        raise ValueError("A columns must equal C rows")
+    B = np.zeros((K, N), dtype=A.dtype)
+    bound = np.zeros((K, N), dtype=np.float64)
+    f = _load().oracle_tsmm_z if is_c else _load().oracle_tsmm_d
+    f(K, M, N, _ptr(A), _ptr(C), _ptr(B), _ptr(bound))
+    return B, bound
+
+
+def max_err_ratio(got: np.ndarray, ref: np.ndarray, bound: np.ndarray):
+    """Return (max |got-ref|/bound, worst flat index, max |got-ref|).
+
+    Complex inputs use the complex modulus of the difference (north star)."""
+    is_c = np.iscomplexobj(ref)
+    got = _prep(np.asarray(got), is_c)
+    ref = _prep(np.asarray(ref), is_c)
+    bound = np.ascontiguousarray(bound, dtype=np.float64)
+    if got.shape != ref.shape or bound.size != ref.size:
+        raise ValueError(f"shape mismatch {got.shape} {ref.shape} {bound.shape}")
+    wi = ctypes.c_int64(0)
+    ma = ctypes.c_double(0)
+    r = _load().oracle_max_err_ratio(ref.size, int(is_c), _ptr(got), _ptr(ref), _ptr(bound),
+                                     ctypes.byref(wi), ctypes.byref(ma))
+    return r, int(wi.value), float(ma.value)
