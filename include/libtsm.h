@@ -1,0 +1,223 @@
+/*
+ * libtsm.h -- C ABI of libtsm, a B200-native (sm_100a) library for the two
+ * tall & skinny matrix products of Ernst, Hager, Thies, Wellein,
+ * "Performance Engineering for Real and Complex Tall & Skinny Matrix
+ * Multiplication Kernels on GPUs" (arXiv 1905.03136; /root/reference/PAPER.md).
+ *
+ *   TSMTTSM   C = A^T B   PAPER.md:64-68 ("A^T B = C"), PAPER.md:342-349 (Listing 1):
+ *             C[m][n] = sum_{k<K} A[k][m] * B[k][n]
+ *   TSMM      B = A C     PAPER.md:64-68 ("A C = B"), PAPER.md:372-375:
+ *             B[k][n] = sum_{m<M} A[k][m] * C[m][n]
+ *
+ * Sizes: 1 <= M, N <= 64 ("skinny"), K >= 1 ("tall" means
+ * K > 10^6 but every K >= 1 is supported).
+ *
+ * Layout (all matrices): row-major and contiguous, leading dimension = width.
+ *   A[k][m] at A + k*M + m (K x M), B[k][n] at B + k*N + n (K x N),
+ *   C[m][n] at C + m*N + n (M x N)   -- PAPER.md:91 "row-major tall & skinny";
+ *   C row-major is DESIGN.md reading R2.
+ * Scalar types: D = IEEE double; Z = complex double as interleaved (re, im)
+ * pairs (tsm_zcomplex; the layout of cuDoubleComplex and torch.complex128),
+ * PAPER.md:70-72, 194-196.  The Z transpose is the PLAIN transpose -- no
+ * conjugation of A in TSMTTSM and none of C in TSMM (reading R1).
+ *
+ * Memory ownership: every matrix / workspace pointer is caller-owned DEVICE
+ * memory (e.g. a torch CUDA tensor) on the plan's device; the library never
+ * allocates device memory.  Base pointers of A, B, C and the workspace must be
+ * 16-byte aligned (TSM_ERR_MISALIGNED otherwise); outputs must not overlap
+ * inputs (TSM_ERR_INVALID_VALUE).  Outputs are fully overwritten (beta = 0).
+ *
+ * Streams: `stream` is a cudaStream_t passed as void* (NULL = legacy default
+ * stream).  Every call only enqueues work on that stream and returns without
+ * synchronising the host; asynchronous device faults surface at the caller's
+ * next synchronisation.  Calls on different streams are safe if each has its
+ * own workspace.
+ *
+ * Determinism: for a fixed (plan, K, inputs, GPU model) results are bitwise
+ * reproducible: the TSMTTSM reduction is a fixed-order two-level sum (no
+ * floating-point atomics; the paper's atomics, are replaced
+ * by a fixed-order grid reduction).  Different plans or K may
+ * differ within the parity tolerance (|dC| <= 1e-12 |A|^T|B|,
+ * |dB| <= 1e-13 |A||C|).
+ *
+ * Errors: every entry point returns tsm_status and never aborts, throws or
+ * prints.  Arguments are validated before any launch; a failed launch maps to
+ * TSM_ERR_CUDA.  tsm_last_error_detail() returns a thread-local description of
+ * the last failure.
+ */
+#ifndef LIBTSM_H
+#define LIBTSM_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TSM_VERSION_MAJOR 0
+#define TSM_VERSION_MINOR 1
+
+typedef enum {
+  TSM_SUCCESS = 0,
+  TSM_ERR_INVALID_VALUE = 1, /* bad size, null pointer, overlap, op/dtype mismatch */
+  TSM_ERR_UNSUPPORTED = 2,   /* shape/feature not available in this build */
+  TSM_ERR_MISALIGNED = 3,    /* a base pointer is not 16-byte aligned */
+  TSM_ERR_WORKSPACE = 4,     /* workspace missing or smaller than required */
+  TSM_ERR_CUDA = 5,          /* CUDA runtime / launch error */
+  TSM_ERR_NCCL = 6,          /* NCCL error or NCCL unavailable */
+  TSM_ERR_INTERNAL = 7
+} tsm_status;
+
+typedef enum { TSM_OP_TSMTTSM = 0, TSM_OP_TSMM = 1 } tsm_op;
+typedef enum { TSM_D = 0, TSM_Z = 1 } tsm_dtype;
+
+typedef struct tsm_zcomplex {
+  double re, im;
+} tsm_zcomplex;
+
+typedef struct tsm_plan_s *tsm_plan;
+typedef struct tsm_comm_s *tsm_comm;
+typedef void *tsm_stream; /* cudaStream_t */
+
+/* ------------------------------------------------------------------------ */
+/* Plans (pick the (M,N,type) instantiation    */
+/* and its B200-tuned launch parameters).                                    */
+/* ------------------------------------------------------------------------ */
+
+/* Create a plan for one (op, dtype, M, N) on CUDA device `device`.
+ * Selects the width-specialised kernel instantiated for exactly (M, N, dtype)
+ * and its tuned launch parameters (tile, threads, pipeline depth, grid).
+ * Benchmark shapes are compiled ahead of time; any other (M, N) is compiled
+ * on first use by NVRTC (sm_100a) from the same C++ template and cached.
+ * Errors: TSM_ERR_INVALID_VALUE (M or N outside [1,64], bad enum, out==NULL),
+ *         TSM_ERR_UNSUPPORTED (shared memory / occupancy cannot be met),
+ *         TSM_ERR_INTERNAL (run-time compilation failed),
+ *         TSM_ERR_CUDA (device query failed).  The plan owns host state only;
+ *         it is immutable and may be used from several threads. */
+tsm_status tsm_plan_create(tsm_plan *out, tsm_op op, tsm_dtype dtype, int M, int N,
+                           int device);
+
+/* Kernel configuration of a plan (the autotuning space):
+ *   TSMTTSM: p0 = MT, p1 = NTL: register tiles per row along m / n (powers of
+ *            two <= M, N; tile = ceil(M/MT) x ceil(N/NTL) cells per thread,
+ *            interleaved "transposed" mapping); p2 unused.
+ *   TSMM:    p0 = NTL lanes along n (interleaved columns),
+ *            p1 = MSPLIT lanes splitting the m-sum, p2 = U rows per thread
+ *            (C reuse); NTL*MSPLIT <= 32, powers of two.
+ *   threads: block size (multiple of 32); rows_per_chunk: rows per pipeline
+ *   stage (even); stages: smem ring depth; ctas_per_sm: resident CTAs per SM
+ *   (clipped by occupancy). */
+typedef struct tsm_config {
+  int threads;
+  int rows_per_chunk;
+  int p0, p1, p2;
+  int stages;
+  int ctas_per_sm;
+} tsm_config;
+
+/* Create a plan with an explicit configuration (used by the on-B200
+ * autotuner, tools/autotune.py).  If the configuration is not one of the
+ * ahead-of-time instantiations, the kernel is compiled at run time by NVRTC
+ * from the same template source.  Errors as tsm_plan_create, plus
+ * TSM_ERR_INVALID_VALUE for an inconsistent configuration and
+ * TSM_ERR_INTERNAL if run-time compilation fails. */
+tsm_status tsm_plan_create_config(tsm_plan *out, tsm_op op, tsm_dtype dtype, int M, int N,
+                                  int device, const tsm_config *cfg);
+
+/* The configuration a plan resolved to (stages/ctas after clipping). */
+tsm_status tsm_plan_get_config(tsm_plan p, tsm_config *cfg);
+
+/* Bytes of device workspace a TSMTTSM call with K rows needs (partials of the
+ * fixed-order grid reduction plus 2 counter words); 0 for TSMM plans.
+ * The first 256 bytes hold counters that MUST be zero before the first use of
+ * a workspace (cudaMemset / torch.zeros, or tsm_workspace_init); every
+ * successful call leaves them zero again. */
+tsm_status tsm_plan_workspace_bytes(tsm_plan p, int64_t K, size_t *bytes);
+
+/* Zero the counter words of a workspace (enqueued on `stream`). */
+tsm_status tsm_workspace_init(void *ws, size_t ws_bytes, tsm_stream stream);
+
+/* Human/JSON-readable description of the chosen instantiation and launch
+ * parameters for K rows, written into buf (NUL-terminated, truncated to len). */
+tsm_status tsm_plan_describe(tsm_plan p, int64_t K, char *buf, size_t len);
+
+tsm_status tsm_plan_destroy(tsm_plan p);
+
+const char *tsm_status_string(tsm_status s);
+const char *tsm_last_error_detail(void);
+
+/* ------------------------------------------------------------------------ */
+/* TSMTTSM  C = A^T B                         */
+/*   A: K x M device, B: K x N device, C: M x N device (overwritten).        */
+/*   ws: workspace of >= tsm_plan_workspace_bytes(p, K) bytes.               */
+/* ------------------------------------------------------------------------ */
+tsm_status tsmttsm_d(tsm_plan p, int64_t K, const double *A, const double *B, double *C,
+                     void *ws, size_t ws_bytes, tsm_stream stream);
+tsm_status tsmttsm_z(tsm_plan p, int64_t K, const tsm_zcomplex *A, const tsm_zcomplex *B,
+                     tsm_zcomplex *C, void *ws, size_t ws_bytes, tsm_stream stream);
+
+/* ------------------------------------------------------------------------ */
+/* TSMM  B = A C                              */
+/*   A: K x M device, C: M x N device, B: K x N device (overwritten).        */
+/* ------------------------------------------------------------------------ */
+tsm_status tsmm_d(tsm_plan p, int64_t K, const double *A, const double *C, double *B,
+                  tsm_stream stream);
+tsm_status tsmm_z(tsm_plan p, int64_t K, const tsm_zcomplex *A, const tsm_zcomplex *C,
+                  tsm_zcomplex *B, tsm_stream stream);
+
+/* ------------------------------------------------------------------------ */
+/* Device input generator (same counter-based generator as  */
+/* the Python module tsminputs, implemented independently):                  */
+/*   dst[i] = value(mix64(seed*0xD1B54A32D192ED03 + (mat_id<<48) + start+i))  */
+/*   for i < n (n real values; a complex matrix of e elements is n = 2e).     */
+/*   mode 0 = "fp" uniform [-1,1), mode 1 = "int" integers in [-1024,1023].   */
+/* ------------------------------------------------------------------------ */
+tsm_status tsm_fill(double *dst, int64_t n, uint64_t seed, int mat_id, int mode,
+                    int64_t start, tsm_stream stream);
+
+/* L2 flush helper for benchmarks: overwrite `bytes` of scratch device memory. */
+tsm_status tsm_l2_flush(void *scratch, size_t bytes, tsm_stream stream);
+
+/* ------------------------------------------------------------------------ */
+/* Multi-GPU: one process per GPU, K sharded by rows.      */
+/* The 128-byte NCCL unique id is created on rank 0 with tsm_comm_unique_id  */
+/* and exchanged by the caller (torch.distributed).  NCCL is loaded          */
+/* dynamically (the libnccl.so.2 already in the process, e.g. torch's);      */
+/* TSM_ERR_NCCL if unavailable.                                              */
+/* ------------------------------------------------------------------------ */
+#define TSM_COMM_DETERMINISTIC 1 /* allgather partials + fixed rank-order sum */
+
+tsm_status tsm_comm_unique_id(void *uid128);
+tsm_status tsm_comm_init(tsm_comm *out, const void *uid128, int nranks, int rank, int device,
+                         int flags);
+tsm_status tsm_comm_destroy(tsm_comm c);
+/* Workspace for the sharded TSMTTSM: tsm_plan_workspace_bytes(p, K_local) plus
+ * this many extra bytes (deterministic mode gathers nranks partial C's). */
+tsm_status tsm_comm_workspace_extra_bytes(tsm_comm c, tsm_plan p, size_t *bytes);
+
+/* Local TSMTTSM over this rank's K_local rows, then a sum of C over ranks
+ * (ncclAllReduce, or allgather + fixed-order sum with TSM_COMM_DETERMINISTIC).
+ * C ends replicated on every rank.  K_local may be 0 (contributes zeros). */
+tsm_status tsmttsm_allreduce_d(tsm_plan p, tsm_comm c, int64_t K_local, const double *A,
+                               const double *B, double *C, void *ws, size_t ws_bytes,
+                               tsm_stream stream);
+tsm_status tsmttsm_allreduce_z(tsm_plan p, tsm_comm c, int64_t K_local, const tsm_zcomplex *A,
+                               const tsm_zcomplex *B, tsm_zcomplex *C, void *ws,
+                               size_t ws_bytes, tsm_stream stream);
+
+/* Broadcast C from `root` (in place; input on root, output elsewhere), then
+ * the local TSMM B_local = A_local C.  K_local may be 0. */
+tsm_status tsmm_bcast_d(tsm_plan p, tsm_comm c, int root, int64_t K_local, const double *A,
+                        double *C, double *B, tsm_stream stream);
+tsm_status tsmm_bcast_z(tsm_plan p, tsm_comm c, int root, int64_t K_local,
+                        const tsm_zcomplex *A, tsm_zcomplex *C, tsm_zcomplex *B,
+                        tsm_stream stream);
+
+/* Library / build information (JSON), e.g. the list of AOT instantiations. */
+const char *tsm_build_info(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LIBTSM_H */

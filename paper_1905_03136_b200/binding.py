@@ -1,0 +1,370 @@
+"""Thin ctypes binding of libtsm (include/libtsm.h).
+
+Argument marshalling only: every step of TSMTTSM / TSMM runs in libtsm.so's
+CUDA kernels.  The raw functions keep the C names (``tsmttsm_d`` ...) and take
+integer device pointers; the ``tsmttsm`` / ``tsmm`` helpers accept torch CUDA
+tensors (PyTorch supplies device memory and the current stream only).
+
+There is deliberately no CPU fallback: if libtsm.so is missing or cannot be
+loaded, importing this module raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.environ.get("TSM_LIB", os.path.join(PKG, "libtsm.so"))
+
+TSM_SUCCESS = 0
+STATUS = {0: "TSM_SUCCESS", 1: "TSM_ERR_INVALID_VALUE", 2: "TSM_ERR_UNSUPPORTED",
+          3: "TSM_ERR_MISALIGNED", 4: "TSM_ERR_WORKSPACE", 5: "TSM_ERR_CUDA",
+          6: "TSM_ERR_NCCL", 7: "TSM_ERR_INTERNAL"}
+OP = {"tsmttsm": 0, "tsmm": 1}
+DTYPE = {"d": 0, "z": 1}
+TSM_COMM_DETERMINISTIC = 1
+MAT_ID = {"A": 1, "B": 2, "C": 3}
+
+# exported symbols declared in include/libtsm.h (checked by tests/test_abi.py)
+EXPORTS = [
+    "tsm_plan_create", "tsm_plan_create_config", "tsm_plan_get_config", "tsm_plan_workspace_bytes", "tsm_workspace_init", "tsm_plan_describe",
+    "tsm_plan_destroy", "tsm_status_string", "tsm_last_error_detail",
+    "tsmttsm_d", "tsmttsm_z", "tsmm_d", "tsmm_z", "tsm_fill", "tsm_l2_flush",
+    "tsm_comm_unique_id", "tsm_comm_init", "tsm_comm_destroy", "tsm_comm_workspace_extra_bytes",
+    "tsmttsm_allreduce_d", "tsmttsm_allreduce_z", "tsmm_bcast_d", "tsmm_bcast_z",
+    "tsm_build_info",
+]
+
+
+class TsmConfig(ctypes.Structure):
+    """tsm_config (include/libtsm.h)."""
+    _fields_ = [("threads", ctypes.c_int), ("rows_per_chunk", ctypes.c_int), ("p0", ctypes.c_int),
+                ("p1", ctypes.c_int), ("p2", ctypes.c_int), ("stages", ctypes.c_int),
+                ("ctas_per_sm", ctypes.c_int)]
+
+    def as_dict(self):
+        return {f: getattr(self, f) for f, _ in self._fields_}
+
+
+class TsmError(RuntimeError):
+    def __init__(self, status: int, where: str, detail: str = ""):
+        self.status = status
+        super().__init__(f"{where}: {STATUS.get(status, status)}" + (f" ({detail})" if detail else ""))
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"libtsm.so not found at {LIB_PATH}; run __graft_entry__.build() "
+                          "(there is no CPU fallback)")
+    lib = ctypes.CDLL(LIB_PATH, mode=ctypes.RTLD_GLOBAL)
+    P, I, I64, SZ, VP = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_size_t, ctypes.c_void_p
+    sig = {
+        "tsm_plan_create": [ctypes.POINTER(P), I, I, I, I, I],
+        "tsm_plan_create_config": [ctypes.POINTER(P), I, I, I, I, I, ctypes.POINTER(TsmConfig)],
+        "tsm_plan_get_config": [P, ctypes.POINTER(TsmConfig)],
+        "tsm_plan_workspace_bytes": [P, I64, ctypes.POINTER(SZ)],
+        "tsm_workspace_init": [VP, SZ, VP],
+        "tsm_plan_describe": [P, I64, ctypes.c_char_p, SZ],
+        "tsm_plan_destroy": [P],
+        "tsm_status_string": [I],
+        "tsm_last_error_detail": [],
+        "tsmttsm_d": [P, I64, VP, VP, VP, VP, SZ, VP],
+        "tsmttsm_z": [P, I64, VP, VP, VP, VP, SZ, VP],
+        "tsmm_d": [P, I64, VP, VP, VP, VP],
+        "tsmm_z": [P, I64, VP, VP, VP, VP],
+        "tsm_fill": [VP, I64, ctypes.c_uint64, I, I, I64, VP],
+        "tsm_l2_flush": [VP, SZ, VP],
+        "tsm_comm_unique_id": [VP],
+        "tsm_comm_init": [ctypes.POINTER(P), VP, I, I, I, I],
+        "tsm_comm_destroy": [P],
+        "tsm_comm_workspace_extra_bytes": [P, P, ctypes.POINTER(SZ)],
+        "tsmttsm_allreduce_d": [P, P, I64, VP, VP, VP, VP, SZ, VP],
+        "tsmttsm_allreduce_z": [P, P, I64, VP, VP, VP, VP, SZ, VP],
+        "tsmm_bcast_d": [P, P, I, I64, VP, VP, VP, VP],
+        "tsmm_bcast_z": [P, P, I, I64, VP, VP, VP, VP],
+        "tsm_build_info": [],
+    }
+    for name, args in sig.items():
+        f = getattr(lib, name)
+        f.argtypes = args
+        f.restype = ctypes.c_char_p if name in ("tsm_status_string", "tsm_last_error_detail",
+                                               "tsm_build_info") else ctypes.c_int
+    return lib
+
+
+lib = _load()
+
+
+def check(status: int, where: str) -> None:
+    if status != TSM_SUCCESS:
+        raise TsmError(status, where, lib.tsm_last_error_detail().decode(errors="replace"))
+
+
+# ---------------------------------------------------------------------------
+# Raw C-ABI functions (same names as include/libtsm.h; pointers as ints)
+# ---------------------------------------------------------------------------
+def tsm_plan_create(op: str, dtype: str, M: int, N: int, device: int) -> int:
+    h = ctypes.c_void_p()
+    check(lib.tsm_plan_create(ctypes.byref(h), OP[op], DTYPE[dtype], M, N, device),
+          f"tsm_plan_create({op},{dtype},{M},{N})")
+    return h.value
+
+
+def tsm_plan_create_config(op: str, dtype: str, M: int, N: int, device: int, cfg: dict) -> int:
+    h = ctypes.c_void_p()
+    c = TsmConfig(**cfg)
+    check(lib.tsm_plan_create_config(ctypes.byref(h), OP[op], DTYPE[dtype], M, N, device,
+                                     ctypes.byref(c)), f"tsm_plan_create_config({op},{dtype},{M},{N})")
+    return h.value
+
+
+def tsm_plan_get_config(plan: int) -> dict:
+    c = TsmConfig()
+    check(lib.tsm_plan_get_config(plan, ctypes.byref(c)), "tsm_plan_get_config")
+    return c.as_dict()
+
+
+def tsm_plan_destroy(plan: int) -> None:
+    check(lib.tsm_plan_destroy(plan), "tsm_plan_destroy")
+
+
+def tsm_plan_workspace_bytes(plan: int, K: int) -> int:
+    n = ctypes.c_size_t()
+    check(lib.tsm_plan_workspace_bytes(plan, K, ctypes.byref(n)), "tsm_plan_workspace_bytes")
+    return n.value
+
+
+def tsm_plan_describe(plan: int, K: int) -> str:
+    buf = ctypes.create_string_buffer(1024)
+    check(lib.tsm_plan_describe(plan, K, buf, 1024), "tsm_plan_describe")
+    return buf.value.decode()
+
+
+def tsm_workspace_init(ws: int, nbytes: int, stream: int) -> None:
+    check(lib.tsm_workspace_init(ws, nbytes, stream), "tsm_workspace_init")
+
+
+def tsmttsm_d(plan, K, A, B, C, ws, ws_bytes, stream):
+    check(lib.tsmttsm_d(plan, K, A, B, C, ws, ws_bytes, stream), "tsmttsm_d")
+
+
+def tsmttsm_z(plan, K, A, B, C, ws, ws_bytes, stream):
+    check(lib.tsmttsm_z(plan, K, A, B, C, ws, ws_bytes, stream), "tsmttsm_z")
+
+
+def tsmm_d(plan, K, A, C, B, stream):
+    check(lib.tsmm_d(plan, K, A, C, B, stream), "tsmm_d")
+
+
+def tsmm_z(plan, K, A, C, B, stream):
+    check(lib.tsmm_z(plan, K, A, C, B, stream), "tsmm_z")
+
+
+def tsm_fill(dst, n, seed, mat_id, mode, start, stream):
+    check(lib.tsm_fill(dst, n, seed, mat_id, mode, start, stream), "tsm_fill")
+
+
+def tsm_l2_flush(scratch, nbytes, stream):
+    check(lib.tsm_l2_flush(scratch, nbytes, stream), "tsm_l2_flush")
+
+
+def tsm_build_info() -> str:
+    return lib.tsm_build_info().decode()
+
+
+# ---------------------------------------------------------------------------
+# torch-tensor convenience layer (device memory + current stream from torch)
+# ---------------------------------------------------------------------------
+_plans: dict = {}
+_ws: dict = {}
+_mu = threading.Lock()
+
+
+class Plan:
+    """Owning wrapper of a tsm_plan handle."""
+
+    def __init__(self, op: str, dtype: str, M: int, N: int, device: int = 0,
+                 config: dict | None = None):
+        self.op, self.dtype, self.M, self.N, self.device = op, dtype, M, N, device
+        self.handle = None
+        if config is None:
+            self.handle = tsm_plan_create(op, dtype, M, N, device)
+        else:
+            self.handle = tsm_plan_create_config(op, dtype, M, N, device, config)
+
+    def config(self) -> dict:
+        return tsm_plan_get_config(self.handle)
+
+    def workspace_bytes(self, K: int) -> int:
+        return tsm_plan_workspace_bytes(self.handle, K)
+
+    def describe(self, K: int = 1 << 24) -> dict:
+        import json
+        return json.loads(tsm_plan_describe(self.handle, K))
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h and lib is not None:
+            lib.tsm_plan_destroy(h)
+            self.handle = None
+
+
+def get_plan(op: str, dtype: str, M: int, N: int, device: int) -> Plan:
+    key = (op, dtype, M, N, device)
+    with _mu:
+        p = _plans.get(key)
+        if p is None:
+            p = Plan(op, dtype, M, N, device)
+            _plans[key] = p
+    return p
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def _dtype_code(t) -> str:
+    torch = _torch()
+    if t.dtype == torch.float64:
+        return "d"
+    if t.dtype == torch.complex128:
+        return "z"
+    raise TypeError(f"libtsm supports float64 (D) and complex128 (Z), got {t.dtype}")
+
+
+def _check_cuda(*ts):
+    for t in ts:
+        if not t.is_cuda:
+            raise ValueError("libtsm needs CUDA tensors (there is no CPU path)")
+        if not t.is_contiguous():
+            raise ValueError("libtsm needs contiguous row-major tensors")
+
+
+def workspace(plan: Plan, K: int, stream: int, min_bytes: int = 0):
+    """Cached, counter-zeroed workspace for (device, stream); grows as needed."""
+    torch = _torch()
+    need = max(plan.workspace_bytes(K), min_bytes, 256)
+    key = (plan.device, stream)
+    with _mu:
+        buf = _ws.get(key)
+        if buf is None or buf.numel() < need:
+            buf = torch.zeros(need + (1 << 20), dtype=torch.uint8, device=f"cuda:{plan.device}")
+            _ws[key] = buf
+    return buf
+
+
+def tsmttsm(A, B, out=None, plan: Plan | None = None):
+    """C = A^T B (plain transpose) for torch CUDA tensors A (K x M), B (K x N)."""
+    torch = _torch()
+    _check_cuda(A, B)
+    dt = _dtype_code(A)
+    if B.dtype != A.dtype or A.dim() != 2 or B.dim() != 2 or A.shape[0] != B.shape[0]:
+        raise ValueError("A and B must be 2-D, same dtype, same row count")
+    K, M = A.shape
+    N = B.shape[1]
+    dev = A.device.index
+    plan = plan or get_plan("tsmttsm", dt, M, N, dev)
+    C = out if out is not None else torch.empty((M, N), dtype=A.dtype, device=A.device)
+    _check_cuda(C)
+    stream = torch.cuda.current_stream(A.device).cuda_stream
+    ws = workspace(plan, K, stream)
+    f = tsmttsm_z if dt == "z" else tsmttsm_d
+    f(plan.handle, K, A.data_ptr(), B.data_ptr(), C.data_ptr(), ws.data_ptr(), ws.numel(), stream)
+    return C
+
+
+def tsmm(A, C, out=None, plan: Plan | None = None):
+    """B = A C for torch CUDA tensors A (K x M), C (M x N)."""
+    torch = _torch()
+    _check_cuda(A, C)
+    dt = _dtype_code(A)
+    if C.dtype != A.dtype or A.dim() != 2 or C.dim() != 2 or A.shape[1] != C.shape[0]:
+        raise ValueError("A (K x M) and C (M x N) must be 2-D with matching M and dtype")
+    K, M = A.shape
+    N = C.shape[1]
+    dev = A.device.index
+    plan = plan or get_plan("tsmm", dt, M, N, dev)
+    B = out if out is not None else torch.empty((K, N), dtype=A.dtype, device=A.device)
+    _check_cuda(B)
+    stream = torch.cuda.current_stream(A.device).cuda_stream
+    f = tsmm_z if dt == "z" else tsmm_d
+    f(plan.handle, K, A.data_ptr(), C.data_ptr(), B.data_ptr(), stream)
+    return B
+
+
+def fill(t, mat: str, seed: int, mode: str = "fp"):
+    """Fill a float64/complex128 CUDA tensor with the counter-based generator
+    (the same values tsminputs.matrix() produces on the host)."""
+    torch = _torch()
+    _check_cuda(t)
+    n = t.numel() * (2 if t.dtype == torch.complex128 else 1)
+    if t.dtype not in (torch.float64, torch.complex128):
+        raise TypeError("fill expects float64 or complex128")
+    stream = torch.cuda.current_stream(t.device).cuda_stream
+    tsm_fill(t.data_ptr(), n, seed, MAT_ID[mat], 0 if mode == "fp" else 1, 0, stream)
+    return t
+
+
+# ---------------------------------------------------------------------------
+# multi-GPU (one process per GPU; NCCL id exchanged through torch.distributed)
+# ---------------------------------------------------------------------------
+class Comm:
+    def __init__(self, rank: int, world: int, device: int, deterministic: bool = False,
+                 group=None):
+        import torch.distributed as dist
+        uid = ctypes.create_string_buffer(128)
+        if rank == 0:
+            check(lib.tsm_comm_unique_id(uid), "tsm_comm_unique_id")
+        obj = [bytes(uid.raw) if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0, group=group)
+        uid = ctypes.create_string_buffer(obj[0], 128)
+        h = ctypes.c_void_p()
+        flags = TSM_COMM_DETERMINISTIC if deterministic else 0
+        check(lib.tsm_comm_init(ctypes.byref(h), uid, world, rank, device, flags), "tsm_comm_init")
+        self.handle = h.value
+        self.rank, self.world, self.device, self.deterministic = rank, world, device, deterministic
+
+    def extra_bytes(self, plan: Plan) -> int:
+        n = ctypes.c_size_t()
+        check(lib.tsm_comm_workspace_extra_bytes(self.handle, plan.handle, ctypes.byref(n)),
+              "tsm_comm_workspace_extra_bytes")
+        return n.value
+
+    def close(self):
+        if self.handle:
+            check(lib.tsm_comm_destroy(self.handle), "tsm_comm_destroy")
+            self.handle = None
+
+
+def tsmttsm_allreduce(comm: Comm, A, B, out=None):
+    torch = _torch()
+    _check_cuda(A, B)
+    dt = _dtype_code(A)
+    K, M = A.shape
+    N = B.shape[1]
+    plan = get_plan("tsmttsm", dt, M, N, A.device.index)
+    C = out if out is not None else torch.empty((M, N), dtype=A.dtype, device=A.device)
+    stream = torch.cuda.current_stream(A.device).cuda_stream
+    need = plan.workspace_bytes(K) + 256 + comm.extra_bytes(plan)
+    ws = workspace(plan, K, stream, need)
+    f = lib.tsmttsm_allreduce_z if dt == "z" else lib.tsmttsm_allreduce_d
+    check(f(plan.handle, comm.handle, K, A.data_ptr(), B.data_ptr(), C.data_ptr(), ws.data_ptr(),
+            ws.numel(), stream), "tsmttsm_allreduce")
+    return C
+
+
+def tsmm_bcast(comm: Comm, A, C, root: int = 0, out=None):
+    torch = _torch()
+    _check_cuda(A, C)
+    dt = _dtype_code(A)
+    K, M = A.shape
+    N = C.shape[1]
+    plan = get_plan("tsmm", dt, M, N, A.device.index)
+    B = out if out is not None else torch.empty((K, N), dtype=A.dtype, device=A.device)
+    stream = torch.cuda.current_stream(A.device).cuda_stream
+    f = lib.tsmm_bcast_z if dt == "z" else lib.tsmm_bcast_d
+    check(f(plan.handle, comm.handle, root, K, A.data_ptr(), C.data_ptr(), B.data_ptr(), stream),
+          "tsmm_bcast")
+    return B

@@ -1,0 +1,508 @@
+// tsm_api.cu -- libtsm C ABI (include/libtsm.h): plans, validation, launches.
+//
+// Host side of SURVEY.md §8(a) rows T0 / S0 ("plan / dispatch"): pick the
+// (M,N,type) instantiation and its launch parameters, validate, launch on the
+// caller's stream.  No device memory is allocated here; no host sync.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/libtsm.h"
+#include "tsm_internal.h"
+#include "tsm_kernels.cuh"
+#include "tsm_registry.h"
+
+namespace tsm {
+
+static thread_local std::string g_detail;
+
+tsm_status fail(tsm_status s, const std::string& why) {
+  g_detail = why;
+  return s;
+}
+
+tsm_status cuda_fail(cudaError_t e, const char* what) {
+  g_detail = std::string(what) + ": " + cudaGetErrorString(e);
+  return TSM_ERR_CUDA;
+}
+
+// ---- device properties cache ----
+struct DevInfo {
+  int sms = 0;
+  size_t smem_optin = 0;
+  bool ok = false;
+};
+static std::mutex g_mu;
+static std::vector<DevInfo> g_dev;
+
+tsm_status dev_info(int device, DevInfo* out) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (device < 0) return fail(TSM_ERR_INVALID_VALUE, "negative device id");
+  if (static_cast<int>(g_dev.size()) <= device) g_dev.resize(device + 1);
+  if (!g_dev[device].ok) {
+    int sms = 0, optin = 0;
+    cudaError_t e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceGetAttribute(SM count)");
+    e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceGetAttribute(smem optin)");
+    g_dev[device].sms = sms;
+    g_dev[device].smem_optin = static_cast<size_t>(optin);
+    g_dev[device].ok = true;
+  }
+  *out = g_dev[device];
+  return TSM_SUCCESS;
+}
+
+// RAII: make `device` current for the duration of a call.
+struct DeviceGuard {
+  int prev = -1;
+  cudaError_t err = cudaSuccess;
+  explicit DeviceGuard(int device) {
+    err = cudaGetDevice(&prev);
+    if (err == cudaSuccess && prev != device) err = cudaSetDevice(device);
+    else prev = -1;
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+size_t smem_bytes(const KernelEntry& k, int stages) {
+  const long long S = k.dt == TSM_Z ? 2 : 1;
+  if (k.op == KIND_TSMTTSM) {
+    const long long stage = static_cast<long long>(k.R) * (k.M + k.N) * S;
+    const long long cells = static_cast<long long>(k.M) * k.N * S;
+    long long need = std::max<long long>(stages * stage, std::max<long long>(cells, k.NT));
+    return static_cast<size_t>(128 + need * 8);
+  }
+  const long long cdbl = static_cast<long long>(k.M) * k.N * S;
+  const long long cpad = ((cdbl + 15) / 16) * 16;
+  const long long rpp = static_cast<long long>(k.NT / (k.p0 * k.p1)) * k.p2;  // rows per pass
+  const long long out = rpp * k.N * S;
+  const long long a = static_cast<long long>(k.R) * k.M * S;
+  return static_cast<size_t>(128 + (cpad + 2 * out + stages * a) * 8);
+}
+
+// ==========================================================================
+// Device input generator (same counter-based generator as tsminputs).
+// ==========================================================================
+__device__ __forceinline__ u64 mix64(u64 z) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+__global__ void fill_kernel(double* __restrict__ dst, long long n, u64 base, int mode,
+                            long long start) {
+  long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  const long long st = static_cast<long long>(gridDim.x) * blockDim.x;
+  for (; i < n; i += st) {
+    const u64 h = mix64(base + static_cast<u64>(start + i));
+    double v;
+    if (mode == 0)
+      v = static_cast<double>(static_cast<long long>(h >> 11) - (1LL << 52)) * 0x1p-52;
+    else
+      v = static_cast<double>(static_cast<long long>(h >> 53) - 1024LL);
+    dst[i] = v;
+  }
+}
+
+__global__ void l2_flush_kernel(double4* __restrict__ dst, long long n4) {
+  long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  const long long st = static_cast<long long>(gridDim.x) * blockDim.x;
+  for (; i < n4; i += st) dst[i] = make_double4(0.0, 0.0, 0.0, static_cast<double>(i));
+}
+
+}  // namespace tsm
+
+using namespace tsm;
+
+struct tsm_plan_s {
+  int op, dt, M, N, device;
+  const KernelEntry* k;
+  int sms;
+  int stages;
+  int ctas_per_sm;
+  size_t smem;
+  bool jit;  // kernel compiled at run time by NVRTC (shape/config outside the AOT set)
+};
+
+extern "C" {
+
+const char* tsm_status_string(tsm_status s) {
+  switch (s) {
+    case TSM_SUCCESS: return "TSM_SUCCESS";
+    case TSM_ERR_INVALID_VALUE: return "TSM_ERR_INVALID_VALUE";
+    case TSM_ERR_UNSUPPORTED: return "TSM_ERR_UNSUPPORTED";
+    case TSM_ERR_MISALIGNED: return "TSM_ERR_MISALIGNED";
+    case TSM_ERR_WORKSPACE: return "TSM_ERR_WORKSPACE";
+    case TSM_ERR_CUDA: return "TSM_ERR_CUDA";
+    case TSM_ERR_NCCL: return "TSM_ERR_NCCL";
+    case TSM_ERR_INTERNAL: return "TSM_ERR_INTERNAL";
+  }
+  return "TSM_ERR_UNKNOWN";
+}
+
+const char* tsm_last_error_detail(void) { return g_detail.c_str(); }
+
+}  // extern "C"
+
+namespace tsm {
+
+static bool is_pow2(int x) { return x > 0 && (x & (x - 1)) == 0; }
+
+// Mirror of the static_asserts of TsmttsmCfg / TsmmCfg, so a bad explicit
+// configuration is rejected with a clear message before any compilation.
+static tsm_status validate_config(const KernelEntry& e) {
+  auto bad = [](const std::string& w) { return fail(TSM_ERR_INVALID_VALUE, "bad config: " + w); };
+  if (e.NT < 32 || e.NT > 1024 || e.NT % 32) return bad("threads must be a multiple of 32 in [32, 1024]");
+  if (e.R < 2 || e.R % 2) return bad("rows_per_chunk must be even and >= 2");
+  if (e.stages < 2 || e.stages > 16) return bad("stages must be in [2, 16]");
+  if (e.ctas_per_sm < 1) return bad("ctas_per_sm must be >= 1");
+  if (e.op == KIND_TSMTTSM) {
+    if (!is_pow2(e.p0) || !is_pow2(e.p1) || e.p0 > e.M || e.p1 > e.N)
+      return bad("MT, NTL must be powers of two <= M, N");
+    if (e.NT % (e.p0 * e.p1)) return bad("MT*NTL must divide threads");
+  } else {
+    if (!is_pow2(e.p0) || !is_pow2(e.p1) || e.p0 > e.N || e.p1 > e.M || e.p0 * e.p1 > 32)
+      return bad("NTL <= N, MSPLIT <= M powers of two with NTL*MSPLIT <= 32");
+    if (e.p2 < 1 || e.p2 > 64) return bad("U must be in [1, 64]");
+    const int rpp = (e.NT / (e.p0 * e.p1)) * e.p2;
+    if (rpp % 2 || e.R % rpp) return bad("rows per pass must be even and divide rows_per_chunk");
+  }
+  return TSM_SUCCESS;
+}
+
+// Common tail of plan creation: resolve the kernel (AOT or JIT), size smem,
+// query occupancy, build the plan.
+static tsm_status make_plan(tsm_plan* out, const KernelEntry& want, int device, bool exact) {
+  DevInfo di;
+  tsm_status st = dev_info(device, &di);
+  if (st != TSM_SUCCESS) return st;
+  DeviceGuard dg(device);
+  if (dg.err != cudaSuccess) return cuda_fail(dg.err, "cudaSetDevice");
+  const KernelEntry* k = exact ? find_aot_config(want) : find_aot(want.op, want.dt, want.M, want.N);
+  bool jit = false;
+  if (!k) {
+    st = jit_kernel(want, &k);
+    if (st != TSM_SUCCESS) return st;
+    jit = true;
+  }
+  int stages = exact ? want.stages : k->stages;
+  size_t smem = smem_bytes(*k, stages);
+  while (smem > di.smem_optin && stages > 2) smem = smem_bytes(*k, --stages);
+  if (smem > di.smem_optin) return fail(TSM_ERR_UNSUPPORTED, "shared memory request too large");
+  cudaError_t e = cudaFuncSetAttribute(k->func, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem));
+  if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(MaxDynamicSharedMemorySize)");
+  int occ = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k->func, k->NT, smem);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
+  if (occ < 1) return fail(TSM_ERR_UNSUPPORTED, "kernel cannot be resident (occupancy 0)");
+
+  tsm_plan p = new (std::nothrow) tsm_plan_s;
+  if (!p) return fail(TSM_ERR_INTERNAL, "out of host memory");
+  p->op = want.op;
+  p->dt = want.dt;
+  p->M = want.M;
+  p->N = want.N;
+  p->device = device;
+  p->k = k;
+  p->sms = di.sms;
+  p->stages = stages;
+  p->ctas_per_sm = std::min(occ, std::max(1, exact ? want.ctas_per_sm : k->ctas_per_sm));
+  p->smem = smem;
+  p->jit = jit;
+  *out = p;
+  return TSM_SUCCESS;
+}
+
+}  // namespace tsm
+
+extern "C" {
+
+tsm_status tsm_plan_create(tsm_plan* out, tsm_op op, tsm_dtype dtype, int M, int N, int device) {
+  if (!out) return fail(TSM_ERR_INVALID_VALUE, "out == NULL");
+  *out = nullptr;
+  if (op != TSM_OP_TSMTTSM && op != TSM_OP_TSMM) return fail(TSM_ERR_INVALID_VALUE, "bad op");
+  if (dtype != TSM_D && dtype != TSM_Z) return fail(TSM_ERR_INVALID_VALUE, "bad dtype");
+  if (M < 1 || M > 64 || N < 1 || N > 64)
+    return fail(TSM_ERR_INVALID_VALUE, "M and N must be in [1, 64] (PAPER.md:57-58)");
+  const KernelEntry* d = default_params(op, dtype, M, N);
+  if (!d) return fail(TSM_ERR_INTERNAL, "no default parameters");
+  return make_plan(out, *d, device, false);
+}
+
+tsm_status tsm_plan_create_config(tsm_plan* out, tsm_op op, tsm_dtype dtype, int M, int N,
+                                  int device, const tsm_config* cfg) {
+  if (!out || !cfg) return fail(TSM_ERR_INVALID_VALUE, "null argument");
+  *out = nullptr;
+  if (op != TSM_OP_TSMTTSM && op != TSM_OP_TSMM) return fail(TSM_ERR_INVALID_VALUE, "bad op");
+  if (dtype != TSM_D && dtype != TSM_Z) return fail(TSM_ERR_INVALID_VALUE, "bad dtype");
+  if (M < 1 || M > 64 || N < 1 || N > 64)
+    return fail(TSM_ERR_INVALID_VALUE, "M and N must be in [1, 64] (PAPER.md:57-58)");
+  KernelEntry e{};
+  e.op = op;
+  e.dt = dtype;
+  e.M = M;
+  e.N = N;
+  e.func = nullptr;
+  e.NT = cfg->threads;
+  e.R = cfg->rows_per_chunk;
+  e.p0 = cfg->p0;
+  e.p1 = cfg->p1;
+  e.p2 = op == TSM_OP_TSMTTSM ? 0 : cfg->p2;
+  e.stages = cfg->stages;
+  e.ctas_per_sm = cfg->ctas_per_sm;
+  tsm_status st = validate_config(e);
+  if (st != TSM_SUCCESS) return st;
+  return make_plan(out, e, device, true);
+}
+
+tsm_status tsm_plan_get_config(tsm_plan p, tsm_config* cfg) {
+  if (!p || !cfg) return fail(TSM_ERR_INVALID_VALUE, "null argument");
+  cfg->threads = p->k->NT;
+  cfg->rows_per_chunk = p->k->R;
+  cfg->p0 = p->k->p0;
+  cfg->p1 = p->k->p1;
+  cfg->p2 = p->k->p2;
+  cfg->stages = p->stages;
+  cfg->ctas_per_sm = p->ctas_per_sm;
+  return TSM_SUCCESS;
+}
+
+tsm_status tsm_plan_destroy(tsm_plan p) {
+  delete p;
+  return TSM_SUCCESS;
+}
+
+}  // extern "C"
+
+namespace tsm {
+
+// Launch geometry for K rows: persistent grid, clipped for small K
+// (the paper's "opportunistically reduce the amount of launched threads for
+// small row counts").
+struct Geometry {
+  int grid;
+  long long nchunks;
+  int nfin;
+};
+
+Geometry geometry(const tsm_plan_s* p, long long K) {
+  Geometry g;
+  const long long K_even = K & ~1LL;
+  g.nchunks = (K_even + p->k->R - 1) / p->k->R;
+  const long long gmax = static_cast<long long>(p->sms) * p->ctas_per_sm;
+  g.grid = static_cast<int>(std::max<long long>(1, std::min(gmax, g.nchunks)));
+  if (p->op == TSM_OP_TSMTTSM) {
+    // finisher blocks: about 16 partial values per finisher thread, at most
+    // 64 blocks and at most half the grid (so finishers rarely wait).
+    const long long S = p->dt == TSM_Z ? 2 : 1;
+    const long long cells = static_cast<long long>(p->M) * p->N * S;
+    long long nf = (cells * g.grid + 16LL * p->k->NT - 1) / (16LL * p->k->NT);
+    nf = std::min<long long>(nf, 64);
+    nf = std::min<long long>(nf, std::max(1, g.grid / 2));
+    nf = std::min<long long>(nf, cells);
+    g.nfin = static_cast<int>(std::max<long long>(1, nf));
+  } else {
+    g.nfin = 0;
+  }
+  return g;
+}
+
+size_t workspace_bytes(const tsm_plan_s* p, long long K) {
+  if (p->op != TSM_OP_TSMTTSM) return 0;
+  const Geometry g = geometry(p, K);
+  const size_t S = p->dt == TSM_Z ? 2 : 1;
+  return WsLayout::kCounterBytes + static_cast<size_t>(g.grid) * p->M * p->N * S * 8;
+}
+
+static bool misaligned(const void* ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15u) != 0; }
+
+static bool overlap(const void* a, size_t na, const void* b, size_t nb) {
+  const uintptr_t x = reinterpret_cast<uintptr_t>(a), y = reinterpret_cast<uintptr_t>(b);
+  return na && nb && x < y + nb && y < x + na;
+}
+
+tsm_status launch_tsmttsm(const tsm_plan_s* p, int dt, long long K, const void* A, const void* B,
+                          void* C, void* ws, size_t ws_bytes, void* stream, bool allow_k0) {
+  if (!p) return fail(TSM_ERR_INVALID_VALUE, "plan == NULL");
+  if (p->op != TSM_OP_TSMTTSM || p->dt != dt)
+    return fail(TSM_ERR_INVALID_VALUE, "plan op/dtype does not match the call");
+  if (K < (allow_k0 ? 0 : 1)) return fail(TSM_ERR_INVALID_VALUE, "K must be >= 1");
+  if (!C || !ws || (K > 0 && (!A || !B))) return fail(TSM_ERR_INVALID_VALUE, "null pointer");
+  if (misaligned(A) || misaligned(B) || misaligned(C) || misaligned(ws))
+    return fail(TSM_ERR_MISALIGNED, "A, B, C and ws must be 16-byte aligned");
+  const size_t s = (dt == TSM_Z ? 16 : 8);
+  const size_t nA = static_cast<size_t>(K) * p->M * s, nB = static_cast<size_t>(K) * p->N * s;
+  const size_t nC = static_cast<size_t>(p->M) * p->N * s;
+  const size_t need = workspace_bytes(p, K);
+  if (ws_bytes < need)
+    return fail(TSM_ERR_WORKSPACE, "workspace too small: need " + std::to_string(need) + " bytes");
+  if (overlap(C, nC, A, nA) || overlap(C, nC, B, nB) || overlap(ws, need, A, nA) ||
+      overlap(ws, need, B, nB) || overlap(ws, need, C, nC))
+    return fail(TSM_ERR_INVALID_VALUE, "C / workspace overlap an input");
+  DeviceGuard dg(p->device);
+  if (dg.err != cudaSuccess) return cuda_fail(dg.err, "cudaSetDevice");
+  const Geometry g = geometry(p, K);
+  TsmttsmArgs a;
+  a.A = static_cast<const double*>(A);
+  a.B = static_cast<const double*>(B);
+  a.C = static_cast<double*>(C);
+  a.counters = static_cast<u32*>(ws);
+  a.partials = reinterpret_cast<double*>(static_cast<char*>(ws) + WsLayout::kCounterBytes);
+  a.K = K;
+  a.nchunks = g.nchunks;
+  a.stages = p->stages;
+  a.nfin = g.nfin;
+  void* args[] = {&a};
+  cudaError_t e = cudaLaunchKernel(p->k->func, dim3(g.grid), dim3(p->k->NT), args, p->smem,
+                                   static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "cudaLaunchKernel(tsmttsm)");
+  return TSM_SUCCESS;
+}
+
+tsm_status launch_tsmm(const tsm_plan_s* p, int dt, long long K, const void* A, const void* C,
+                       void* B, void* stream, bool allow_k0) {
+  if (!p) return fail(TSM_ERR_INVALID_VALUE, "plan == NULL");
+  if (p->op != TSM_OP_TSMM || p->dt != dt)
+    return fail(TSM_ERR_INVALID_VALUE, "plan op/dtype does not match the call");
+  if (K < (allow_k0 ? 0 : 1)) return fail(TSM_ERR_INVALID_VALUE, "K must be >= 1");
+  if (!C || (K > 0 && (!A || !B))) return fail(TSM_ERR_INVALID_VALUE, "null pointer");
+  if (misaligned(A) || misaligned(B) || misaligned(C))
+    return fail(TSM_ERR_MISALIGNED, "A, B and C must be 16-byte aligned");
+  const size_t s = (dt == TSM_Z ? 16 : 8);
+  const size_t nA = static_cast<size_t>(K) * p->M * s, nB = static_cast<size_t>(K) * p->N * s;
+  const size_t nC = static_cast<size_t>(p->M) * p->N * s;
+  if (overlap(B, nB, A, nA) || overlap(B, nB, C, nC))
+    return fail(TSM_ERR_INVALID_VALUE, "B overlaps A or C");
+  if (K == 0) return TSM_SUCCESS;
+  DeviceGuard dg(p->device);
+  if (dg.err != cudaSuccess) return cuda_fail(dg.err, "cudaSetDevice");
+  const Geometry g = geometry(p, K);
+  TsmmArgs a;
+  a.A = static_cast<const double*>(A);
+  a.C = static_cast<const double*>(C);
+  a.B = static_cast<double*>(B);
+  a.K = K;
+  a.nchunks = g.nchunks;
+  a.stages = p->stages;
+  void* args[] = {&a};
+  cudaError_t e = cudaLaunchKernel(p->k->func, dim3(g.grid), dim3(p->k->NT), args, p->smem,
+                                   static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "cudaLaunchKernel(tsmm)");
+  return TSM_SUCCESS;
+}
+
+int plan_device(const tsm_plan_s* p) { return p->device; }
+int plan_cells(const tsm_plan_s* p) { return p->M * p->N * (p->dt == TSM_Z ? 2 : 1); }
+int plan_op(const tsm_plan_s* p) { return p->op; }
+int plan_dt(const tsm_plan_s* p) { return p->dt; }
+
+}  // namespace tsm
+
+extern "C" {
+
+tsm_status tsm_plan_workspace_bytes(tsm_plan p, int64_t K, size_t* bytes) {
+  if (!p || !bytes) return fail(TSM_ERR_INVALID_VALUE, "null argument");
+  if (K < 0) return fail(TSM_ERR_INVALID_VALUE, "K < 0");
+  *bytes = workspace_bytes(p, K);
+  return TSM_SUCCESS;
+}
+
+tsm_status tsm_workspace_init(void* ws, size_t ws_bytes, tsm_stream stream) {
+  if (!ws || ws_bytes < WsLayout::kCounterBytes)
+    return fail(TSM_ERR_WORKSPACE, "workspace smaller than the counter block");
+  cudaError_t e = cudaMemsetAsync(ws, 0, WsLayout::kCounterBytes, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(workspace counters)");
+  return TSM_SUCCESS;
+}
+
+tsm_status tsm_plan_describe(tsm_plan p, int64_t K, char* buf, size_t len) {
+  if (!p || !buf || len == 0) return fail(TSM_ERR_INVALID_VALUE, "null argument");
+  const Geometry g = geometry(p, K < 0 ? 0 : K);
+  const KernelEntry* k = p->k;
+  char tmp[512];
+  if (p->op == TSM_OP_TSMTTSM)
+    snprintf(tmp, sizeof tmp,
+             "{\"op\":\"tsmttsm\",\"dtype\":\"%c\",\"M\":%d,\"N\":%d,\"MT\":%d,\"NTL\":%d,"
+             "\"TM\":%d,\"TN\":%d,\"threads\":%d,\"rows_per_chunk\":%d,\"stages\":%d,"
+             "\"ctas_per_sm\":%d,\"smem\":%zu,\"grid\":%d,\"nchunks\":%lld,\"nfin\":%d,\"jit\":%s}",
+             p->dt ? 'z' : 'd', p->M, p->N, k->p0, k->p1, (p->M + k->p0 - 1) / k->p0,
+             (p->N + k->p1 - 1) / k->p1, k->NT, k->R, p->stages, p->ctas_per_sm, p->smem, g.grid,
+             g.nchunks, g.nfin, p->jit ? "true" : "false");
+  else
+    snprintf(tmp, sizeof tmp,
+             "{\"op\":\"tsmm\",\"dtype\":\"%c\",\"M\":%d,\"N\":%d,\"NTL\":%d,\"MSPLIT\":%d,"
+             "\"U\":%d,\"threads\":%d,\"rows_per_chunk\":%d,\"stages\":%d,\"ctas_per_sm\":%d,"
+             "\"smem\":%zu,\"grid\":%d,\"nchunks\":%lld,\"jit\":%s}",
+             p->dt ? 'z' : 'd', p->M, p->N, k->p0, k->p1, k->p2, k->NT, k->R, p->stages,
+             p->ctas_per_sm, p->smem, g.grid, g.nchunks, p->jit ? "true" : "false");
+  snprintf(buf, len, "%s", tmp);
+  return TSM_SUCCESS;
+}
+
+tsm_status tsmttsm_d(tsm_plan p, int64_t K, const double* A, const double* B, double* C, void* ws,
+                     size_t ws_bytes, tsm_stream stream) {
+  return launch_tsmttsm(p, TSM_D, K, A, B, C, ws, ws_bytes, stream, false);
+}
+tsm_status tsmttsm_z(tsm_plan p, int64_t K, const tsm_zcomplex* A, const tsm_zcomplex* B,
+                     tsm_zcomplex* C, void* ws, size_t ws_bytes, tsm_stream stream) {
+  return launch_tsmttsm(p, TSM_Z, K, A, B, C, ws, ws_bytes, stream, false);
+}
+tsm_status tsmm_d(tsm_plan p, int64_t K, const double* A, const double* C, double* B,
+                  tsm_stream stream) {
+  return launch_tsmm(p, TSM_D, K, A, C, B, stream, false);
+}
+tsm_status tsmm_z(tsm_plan p, int64_t K, const tsm_zcomplex* A, const tsm_zcomplex* C,
+                  tsm_zcomplex* B, tsm_stream stream) {
+  return launch_tsmm(p, TSM_Z, K, A, C, B, stream, false);
+}
+
+tsm_status tsm_fill(double* dst, int64_t n, uint64_t seed, int mat_id, int mode, int64_t start,
+                    tsm_stream stream) {
+  if (n < 0 || start < 0) return fail(TSM_ERR_INVALID_VALUE, "n and start must be >= 0");
+  if (mode != 0 && mode != 1) return fail(TSM_ERR_INVALID_VALUE, "mode must be 0 (fp) or 1 (int)");
+  if (mat_id < 0 || mat_id > 0xffff) return fail(TSM_ERR_INVALID_VALUE, "mat_id out of range");
+  if (n == 0) return TSM_SUCCESS;
+  if (!dst) return fail(TSM_ERR_INVALID_VALUE, "dst == NULL");
+  const u64 base = seed * 0xD1B54A32D192ED03ull + (static_cast<u64>(mat_id) << 48);
+  int dev = 0;
+  cudaGetDevice(&dev);
+  DevInfo di;
+  tsm_status st = dev_info(dev, &di);
+  if (st != TSM_SUCCESS) return st;
+  const long long want = (n + 255) / 256;
+  const int grid = static_cast<int>(std::min<long long>(want, di.sms * 16LL));
+  fill_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(dst, n, base, mode, start);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "fill_kernel launch");
+  return TSM_SUCCESS;
+}
+
+tsm_status tsm_l2_flush(void* scratch, size_t bytes, tsm_stream stream) {
+  if (!scratch || misaligned(scratch)) return fail(TSM_ERR_INVALID_VALUE, "bad scratch buffer");
+  const long long n4 = static_cast<long long>(bytes / 32);
+  if (n4 == 0) return TSM_SUCCESS;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  DevInfo di;
+  tsm_status st = dev_info(dev, &di);
+  if (st != TSM_SUCCESS) return st;
+  l2_flush_kernel<<<di.sms * 8, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<double4*>(scratch), n4);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "l2_flush_kernel launch");
+  return TSM_SUCCESS;
+}
+
+const char* tsm_build_info(void) { return build_info_json(); }
+
+}  // extern "C"

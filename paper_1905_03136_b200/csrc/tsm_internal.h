@@ -1,0 +1,37 @@
+// tsm_internal.h -- internal host-side interfaces shared by the libtsm sources.
+#pragma once
+#include <string>
+
+#include "../../include/libtsm.h"
+#include "tsm_registry.h"
+
+namespace tsm {
+
+// Registry (tsm_registry.cpp + generated tables).
+const KernelEntry* find_aot(int op, int dt, int M, int N);
+const KernelEntry* find_aot_config(const KernelEntry& want);  // same shape AND config
+const KernelEntry* default_params(int op, int dt, int M, int N);
+const char* build_info_json();
+
+// NVRTC run-time instantiation (tsm_jit.cpp).
+tsm_status jit_kernel(const KernelEntry& want, const KernelEntry** out);
+int jit_count();
+
+// Error helpers (tsm_api.cu): record a thread-local detail string.
+tsm_status fail(tsm_status s, const std::string& why);
+
+// Launch paths (tsm_api.cu).  allow_k0: the sharded layer may pass K = 0.
+tsm_status launch_tsmttsm(const tsm_plan_s* p, int dt, long long K, const void* A, const void* B,
+                          void* C, void* ws, size_t ws_bytes, void* stream, bool allow_k0);
+tsm_status launch_tsmm(const tsm_plan_s* p, int dt, long long K, const void* A, const void* C,
+                       void* B, void* stream, bool allow_k0);
+size_t workspace_bytes(const tsm_plan_s* p, long long K);
+int plan_device(const tsm_plan_s* p);
+int plan_cells(const tsm_plan_s* p);  // doubles in C
+int plan_op(const tsm_plan_s* p);
+int plan_dt(const tsm_plan_s* p);
+
+// Fixed rank-order sum of nranks gathered partial C's (tsm_comm.cu).
+tsm_status rank_sum(const double* gathered, double* C, int nranks, int cells, void* stream);
+
+}  // namespace tsm

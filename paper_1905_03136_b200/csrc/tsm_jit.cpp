@@ -1,0 +1,174 @@
+// tsm_jit.cpp -- run-time instantiation of the width-specialised kernels.
+//
+// The AOT build instantiates the benchmark shapes (tools/gen_instances.py).
+// Every other (op, dtype, M, N) -- and every explicit configuration the
+// autotuner asks for -- is compiled at plan-creation time by NVRTC from the
+// SAME template source (csrc/tsm_kernels.cuh, embedded at build time) for
+// sm_100a, loaded with cudaLibraryLoadData and launched like the AOT kernels.
+// Compiled cubins are memoised in-process and, optionally, on disk
+// (TSM_JIT_CACHE_DIR, default $HOME/.cache/libtsm; set to "" to disable).
+#include <cuda_runtime.h>
+#include <nvrtc.h>
+
+#include <cstdio>
+#include <cstdlib>
+#include <deque>
+#include <fstream>
+#include <map>
+#include <mutex>
+#include <sstream>
+#include <string>
+#include <sys/stat.h>
+#include <unistd.h>
+#include <vector>
+
+#include "tsm_internal.h"
+#include "tsm_registry.h"
+
+#include "gen/kernel_source.inc"  // static const char* kTsmKernelSource
+
+namespace tsm {
+
+namespace {
+
+std::mutex g_jit_mu;
+std::deque<KernelEntry> g_jit_entries;  // stable addresses
+std::map<std::string, const KernelEntry*> g_jit_index;
+
+std::string cfg_type(const KernelEntry& e) {
+  std::ostringstream os;
+  const char* z = e.dt ? "true" : "false";
+  if (e.op == KIND_TSMTTSM)
+    os << "tsm::TsmttsmCfg<" << e.M << ", " << e.N << ", " << z << ", " << e.p0 << ", " << e.p1
+       << ", " << e.NT << ", " << e.R << ">";
+  else
+    os << "tsm::TsmmCfg<" << e.M << ", " << e.N << ", " << z << ", " << e.p0 << ", " << e.p1
+       << ", " << e.p2 << ", " << e.NT << ", " << e.R << ">";
+  return os.str();
+}
+
+std::string kernel_name(const KernelEntry& e) {
+  return std::string(e.op == KIND_TSMTTSM ? "tsm::tsmttsm_kernel<" : "tsm::tsmm_kernel<") +
+         cfg_type(e) + ">";
+}
+
+unsigned long long fnv1a(const std::string& s, unsigned long long h = 1469598103934665603ull) {
+  for (unsigned char c : s) {
+    h ^= c;
+    h *= 1099511628211ull;
+  }
+  return h;
+}
+
+std::string cache_dir() {
+  const char* d = getenv("TSM_JIT_CACHE_DIR");
+  if (d) return std::string(d);
+  const char* home = getenv("HOME");
+  return home ? std::string(home) + "/.cache/libtsm" : std::string();
+}
+
+bool read_file(const std::string& path, std::vector<char>* out) {
+  std::ifstream f(path, std::ios::binary);
+  if (!f) return false;
+  out->assign(std::istreambuf_iterator<char>(f), std::istreambuf_iterator<char>());
+  return !out->empty();
+}
+
+void write_file_atomic(const std::string& dir, const std::string& name, const std::vector<char>& data) {
+  if (dir.empty()) return;
+  std::string cur;
+  for (size_t i = 0; i <= dir.size(); i++) {  // mkdir -p
+    if (i == dir.size() || dir[i] == '/') {
+      if (!cur.empty()) mkdir(cur.c_str(), 0755);
+    }
+    if (i < dir.size()) cur += dir[i];
+  }
+  const std::string tmp = dir + "/" + name + ".tmp" + std::to_string(getpid());
+  {
+    std::ofstream f(tmp, std::ios::binary);
+    if (!f) return;
+    f.write(data.data(), static_cast<std::streamsize>(data.size()));
+  }
+  std::rename(tmp.c_str(), (dir + "/" + name).c_str());
+}
+
+tsm_status compile(const KernelEntry& e, std::vector<char>* cubin, std::string* lowered) {
+  const std::string name = kernel_name(e);
+  nvrtcProgram prog;
+  nvrtcResult r = nvrtcCreateProgram(&prog, kTsmKernelSource, "tsm_kernels.cuh", 0, nullptr, nullptr);
+  if (r != NVRTC_SUCCESS) return fail(TSM_ERR_INTERNAL, std::string("nvrtcCreateProgram: ") + nvrtcGetErrorString(r));
+  nvrtcAddNameExpression(prog, name.c_str());
+  const char* opts[] = {"--gpu-architecture=sm_100a", "-std=c++17", "-default-device",
+                        "-DTSM_NVRTC", "-lineinfo"};
+  r = nvrtcCompileProgram(prog, 5, opts);
+  if (r != NVRTC_SUCCESS) {
+    size_t n = 0;
+    nvrtcGetProgramLogSize(prog, &n);
+    std::string log(n, '\0');
+    nvrtcGetProgramLog(prog, &log[0]);
+    nvrtcDestroyProgram(&prog);
+    return fail(TSM_ERR_INTERNAL, "NVRTC compile of " + name + " failed:\n" + log);
+  }
+  const char* low = nullptr;
+  nvrtcGetLoweredName(prog, name.c_str(), &low);
+  *lowered = low ? low : "";
+  size_t n = 0;
+  nvrtcGetCUBINSize(prog, &n);
+  cubin->resize(n);
+  nvrtcGetCUBIN(prog, cubin->data());
+  nvrtcDestroyProgram(&prog);
+  if (lowered->empty() || cubin->empty()) return fail(TSM_ERR_INTERNAL, "NVRTC produced no cubin");
+  return TSM_SUCCESS;
+}
+
+}  // namespace
+
+// Returns a registry entry whose func is a JIT-compiled kernel for `want`.
+tsm_status jit_kernel(const KernelEntry& want, const KernelEntry** out) {
+  std::lock_guard<std::mutex> lk(g_jit_mu);
+  const std::string key = kernel_name(want);
+  auto it = g_jit_index.find(key);
+  if (it != g_jit_index.end()) {
+    *out = it->second;
+    return TSM_SUCCESS;
+  }
+  int ver = 0;
+  nvrtcVersion(&ver, &ver);
+  const std::string dir = cache_dir();
+  char hbuf[32];
+  snprintf(hbuf, sizeof hbuf, "%016llx", fnv1a(key, fnv1a(kTsmKernelSource)));
+  const std::string cname = std::string("tsm_") + hbuf + ".cubin";
+  const std::string lname = std::string("tsm_") + hbuf + ".name";
+  std::vector<char> cubin, lowv;
+  std::string lowered;
+  if (!dir.empty() && read_file(dir + "/" + cname, &cubin) && read_file(dir + "/" + lname, &lowv)) {
+    lowered.assign(lowv.begin(), lowv.end());
+  } else {
+    tsm_status st = compile(want, &cubin, &lowered);
+    if (st != TSM_SUCCESS) return st;
+    write_file_atomic(dir, cname, cubin);
+    write_file_atomic(dir, lname, std::vector<char>(lowered.begin(), lowered.end()));
+  }
+  cudaLibrary_t lib;
+  cudaError_t e = cudaLibraryLoadData(&lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0);
+  if (e != cudaSuccess)
+    return fail(TSM_ERR_CUDA, std::string("cudaLibraryLoadData: ") + cudaGetErrorString(e));
+  cudaKernel_t k;
+  e = cudaLibraryGetKernel(&k, lib, lowered.c_str());
+  if (e != cudaSuccess)
+    return fail(TSM_ERR_CUDA, std::string("cudaLibraryGetKernel: ") + cudaGetErrorString(e));
+  KernelEntry ent = want;
+  ent.func = reinterpret_cast<const void*>(k);
+  g_jit_entries.push_back(ent);
+  const KernelEntry* p = &g_jit_entries.back();
+  g_jit_index[key] = p;
+  *out = p;
+  return TSM_SUCCESS;
+}
+
+int jit_count() {
+  std::lock_guard<std::mutex> lk(g_jit_mu);
+  return static_cast<int>(g_jit_entries.size());
+}
+
+}  // namespace tsm

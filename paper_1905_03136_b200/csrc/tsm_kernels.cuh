@@ -1,0 +1,616 @@
+// tsm_kernels.cuh -- libtsm device code for sm_100a (B200).
+//
+// Width-specialised kernel templates, instantiated per (M, N, type) and tile
+// configuration by csrc/gen/ (generated from tune/b200.json).
+//
+//   tsmttsm_kernel  C = A^T B
+//   tsmm_kernel     B = A C
+//
+// Design (DESIGN.md §4 has the roofline for each):
+//  * Persistent grid, grid-stride over CONTIGUOUS row chunks (the paper's grid
+//    stride loop, at chunk granularity).  A chunk of R rows
+//    of a row-major K x M matrix is one contiguous R*M*s byte range, so it is
+//    moved with ONE cp.async.bulk (TMA bulk copy, SASS UBLKCP) into a
+//    multi-stage shared-memory ring completed on mbarriers.  This is the
+//    B200 replacement of the paper's leap frogging: the
+//    next chunks are in flight while the current one is consumed, with no
+//    registers spent on staging.  R is even, so chunk sizes are multiples of
+//    16 B even for odd widths (the paper's misalignment hurdle,
+//    PAPER.md:1100-1108); a single odd last row is handled from global.
+//  * TSMTTSM: each thread owns an interleaved ("transposed")
+//    register tile of TM x TN cells of C (Listing 5), with
+//    MT x NTL tiles per row (powers of two).  Threads of a warp work on the
+//    same row(s) so shared-memory reads are broadcasts / contiguous.
+//    Thread-local sums -> warp butterfly -> fixed-order block sum in smem ->
+//    per-block partial in the workspace -> the last NFIN blocks to finish
+//    (ticket counter) sum the partials in fixed block order (T3/T4).  No
+//    floating-point atomics: results are deterministic.
+//  * TSMM: C is staged in smem once per persistent block;
+//    each thread computes TN interleaved columns of U rows
+//    (K-unroll with C reuse), optionally splitting the M
+//    reduction over MSPLIT lanes (butterfly-combined).  Output rows are
+//    staged in smem and written with cp.async.bulk stores: every B byte is
+//    written once, in full sectors, with no write-allocate (S4).
+//
+// This file has NO dependency on the oracle (oracle/) or on any host header
+// besides the CUDA toolkit built-ins, so the same source can also be compiled
+// at run time by NVRTC for shapes outside the AOT set.
+#pragma once
+
+#ifndef TSM_NVRTC
+#include <cstdint>
+#endif
+
+namespace tsm {
+
+typedef unsigned long long u64;
+typedef unsigned int u32;
+
+// --------------------------------------------------------------------------
+// PTX helpers: mbarrier, bulk async copies, proxy fences.
+// --------------------------------------------------------------------------
+__device__ __forceinline__ u32 smem_u32(const void* p) {
+  return static_cast<u32>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(u64* bar, u32 count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(u64* bar, u32 bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(
+                   smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(u64* bar, u32 parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "TSM_WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra TSM_WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// Global -> shared bulk copy completing `bytes` transaction bytes on `bar`.
+// Streaming data: evict-first L2 policy (each byte is read exactly once).
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, u32 bytes, u64* bar,
+                                         u64 policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+      "[%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ u64 policy_evict_first() {
+  u64 pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+// Shared -> global bulk store (bulk-group completion).
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, u32 bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
+               "r"(smem_u32(src)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() {
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() {
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+__device__ __forceinline__ u32 ld_acquire_gpu(const u32* p) {
+  u32 v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Complex multiply-add on (re, im) accumulators, plain (non-conjugating):
+//   re += ar*br - ai*bi ; im += ar*bi + ai*br   (4 DFMA, 8 flops)
+__device__ __forceinline__ void zfma(double& re, double& im, double ar, double ai, double br,
+                                     double bi) {
+  re = fma(ar, br, re);
+  re = fma(-ai, bi, re);
+  im = fma(ar, bi, im);
+  im = fma(ai, br, im);
+}
+
+// Workspace layout shared by host and device code.
+struct WsLayout {
+  static constexpr int kCounterBytes = 256;  // u32 ticket, u32 done, padding
+};
+
+// ==========================================================================
+// TSMTTSM
+// ==========================================================================
+struct TsmttsmArgs {
+  const double* A;     // K x M (x2 doubles for Z), row-major
+  const double* B;     // K x N
+  double* C;           // M x N
+  double* partials;    // gridDim.x x (M*N*S) doubles
+  u32* counters;       // [0] ticket, [1] done
+  long long K;         // rows
+  long long nchunks;   // ceil(K_even / R)
+  int stages;          // smem ring depth
+  int nfin;            // finisher blocks of the grid reduction
+};
+
+// M, N: widths.  Z: complex.  MT, NTL: tiles per row along m / n (powers of
+// two).  NT: threads per block.  R: rows per chunk (even).
+template <int M_, int N_, bool Z_, int MT_, int NTL_, int NT_, int R_>
+struct TsmttsmCfg {
+  static constexpr int M = M_, N = N_, MT = MT_, NTL = NTL_, NT = NT_, R = R_;
+  static constexpr bool Z = Z_;
+  static constexpr int S = Z ? 2 : 1;  // doubles per element
+  static constexpr int TM = (M + MT - 1) / MT;
+  static constexpr int TN = (N + NTL - 1) / NTL;
+  static constexpr int TPR = MT * NTL;  // threads per row
+  static constexpr int RB = NT / TPR;   // row slots per block
+  static constexpr int CELLS = M * N * S;
+  static constexpr int STAGE_DOUBLES = R * (M + N) * S;
+  static_assert(NT % 32 == 0 && NT % TPR == 0, "TPR must divide NT");
+  static_assert((TPR & (TPR - 1)) == 0, "TPR must be a power of two");
+  static_assert(R % 2 == 0, "R must be even (16-byte bulk copies)");
+  static_assert(TM * MT >= M && TN * NTL >= N, "tiles must cover C");
+  static_assert(MT <= M || M == 0, "no empty tiles along m");
+  static_assert(NTL <= N || N == 0, "no empty tiles along n");
+};
+
+template <class Cfg>
+__device__ __forceinline__ void tsmttsm_row(const double* __restrict__ ar,
+                                            const double* __restrict__ br, int tm, int tn,
+                                            double (&c)[Cfg::TM][Cfg::TN][Cfg::S]) {
+  constexpr int TM = Cfg::TM, TN = Cfg::TN, MT = Cfg::MT, NTL = Cfg::NTL;
+  constexpr int M = Cfg::M, N = Cfg::N;
+  if constexpr (!Cfg::Z) {
+    double a[TM], b[TN];
+#pragma unroll
+    for (int i = 0; i < TM; i++) {
+      const int m = tm + i * MT;
+      if ((i + 1) * MT <= M)
+        a[i] = ar[m];
+      else
+        a[i] = (m < M) ? ar[m] : 0.0;
+    }
+#pragma unroll
+    for (int j = 0; j < TN; j++) {
+      const int n = tn + j * NTL;
+      if ((j + 1) * NTL <= N)
+        b[j] = br[n];
+      else
+        b[j] = (n < N) ? br[n] : 0.0;
+    }
+#pragma unroll
+    for (int i = 0; i < TM; i++)
+#pragma unroll
+      for (int j = 0; j < TN; j++) c[i][j][0] = fma(a[i], b[j], c[i][j][0]);
+  } else {
+    const double2* ar2 = reinterpret_cast<const double2*>(ar);
+    const double2* br2 = reinterpret_cast<const double2*>(br);
+    double2 a[TM], b[TN];
+#pragma unroll
+    for (int i = 0; i < TM; i++) {
+      const int m = tm + i * MT;
+      if ((i + 1) * MT <= M)
+        a[i] = ar2[m];
+      else
+        a[i] = (m < M) ? ar2[m] : make_double2(0.0, 0.0);
+    }
+#pragma unroll
+    for (int j = 0; j < TN; j++) {
+      const int n = tn + j * NTL;
+      if ((j + 1) * NTL <= N)
+        b[j] = br2[n];
+      else
+        b[j] = (n < N) ? br2[n] : make_double2(0.0, 0.0);
+    }
+#pragma unroll
+    for (int i = 0; i < TM; i++)
+#pragma unroll
+      for (int j = 0; j < TN; j++)
+        zfma(c[i][j][0], c[i][j][1], a[i].x, a[i].y, b[j].x, b[j].y);
+  }
+}
+
+template <class Cfg>
+__global__ void __launch_bounds__(Cfg::NT) tsmttsm_kernel(const TsmttsmArgs p) {
+  constexpr int M = Cfg::M, N = Cfg::N, S = Cfg::S, R = Cfg::R, NT = Cfg::NT;
+  constexpr int TM = Cfg::TM, TN = Cfg::TN, MT = Cfg::MT, NTL = Cfg::NTL;
+  constexpr int TPR = Cfg::TPR, RB = Cfg::RB, CELLS = Cfg::CELLS;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  u64* full = reinterpret_cast<u64*>(smem_raw);
+  double* ring = reinterpret_cast<double*>(smem_raw + 128);
+  __shared__ u32 s_ticket;
+
+  const int tid = threadIdx.x;
+  const int rs = tid / TPR;  // row slot
+  const int tile = tid % TPR;
+  const int tm = tile % MT;  // threads mapped in M direction first
+  const int tn = tile / MT;
+  const long long K = p.K;
+  const long long K_even = K & ~1LL;
+  const int G = gridDim.x;
+  const int stages = p.stages;
+
+  if (tid == 0) {
+    for (int s = 0; s < stages; s++) mbar_init(&full[s], 1);
+    fence_mbar_init();
+    fence_proxy_async_smem();
+  }
+  __syncthreads();
+
+  u64 pol = 0;
+  auto issue = [&](long long c, int s) {
+    const long long r0 = c * R;
+    const long long rows = (K_even - r0 < R) ? (K_even - r0) : R;
+    const u32 ba = static_cast<u32>(rows * M * S * 8);
+    const u32 bb = static_cast<u32>(rows * N * S * 8);
+    double* dA = ring + static_cast<long long>(s) * Cfg::STAGE_DOUBLES;
+    double* dB = dA + R * M * S;
+    mbar_arrive_expect_tx(&full[s], ba + bb);
+    bulk_g2s(dA, p.A + r0 * M * S, ba, &full[s], pol);
+    bulk_g2s(dB, p.B + r0 * N * S, bb, &full[s], pol);
+  };
+  if (tid == 0) {
+    pol = policy_evict_first();
+    for (int s = 0; s < stages; s++) {
+      const long long c = blockIdx.x + static_cast<long long>(s) * G;
+      if (c < p.nchunks) issue(c, s);
+    }
+  }
+
+  double acc[TM][TN][S];
+#pragma unroll
+  for (int i = 0; i < TM; i++)
+#pragma unroll
+    for (int j = 0; j < TN; j++)
+#pragma unroll
+      for (int q = 0; q < S; q++) acc[i][j][q] = 0.0;
+
+  int it = 0;
+  for (long long c = blockIdx.x; c < p.nchunks; c += G, it++) {
+    const int s = it % stages;
+    mbar_wait(&full[s], static_cast<u32>((it / stages) & 1));
+    const double* sA = ring + static_cast<long long>(s) * Cfg::STAGE_DOUBLES;
+    const double* sB = sA + R * M * S;
+    const long long r0 = c * R;
+    const int rows = static_cast<int>((K_even - r0 < R) ? (K_even - r0) : R);
+    if (rows == R) {
+#pragma unroll 2
+      for (int r = rs; r < R; r += RB)
+        tsmttsm_row<Cfg>(sA + r * M * S, sB + r * N * S, tm, tn, acc);
+    } else {
+      for (int r = rs; r < rows; r += RB)
+        tsmttsm_row<Cfg>(sA + r * M * S, sB + r * N * S, tm, tn, acc);
+    }
+    __syncthreads();  // stage s fully consumed by every thread
+    if (tid == 0) {
+      const long long c2 = c + static_cast<long long>(stages) * G;
+      if (c2 < p.nchunks) issue(c2, s);
+    }
+  }
+  // Odd last row (K odd): block 0, slot 0 reads it straight from global.
+  if ((K & 1) && blockIdx.x == 0 && rs == 0)
+    tsmttsm_row<Cfg>(p.A + (K - 1) * M * S, p.B + (K - 1) * N * S, tm, tn, acc);
+
+  // ---- T3: block-level reduction (fixed order) ----
+  // (a) butterfly over the row-slot lanes of a warp (same tile, TPR < 32).
+  if constexpr (TPR < 32) {
+#pragma unroll
+    for (int off = TPR; off < 32; off <<= 1)
+#pragma unroll
+      for (int i = 0; i < TM; i++)
+#pragma unroll
+        for (int j = 0; j < TN; j++)
+#pragma unroll
+          for (int q = 0; q < S; q++)
+            acc[i][j][q] += __shfl_xor_sync(0xffffffffu, acc[i][j][q], off);
+  }
+  // (b) holders add into the smem block partial slot by slot, in slot order.
+  constexpr int NSLOT = (TPR < 32) ? NT / 32 : RB;
+  const int slot = (TPR < 32) ? tid / 32 : rs;
+  const bool holder = (TPR < 32) ? ((tid & 31) < TPR) : true;
+  double* sP = ring;  // ring is idle now (every issued chunk was consumed)
+#pragma unroll 1
+  for (int sl = 0; sl < NSLOT; sl++) {
+    if (holder && slot == sl) {
+#pragma unroll
+      for (int i = 0; i < TM; i++) {
+        const int m = tm + i * MT;
+#pragma unroll
+        for (int j = 0; j < TN; j++) {
+          const int n = tn + j * NTL;
+          if (m < M && n < N) {
+#pragma unroll
+            for (int q = 0; q < S; q++) {
+              const int idx = (m * N + n) * S + q;
+              sP[idx] = (sl == 0) ? acc[i][j][q] : sP[idx] + acc[i][j][q];
+            }
+          }
+        }
+      }
+    }
+    __syncthreads();
+  }
+  double* myP = p.partials + static_cast<long long>(blockIdx.x) * CELLS;
+  for (int idx = tid; idx < CELLS; idx += NT) __stcg(&myP[idx], sP[idx]);
+
+  // ---- T4: deterministic grid reduction by the last NFIN blocks ----
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) s_ticket = atomicAdd(&p.counters[0], 1u);
+  __syncthreads();
+  const int nfin = p.nfin;
+  const int t = static_cast<int>(s_ticket);
+  if (t < G - nfin) return;
+  const int f = t - (G - nfin);
+  if (tid == 0) {
+    while (ld_acquire_gpu(&p.counters[0]) < static_cast<u32>(G)) __nanosleep(64);
+  }
+  __syncthreads();
+  // finisher f owns cells [c0, c1); TPC threads per cell split the block
+  // range into contiguous segments, combined afterwards in segment order.
+  const int cpf = (CELLS + nfin - 1) / nfin;
+  const int c0 = f * cpf;
+  const int c1 = (c0 + cpf < CELLS) ? c0 + cpf : CELLS;
+  const int ncell = c1 - c0;
+  if (ncell > 0) {
+    int tpc = NT / ncell;
+    if (tpc < 1) tpc = 1;
+    if (tpc > 32) tpc = 32;
+    double* sSeg = ring;  // [tpc][ncell] when tpc > 1
+    const int seg = tid / ncell;
+    const int cl = tid % ncell;
+    if (tpc == 1) {
+      for (int idx = c0 + tid; idx < c1; idx += NT) {
+        double s0 = 0.0;
+#pragma unroll 8
+        for (int g = 0; g < G; g++) s0 += __ldcg(&p.partials[static_cast<long long>(g) * CELLS + idx]);
+        p.C[idx] = s0;
+      }
+    } else {
+      if (seg < tpc) {
+        const int g0 = static_cast<int>((static_cast<long long>(G) * seg) / tpc);
+        const int g1 = static_cast<int>((static_cast<long long>(G) * (seg + 1)) / tpc);
+        double s0 = 0.0;
+#pragma unroll 8
+        for (int g = g0; g < g1; g++)
+          s0 += __ldcg(&p.partials[static_cast<long long>(g) * CELLS + c0 + cl]);
+        sSeg[seg * ncell + cl] = s0;
+      }
+      __syncthreads();
+      if (tid < ncell) {
+        double s0 = sSeg[tid];
+        for (int q = 1; q < tpc; q++) s0 += sSeg[q * ncell + tid];
+        p.C[c0 + tid] = s0;
+      }
+    }
+  }
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) {
+    const u32 d = atomicAdd(&p.counters[1], 1u);
+    if (d == static_cast<u32>(nfin - 1)) {  // last finisher: reset for the next call
+      p.counters[0] = 0;
+      p.counters[1] = 0;
+    }
+  }
+}
+
+// ==========================================================================
+// TSMM
+// ==========================================================================
+struct TsmmArgs {
+  const double* A;    // K x M
+  const double* C;    // M x N
+  double* B;          // K x N
+  long long K;
+  long long nchunks;  // ceil(K_even / R)
+  int stages;
+};
+
+// NTL: threads per row along n (interleaved columns), MSPLIT: lanes sharing
+// one output that split the m-sum (butterfly-combined), U: rows per thread per
+// pass (C reuse), NT: threads per block, R: rows per chunk.
+template <int M_, int N_, bool Z_, int NTL_, int MSPLIT_, int U_, int NT_, int R_>
+struct TsmmCfg {
+  static constexpr int M = M_, N = N_, NTL = NTL_, MSPLIT = MSPLIT_, U = U_, NT = NT_, R = R_;
+  static constexpr bool Z = Z_;
+  static constexpr int S = Z ? 2 : 1;
+  static constexpr int TN = (N + NTL - 1) / NTL;      // outputs per thread per row
+  static constexpr int MQ = (M + MSPLIT - 1) / MSPLIT;  // m terms per thread
+  static constexpr int GS = NTL * MSPLIT;               // threads per row group
+  static constexpr int RB = NT / GS;                    // row slots per block
+  static constexpr int ROWS_PER_PASS = RB * U;
+  static constexpr int A_STAGE_DOUBLES = R * M * S;
+  static constexpr int OUT_DOUBLES = ROWS_PER_PASS * N * S;  // one pass, double-buffered
+  static constexpr int C_DOUBLES = M * N * S;
+  static_assert(NT % 32 == 0 && NT % GS == 0, "GS must divide NT");
+  static_assert((GS & (GS - 1)) == 0 && GS <= 32, "GS power of two <= 32");
+  static_assert((MSPLIT & (MSPLIT - 1)) == 0 && MSPLIT <= 32, "MSPLIT power of two <= 32");
+  static_assert(R % ROWS_PER_PASS == 0 && ROWS_PER_PASS % 2 == 0,
+                "R multiple of rows per pass; passes of even rows (16-byte bulk stores)");
+  static_assert(NTL <= N && MSPLIT <= M, "no empty lanes");
+};
+
+template <class Cfg>
+__global__ void __launch_bounds__(Cfg::NT) tsmm_kernel(const TsmmArgs p) {
+  constexpr int M = Cfg::M, N = Cfg::N, S = Cfg::S, R = Cfg::R, NT = Cfg::NT;
+  constexpr int NTL = Cfg::NTL, MSPLIT = Cfg::MSPLIT, U = Cfg::U, TN = Cfg::TN, MQ = Cfg::MQ;
+  constexpr int GS = Cfg::GS, RB = Cfg::RB;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  u64* full = reinterpret_cast<u64*>(smem_raw);
+  double* sC = reinterpret_cast<double*>(smem_raw + 128);
+  constexpr int C_PAD = ((Cfg::C_DOUBLES + 15) / 16) * 16;  // keep 128 B alignment
+  double* sOut = sC + C_PAD;                                 // 2 x OUT_DOUBLES
+  double* ring = sOut + 2 * Cfg::OUT_DOUBLES;                // stages x A_STAGE_DOUBLES
+
+  const int tid = threadIdx.x;
+  const int g = tid % GS;
+  const int ms = g % MSPLIT;
+  const int tn = g / MSPLIT;
+  const int rs = tid / GS;
+  const long long K = p.K;
+  const long long K_even = K & ~1LL;
+  const int G = gridDim.x;
+  const int stages = p.stages;
+
+  if (tid == 0) {
+    for (int s = 0; s < stages; s++) mbar_init(&full[s], 1);
+    fence_mbar_init();
+    fence_proxy_async_smem();
+  }
+  // S1: stage C once per persistent block.
+  for (int i = tid; i < Cfg::C_DOUBLES; i += NT) sC[i] = __ldg(&p.C[i]);
+  __syncthreads();
+
+  u64 pol = 0;
+  auto issue = [&](long long c, int s) {
+    const long long r0 = c * R;
+    const long long rows = (K_even - r0 < R) ? (K_even - r0) : R;
+    const u32 ba = static_cast<u32>(rows * M * S * 8);
+    double* dA = ring + static_cast<long long>(s) * Cfg::A_STAGE_DOUBLES;
+    mbar_arrive_expect_tx(&full[s], ba);
+    bulk_g2s(dA, p.A + r0 * M * S, ba, &full[s], pol);
+  };
+  if (tid == 0) {
+    pol = policy_evict_first();
+    for (int s = 0; s < stages; s++) {
+      const long long c = blockIdx.x + static_cast<long long>(s) * G;
+      if (c < p.nchunks) issue(c, s);
+    }
+  }
+
+  // Compute U rows x TN columns for rows r_u = base + rs + u*RB.
+  auto compute_pass = [&](const double* __restrict__ sA, int base, int rows, double* out) {
+    double acc[U][TN][S];
+#pragma unroll
+    for (int u = 0; u < U; u++)
+#pragma unroll
+      for (int j = 0; j < TN; j++)
+#pragma unroll
+        for (int q = 0; q < S; q++) acc[u][j][q] = 0.0;
+#pragma unroll 4
+    for (int qm = 0; qm < MQ; qm++) {
+      const int m = ms + qm * MSPLIT;
+      const bool mv = ((qm + 1) * MSPLIT <= M) || (m < M);
+      if constexpr (!Cfg::Z) {
+        double cv[TN], av[U];
+#pragma unroll
+        for (int j = 0; j < TN; j++) {
+          const int n = tn + j * NTL;
+          cv[j] = (mv && n < N) ? sC[m * N + n] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+          const int r = base + rs + u * RB;
+          av[u] = (mv && r < rows) ? sA[r * M + m] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < U; u++)
+#pragma unroll
+          for (int j = 0; j < TN; j++) acc[u][j][0] = fma(av[u], cv[j], acc[u][j][0]);
+      } else {
+        const double2* sC2 = reinterpret_cast<const double2*>(sC);
+        const double2* sA2 = reinterpret_cast<const double2*>(sA);
+        double2 cv[TN], av[U];
+#pragma unroll
+        for (int j = 0; j < TN; j++) {
+          const int n = tn + j * NTL;
+          cv[j] = (mv && n < N) ? sC2[m * N + n] : make_double2(0.0, 0.0);
+        }
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+          const int r = base + rs + u * RB;
+          av[u] = (mv && r < rows) ? sA2[r * M + m] : make_double2(0.0, 0.0);
+        }
+#pragma unroll
+        for (int u = 0; u < U; u++)
+#pragma unroll
+          for (int j = 0; j < TN; j++)
+            zfma(acc[u][j][0], acc[u][j][1], av[u].x, av[u].y, cv[j].x, cv[j].y);
+      }
+    }
+    if constexpr (MSPLIT > 1) {
+#pragma unroll
+      for (int off = 1; off < MSPLIT; off <<= 1)
+#pragma unroll
+        for (int u = 0; u < U; u++)
+#pragma unroll
+          for (int j = 0; j < TN; j++)
+#pragma unroll
+            for (int q = 0; q < S; q++)
+              acc[u][j][q] += __shfl_xor_sync(0xffffffffu, acc[u][j][q], off);
+    }
+    // rows are pass-local in `out` (the staging buffer holds one pass)
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      const int r = base + rs + u * RB;
+#pragma unroll
+      for (int j = 0; j < TN; j++) {
+        const int n = tn + j * NTL;
+        if (r < rows && n < N && (j % MSPLIT) == ms) {
+#pragma unroll
+          for (int q = 0; q < S; q++) out[((r - base) * N + n) * S + q] = acc[u][j][q];
+        }
+      }
+    }
+  };
+
+  int it = 0;
+  int pass = 0;  // global pass counter -> output buffer parity
+  for (long long c = blockIdx.x; c < p.nchunks; c += G, it++) {
+    const int s = it % stages;
+    mbar_wait(&full[s], static_cast<u32>((it / stages) & 1));
+    const double* sA = ring + static_cast<long long>(s) * Cfg::A_STAGE_DOUBLES;
+    const long long r0 = c * R;
+    const int rows = static_cast<int>((K_even - r0 < R) ? (K_even - r0) : R);
+#pragma unroll 1
+    for (int base = 0; base < rows; base += Cfg::ROWS_PER_PASS, pass++) {
+      double* out = sOut + (pass & 1) * Cfg::OUT_DOUBLES;
+      if (tid == 0) bulk_wait_read<1>();  // the store of pass-2 has read this buffer
+      __syncthreads();
+      compute_pass(sA, base, rows, out);
+      fence_proxy_async_smem();  // generic-proxy smem writes -> visible to the bulk store
+      __syncthreads();           // pass complete (and, on the last pass, stage s consumed)
+      if (tid == 0) {
+        const int prow = (rows - base < Cfg::ROWS_PER_PASS) ? rows - base : Cfg::ROWS_PER_PASS;
+        bulk_s2g(p.B + (r0 + base) * N * S, out, static_cast<u32>(prow * N * S * 8));
+        bulk_commit();
+      }
+    }
+    if (tid == 0) {
+      const long long c2 = c + static_cast<long long>(stages) * G;
+      if (c2 < p.nchunks) issue(c2, s);
+    }
+  }
+  // Odd last row (K odd): block 0 computes it from global A and smem C.
+  if ((K & 1) && blockIdx.x == 0) {
+    const double* a = p.A + (K - 1) * M * S;
+    for (int n = tid; n < N; n += NT) {
+      if constexpr (!Cfg::Z) {
+        double s0 = 0.0;
+        for (int m = 0; m < M; m++) s0 = fma(a[m], sC[m * N + n], s0);
+        p.B[(K - 1) * N + n] = s0;
+      } else {
+        double re = 0.0, im = 0.0;
+        for (int m = 0; m < M; m++)
+          zfma(re, im, a[2 * m], a[2 * m + 1], sC[2 * (m * N + n)], sC[2 * (m * N + n) + 1]);
+        p.B[2 * ((K - 1) * N + n)] = re;
+        p.B[2 * ((K - 1) * N + n) + 1] = im;
+      }
+    }
+  }
+  if (tid == 0) bulk_wait_all();
+}
+
+}  // namespace tsm

@@ -1,0 +1,27 @@
+// tsm_registry.h -- table of AOT-instantiated kernels (host side).
+// Entries are emitted by tools/gen_instances.py into csrc/gen/*.cu.
+#pragma once
+
+namespace tsm {
+
+enum KernelKind { KIND_TSMTTSM = 0, KIND_TSMM = 1 };
+
+struct KernelEntry {
+  int op;   // KernelKind
+  int dt;   // 0 = D, 1 = Z
+  int M, N;
+  const void* func;  // __global__ function (launched with cudaLaunchKernel)
+  int NT;            // threads per block
+  int R;             // rows per chunk
+  // tile description (TSMTTSM: MT, NTL; TSMM: NTL, MSPLIT, U)
+  int p0, p1, p2;
+  int stages;        // default pipeline depth
+  int ctas_per_sm;   // target resident CTAs per SM (clipped by occupancy)
+};
+
+struct KernelTable {
+  const KernelEntry* entries;
+  int count;
+};
+
+}  // namespace tsm

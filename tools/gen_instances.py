@@ -1,0 +1,235 @@
+#!/usr/bin/env python3
+"""Emit the AOT instantiation set of libtsm's width-specialised kernels.
+
+For every (op, dtype, M, N) in the AOT shape set this writes one explicit
+template instantiation (C++ templates, csrc/tsm_kernels.cuh) plus a registry
+entry carrying its launch parameters.  Tile / launch parameters come from
+``tune/b200.json`` (autotuned on the B200, tools/autotune.py) when present,
+otherwise from the heuristics below.
+
+Output: paper_1905_03136_b200/csrc/gen/{inst_*.cu, registry_gen.cpp}
+"""
+from __future__ import annotations
+
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+GEN = os.path.join(ROOT, "paper_1905_03136_b200", "csrc", "gen")
+TUNE = os.path.join(ROOT, "tune", "b200.json")
+
+# shapes instantiated ahead of time (both ops, both dtypes)
+SQUARE = [(w, w) for w in range(1, 65)]
+NONSQUARE = [(1, 64), (64, 1), (16, 48), (48, 16),             # BASELINE configs[3]
+             (1, 2), (2, 1), (3, 5), (5, 3), (7, 2), (13, 29), (29, 13),
+             (33, 17), (17, 33), (5, 64), (64, 5), (1, 7), (9, 1), (63, 64), (64, 63)]
+SHAPES = SQUARE + [s for s in NONSQUARE if s[0] != s[1]]
+
+
+def pow2ceil(x: int) -> int:
+    p = 1
+    while p < x:
+        p <<= 1
+    return p
+
+
+def pow2floor(x: int) -> int:
+    p = 1
+    while p * 2 <= x:
+        p <<= 1
+    return p
+
+
+def cdiv(a: int, b: int) -> int:
+    return -(-a // b)
+
+
+def tsmttsm_default(M: int, N: int, z: bool) -> dict:
+    """Register-tile choice: big tiles for FMA/load, but at
+    least 32 threads per row (a warp shares one row -> broadcast smem reads)
+    whenever the row has >= 32 cells."""
+    tmax_m, tmax_n = (4, 8) if z else (8, 8)
+    MT = 1
+    while cdiv(M, MT) > tmax_m and MT * 2 <= M:
+        MT *= 2
+    NTL = 1
+    while cdiv(N, NTL) > tmax_n and NTL * 2 <= N:
+        NTL *= 2
+    tpr_min = min(32, pow2floor(M) * pow2floor(N))
+    while MT * NTL < tpr_min:
+        TM, TN = cdiv(M, MT), cdiv(N, NTL)
+        can_m, can_n = MT * 2 <= M, NTL * 2 <= N
+        if can_n and (TN >= TM or not can_m):
+            NTL *= 2
+        elif can_m:
+            MT *= 2
+        else:
+            break
+    NT = 256
+    RB = NT // (MT * NTL)
+    S = 2 if z else 1
+    row_bytes = (M + N) * 8 * S
+    R = max(2, (16384 // row_bytes))
+    step = max(2, RB) if RB % 2 == 0 or RB == 1 else 2 * RB
+    R = max(step, (R // step) * step)
+    return dict(MT=MT, NTL=NTL, NT=NT, R=R, stages=4, ctas=4)
+
+
+def tsmm_default(M: int, N: int, z: bool) -> dict:
+    """C in smem; TN interleaved columns x U rows per thread
+    (PAPER.md:661-714); MSPLIT lanes share an output so a warp reads one row
+    group of A (broadcast)."""
+    # lanes along n first (coalesced outputs, broadcast A reads), then MSPLIT
+    # lanes split the m-sum to fill the warp (one butterfly per output).
+    S = 2 if z else 1
+    NTL = min(32, pow2floor(N))
+    TN = cdiv(N, NTL)
+    MSPLIT = 1
+    while NTL * MSPLIT * 2 <= 32 and MSPLIT * 2 <= M:
+        MSPLIT *= 2
+    GS = NTL * MSPLIT
+    acc_max = 16 if z else 32  # accumulator doubles per thread: U*TN*S <= 32
+    U = max(1, min(16, acc_max // TN))
+    NT = 256
+    # staging buffers (A chunk, output pass) of at most ~16 KB, 32 KB when
+    # the shape is FMA-heavy (big U amortises the C loads)
+    T = 32768 if M * N >= 1024 else 16384
+    rows_cap = max(2, T // (max(M, N) * S * 8))
+    while (NT // GS) * U > rows_cap:
+        if NT > 128:
+            NT //= 2
+        elif U > 4:
+            U //= 2
+        elif NT > 32:
+            NT //= 2
+        elif U > 1:
+            U //= 2
+        else:
+            break
+    rpp = (NT // GS) * U
+    if rpp % 2:
+        U *= 2
+        rpp *= 2
+    R = rpp * max(1, round(T / (rpp * M * 8 * S)))
+    return dict(NTL=NTL, MSPLIT=MSPLIT, U=U, NT=NT, R=R, stages=4, ctas=4)
+
+
+def load_tune() -> dict:
+    if os.path.exists(TUNE):
+        with open(TUNE) as f:
+            return json.load(f).get("entries", {})
+    return {}
+
+
+def entries():
+    tune = load_tune()
+    out = []
+    for op in ("tsmttsm", "tsmm"):
+        for dt in ("d", "z"):
+            for (M, N) in SHAPES:
+                key = f"{op}_{dt}_{M}_{N}"
+                cfg = (tsmttsm_default if op == "tsmttsm" else tsmm_default)(M, N, dt == "z")
+                cfg.update(tune.get(key, {}).get("cfg", {}))
+                out.append((op, dt, M, N, cfg))
+    return out
+
+
+def cfg_type(op, dt, M, N, c) -> str:
+    z = "true" if dt == "z" else "false"
+    if op == "tsmttsm":
+        return f"tsm::TsmttsmCfg<{M}, {N}, {z}, {c['MT']}, {c['NTL']}, {c['NT']}, {c['R']}>"
+    return f"tsm::TsmmCfg<{M}, {N}, {z}, {c['NTL']}, {c['MSPLIT']}, {c['U']}, {c['NT']}, {c['R']}>"
+
+
+def entry_init(op, dt, M, N, c) -> str:
+    t = cfg_type(op, dt, M, N, c)
+    if op == "tsmttsm":
+        fn = f"(const void*)&tsm::tsmttsm_kernel<{t}>"
+        p = (c["MT"], c["NTL"], 0)
+        kind = "tsm::KIND_TSMTTSM"
+    else:
+        fn = f"(const void*)&tsm::tsmm_kernel<{t}>"
+        p = (c["NTL"], c["MSPLIT"], c["U"])
+        kind = "tsm::KIND_TSMM"
+    return (f"  {{{kind}, {1 if dt == 'z' else 0}, {M}, {N}, {fn}, {c['NT']}, {c['R']}, "
+            f"{p[0]}, {p[1]}, {p[2]}, {c['stages']}, {c['ctas']}}},")
+
+
+def main(per_file: int = 12) -> int:
+    os.makedirs(GEN, exist_ok=True)
+    ents = entries()
+    files = []
+    for i in range(0, len(ents), per_file):
+        batch = ents[i:i + per_file]
+        idx = i // per_file
+        name = f"inst_{idx:03d}.cu"
+        lines = ["// GENERATED by tools/gen_instances.py -- do not edit.",
+                 '#include "../tsm_kernels.cuh"', '#include "../tsm_registry.h"', "",
+                 f"extern const tsm::KernelEntry tsm_gen_table_{idx:03d}[] = {{"]
+        lines += [entry_init(*e) for e in batch]
+        lines += ["};", f"extern const int tsm_gen_count_{idx:03d} = {len(batch)};", ""]
+        src = "\n".join(lines)
+        path = os.path.join(GEN, name)
+        if not os.path.exists(path) or open(path).read() != src:
+            with open(path, "w") as f:
+                f.write(src)
+        files.append(idx)
+    # drop stale batch files
+    for fn in os.listdir(GEN):
+        if fn.startswith("inst_") and fn.endswith(".cu") and int(fn[5:8]) not in files:
+            os.remove(os.path.join(GEN, fn))
+    reg = ["// GENERATED by tools/gen_instances.py -- do not edit.", '#include "../tsm_registry.h"', ""]
+    for idx in files:
+        reg.append(f"extern const tsm::KernelEntry tsm_gen_table_{idx:03d}[];")
+        reg.append(f"extern const int tsm_gen_count_{idx:03d};")
+    reg.append("")
+    reg.append("namespace tsm {")
+    reg.append("extern const KernelTable g_gen_tables[] = {")
+    for idx in files:
+        reg.append(f"  {{tsm_gen_table_{idx:03d}, tsm_gen_count_{idx:03d}}},")
+    reg.append("};")
+    reg.append(f"extern const int g_gen_ntables = {len(files)};")
+    shapes = ",".join(f"[{M},{N}]" for (M, N) in SHAPES)
+    reg.append(f'const char* g_gen_info = "{{\\"aot_shapes\\":[{shapes}],\\"instances\\":{len(ents)}}}";')
+    reg.append("}  // namespace tsm")
+    src = "\n".join(reg) + "\n"
+    _write(os.path.join(GEN, "registry_gen.cpp"), src)
+
+    # default launch parameters for EVERY (op, dtype, M, N): the JIT path
+    # instantiates these for shapes outside the AOT set.  Index:
+    # ((op*2 + dt)*64 + (M-1))*64 + (N-1).
+    tune = load_tune()
+    lines = ["// GENERATED by tools/gen_instances.py -- do not edit.", '#include "../tsm_registry.h"',
+             "", "namespace tsm {", "extern const KernelEntry g_param_table[] = {"]
+    for op in ("tsmttsm", "tsmm"):
+        for dt in ("d", "z"):
+            for M in range(1, 65):
+                for N in range(1, 65):
+                    c = (tsmttsm_default if op == "tsmttsm" else tsmm_default)(M, N, dt == "z")
+                    c.update(tune.get(f"{op}_{dt}_{M}_{N}", {}).get("cfg", {}))
+                    p = (c["MT"], c["NTL"], 0) if op == "tsmttsm" else (c["NTL"], c["MSPLIT"], c["U"])
+                    lines.append(f"  {{{0 if op == 'tsmttsm' else 1}, {1 if dt == 'z' else 0}, {M}, {N}, "
+                                 f"nullptr, {c['NT']}, {c['R']}, {p[0]}, {p[1]}, {p[2]}, "
+                                 f"{c['stages']}, {c['ctas']}}},")
+    lines += ["};", "}  // namespace tsm", ""]
+    _write(os.path.join(GEN, "params_gen.cpp"), "\n".join(lines))
+
+    # the kernel template source, embedded for NVRTC
+    ksrc = open(os.path.join(os.path.dirname(GEN), "tsm_kernels.cuh")).read()
+    assert ")TSMSRC\"" not in ksrc
+    _write(os.path.join(GEN, "kernel_source.inc"),
+           "// GENERATED by tools/gen_instances.py from csrc/tsm_kernels.cuh -- do not edit.\n"
+           f"static const char* kTsmKernelSource = R\"TSMSRC({ksrc})TSMSRC\";\n")
+    print(f"{len(ents)} instances in {len(files)} files")
+    return 0
+
+
+def _write(path: str, src: str) -> None:
+    if not os.path.exists(path) or open(path).read() != src:
+        with open(path, "w") as f:
+            f.write(src)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -79,6 +79,45 @@ def raw_values(n: int, seed: int, mat: str, mode: str, start: int = 0) -> np.nda
     return out
 
 
+def values_at(idx: np.ndarray, seed: int, mat: str, mode: str) -> np.ndarray:
+    """Real values at arbitrary flat indices (same generator as raw_values)."""
+    idx = np.asarray(idx, dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        h = mix64(idx + key(seed, mat))
+    if mode == "fp":
+        return ((h >> np.uint64(11)).astype(np.int64) - (1 << 52)).astype(np.float64) * 2.0 ** -52
+    if mode == "int":
+        return ((h >> np.uint64(53)).astype(np.int64) - 1024).astype(np.float64)
+    raise ValueError(f"unknown mode {mode!r}")
+
+
+def column(K: int, width: int, col: int, mat: str, *, complex_: bool = False, mode: str = "fp",
+           seed: int | None = None) -> np.ndarray:
+    """Column `col` (length K) of the K x width matrix(K, width, mat, ...)."""
+    if seed is None:
+        seed = SEED_FP if mode == "fp" else SEED_INT
+    elem = np.arange(K, dtype=np.uint64) * np.uint64(width) + np.uint64(col)
+    if complex_:
+        re = values_at(2 * elem, seed, mat, mode)
+        im = values_at(2 * elem + np.uint64(1), seed, mat, mode)
+        return re + 1j * im
+    return values_at(elem, seed, mat, mode)
+
+
+def rows(row_idx: np.ndarray, width: int, mat: str, *, complex_: bool = False, mode: str = "fp",
+         seed: int | None = None) -> np.ndarray:
+    """Selected rows (len(row_idx) x width) of matrix(K, width, mat, ...)."""
+    if seed is None:
+        seed = SEED_FP if mode == "fp" else SEED_INT
+    r = np.asarray(row_idx, dtype=np.uint64)[:, None]
+    elem = r * np.uint64(width) + np.arange(width, dtype=np.uint64)[None, :]
+    if complex_:
+        re = values_at(2 * elem, seed, mat, mode)
+        im = values_at(2 * elem + np.uint64(1), seed, mat, mode)
+        return re + 1j * im
+    return values_at(elem, seed, mat, mode)
+
+
 def matrix(rows: int, cols: int, mat: str, *, complex_: bool = False, mode: str = "fp",
            seed: int | None = None) -> np.ndarray:
     """Row-major rows x cols matrix (float64 or complex128) from the generator."""
