@@ -114,6 +114,10 @@ typedef struct tsm_config {
   int p0, p1, p2;
   int stages;
   int ctas_per_sm;
+  int kernel; /* 0 = register-tile DFMA kernel; 1 = DMMA kernel (TSMTTSM only): FP64
+                 tensor-pipe mma.sync m8n8k4, p0 = WM, p1 = WN 8x8 accumulator blocks per
+                 warp, threads = 32 * (consumer warps + 1 producer warp), rows_per_chunk
+                 a multiple of 4 */
 } tsm_config;
 
 /* Create a plan with an explicit configuration (used by the on-B200

@@ -41,7 +41,7 @@ class TsmConfig(ctypes.Structure):
     """tsm_config (include/libtsm.h)."""
     _fields_ = [("threads", ctypes.c_int), ("rows_per_chunk", ctypes.c_int), ("p0", ctypes.c_int),
                 ("p1", ctypes.c_int), ("p2", ctypes.c_int), ("stages", ctypes.c_int),
-                ("ctas_per_sm", ctypes.c_int)]
+                ("ctas_per_sm", ctypes.c_int), ("kernel", ctypes.c_int)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}

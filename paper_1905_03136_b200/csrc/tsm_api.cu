@@ -77,6 +77,10 @@ size_t smem_bytes(const KernelEntry& k, int stages) {
   if (k.op == KIND_TSMTTSM) {
     const long long stage = static_cast<long long>(k.R) * (k.M + k.N) * S;
     const long long cells = static_cast<long long>(k.M) * k.N * S;
+    if (k.impl == 1) {  // DMMA kernel: 2 x 16 mbarriers, ring; partial + finisher scratch
+      long long need = std::max<long long>(stages * stage, cells + k.NT);
+      return static_cast<size_t>(256 + need * 8);
+    }
     long long need = std::max<long long>(stages * stage, std::max<long long>(cells, k.NT));
     return static_cast<size_t>(128 + need * 8);
   }
@@ -165,11 +169,20 @@ static tsm_status validate_config(const KernelEntry& e) {
   if (e.R < 2 || e.R % 2) return bad("rows_per_chunk must be even and >= 2");
   if (e.stages < 2 || e.stages > 16) return bad("stages must be in [2, 16]");
   if (e.ctas_per_sm < 1) return bad("ctas_per_sm must be >= 1");
-  if (e.op == KIND_TSMTTSM) {
+  if (e.impl != 0 && e.impl != 1) return bad("kernel must be 0 (DFMA tile) or 1 (DMMA)");
+  if (e.op == KIND_TSMTTSM && e.impl == 1) {
+    const int MB = (e.M + 7) / 8, NB = (e.N + 7) / 8;
+    if (e.p0 < 1 || e.p1 < 1 || e.p0 > MB || e.p1 > NB) return bad("WM, WN must be in [1, ceil(M/8)], [1, ceil(N/8)]");
+    const int WT = ((MB + e.p0 - 1) / e.p0) * ((NB + e.p1 - 1) / e.p1);
+    const int NW = e.NT / 32 - 1;
+    if (NW < WT || NW % WT) return bad("threads/32 - 1 consumer warps must be a multiple of the warp tiles");
+    if (e.R % 4) return bad("rows_per_chunk must be a multiple of 4 for the DMMA kernel");
+  } else if (e.op == KIND_TSMTTSM) {
     if (!is_pow2(e.p0) || !is_pow2(e.p1) || e.p0 > e.M || e.p1 > e.N)
       return bad("MT, NTL must be powers of two <= M, N");
     if (e.NT % (e.p0 * e.p1)) return bad("MT*NTL must divide threads");
   } else {
+    if (e.impl != 0) return bad("TSMM has only the DFMA kernel (kernel = 0) in this build");
     if (!is_pow2(e.p0) || !is_pow2(e.p1) || e.p0 > e.N || e.p1 > e.M || e.p0 * e.p1 > 32)
       return bad("NTL <= N, MSPLIT <= M powers of two with NTL*MSPLIT <= 32");
     if (e.p2 < 1 || e.p2 > 64) return bad("U must be in [1, 64]");
@@ -258,6 +271,7 @@ tsm_status tsm_plan_create_config(tsm_plan* out, tsm_op op, tsm_dtype dtype, int
   e.p0 = cfg->p0;
   e.p1 = cfg->p1;
   e.p2 = op == TSM_OP_TSMTTSM ? 0 : cfg->p2;
+  e.impl = cfg->kernel;
   e.stages = cfg->stages;
   e.ctas_per_sm = cfg->ctas_per_sm;
   tsm_status st = validate_config(e);
@@ -272,6 +286,7 @@ tsm_status tsm_plan_get_config(tsm_plan p, tsm_config* cfg) {
   cfg->p0 = p->k->p0;
   cfg->p1 = p->k->p1;
   cfg->p2 = p->k->p2;
+  cfg->kernel = p->k->impl;
   cfg->stages = p->stages;
   cfg->ctas_per_sm = p->ctas_per_sm;
   return TSM_SUCCESS;
@@ -430,14 +445,23 @@ tsm_status tsm_plan_describe(tsm_plan p, int64_t K, char* buf, size_t len) {
   const Geometry g = geometry(p, K < 0 ? 0 : K);
   const KernelEntry* k = p->k;
   char tmp[512];
-  if (p->op == TSM_OP_TSMTTSM)
+  if (p->op == TSM_OP_TSMTTSM && k->impl == 1)
+    snprintf(tmp, sizeof tmp,
+             "{\"op\":\"tsmttsm\",\"dtype\":\"%c\",\"M\":%d,\"N\":%d,\"WM\":%d,\"WN\":%d,"
+             "\"threads\":%d,\"rows_per_chunk\":%d,\"stages\":%d,"
+             "\"ctas_per_sm\":%d,\"smem\":%zu,\"grid\":%d,\"nchunks\":%lld,\"nfin\":%d,\"jit\":%s,"
+             "\"kernel\":\"dmma\"}",
+             p->dt ? 'z' : 'd', p->M, p->N, k->p0, k->p1, k->NT, k->R, p->stages, p->ctas_per_sm,
+             p->smem, g.grid, g.nchunks, g.nfin, p->jit ? "true" : "false");
+  else if (p->op == TSM_OP_TSMTTSM)
     snprintf(tmp, sizeof tmp,
              "{\"op\":\"tsmttsm\",\"dtype\":\"%c\",\"M\":%d,\"N\":%d,\"MT\":%d,\"NTL\":%d,"
              "\"TM\":%d,\"TN\":%d,\"threads\":%d,\"rows_per_chunk\":%d,\"stages\":%d,"
-             "\"ctas_per_sm\":%d,\"smem\":%zu,\"grid\":%d,\"nchunks\":%lld,\"nfin\":%d,\"jit\":%s}",
+             "\"ctas_per_sm\":%d,\"smem\":%zu,\"grid\":%d,\"nchunks\":%lld,\"nfin\":%d,\"jit\":%s,"
+             "\"kernel\":\"%s\"}",
              p->dt ? 'z' : 'd', p->M, p->N, k->p0, k->p1, (p->M + k->p0 - 1) / k->p0,
              (p->N + k->p1 - 1) / k->p1, k->NT, k->R, p->stages, p->ctas_per_sm, p->smem, g.grid,
-             g.nchunks, g.nfin, p->jit ? "true" : "false");
+             g.nchunks, g.nfin, p->jit ? "true" : "false", k->impl ? "dmma" : "dfma");
   else
     snprintf(tmp, sizeof tmp,
              "{\"op\":\"tsmm\",\"dtype\":\"%c\",\"M\":%d,\"N\":%d,\"NTL\":%d,\"MSPLIT\":%d,"

@@ -38,7 +38,10 @@ std::map<std::string, const KernelEntry*> g_jit_index;
 std::string cfg_type(const KernelEntry& e) {
   std::ostringstream os;
   const char* z = e.dt ? "true" : "false";
-  if (e.op == KIND_TSMTTSM)
+  if (e.op == KIND_TSMTTSM && e.impl == 1)
+    os << "tsm::TsmttsmMmaCfg<" << e.M << ", " << e.N << ", " << z << ", " << e.p0 << ", " << e.p1
+       << ", " << (e.NT / 32 - 1) << ", " << e.R << ">";
+  else if (e.op == KIND_TSMTTSM)
     os << "tsm::TsmttsmCfg<" << e.M << ", " << e.N << ", " << z << ", " << e.p0 << ", " << e.p1
        << ", " << e.NT << ", " << e.R << ">";
   else
@@ -48,8 +51,9 @@ std::string cfg_type(const KernelEntry& e) {
 }
 
 std::string kernel_name(const KernelEntry& e) {
-  return std::string(e.op == KIND_TSMTTSM ? "tsm::tsmttsm_kernel<" : "tsm::tsmm_kernel<") +
-         cfg_type(e) + ">";
+  const char* fn = e.op == KIND_TSMM ? "tsm::tsmm_kernel<"
+                   : (e.impl == 1 ? "tsm::tsmttsm_mma_kernel<" : "tsm::tsmttsm_kernel<");
+  return std::string(fn) + cfg_type(e) + ">";
 }
 
 unsigned long long fnv1a(const std::string& s, unsigned long long h = 1469598103934665603ull) {
@@ -125,15 +129,16 @@ tsm_status compile(const KernelEntry& e, std::vector<char>* cubin, std::string* 
 
 // Returns a registry entry whose func is a JIT-compiled kernel for `want`.
 tsm_status jit_kernel(const KernelEntry& want, const KernelEntry** out) {
-  std::lock_guard<std::mutex> lk(g_jit_mu);
   const std::string key = kernel_name(want);
-  auto it = g_jit_index.find(key);
-  if (it != g_jit_index.end()) {
-    *out = it->second;
-    return TSM_SUCCESS;
+  {
+    std::lock_guard<std::mutex> lk(g_jit_mu);
+    auto it = g_jit_index.find(key);
+    if (it != g_jit_index.end()) {
+      *out = it->second;
+      return TSM_SUCCESS;
+    }
   }
-  int ver = 0;
-  nvrtcVersion(&ver, &ver);
+  // compile / load outside the lock: independent plans JIT in parallel
   const std::string dir = cache_dir();
   char hbuf[32];
   snprintf(hbuf, sizeof hbuf, "%016llx", fnv1a(key, fnv1a(kTsmKernelSource)));
@@ -159,6 +164,12 @@ tsm_status jit_kernel(const KernelEntry& want, const KernelEntry** out) {
     return fail(TSM_ERR_CUDA, std::string("cudaLibraryGetKernel: ") + cudaGetErrorString(e));
   KernelEntry ent = want;
   ent.func = reinterpret_cast<const void*>(k);
+  std::lock_guard<std::mutex> lk(g_jit_mu);
+  auto it = g_jit_index.find(key);
+  if (it != g_jit_index.end()) {  // another thread finished first: keep one entry
+    *out = it->second;
+    return TSM_SUCCESS;
+  }
   g_jit_entries.push_back(ent);
   const KernelEntry* p = &g_jit_entries.back();
   g_jit_index[key] = p;

@@ -221,6 +221,80 @@ __device__ __forceinline__ void tsmttsm_row(const double* __restrict__ ar,
   }
 }
 
+// T3 -> T4: write this block's M x N partial (in smem sP) to the workspace,
+// take a ticket; the last NFIN blocks to arrive sum all partials in fixed
+// block order (each cell by one thread, its g-range split into fixed
+// contiguous segments combined in segment order).  No floating-point atomics.
+template <int NT, int CELLS>
+__device__ __forceinline__ void grid_reduce(const TsmttsmArgs& p, const double* sP, double* scratch) {
+  __shared__ u32 s_ticket;
+  const int tid = threadIdx.x;
+  const int G = gridDim.x;
+  double* myP = p.partials + static_cast<long long>(blockIdx.x) * CELLS;
+  for (int idx = tid; idx < CELLS; idx += NT) __stcg(&myP[idx], sP[idx]);
+
+  // ---- T4: deterministic grid reduction by the last NFIN blocks ----
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) s_ticket = atomicAdd(&p.counters[0], 1u);
+  __syncthreads();
+  const int nfin = p.nfin;
+  const int t = static_cast<int>(s_ticket);
+  if (t < G - nfin) return;
+  const int f = t - (G - nfin);
+  if (tid == 0) {
+    while (ld_acquire_gpu(&p.counters[0]) < static_cast<u32>(G)) __nanosleep(64);
+  }
+  __syncthreads();
+  // finisher f owns cells [c0, c1); TPC threads per cell split the block
+  // range into contiguous segments, combined afterwards in segment order.
+  const int cpf = (CELLS + nfin - 1) / nfin;
+  const int c0 = f * cpf;
+  const int c1 = (c0 + cpf < CELLS) ? c0 + cpf : CELLS;
+  const int ncell = c1 - c0;
+  if (ncell > 0) {
+    int tpc = NT / ncell;
+    if (tpc < 1) tpc = 1;
+    if (tpc > 32) tpc = 32;
+    double* sSeg = scratch;  // [tpc][ncell] when tpc > 1
+    const int seg = tid / ncell;
+    const int cl = tid % ncell;
+    if (tpc == 1) {
+      for (int idx = c0 + tid; idx < c1; idx += NT) {
+        double s0 = 0.0;
+#pragma unroll 8
+        for (int g = 0; g < G; g++) s0 += __ldcg(&p.partials[static_cast<long long>(g) * CELLS + idx]);
+        p.C[idx] = s0;
+      }
+    } else {
+      if (seg < tpc) {
+        const int g0 = static_cast<int>((static_cast<long long>(G) * seg) / tpc);
+        const int g1 = static_cast<int>((static_cast<long long>(G) * (seg + 1)) / tpc);
+        double s0 = 0.0;
+#pragma unroll 8
+        for (int g = g0; g < g1; g++)
+          s0 += __ldcg(&p.partials[static_cast<long long>(g) * CELLS + c0 + cl]);
+        sSeg[seg * ncell + cl] = s0;
+      }
+      __syncthreads();
+      if (tid < ncell) {
+        double s0 = sSeg[tid];
+        for (int q = 1; q < tpc; q++) s0 += sSeg[q * ncell + tid];
+        p.C[c0 + tid] = s0;
+      }
+    }
+  }
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) {
+    const u32 d = atomicAdd(&p.counters[1], 1u);
+    if (d == static_cast<u32>(nfin - 1)) {  // last finisher: reset for the next call
+      p.counters[0] = 0;
+      p.counters[1] = 0;
+    }
+  }
+}
+
 template <class Cfg>
 __global__ void __launch_bounds__(Cfg::NT) tsmttsm_kernel(const TsmttsmArgs p) {
   constexpr int M = Cfg::M, N = Cfg::N, S = Cfg::S, R = Cfg::R, NT = Cfg::NT;
@@ -229,8 +303,6 @@ __global__ void __launch_bounds__(Cfg::NT) tsmttsm_kernel(const TsmttsmArgs p) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   u64* full = reinterpret_cast<u64*>(smem_raw);
   double* ring = reinterpret_cast<double*>(smem_raw + 128);
-  __shared__ u32 s_ticket;
-
   const int tid = threadIdx.x;
   const int rs = tid / TPR;  // row slot
   const int tile = tid % TPR;
@@ -341,69 +413,214 @@ __global__ void __launch_bounds__(Cfg::NT) tsmttsm_kernel(const TsmttsmArgs p) {
     }
     __syncthreads();
   }
-  double* myP = p.partials + static_cast<long long>(blockIdx.x) * CELLS;
-  for (int idx = tid; idx < CELLS; idx += NT) __stcg(&myP[idx], sP[idx]);
+  grid_reduce<NT, CELLS>(p, sP, ring);
+}
 
-  // ---- T4: deterministic grid reduction by the last NFIN blocks ----
-  __threadfence();
-  __syncthreads();
-  if (tid == 0) s_ticket = atomicAdd(&p.counters[0], 1u);
-  __syncthreads();
-  const int nfin = p.nfin;
-  const int t = static_cast<int>(s_ticket);
-  if (t < G - nfin) return;
-  const int f = t - (G - nfin);
+// ==========================================================================
+// TSMTTSM on the FP64 tensor pipe (DMMA.8x8x4, mma.sync m8n8k4 f64)
+// ==========================================================================
+// For FMA-heavy widths the register-tile kernel above is issue/latency bound
+// (ncu r01: FP64 pipe 48 % at M=N=64 with 8 warps/SM).  Here each consumer
+// warp owns a (8*WM) x (8*WN) region of C as WM x WN 8x8 accumulator blocks and
+// consumes 4 rows (one k-step) per mma.sync: per 4 rows a warp issues WM + WN
+// fragment loads and WM*WN DMMAs (256 FMAs each) instead of 4*TM*TN DFMAs per
+// lane.  Operands (PTX m8n8k4 .row.col fragment layout; g = lane/4, q = lane%4):
+//   MMA-A = A^T block (8 m x 4 k):  lane holds A[k0+q][m0+g]
+//   MMA-B = B block   (4 k x 8 n):  lane holds B[k0+q][n0+g]
+//   acc   = C block   (8 m x 8 n):  lane holds C[m0+g][n0+2q], C[m0+g][n0+2q+1]
+// Z: re += Ar Br + (-Ai) Bi ; im += Ar Bi + Ai Br  (4 real DMMAs per block).
+// Warp specialisation: warp NW is the TMA producer (one elected lane issues the
+// bulk copies after the consumers release a stage on its `empty` mbarrier),
+// warps 0..NW-1 consume; there is no block-wide barrier in the main loop.
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+__device__ __forceinline__ void mbar_arrive(u64* bar) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
+// WM x WN: 8x8 blocks per warp tile; NW: consumer warps; R: rows per chunk.
+template <int M_, int N_, bool Z_, int WM_, int WN_, int NW_, int R_>
+struct TsmttsmMmaCfg {
+  static constexpr int M = M_, N = N_, WM = WM_, WN = WN_, NW = NW_, R = R_;
+  static constexpr bool Z = Z_;
+  static constexpr int S = Z ? 2 : 1;
+  static constexpr int MB = (M + 7) / 8, NB = (N + 7) / 8;      // 8x8 blocks of C
+  static constexpr int WTM = (MB + WM - 1) / WM, WTN = (NB + WN - 1) / WN;
+  static constexpr int WT = WTM * WTN;                          // warp tiles covering C
+  static constexpr int RS = NW / WT;                            // row slots (k-step groups)
+  static constexpr int NT = (NW + 1) * 32;                      // + producer warp
+  static constexpr int CELLS = M * N * S;
+  static constexpr int STAGE_DOUBLES = R * (M + N) * S;
+  static_assert(NW % WT == 0 && RS >= 1, "consumer warps must be a multiple of the warp tiles");
+  static_assert(R % 4 == 0, "R must be a multiple of the k-step (4 rows)");
+  static_assert(WM <= MB && WN <= NB, "warp tile larger than C");
+};
+
+template <class Cfg>
+__global__ void __launch_bounds__(Cfg::NT) tsmttsm_mma_kernel(const TsmttsmArgs p) {
+  constexpr int M = Cfg::M, N = Cfg::N, S = Cfg::S, R = Cfg::R, NW = Cfg::NW;
+  constexpr int WM = Cfg::WM, WN = Cfg::WN, WTM = Cfg::WTM, MB = Cfg::MB, NB = Cfg::NB;
+  constexpr int WT = Cfg::WT, RS = Cfg::RS, CELLS = Cfg::CELLS;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  u64* full = reinterpret_cast<u64*>(smem_raw);
+  u64* empty = full + 16;
+  double* ring = reinterpret_cast<double*>(smem_raw + 256);
+
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, q = lane & 3;
+  const long long K = p.K;
+  const long long K_even = K & ~1LL;
+  const int G = gridDim.x;
+  const int stages = p.stages;
+
   if (tid == 0) {
-    while (ld_acquire_gpu(&p.counters[0]) < static_cast<u32>(G)) __nanosleep(64);
+    for (int s = 0; s < stages; s++) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NW);
+    }
+    fence_mbar_init();
+    fence_proxy_async_smem();
   }
   __syncthreads();
-  // finisher f owns cells [c0, c1); TPC threads per cell split the block
-  // range into contiguous segments, combined afterwards in segment order.
-  const int cpf = (CELLS + nfin - 1) / nfin;
-  const int c0 = f * cpf;
-  const int c1 = (c0 + cpf < CELLS) ? c0 + cpf : CELLS;
-  const int ncell = c1 - c0;
-  if (ncell > 0) {
-    int tpc = NT / ncell;
-    if (tpc < 1) tpc = 1;
-    if (tpc > 32) tpc = 32;
-    double* sSeg = ring;  // [tpc][ncell] when tpc > 1
-    const int seg = tid / ncell;
-    const int cl = tid % ncell;
-    if (tpc == 1) {
-      for (int idx = c0 + tid; idx < c1; idx += NT) {
-        double s0 = 0.0;
-#pragma unroll 8
-        for (int g = 0; g < G; g++) s0 += __ldcg(&p.partials[static_cast<long long>(g) * CELLS + idx]);
-        p.C[idx] = s0;
+
+  // accumulators: [WM][WN] blocks x 2 doubles (x re/im)
+  double acc[WM][WN][S][2];
+#pragma unroll
+  for (int i = 0; i < WM; i++)
+#pragma unroll
+    for (int j = 0; j < WN; j++)
+#pragma unroll
+      for (int z = 0; z < S; z++) acc[i][j][z][0] = acc[i][j][z][1] = 0.0;
+
+  const int slot = warp / WT;
+  const int wt = warp % WT;
+  const int wm = wt % WTM, wn = wt / WTM;
+
+  // one k-step: rows k0..k0+3 of the stage (or of global memory for the tail)
+  auto kstep = [&](const double* __restrict__ sA, const double* __restrict__ sB, int k0, int rows) {
+    const bool rv = (k0 + q) < rows;
+    if constexpr (!Cfg::Z) {
+      double a[WM], b[WN];
+#pragma unroll
+      for (int i = 0; i < WM; i++) {
+        const int m = (wm * WM + i) * 8 + g;
+        a[i] = (rv && m < M) ? sA[(k0 + q) * M + m] : 0.0;
       }
+#pragma unroll
+      for (int j = 0; j < WN; j++) {
+        const int n = (wn * WN + j) * 8 + g;
+        b[j] = (rv && n < N) ? sB[(k0 + q) * N + n] : 0.0;
+      }
+#pragma unroll
+      for (int i = 0; i < WM; i++)
+#pragma unroll
+        for (int j = 0; j < WN; j++)
+          if ((wm * WM + i) < MB && (wn * WN + j) < NB) dmma(acc[i][j][0][0], acc[i][j][0][1], a[i], b[j]);
     } else {
-      if (seg < tpc) {
-        const int g0 = static_cast<int>((static_cast<long long>(G) * seg) / tpc);
-        const int g1 = static_cast<int>((static_cast<long long>(G) * (seg + 1)) / tpc);
-        double s0 = 0.0;
-#pragma unroll 8
-        for (int g = g0; g < g1; g++)
-          s0 += __ldcg(&p.partials[static_cast<long long>(g) * CELLS + c0 + cl]);
-        sSeg[seg * ncell + cl] = s0;
+      const double2* sA2 = reinterpret_cast<const double2*>(sA);
+      const double2* sB2 = reinterpret_cast<const double2*>(sB);
+      double2 a[WM], b[WN];
+#pragma unroll
+      for (int i = 0; i < WM; i++) {
+        const int m = (wm * WM + i) * 8 + g;
+        a[i] = (rv && m < M) ? sA2[(k0 + q) * M + m] : make_double2(0.0, 0.0);
       }
-      __syncthreads();
-      if (tid < ncell) {
-        double s0 = sSeg[tid];
-        for (int q = 1; q < tpc; q++) s0 += sSeg[q * ncell + tid];
-        p.C[c0 + tid] = s0;
+#pragma unroll
+      for (int j = 0; j < WN; j++) {
+        const int n = (wn * WN + j) * 8 + g;
+        b[j] = (rv && n < N) ? sB2[(k0 + q) * N + n] : make_double2(0.0, 0.0);
+      }
+#pragma unroll
+      for (int i = 0; i < WM; i++) {
+        const double nai = -a[i].y;
+#pragma unroll
+        for (int j = 0; j < WN; j++)
+          if ((wm * WM + i) < MB && (wn * WN + j) < NB) {
+            dmma(acc[i][j][0][0], acc[i][j][0][1], a[i].x, b[j].x);  // re += ar br
+            dmma(acc[i][j][0][0], acc[i][j][0][1], nai, b[j].y);     // re -= ai bi
+            dmma(acc[i][j][1][0], acc[i][j][1][1], a[i].x, b[j].y);  // im += ar bi
+            dmma(acc[i][j][1][0], acc[i][j][1][1], a[i].y, b[j].x);  // im += ai br
+          }
       }
     }
-  }
-  __threadfence();
-  __syncthreads();
-  if (tid == 0) {
-    const u32 d = atomicAdd(&p.counters[1], 1u);
-    if (d == static_cast<u32>(nfin - 1)) {  // last finisher: reset for the next call
-      p.counters[0] = 0;
-      p.counters[1] = 0;
+  };
+
+  if (warp == NW) {
+    // ---------------- producer warp: bulk copies into the ring ----------------
+    if (lane == 0) {
+      const u64 pol = policy_evict_first();
+      int it = 0;
+      for (long long c = blockIdx.x; c < p.nchunks; c += G, it++) {
+        const int s = it % stages;
+        if (it >= stages) mbar_wait(&empty[s], static_cast<u32>(((it / stages) - 1) & 1));
+        const long long r0 = c * R;
+        const long long rows = (K_even - r0 < R) ? (K_even - r0) : R;
+        const u32 ba = static_cast<u32>(rows * M * S * 8);
+        const u32 bb = static_cast<u32>(rows * N * S * 8);
+        double* dA = ring + static_cast<long long>(s) * Cfg::STAGE_DOUBLES;
+        double* dB = dA + R * M * S;
+        mbar_arrive_expect_tx(&full[s], ba + bb);
+        bulk_g2s(dA, p.A + r0 * M * S, ba, &full[s], pol);
+        bulk_g2s(dB, p.B + r0 * N * S, bb, &full[s], pol);
+      }
     }
+  } else {
+    // ---------------- consumer warps ----------------
+    int it = 0;
+    for (long long c = blockIdx.x; c < p.nchunks; c += G, it++) {
+      const int s = it % stages;
+      mbar_wait(&full[s], static_cast<u32>((it / stages) & 1));
+      const double* sA = ring + static_cast<long long>(s) * Cfg::STAGE_DOUBLES;
+      const double* sB = sA + R * M * S;
+      const long long r0 = c * R;
+      const int rows = static_cast<int>((K_even - r0 < R) ? (K_even - r0) : R);
+      if (rows == R) {
+#pragma unroll 2
+        for (int k0 = slot * 4; k0 < R; k0 += RS * 4) kstep(sA, sB, k0, R);
+      } else {
+        for (int k0 = slot * 4; k0 < rows; k0 += RS * 4) kstep(sA, sB, k0, rows);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+    }
+    // odd last row: a k-step whose rows 1..3 are zero, from global memory
+    if ((K & 1) && blockIdx.x == 0 && slot == 0)
+      kstep(p.A + (K - 1) * M * S, p.B + (K - 1) * N * S, 0, 1);
   }
+  __syncthreads();  // ring idle: every issued chunk was consumed
+
+  // ---- T3: block partial, slot by slot in slot order ----
+  double* sP = ring;
+#pragma unroll 1
+  for (int sl = 0; sl < RS; sl++) {
+    if (warp < NW && slot == sl) {
+#pragma unroll
+      for (int i = 0; i < WM; i++) {
+        const int m = (wm * WM + i) * 8 + g;
+#pragma unroll
+        for (int j = 0; j < WN; j++) {
+#pragma unroll
+          for (int e = 0; e < 2; e++) {
+            const int n = (wn * WN + j) * 8 + 2 * q + e;
+            if (m < M && n < N && (wm * WM + i) < MB && (wn * WN + j) < NB) {
+#pragma unroll
+              for (int z = 0; z < S; z++) {
+                const int idx = (m * N + n) * S + z;
+                sP[idx] = (sl == 0) ? acc[i][j][z][e] : sP[idx] + acc[i][j][z][e];
+              }
+            }
+          }
+        }
+      }
+    }
+    __syncthreads();
+  }
+  grid_reduce<Cfg::NT, CELLS>(p, sP, ring + CELLS);
 }
 
 // ==========================================================================

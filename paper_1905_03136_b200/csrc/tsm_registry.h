@@ -17,6 +17,7 @@ struct KernelEntry {
   int p0, p1, p2;
   int stages;        // default pipeline depth
   int ctas_per_sm;   // target resident CTAs per SM (clipped by occupancy)
+  int impl;          // 0 = register-tile DFMA kernel, 1 = DMMA (mma.sync m8n8k4 f64) kernel
 };
 
 struct KernelTable {

@@ -255,7 +255,7 @@ def test_workspace_reuse_across_shapes(tsm):
 # Shapes outside the AOT set: NVRTC run-time instantiation of the same
 # templates; explicit configurations (the autotuner's search space).
 # ---------------------------------------------------------------------------
-JIT_SHAPES = [(12, 20), (37, 5), (2, 63), (64, 9), (11, 11)]
+JIT_SHAPES = [(12, 20), (37, 5), (2, 63), (64, 9), (11, 12)]
 
 
 @pytest.mark.parametrize("cplx", [False, True], ids=["D", "Z"])

@@ -73,7 +73,49 @@ def tsmttsm_default(M: int, N: int, z: bool) -> dict:
     R = max(2, (16384 // row_bytes))
     step = max(2, RB) if RB % 2 == 0 or RB == 1 else 2 * RB
     R = max(step, (R // step) * step)
-    return dict(MT=MT, NTL=NTL, NT=NT, R=R, stages=4, ctas=4)
+    return dict(MT=MT, NTL=NTL, NT=NT, R=R, stages=4, ctas=4, impl=0)
+
+
+def use_mma(M: int, N: int, z: bool) -> bool:
+    """DMMA where the FP64 work per byte is high (PAPER.md:126-143 intensity
+    I = f*M*N / (s*(M+N))): at I >= ~2 flop/B the FP64 pipe must run at >= ~40 %
+    of peak just to keep up with HBM, where the register-tile kernel becomes
+    issue-bound (ncu r01)."""
+    f, s = (8, 16) if z else (2, 8)
+    return f * M * N / (s * (M + N)) >= 2.0 and min(M, N) >= 8
+
+
+def tsmttsm_mma_default(M: int, N: int, z: bool) -> dict:
+    """DMMA kernel: WM x WN 8x8 accumulator blocks per warp (<= 32 accumulator
+    doubles per lane), NW consumer warps (a multiple of the warp tiles) + 1
+    producer warp, ~24 KB stages."""
+    MB, NB = cdiv(M, 8), cdiv(N, 8)
+    wmax = 8 if z else 16  # WM*WN blocks per warp
+    best = None
+    for WM in range(1, min(MB, 4) + 1):
+        for WN in range(1, min(NB, 4) + 1):
+            if WM * WN > wmax:
+                continue
+            if cdiv(MB, WM) * cdiv(NB, WN) > 16:
+                continue
+            # load balance (padded / useful blocks) x fragment loads per DMMA
+            bal = cdiv(MB, WM) * WM * cdiv(NB, WN) * WN / (MB * NB)
+            key = (bal * (1 + 0.5 * (WM + WN) / (WM * WN)), abs(WM - WN))
+            if best is None or key < best[0]:
+                best = (key, WM, WN)
+    _, WM, WN = best
+    WT = cdiv(MB, WM) * cdiv(NB, WN)
+    NW = WT * max(1, 8 // WT)
+    RS = NW // WT
+    S = 2 if z else 1
+    row_bytes = (M + N) * 8 * S
+    step = 4 * RS
+    R = max(step, (24576 // row_bytes) // step * step)
+    return dict(MT=WM, NTL=WN, NT=(NW + 1) * 32, R=R, stages=4, ctas=2, impl=1)
+
+
+def tsmttsm_pick(M: int, N: int, z: bool) -> dict:
+    return tsmttsm_mma_default(M, N, z) if use_mma(M, N, z) else tsmttsm_default(M, N, z)
 
 
 def tsmm_default(M: int, N: int, z: bool) -> dict:
@@ -112,7 +154,7 @@ def tsmm_default(M: int, N: int, z: bool) -> dict:
         U *= 2
         rpp *= 2
     R = rpp * max(1, round(T / (rpp * M * 8 * S)))
-    return dict(NTL=NTL, MSPLIT=MSPLIT, U=U, NT=NT, R=R, stages=4, ctas=4)
+    return dict(NTL=NTL, MSPLIT=MSPLIT, U=U, NT=NT, R=R, stages=4, ctas=4, impl=0)
 
 
 def load_tune() -> dict:
@@ -129,7 +171,7 @@ def entries():
         for dt in ("d", "z"):
             for (M, N) in SHAPES:
                 key = f"{op}_{dt}_{M}_{N}"
-                cfg = (tsmttsm_default if op == "tsmttsm" else tsmm_default)(M, N, dt == "z")
+                cfg = (tsmttsm_pick if op == "tsmttsm" else tsmm_default)(M, N, dt == "z")
                 cfg.update(tune.get(key, {}).get("cfg", {}))
                 out.append((op, dt, M, N, cfg))
     return out
@@ -137,6 +179,8 @@ def entries():
 
 def cfg_type(op, dt, M, N, c) -> str:
     z = "true" if dt == "z" else "false"
+    if op == "tsmttsm" and c.get("impl", 0) == 1:
+        return f"tsm::TsmttsmMmaCfg<{M}, {N}, {z}, {c['MT']}, {c['NTL']}, {c['NT'] // 32 - 1}, {c['R']}>"
     if op == "tsmttsm":
         return f"tsm::TsmttsmCfg<{M}, {N}, {z}, {c['MT']}, {c['NTL']}, {c['NT']}, {c['R']}>"
     return f"tsm::TsmmCfg<{M}, {N}, {z}, {c['NTL']}, {c['MSPLIT']}, {c['U']}, {c['NT']}, {c['R']}>"
@@ -145,7 +189,8 @@ def cfg_type(op, dt, M, N, c) -> str:
 def entry_init(op, dt, M, N, c) -> str:
     t = cfg_type(op, dt, M, N, c)
     if op == "tsmttsm":
-        fn = f"(const void*)&tsm::tsmttsm_kernel<{t}>"
+        kn = "tsmttsm_mma_kernel" if c.get("impl", 0) == 1 else "tsmttsm_kernel"
+        fn = f"(const void*)&tsm::{kn}<{t}>"
         p = (c["MT"], c["NTL"], 0)
         kind = "tsm::KIND_TSMTTSM"
     else:
@@ -153,7 +198,7 @@ def entry_init(op, dt, M, N, c) -> str:
         p = (c["NTL"], c["MSPLIT"], c["U"])
         kind = "tsm::KIND_TSMM"
     return (f"  {{{kind}, {1 if dt == 'z' else 0}, {M}, {N}, {fn}, {c['NT']}, {c['R']}, "
-            f"{p[0]}, {p[1]}, {p[2]}, {c['stages']}, {c['ctas']}}},")
+            f"{p[0]}, {p[1]}, {p[2]}, {c['stages']}, {c['ctas']}, {c.get('impl', 0)}}},")
 
 
 def main(per_file: int = 12) -> int:
@@ -206,12 +251,12 @@ def main(per_file: int = 12) -> int:
         for dt in ("d", "z"):
             for M in range(1, 65):
                 for N in range(1, 65):
-                    c = (tsmttsm_default if op == "tsmttsm" else tsmm_default)(M, N, dt == "z")
+                    c = (tsmttsm_pick if op == "tsmttsm" else tsmm_default)(M, N, dt == "z")
                     c.update(tune.get(f"{op}_{dt}_{M}_{N}", {}).get("cfg", {}))
                     p = (c["MT"], c["NTL"], 0) if op == "tsmttsm" else (c["NTL"], c["MSPLIT"], c["U"])
                     lines.append(f"  {{{0 if op == 'tsmttsm' else 1}, {1 if dt == 'z' else 0}, {M}, {N}, "
                                  f"nullptr, {c['NT']}, {c['R']}, {p[0]}, {p[1]}, {p[2]}, "
-                                 f"{c['stages']}, {c['ctas']}}},")
+                                 f"{c['stages']}, {c['ctas']}, {c.get('impl', 0)}}},")
     lines += ["};", "}  // namespace tsm", ""]
     _write(os.path.join(GEN, "params_gen.cpp"), "\n".join(lines))
 
@@ -233,3 +278,104 @@ def _write(path: str, src: str) -> None:
 
 if __name__ == "__main__":
     sys.exit(main())
+
+
+# ---------------------------------------------------------------------------
+# Autotuning search space (tools/autotune.py measures these on the B200).
+# Compile-time parameters only; stages / ctas are run-time and swept there.
+# ---------------------------------------------------------------------------
+def _rows(step: int, row_bytes: int, target: int) -> int:
+    return max(step, (target // row_bytes) // step * step)
+
+
+def candidates(op: str, M: int, N: int, z: bool) -> list:
+    S = 2 if z else 1
+    row = (M + N) * 8 * S
+    out = []
+    if op == "tsmttsm":
+        amax = 32 if z else 64
+        tiles = []
+        MT = 1
+        while MT <= M:
+            NTL = 1
+            while NTL <= N:
+                TM, TN = cdiv(M, MT), cdiv(N, NTL)
+                TPR = MT * NTL
+                if TM * TN <= amax and TPR <= 256:
+                    waste = MT * TM * NTL * TN / (M * N)
+                    lds = (TM + TN) / (TM * TN)
+                    conflict = 0 if TPR >= 16 or TPR >= pow2floor(M) * pow2floor(N) else 1
+                    tiles.append((conflict, waste * (1 + lds), MT, NTL))
+                NTL *= 2
+            MT *= 2
+        tiles.sort()
+        for (_, _, MT, NTL) in tiles[:5]:
+            for NT in (128, 256):
+                if NT % (MT * NTL):
+                    continue
+                RB = NT // (MT * NTL)
+                step = RB if RB % 2 == 0 else 2 * RB
+                for tgt in (12288, 24576):
+                    out.append(dict(MT=MT, NTL=NTL, NT=NT, R=_rows(step, row, tgt), impl=0))
+        if min(M, N) >= 4:
+            MB, NB = cdiv(M, 8), cdiv(N, 8)
+            wmax = 8 if z else 16
+            wt = []
+            for WM in range(1, min(MB, 4) + 1):
+                for WN in range(1, min(NB, 4) + 1):
+                    if WM * WN > wmax or cdiv(MB, WM) * cdiv(NB, WN) > 16:
+                        continue
+                    bal = cdiv(MB, WM) * WM * cdiv(NB, WN) * WN / (MB * NB)
+                    wt.append((bal * (1 + 0.5 * (WM + WN) / (WM * WN)), WM, WN))
+            wt.sort()
+            for (_, WM, WN) in wt[:3]:
+                WT = cdiv(MB, WM) * cdiv(NB, WN)
+                for k in (1, 2, 4, 8):
+                    NW = WT * k
+                    if NW < 4 and k < 8 and WT * (k * 2) <= 16:
+                        continue
+                    if NW > 16:
+                        break
+                    for tgt in (16384, 32768):
+                        out.append(dict(MT=WM, NTL=WN, NT=(NW + 1) * 32,
+                                        R=_rows(4 * k, row, tgt), impl=1))
+    else:
+        acc_max = 16 if z else 32
+        NTL = 1
+        ntls = []
+        while NTL <= min(N, 32):
+            ntls.append(NTL)
+            NTL *= 2
+        for NTL in ntls[-3:]:
+            TN = cdiv(N, NTL)
+            MS = 1
+            while NTL * MS <= 32 and MS <= M:
+                us = [U for U in (2, 4, 8, 16) if U * TN <= acc_max][-2:]
+                for U in us:
+                    for NT in (256, 128):
+                        GS = NTL * MS
+                        rpp = (NT // GS) * U
+                        if rpp % 2 or rpp * max(M, N) * S * 8 > 65536:
+                            continue
+                        R = rpp * max(1, round(16384 / (rpp * M * 8 * S)))
+                        out.append(dict(NTL=NTL, MSPLIT=MS, U=U, NT=NT, R=R, impl=0))
+                        break
+                MS *= 2
+    # dedupe
+    seen, uniq = set(), []
+    for c in out:
+        k = tuple(sorted(c.items()))
+        if k not in seen:
+            seen.add(k)
+            uniq.append(c)
+    return uniq
+
+
+def to_tsm_config(op: str, c: dict, stages: int, ctas: int) -> dict:
+    """gen-style cfg -> tsm_config field dict (include/libtsm.h)."""
+    if op == "tsmttsm":
+        p = (c["MT"], c["NTL"], 0)
+    else:
+        p = (c["NTL"], c["MSPLIT"], c["U"])
+    return dict(threads=c["NT"], rows_per_chunk=c["R"], p0=p[0], p1=p[1], p2=p[2],
+                stages=stages, ctas_per_sm=ctas, kernel=c.get("impl", 0))
