@@ -226,10 +226,12 @@ def main():
     Abuf = torch.empty(K * maxw, dtype=tdt, device=dev)
     Bbuf = torch.empty(K * maxw, dtype=tdt, device=dev)
     Obuf = torch.empty(K * maxw, dtype=tdt, device=dev)
-    # rank r holds rows [r*K, (r+1)*K) of the global matrices: generator offset
+    # rank r holds rows [r*K, (r+1)*K) of the global (world*K) x 64 matrices:
+    # generator offset r*K*64 (x2 complex) -- weak scaling, K rows per GPU
     seed = 42
-    tsm.fill(Abuf, "A", seed)
-    tsm.fill(Bbuf, "B", seed)
+    off = rank * K * maxw * (2 if z else 1)
+    tsm.fill(Abuf, "A", seed, start=off)
+    tsm.fill(Bbuf, "B", seed, start=off)
     Cs = {M: torch.empty(M, M, dtype=tdt, device=dev) for M in widths}
     plans = {(op, M): tsm.get_plan(op, args.dtype, M, M, local) for op in ("tsmttsm", "tsmm")
              for M in widths}

@@ -114,10 +114,14 @@ typedef struct tsm_config {
   int p0, p1, p2;
   int stages;
   int ctas_per_sm;
-  int kernel; /* 0 = register-tile DFMA kernel; 1 = DMMA kernel (TSMTTSM only): FP64
-                 tensor-pipe mma.sync m8n8k4, p0 = WM, p1 = WN 8x8 accumulator blocks per
-                 warp, threads = 32 * (consumer warps + 1 producer warp), rows_per_chunk
-                 a multiple of 4 */
+  int kernel; /* 0 = register-tile DFMA kernel; 1 = DMMA kernel (FP64 tensor pipe,
+                 mma.sync m8n8k4 f64; threads = 32 * (consumer warps + 1 producer warp)):
+                 TSMTTSM: p0 = WM, p1 = WN 8x8 accumulator blocks per warp, p2 = AP,
+                          p3 = BP smem row strides (elements) of A and B (= M, N: dense);
+                          rows_per_chunk a multiple of 4.
+                 TSMM:    p0 = WR 8-row blocks per warp, p1 = AP smem row stride of A,
+                          p2 = NOP smem row stride of the output staging. */
+  int p3;
 } tsm_config;
 
 /* Create a plan with an explicit configuration (used by the on-B200

@@ -41,7 +41,7 @@ class TsmConfig(ctypes.Structure):
     """tsm_config (include/libtsm.h)."""
     _fields_ = [("threads", ctypes.c_int), ("rows_per_chunk", ctypes.c_int), ("p0", ctypes.c_int),
                 ("p1", ctypes.c_int), ("p2", ctypes.c_int), ("stages", ctypes.c_int),
-                ("ctas_per_sm", ctypes.c_int), ("kernel", ctypes.c_int)]
+                ("ctas_per_sm", ctypes.c_int), ("kernel", ctypes.c_int), ("p3", ctypes.c_int)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
@@ -294,16 +294,18 @@ def tsmm(A, C, out=None, plan: Plan | None = None):
     return B
 
 
-def fill(t, mat: str, seed: int, mode: str = "fp"):
+def fill(t, mat: str, seed: int, mode: str = "fp", start: int = 0):
     """Fill a float64/complex128 CUDA tensor with the counter-based generator
-    (the same values tsminputs.matrix() produces on the host)."""
+    (the same values tsminputs.matrix() produces on the host).  `start` is the
+    flat real-value index of t[0] in the generator stream (a rank's shard of a
+    global matrix starts at row_offset * width (* 2 for complex))."""
     torch = _torch()
     _check_cuda(t)
     n = t.numel() * (2 if t.dtype == torch.complex128 else 1)
     if t.dtype not in (torch.float64, torch.complex128):
         raise TypeError("fill expects float64 or complex128")
     stream = torch.cuda.current_stream(t.device).cuda_stream
-    tsm_fill(t.data_ptr(), n, seed, MAT_ID[mat], 0 if mode == "fp" else 1, 0, stream)
+    tsm_fill(t.data_ptr(), n, seed, MAT_ID[mat], 0 if mode == "fp" else 1, start, stream)
     return t
 
 

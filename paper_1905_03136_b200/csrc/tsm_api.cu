@@ -77,12 +77,21 @@ size_t smem_bytes(const KernelEntry& k, int stages) {
   if (k.op == KIND_TSMTTSM) {
     const long long stage = static_cast<long long>(k.R) * (k.M + k.N) * S;
     const long long cells = static_cast<long long>(k.M) * k.N * S;
-    if (k.impl == 1) {  // DMMA kernel: 2 x 16 mbarriers, ring; partial + finisher scratch
-      long long need = std::max<long long>(stages * stage, cells + k.NT);
+    if (k.impl == 1) {  // DMMA kernel: 2 x 16 mbarriers, ring (padded rows); partial + scratch
+      const long long pstage = static_cast<long long>(k.R) * (k.p2 + k.p3) * S;
+      long long need = std::max<long long>(stages * pstage, cells + k.NT);
       return static_cast<size_t>(256 + need * 8);
     }
     long long need = std::max<long long>(stages * stage, std::max<long long>(cells, k.NT));
     return static_cast<size_t>(128 + need * 8);
+  }
+  if (k.impl == 1) {  // DMMA TSMM: p0 = WR, p1 = AP, p2 = NOP (must match TsmmMmaCfg)
+    const long long MK = (k.M + 3) / 4, NB = (k.N + 7) / 8;
+    const long long NCP = S == 2 ? 8 * NB + 4 : ((8 * NB) % 16 == 8 ? 8 * NB : 8 * NB + 8);
+    const long long NW = k.NT / 32 - 1;
+    const long long cd = ((MK * 4 * NCP * S + 15) / 16) * 16;
+    const long long od = ((NW * 8 * k.p0 * k.p2 * S + 15) / 16) * 16;
+    return static_cast<size_t>(256 + (cd + od + stages * static_cast<long long>(k.R) * k.p1 * S) * 8);
   }
   const long long cdbl = static_cast<long long>(k.M) * k.N * S;
   const long long cpad = ((cdbl + 15) / 16) * 16;
@@ -177,12 +186,26 @@ static tsm_status validate_config(const KernelEntry& e) {
     const int NW = e.NT / 32 - 1;
     if (NW < WT || NW % WT) return bad("threads/32 - 1 consumer warps must be a multiple of the warp tiles");
     if (e.R % 4) return bad("rows_per_chunk must be a multiple of 4 for the DMMA kernel");
+    const int S = e.dt == TSM_Z ? 2 : 1;
+    if (e.p2 < e.M || (e.p2 != e.M && ((e.p2 * S) % 2 || (e.M * S) % 2)))
+      return bad("AP must be M, or a padded stride >= M with 16-byte rows (M*S even)");
+    if (e.p3 < e.N || (e.p3 != e.N && ((e.p3 * S) % 2 || (e.N * S) % 2)))
+      return bad("BP must be N, or a padded stride >= N with 16-byte rows (N*S even)");
   } else if (e.op == KIND_TSMTTSM) {
     if (!is_pow2(e.p0) || !is_pow2(e.p1) || e.p0 > e.M || e.p1 > e.N)
       return bad("MT, NTL must be powers of two <= M, N");
     if (e.NT % (e.p0 * e.p1)) return bad("MT*NTL must divide threads");
+  } else if (e.impl == 1) {
+    const int S = e.dt == TSM_Z ? 2 : 1;
+    const int NW = e.NT / 32 - 1;
+    if (NW < 1) return bad("DMMA TSMM needs at least one consumer warp (threads >= 64)");
+    if (e.p0 < 1 || e.p0 > 8) return bad("WR (row blocks per warp) must be in [1, 8]");
+    if (e.p1 < e.M || (e.p1 != e.M && ((e.p1 * S) % 2 || (e.M * S) % 2)))
+      return bad("AP must be M, or a padded stride >= M with 16-byte rows (M*S even)");
+    if (e.p2 < e.N || (e.p2 != e.N && ((e.p2 * S) % 2 || (e.N * S) % 2)))
+      return bad("NOP must be N, or a padded stride >= N with 16-byte rows (N*S even)");
+    if (e.R % (8 * e.p0 * NW) || e.R % 2) return bad("rows_per_chunk must be a multiple of 8*WR*consumer warps");
   } else {
-    if (e.impl != 0) return bad("TSMM has only the DFMA kernel (kernel = 0) in this build");
     if (!is_pow2(e.p0) || !is_pow2(e.p1) || e.p0 > e.N || e.p1 > e.M || e.p0 * e.p1 > 32)
       return bad("NTL <= N, MSPLIT <= M powers of two with NTL*MSPLIT <= 32");
     if (e.p2 < 1 || e.p2 > 64) return bad("U must be in [1, 64]");
@@ -270,8 +293,9 @@ tsm_status tsm_plan_create_config(tsm_plan* out, tsm_op op, tsm_dtype dtype, int
   e.R = cfg->rows_per_chunk;
   e.p0 = cfg->p0;
   e.p1 = cfg->p1;
-  e.p2 = op == TSM_OP_TSMTTSM ? 0 : cfg->p2;
   e.impl = cfg->kernel;
+  e.p2 = (op == TSM_OP_TSMTTSM && e.impl == 0) ? 0 : cfg->p2;
+  e.p3 = (op == TSM_OP_TSMTTSM && e.impl == 1) ? cfg->p3 : 0;
   e.stages = cfg->stages;
   e.ctas_per_sm = cfg->ctas_per_sm;
   tsm_status st = validate_config(e);
@@ -286,6 +310,7 @@ tsm_status tsm_plan_get_config(tsm_plan p, tsm_config* cfg) {
   cfg->p0 = p->k->p0;
   cfg->p1 = p->k->p1;
   cfg->p2 = p->k->p2;
+  cfg->p3 = p->k->p3;
   cfg->kernel = p->k->impl;
   cfg->stages = p->stages;
   cfg->ctas_per_sm = p->ctas_per_sm;
@@ -448,11 +473,11 @@ tsm_status tsm_plan_describe(tsm_plan p, int64_t K, char* buf, size_t len) {
   if (p->op == TSM_OP_TSMTTSM && k->impl == 1)
     snprintf(tmp, sizeof tmp,
              "{\"op\":\"tsmttsm\",\"dtype\":\"%c\",\"M\":%d,\"N\":%d,\"WM\":%d,\"WN\":%d,"
-             "\"threads\":%d,\"rows_per_chunk\":%d,\"stages\":%d,"
+             "\"AP\":%d,\"BP\":%d,\"threads\":%d,\"rows_per_chunk\":%d,\"stages\":%d,"
              "\"ctas_per_sm\":%d,\"smem\":%zu,\"grid\":%d,\"nchunks\":%lld,\"nfin\":%d,\"jit\":%s,"
              "\"kernel\":\"dmma\"}",
-             p->dt ? 'z' : 'd', p->M, p->N, k->p0, k->p1, k->NT, k->R, p->stages, p->ctas_per_sm,
-             p->smem, g.grid, g.nchunks, g.nfin, p->jit ? "true" : "false");
+             p->dt ? 'z' : 'd', p->M, p->N, k->p0, k->p1, k->p2, k->p3, k->NT, k->R, p->stages,
+             p->ctas_per_sm, p->smem, g.grid, g.nchunks, g.nfin, p->jit ? "true" : "false");
   else if (p->op == TSM_OP_TSMTTSM)
     snprintf(tmp, sizeof tmp,
              "{\"op\":\"tsmttsm\",\"dtype\":\"%c\",\"M\":%d,\"N\":%d,\"MT\":%d,\"NTL\":%d,"
@@ -466,9 +491,10 @@ tsm_status tsm_plan_describe(tsm_plan p, int64_t K, char* buf, size_t len) {
     snprintf(tmp, sizeof tmp,
              "{\"op\":\"tsmm\",\"dtype\":\"%c\",\"M\":%d,\"N\":%d,\"NTL\":%d,\"MSPLIT\":%d,"
              "\"U\":%d,\"threads\":%d,\"rows_per_chunk\":%d,\"stages\":%d,\"ctas_per_sm\":%d,"
-             "\"smem\":%zu,\"grid\":%d,\"nchunks\":%lld,\"jit\":%s}",
+             "\"smem\":%zu,\"grid\":%d,\"nchunks\":%lld,\"jit\":%s,\"kernel\":\"%s\"}",
              p->dt ? 'z' : 'd', p->M, p->N, k->p0, k->p1, k->p2, k->NT, k->R, p->stages,
-             p->ctas_per_sm, p->smem, g.grid, g.nchunks, p->jit ? "true" : "false");
+             p->ctas_per_sm, p->smem, g.grid, g.nchunks, p->jit ? "true" : "false",
+             k->impl ? "dmma(p0=WR,p1=AP,p2=NOP)" : "dfma");
   snprintf(buf, len, "%s", tmp);
   return TSM_SUCCESS;
 }

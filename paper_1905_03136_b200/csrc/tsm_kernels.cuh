@@ -442,10 +442,15 @@ __device__ __forceinline__ void mbar_arrive(u64* bar) {
                : "memory");
 }
 
-// WM x WN: 8x8 blocks per warp tile; NW: consumer warps; R: rows per chunk.
-template <int M_, int N_, bool Z_, int WM_, int WN_, int NW_, int R_>
+// WM x WN: 8x8 blocks per warp tile; NW: consumer warps; R: rows per chunk;
+// AP, BP: smem row strides (elements) of the A and B stages.  AP = M / BP = N
+// is the dense layout (one bulk copy per chunk); a padded stride (A row
+// stride = 8 mod 16 words for D, 4 mod 8 16-byte units for Z) makes the
+// fragment loads (4 rows x 8 consecutive elements) hit the minimum number of
+// smem wavefronts; the producer then issues one bulk copy per row.
+template <int M_, int N_, bool Z_, int WM_, int WN_, int NW_, int R_, int AP_ = M_, int BP_ = N_>
 struct TsmttsmMmaCfg {
-  static constexpr int M = M_, N = N_, WM = WM_, WN = WN_, NW = NW_, R = R_;
+  static constexpr int M = M_, N = N_, WM = WM_, WN = WN_, NW = NW_, R = R_, AP = AP_, BP = BP_;
   static constexpr bool Z = Z_;
   static constexpr int S = Z ? 2 : 1;
   static constexpr int MB = (M + 7) / 8, NB = (N + 7) / 8;      // 8x8 blocks of C
@@ -454,17 +459,19 @@ struct TsmttsmMmaCfg {
   static constexpr int RS = NW / WT;                            // row slots (k-step groups)
   static constexpr int NT = (NW + 1) * 32;                      // + producer warp
   static constexpr int CELLS = M * N * S;
-  static constexpr int STAGE_DOUBLES = R * (M + N) * S;
+  static constexpr int STAGE_DOUBLES = R * (AP + BP) * S;
   static_assert(NW % WT == 0 && RS >= 1, "consumer warps must be a multiple of the warp tiles");
   static_assert(R % 4 == 0, "R must be a multiple of the k-step (4 rows)");
   static_assert(WM <= MB && WN <= NB, "warp tile larger than C");
+  static_assert(AP == M || ((AP * S) % 2 == 0 && (M * S) % 2 == 0), "padded A rows: 16-byte rows");
+  static_assert(BP == N || ((BP * S) % 2 == 0 && (N * S) % 2 == 0), "padded B rows: 16-byte rows");
 };
 
 template <class Cfg>
 __global__ void __launch_bounds__(Cfg::NT) tsmttsm_mma_kernel(const TsmttsmArgs p) {
   constexpr int M = Cfg::M, N = Cfg::N, S = Cfg::S, R = Cfg::R, NW = Cfg::NW;
   constexpr int WM = Cfg::WM, WN = Cfg::WN, WTM = Cfg::WTM, MB = Cfg::MB, NB = Cfg::NB;
-  constexpr int WT = Cfg::WT, RS = Cfg::RS, CELLS = Cfg::CELLS;
+  constexpr int WT = Cfg::WT, RS = Cfg::RS, CELLS = Cfg::CELLS, AP = Cfg::AP, BP = Cfg::BP;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   u64* full = reinterpret_cast<u64*>(smem_raw);
   u64* empty = full + 16;
@@ -501,20 +508,22 @@ __global__ void __launch_bounds__(Cfg::NT) tsmttsm_mma_kernel(const TsmttsmArgs 
   const int wt = warp % WT;
   const int wm = wt % WTM, wn = wt / WTM;
 
-  // one k-step: rows k0..k0+3 of the stage (or of global memory for the tail)
-  auto kstep = [&](const double* __restrict__ sA, const double* __restrict__ sB, int k0, int rows) {
+  // one k-step: rows k0..k0+3 of the stage (row strides ap, bp elements), or
+  // of global memory for the odd tail row (strides M, N)
+  auto kstep = [&](const double* __restrict__ sA, const double* __restrict__ sB, int k0, int rows,
+                   int ap, int bp) {
     const bool rv = (k0 + q) < rows;
     if constexpr (!Cfg::Z) {
       double a[WM], b[WN];
 #pragma unroll
       for (int i = 0; i < WM; i++) {
         const int m = (wm * WM + i) * 8 + g;
-        a[i] = (rv && m < M) ? sA[(k0 + q) * M + m] : 0.0;
+        a[i] = (rv && m < M) ? sA[(k0 + q) * ap + m] : 0.0;
       }
 #pragma unroll
       for (int j = 0; j < WN; j++) {
         const int n = (wn * WN + j) * 8 + g;
-        b[j] = (rv && n < N) ? sB[(k0 + q) * N + n] : 0.0;
+        b[j] = (rv && n < N) ? sB[(k0 + q) * bp + n] : 0.0;
       }
 #pragma unroll
       for (int i = 0; i < WM; i++)
@@ -528,12 +537,12 @@ __global__ void __launch_bounds__(Cfg::NT) tsmttsm_mma_kernel(const TsmttsmArgs 
 #pragma unroll
       for (int i = 0; i < WM; i++) {
         const int m = (wm * WM + i) * 8 + g;
-        a[i] = (rv && m < M) ? sA2[(k0 + q) * M + m] : make_double2(0.0, 0.0);
+        a[i] = (rv && m < M) ? sA2[(k0 + q) * ap + m] : make_double2(0.0, 0.0);
       }
 #pragma unroll
       for (int j = 0; j < WN; j++) {
         const int n = (wn * WN + j) * 8 + g;
-        b[j] = (rv && n < N) ? sB2[(k0 + q) * N + n] : make_double2(0.0, 0.0);
+        b[j] = (rv && n < N) ? sB2[(k0 + q) * bp + n] : make_double2(0.0, 0.0);
       }
 #pragma unroll
       for (int i = 0; i < WM; i++) {
@@ -552,21 +561,29 @@ __global__ void __launch_bounds__(Cfg::NT) tsmttsm_mma_kernel(const TsmttsmArgs 
 
   if (warp == NW) {
     // ---------------- producer warp: bulk copies into the ring ----------------
-    if (lane == 0) {
-      const u64 pol = policy_evict_first();
-      int it = 0;
-      for (long long c = blockIdx.x; c < p.nchunks; c += G, it++) {
-        const int s = it % stages;
-        if (it >= stages) mbar_wait(&empty[s], static_cast<u32>(((it / stages) - 1) & 1));
-        const long long r0 = c * R;
-        const long long rows = (K_even - r0 < R) ? (K_even - r0) : R;
-        const u32 ba = static_cast<u32>(rows * M * S * 8);
-        const u32 bb = static_cast<u32>(rows * N * S * 8);
-        double* dA = ring + static_cast<long long>(s) * Cfg::STAGE_DOUBLES;
-        double* dB = dA + R * M * S;
-        mbar_arrive_expect_tx(&full[s], ba + bb);
-        bulk_g2s(dA, p.A + r0 * M * S, ba, &full[s], pol);
-        bulk_g2s(dB, p.B + r0 * N * S, bb, &full[s], pol);
+    const u64 pol = policy_evict_first();
+    int it = 0;
+    for (long long c = blockIdx.x; c < p.nchunks; c += G, it++) {
+      const int s = it % stages;
+      if (it >= stages && lane == 0) mbar_wait(&empty[s], static_cast<u32>(((it / stages) - 1) & 1));
+      __syncwarp();
+      const long long r0 = c * R;
+      const int rows = static_cast<int>((K_even - r0 < R) ? (K_even - r0) : R);
+      double* dA = ring + static_cast<long long>(s) * Cfg::STAGE_DOUBLES;
+      double* dB = dA + R * AP * S;
+      if (lane == 0) mbar_arrive_expect_tx(&full[s], static_cast<u32>(rows * (M + N) * S * 8));
+      __syncwarp();
+      if constexpr (AP == M) {
+        if (lane == 0) bulk_g2s(dA, p.A + r0 * M * S, static_cast<u32>(rows * M * S * 8), &full[s], pol);
+      } else {
+        for (int r = lane; r < rows; r += 32)
+          bulk_g2s(dA + r * AP * S, p.A + (r0 + r) * M * S, static_cast<u32>(M * S * 8), &full[s], pol);
+      }
+      if constexpr (BP == N) {
+        if (lane == 0) bulk_g2s(dB, p.B + r0 * N * S, static_cast<u32>(rows * N * S * 8), &full[s], pol);
+      } else {
+        for (int r = lane; r < rows; r += 32)
+          bulk_g2s(dB + r * BP * S, p.B + (r0 + r) * N * S, static_cast<u32>(N * S * 8), &full[s], pol);
       }
     }
   } else {
@@ -576,21 +593,21 @@ __global__ void __launch_bounds__(Cfg::NT) tsmttsm_mma_kernel(const TsmttsmArgs 
       const int s = it % stages;
       mbar_wait(&full[s], static_cast<u32>((it / stages) & 1));
       const double* sA = ring + static_cast<long long>(s) * Cfg::STAGE_DOUBLES;
-      const double* sB = sA + R * M * S;
+      const double* sB = sA + R * AP * S;
       const long long r0 = c * R;
       const int rows = static_cast<int>((K_even - r0 < R) ? (K_even - r0) : R);
       if (rows == R) {
 #pragma unroll 2
-        for (int k0 = slot * 4; k0 < R; k0 += RS * 4) kstep(sA, sB, k0, R);
+        for (int k0 = slot * 4; k0 < R; k0 += RS * 4) kstep(sA, sB, k0, R, AP, BP);
       } else {
-        for (int k0 = slot * 4; k0 < rows; k0 += RS * 4) kstep(sA, sB, k0, rows);
+        for (int k0 = slot * 4; k0 < rows; k0 += RS * 4) kstep(sA, sB, k0, rows, AP, BP);
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
     }
     // odd last row: a k-step whose rows 1..3 are zero, from global memory
     if ((K & 1) && blockIdx.x == 0 && slot == 0)
-      kstep(p.A + (K - 1) * M * S, p.B + (K - 1) * N * S, 0, 1);
+      kstep(p.A + (K - 1) * M * S, p.B + (K - 1) * N * S, 0, 1, M, N);
   }
   __syncthreads();  // ring idle: every issued chunk was consumed
 
@@ -828,6 +845,232 @@ __global__ void __launch_bounds__(Cfg::NT) tsmm_kernel(const TsmmArgs p) {
     }
   }
   if (tid == 0) bulk_wait_all();
+}
+
+// ==========================================================================
+// TSMM on the FP64 tensor pipe (DMMA.8x8x4)
+// ==========================================================================
+// B rows are computed as (8 rows x 8 n) blocks: B_blk += A_blk (8 rows x 4 m)
+// * C_blk (4 m x 8 n), mma.sync m8n8k4 .row.col:
+//   MMA-A  lane holds A[r0+g][m0+q]      (from the A stage, row stride AP)
+//   MMA-B  lane holds C[m0+q][n0+g]      (from smem C, row stride NCP, zero padded)
+//   acc    lane holds B[r0+g][n0+2q+e]   (e = 0, 1)
+// Each consumer warp owns WR row blocks x all NB column blocks of a pass and
+// writes its own rows: registers -> per-warp smem staging -> cp.async.bulk
+// stores (one contiguous store, or one per row when the staging rows are
+// padded).  Row strides are chosen (tools/gen_instances.py) so fragment loads
+// and accumulator stores hit the minimum number of smem wavefronts; padded A
+// rows are filled by one cp.async.bulk per row from the producer warp.
+template <int M_, int N_, bool Z_, int WR_, int NW_, int R_, int AP_, int NOP_>
+struct TsmmMmaCfg {
+  static constexpr int M = M_, N = N_, WR = WR_, NW = NW_, R = R_, AP = AP_, NOP = NOP_;
+  static constexpr bool Z = Z_;
+  static constexpr int S = Z ? 2 : 1;
+  static constexpr int MK = (M + 3) / 4;  // k-steps over m
+  static constexpr int NB = (N + 7) / 8;  // 8-column blocks
+  // C row stride (elements): D = 8 mod 16 words, Z = 4 mod 8 16-byte units
+  static constexpr int NCP = Z ? (8 * NB + 4) : ((8 * NB) % 16 == 8 ? 8 * NB : 8 * NB + 8);
+  static constexpr int RW = 8 * WR;        // rows per warp per pass
+  static constexpr int RPP = RW * NW;      // rows per pass
+  static constexpr int NT = (NW + 1) * 32;
+  static constexpr bool CREG = MK * NB * S <= 32;  // C fragments held in registers
+  static constexpr int C_DOUBLES = MK * 4 * NCP * S;
+  static constexpr int OUT_DOUBLES = RW * NOP * S;  // per warp
+  static constexpr int STAGE_DOUBLES = R * AP * S;
+  static_assert(R % RPP == 0 && R % 2 == 0, "R must be a multiple of the rows per pass");
+  static_assert(AP >= M && NOP >= N, "strides must cover the rows");
+  static_assert(AP == M || ((AP * S) % 2 == 0 && (M * S) % 2 == 0),
+                "padded A rows: 16-byte aligned rows of 16-byte multiple size");
+  static_assert(NOP == N || ((NOP * S) % 2 == 0 && (N * S) % 2 == 0),
+                "padded output rows: 16-byte aligned rows of 16-byte multiple size");
+};
+
+template <class Cfg>
+__global__ void __launch_bounds__(Cfg::NT) tsmm_mma_kernel(const TsmmArgs p) {
+  constexpr int M = Cfg::M, N = Cfg::N, S = Cfg::S, R = Cfg::R, NW = Cfg::NW, WR = Cfg::WR;
+  constexpr int AP = Cfg::AP, NOP = Cfg::NOP, MK = Cfg::MK, NB = Cfg::NB, NCP = Cfg::NCP;
+  constexpr int RW = Cfg::RW, RPP = Cfg::RPP;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  u64* full = reinterpret_cast<u64*>(smem_raw);
+  u64* empty = full + 16;
+  double* sC = reinterpret_cast<double*>(smem_raw + 256);
+  double* sOut = sC + ((Cfg::C_DOUBLES + 15) / 16) * 16;
+  double* ring = sOut + ((NW * Cfg::OUT_DOUBLES + 15) / 16) * 16;
+
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, q = lane & 3;
+  const long long K = p.K;
+  const long long K_even = K & ~1LL;
+  const int G = gridDim.x;
+  const int stages = p.stages;
+
+  if (tid == 0) {
+    for (int s = 0; s < stages; s++) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NW);
+    }
+    fence_mbar_init();
+    fence_proxy_async_smem();
+  }
+  // S1: C -> smem once, zero padded to MK*4 rows x NCP columns
+  for (int i = tid; i < MK * 4 * NCP; i += Cfg::NT) {
+    const int m = i / NCP, n = i % NCP;
+#pragma unroll
+    for (int z = 0; z < S; z++) sC[i * S + z] = (m < M && n < N) ? __ldg(&p.C[(m * N + n) * S + z]) : 0.0;
+  }
+  __syncthreads();
+
+  if (warp == NW) {
+    // ---------------- producer warp ----------------
+    const u64 pol = policy_evict_first();
+    int it = 0;
+    for (long long c = blockIdx.x; c < p.nchunks; c += G, it++) {
+      const int s = it % stages;
+      if (it >= stages && lane == 0) mbar_wait(&empty[s], static_cast<u32>(((it / stages) - 1) & 1));
+      __syncwarp();
+      const long long r0 = c * R;
+      const int rows = static_cast<int>((K_even - r0 < R) ? (K_even - r0) : R);
+      double* dA = ring + static_cast<long long>(s) * Cfg::STAGE_DOUBLES;
+      if (lane == 0) mbar_arrive_expect_tx(&full[s], static_cast<u32>(rows * M * S * 8));
+      __syncwarp();
+      if constexpr (AP == M) {
+        if (lane == 0) bulk_g2s(dA, p.A + r0 * M * S, static_cast<u32>(rows * M * S * 8), &full[s], pol);
+      } else {
+        for (int r = lane; r < rows; r += 32)
+          bulk_g2s(dA + r * AP * S, p.A + (r0 + r) * M * S, static_cast<u32>(M * S * 8), &full[s], pol);
+      }
+    }
+  } else {
+    // ---------------- consumer warps ----------------
+    double* stg = sOut + warp * Cfg::OUT_DOUBLES;
+    // C fragments (MMA-B): lane holds C[4ks+q][8j+g]
+    double creg[Cfg::CREG ? MK : 1][Cfg::CREG ? NB : 1][S];
+    if constexpr (Cfg::CREG) {
+#pragma unroll
+      for (int ks = 0; ks < MK; ks++)
+#pragma unroll
+        for (int j = 0; j < NB; j++)
+#pragma unroll
+          for (int z = 0; z < S; z++) creg[ks][j][z] = sC[((4 * ks + q) * NCP + 8 * j + g) * S + z];
+    }
+    int it = 0;
+    for (long long c = blockIdx.x; c < p.nchunks; c += G, it++) {
+      const int s = it % stages;
+      mbar_wait(&full[s], static_cast<u32>((it / stages) & 1));
+      const double* sA = ring + static_cast<long long>(s) * Cfg::STAGE_DOUBLES;
+      const long long r0 = c * R;
+      const int rows = static_cast<int>((K_even - r0 < R) ? (K_even - r0) : R);
+#pragma unroll 1
+      for (int pr = 0; pr < rows; pr += RPP) {
+        const int wr0 = pr + warp * RW;
+        if (wr0 >= rows) break;
+        double acc[WR][NB][S][2];
+#pragma unroll
+        for (int i = 0; i < WR; i++)
+#pragma unroll
+          for (int j = 0; j < NB; j++)
+#pragma unroll
+            for (int z = 0; z < S; z++) acc[i][j][z][0] = acc[i][j][z][1] = 0.0;
+#pragma unroll
+        for (int ks = 0; ks < MK; ks++) {
+          const int m = 4 * ks + q;
+          const bool mv = (4 * ks + 4 <= M) || (m < M);
+          double a[WR][S];
+#pragma unroll
+          for (int i = 0; i < WR; i++) {
+            const int r = wr0 + 8 * i + g;
+#pragma unroll
+            for (int z = 0; z < S; z++) a[i][z] = mv ? sA[(r * AP + m) * S + z] : 0.0;
+          }
+          double cf[NB][S];
+#pragma unroll
+          for (int j = 0; j < NB; j++)
+#pragma unroll
+            for (int z = 0; z < S; z++) {
+              if constexpr (Cfg::CREG)
+                cf[j][z] = creg[ks][j][z];
+              else
+                cf[j][z] = sC[((4 * ks + q) * NCP + 8 * j + g) * S + z];
+            }
+#pragma unroll
+          for (int i = 0; i < WR; i++) {
+            if constexpr (!Cfg::Z) {
+#pragma unroll
+              for (int j = 0; j < NB; j++) dmma(acc[i][j][0][0], acc[i][j][0][1], a[i][0], cf[j][0]);
+            } else {
+              const double nai = -a[i][1];
+#pragma unroll
+              for (int j = 0; j < NB; j++) {
+                dmma(acc[i][j][0][0], acc[i][j][0][1], a[i][0], cf[j][0]);  // re += ar cr
+                dmma(acc[i][j][0][0], acc[i][j][0][1], nai, cf[j][1]);      // re -= ai ci
+                dmma(acc[i][j][1][0], acc[i][j][1][1], a[i][0], cf[j][1]);  // im += ar ci
+                dmma(acc[i][j][1][0], acc[i][j][1][1], a[i][1], cf[j][0]);  // im += ai cr
+              }
+            }
+          }
+        }
+        // S4: registers -> staging (after this warp's previous stores read it)
+        bulk_wait_read<0>();
+        __syncwarp();
+#pragma unroll
+        for (int i = 0; i < WR; i++)
+#pragma unroll
+          for (int j = 0; j < NB; j++) {
+            const int n = 8 * j + 2 * q;
+            if constexpr (!Cfg::Z && NOP % 2 == 0) {
+              // 16-byte store; NOP = 2 mod 4 keeps a warp's stores conflict-free
+              double* dst = stg + (8 * i + g) * NOP + n;
+              if (n + 1 < N)
+                *reinterpret_cast<double2*>(dst) = make_double2(acc[i][j][0][0], acc[i][j][0][1]);
+              else if (n < N)
+                dst[0] = acc[i][j][0][0];
+            } else {
+#pragma unroll
+              for (int e = 0; e < 2; e++) {
+                if (n + e < N) {
+#pragma unroll
+                  for (int z = 0; z < S; z++) stg[((8 * i + g) * NOP + n + e) * S + z] = acc[i][j][z][e];
+                }
+              }
+            }
+          }
+        fence_proxy_async_smem();
+        __syncwarp();
+        const int nr = (rows - wr0 < RW) ? rows - wr0 : RW;
+        if constexpr (NOP == N) {
+          if (lane == 0) {
+            bulk_s2g(p.B + (r0 + wr0) * N * S, stg, static_cast<u32>(nr * N * S * 8));
+            bulk_commit();
+          }
+        } else {
+          for (int r = lane; r < nr; r += 32)
+            bulk_s2g(p.B + (r0 + wr0 + r) * N * S, stg + r * NOP * S, static_cast<u32>(N * S * 8));
+          bulk_commit();
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+    }
+    // Odd last row (K odd): warp 0 of block 0, plain fma from global A, smem C.
+    if ((K & 1) && blockIdx.x == 0 && warp == 0) {
+      const double* a = p.A + (K - 1) * M * S;
+      for (int n = lane; n < N; n += 32) {
+        if constexpr (!Cfg::Z) {
+          double s0 = 0.0;
+          for (int m = 0; m < M; m++) s0 = fma(a[m], sC[m * NCP + n], s0);
+          p.B[(K - 1) * N + n] = s0;
+        } else {
+          double re = 0.0, im = 0.0;
+          for (int m = 0; m < M; m++)
+            zfma(re, im, a[2 * m], a[2 * m + 1], sC[2 * (m * NCP + n)], sC[2 * (m * NCP + n) + 1]);
+          p.B[2 * ((K - 1) * N + n)] = re;
+          p.B[2 * ((K - 1) * N + n) + 1] = im;
+        }
+      }
+    }
+    bulk_wait_all();
+  }
 }
 
 }  // namespace tsm

@@ -14,7 +14,7 @@ struct KernelEntry {
   int NT;            // threads per block
   int R;             // rows per chunk
   // tile description (TSMTTSM: MT, NTL; TSMM: NTL, MSPLIT, U)
-  int p0, p1, p2;
+  int p0, p1, p2, p3;  // DMMA TSMTTSM: WM, WN, AP, BP; DMMA TSMM: WR, AP, NOP, -
   int stages;        // default pipeline depth
   int ctas_per_sm;   // target resident CTAs per SM (clipped by occupancy)
   int impl;          // 0 = register-tile DFMA kernel, 1 = DMMA (mma.sync m8n8k4 f64) kernel

@@ -1,0 +1,86 @@
+"""Host-side checks of the kernel configuration space (-m "not gpu").
+
+* every default configuration (all 16384 (op, dtype, M, N)) and every
+  autotuning candidate passes libtsm's own validation (tsm_plan_create_config
+  validates before touching CUDA: valid -> TSM_ERR_CUDA on this GPU-less box,
+  invalid -> TSM_ERR_INVALID_VALUE);
+* the smem bank-conflict model used to pick padded strides reproduces the
+  textbook cases (dense 8x8 fp64 fragment rows with stride 0 mod 16 words are
+  4-way conflicted; stride 8 mod 16 is conflict-free).
+"""
+import ctypes
+import os
+import sys
+
+import pytest
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, os.path.join(ROOT, "tools"))
+
+import gen_instances as gi  # noqa: E402
+
+pytestmark = pytest.mark.skipif(torch.cuda.is_available(), reason="validation-only checks need a GPU-less box")
+
+
+@pytest.fixture(scope="module")
+def tsm():
+    from paper_1905_03136_b200 import binding
+    return binding
+
+
+def _status(tsm, op, dt, M, N, cfgd):
+    h = ctypes.c_void_p()
+    c = tsm.TsmConfig(**cfgd)
+    return tsm.lib.tsm_plan_create_config(ctypes.byref(h), tsm.OP[op], tsm.DTYPE[dt], M, N, 0,
+                                          ctypes.byref(c))
+
+
+def test_default_configs_valid(tsm):
+    bad = []
+    tune = gi.load_tune()
+    for op in ("tsmttsm", "tsmm"):
+        for dt in ("d", "z"):
+            for M in range(1, 65):
+                for N in range(1, 65):
+                    c = gi.resolve(op, M, N, dt == "z", tune.get(f"{op}_{dt}_{M}_{N}", {}).get("cfg"))
+                    st = _status(tsm, op, dt, M, N, gi.to_tsm_config(op, c, c["stages"], c["ctas"]))
+                    if st != 5:
+                        bad.append((op, dt, M, N, st, tsm.lib.tsm_last_error_detail()))
+    assert not bad, bad[:5]
+
+
+@pytest.mark.parametrize("shape", [(1, 1), (3, 5), (8, 8), (17, 33), (32, 32), (48, 16), (64, 64), (64, 1), (1, 64)])
+def test_candidates_valid(tsm, shape):
+    M, N = shape
+    for op in ("tsmttsm", "tsmm"):
+        for dt in ("d", "z"):
+            cands = gi.candidates(op, M, N, dt == "z")
+            assert cands, (op, dt, shape)
+            for c in cands:
+                st = _status(tsm, op, dt, M, N, gi.to_tsm_config(op, c, 3, 2))
+                assert st == 5, (op, dt, shape, c, tsm.lib.tsm_last_error_detail())
+
+
+def test_invalid_config_rejected_before_cuda(tsm):
+    good = gi.to_tsm_config("tsmttsm", gi.tsmttsm_mma_default(64, 64, False), 3, 1)
+    assert _status(tsm, "tsmttsm", "d", 64, 64, good) == 5
+    for k, v in [("rows_per_chunk", 30), ("threads", 100), ("p2", 63), ("kernel", 3)]:
+        bad = dict(good, **{k: v})
+        assert _status(tsm, "tsmttsm", "d", 64, 64, bad) == 1, k
+    # odd-width D rows cannot be padded (not 16-byte multiples)
+    assert _status(tsm, "tsmttsm", "d", 63, 64, dict(good, p2=66)) == 1
+
+
+def test_conflict_model_pins():
+    # TSMTTSM fragment (4 rows x 8 consecutive doubles): stride 64 words -> 4-way
+    assert gi._degree(64, False, "t") == 2.0  # 4 wavefronts vs the 2-wavefront minimum
+    assert gi._degree(72, False, "t") == 1.0  # stride 8 mod 16: minimum
+    assert gi.pick_stride(64, False, "t") in (72, 66, 68, 70) and gi._degree(gi.pick_stride(64, False, "t"), False, "t") == 1.0
+    # complex: 4 rows x 8 consecutive 16-byte elements always use every bank 4x
+    assert gi._degree(64, True, "t") == 1.0
+    # TSMM A fragment (8 rows x 4 consecutive): stride 0 mod 16 words -> 8 rows on 4 words
+    assert gi._degree(64, False, "a") == 4.0
+    assert gi._degree(gi.pick_stride(64, False, "a"), False, "a") == 1.0
+    # odd widths stay dense (rows are not 16-byte multiples)
+    assert gi.pick_stride(63, False, "a") == 63 and gi.pick_stride(33, False, "t") == 33

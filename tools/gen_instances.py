@@ -111,7 +111,8 @@ def tsmttsm_mma_default(M: int, N: int, z: bool) -> dict:
     row_bytes = (M + N) * 8 * S
     step = 4 * RS
     R = max(step, (24576 // row_bytes) // step * step)
-    return dict(MT=WM, NTL=WN, NT=(NW + 1) * 32, R=R, stages=4, ctas=2, impl=1)
+    return dict(MT=WM, NTL=WN, NT=(NW + 1) * 32, R=R, stages=4, ctas=2, impl=1,
+                AP=pick_stride(M, z, "t"), BP=pick_stride(N, z, "t"))
 
 
 def tsmttsm_pick(M: int, N: int, z: bool) -> dict:
@@ -157,6 +158,12 @@ def tsmm_default(M: int, N: int, z: bool) -> dict:
     return dict(NTL=NTL, MSPLIT=MSPLIT, U=U, NT=NT, R=R, stages=4, ctas=4, impl=0)
 
 
+def _tsmm_p(c: dict) -> tuple:
+    if c.get("impl", 0) == 1:
+        return (c["WR"], c["AP"], c["NOP"])
+    return (c["NTL"], c["MSPLIT"], c["U"])
+
+
 def load_tune() -> dict:
     if os.path.exists(TUNE):
         with open(TUNE) as f:
@@ -171,18 +178,33 @@ def entries():
         for dt in ("d", "z"):
             for (M, N) in SHAPES:
                 key = f"{op}_{dt}_{M}_{N}"
-                cfg = (tsmttsm_pick if op == "tsmttsm" else tsmm_default)(M, N, dt == "z")
-                cfg.update(tune.get(key, {}).get("cfg", {}))
-                out.append((op, dt, M, N, cfg))
+                out.append((op, dt, M, N, resolve(op, M, N, dt == "z", tune.get(key, {}).get("cfg"))))
     return out
+
+
+def resolve(op: str, M: int, N: int, z: bool, tuned: dict | None) -> dict:
+    """Default config, overridden by a tuned one; DMMA TSMTTSM configs tuned
+    before padded strides existed get the conflict-free strides."""
+    cfg = (tsmttsm_pick if op == "tsmttsm" else tsmm_pick)(M, N, z)
+    if tuned:
+        if tuned.get("impl", 0) != cfg.get("impl", 0):
+            cfg = {k: v for k, v in cfg.items() if k in ("stages", "ctas")}
+        cfg.update(tuned)
+    if op == "tsmttsm" and cfg.get("impl", 0) == 1 and "AP" not in cfg:
+        cfg["AP"], cfg["BP"] = pick_stride(M, z, "t"), pick_stride(N, z, "t")
+    return cfg
 
 
 def cfg_type(op, dt, M, N, c) -> str:
     z = "true" if dt == "z" else "false"
     if op == "tsmttsm" and c.get("impl", 0) == 1:
-        return f"tsm::TsmttsmMmaCfg<{M}, {N}, {z}, {c['MT']}, {c['NTL']}, {c['NT'] // 32 - 1}, {c['R']}>"
+        return (f"tsm::TsmttsmMmaCfg<{M}, {N}, {z}, {c['MT']}, {c['NTL']}, {c['NT'] // 32 - 1}, "
+                f"{c['R']}, {c.get('AP', M)}, {c.get('BP', N)}>")
     if op == "tsmttsm":
         return f"tsm::TsmttsmCfg<{M}, {N}, {z}, {c['MT']}, {c['NTL']}, {c['NT']}, {c['R']}>"
+    if c.get("impl", 0) == 1:
+        return (f"tsm::TsmmMmaCfg<{M}, {N}, {z}, {c['WR']}, {c['NT'] // 32 - 1}, {c['R']}, "
+                f"{c['AP']}, {c['NOP']}>")
     return f"tsm::TsmmCfg<{M}, {N}, {z}, {c['NTL']}, {c['MSPLIT']}, {c['U']}, {c['NT']}, {c['R']}>"
 
 
@@ -191,14 +213,23 @@ def entry_init(op, dt, M, N, c) -> str:
     if op == "tsmttsm":
         kn = "tsmttsm_mma_kernel" if c.get("impl", 0) == 1 else "tsmttsm_kernel"
         fn = f"(const void*)&tsm::{kn}<{t}>"
-        p = (c["MT"], c["NTL"], 0)
         kind = "tsm::KIND_TSMTTSM"
     else:
-        fn = f"(const void*)&tsm::tsmm_kernel<{t}>"
-        p = (c["NTL"], c["MSPLIT"], c["U"])
+        kn = "tsmm_mma_kernel" if c.get("impl", 0) == 1 else "tsmm_kernel"
+        fn = f"(const void*)&tsm::{kn}<{t}>"
         kind = "tsm::KIND_TSMM"
+    p = params4(op, M, N, c)
     return (f"  {{{kind}, {1 if dt == 'z' else 0}, {M}, {N}, {fn}, {c['NT']}, {c['R']}, "
-            f"{p[0]}, {p[1]}, {p[2]}, {c['stages']}, {c['ctas']}, {c.get('impl', 0)}}},")
+            f"{p[0]}, {p[1]}, {p[2]}, {p[3]}, {c['stages']}, {c['ctas']}, {c.get('impl', 0)}}},")
+
+
+def params4(op: str, M: int, N: int, c: dict) -> tuple:
+    """(p0, p1, p2, p3) of the registry entry / tsm_config for a gen-style cfg."""
+    if op == "tsmttsm":
+        if c.get("impl", 0) == 1:
+            return (c["MT"], c["NTL"], c.get("AP", M), c.get("BP", N))
+        return (c["MT"], c["NTL"], 0, 0)
+    return _tsmm_p(c) + (0,)
 
 
 def main(per_file: int = 12) -> int:
@@ -251,11 +282,10 @@ def main(per_file: int = 12) -> int:
         for dt in ("d", "z"):
             for M in range(1, 65):
                 for N in range(1, 65):
-                    c = (tsmttsm_pick if op == "tsmttsm" else tsmm_default)(M, N, dt == "z")
-                    c.update(tune.get(f"{op}_{dt}_{M}_{N}", {}).get("cfg", {}))
-                    p = (c["MT"], c["NTL"], 0) if op == "tsmttsm" else (c["NTL"], c["MSPLIT"], c["U"])
+                    c = resolve(op, M, N, dt == "z", tune.get(f"{op}_{dt}_{M}_{N}", {}).get("cfg"))
+                    p = params4(op, M, N, c)
                     lines.append(f"  {{{0 if op == 'tsmttsm' else 1}, {1 if dt == 'z' else 0}, {M}, {N}, "
-                                 f"nullptr, {c['NT']}, {c['R']}, {p[0]}, {p[1]}, {p[2]}, "
+                                 f"nullptr, {c['NT']}, {c['R']}, {p[0]}, {p[1]}, {p[2]}, {p[3]}, "
                                  f"{c['stages']}, {c['ctas']}, {c.get('impl', 0)}}},")
     lines += ["};", "}  // namespace tsm", ""]
     _write(os.path.join(GEN, "params_gen.cpp"), "\n".join(lines))
@@ -338,7 +368,8 @@ def candidates(op: str, M: int, N: int, z: bool) -> list:
                         break
                     for tgt in (16384, 32768):
                         out.append(dict(MT=WM, NTL=WN, NT=(NW + 1) * 32,
-                                        R=_rows(4 * k, row, tgt), impl=1))
+                                        R=_rows(4 * k, row, tgt), impl=1,
+                                        AP=pick_stride(M, z, "t"), BP=pick_stride(N, z, "t")))
     else:
         acc_max = 16 if z else 32
         NTL = 1
@@ -361,6 +392,18 @@ def candidates(op: str, M: int, N: int, z: bool) -> list:
                         out.append(dict(NTL=NTL, MSPLIT=MS, U=U, NT=NT, R=R, impl=0))
                         break
                 MS *= 2
+    if op == "tsmm" and N >= 2:
+        d = tsmm_mma_default(M, N, z)
+        S_ = 2 if z else 1
+        NB = cdiv(N, 8)
+        for NW in (4, 8):
+            for WR in (1, 2, 4):
+                if WR * NB * 2 * S_ > 64:
+                    continue
+                rpp = 8 * WR * NW
+                for tgt in (12288, 24576):
+                    R = rpp * max(1, round(tgt / (rpp * d["AP"] * S_ * 8)))
+                    out.append(dict(WR=WR, AP=d["AP"], NOP=d["NOP"], NT=(NW + 1) * 32, R=R, impl=1))
     # dedupe
     seen, uniq = set(), []
     for c in out:
@@ -373,9 +416,72 @@ def candidates(op: str, M: int, N: int, z: bool) -> list:
 
 def to_tsm_config(op: str, c: dict, stages: int, ctas: int) -> dict:
     """gen-style cfg -> tsm_config field dict (include/libtsm.h)."""
-    if op == "tsmttsm":
-        p = (c["MT"], c["NTL"], 0)
+    if op == "tsmttsm" and c.get("impl", 0) == 1:
+        p = (c["MT"], c["NTL"], c["AP"], c["BP"])
+    elif op == "tsmttsm":
+        p = (c["MT"], c["NTL"], 0, 0)
     else:
-        p = (c["NTL"], c["MSPLIT"], c["U"])
-    return dict(threads=c["NT"], rows_per_chunk=c["R"], p0=p[0], p1=p[1], p2=p[2],
+        p = _tsmm_p(c) + (0,)
+    return dict(threads=c["NT"], rows_per_chunk=c["R"], p0=p[0], p1=p[1], p2=p[2], p3=p[3],
                 stages=stages, ctas_per_sm=ctas, kernel=c.get("impl", 0))
+
+
+# ---------------------------------------------------------------------------
+# DMMA TSMM (tsm_kernels.cuh TsmmMmaCfg): smem strides chosen so m8n8k4
+# fragment loads / accumulator stores use the minimum number of wavefronts.
+# ---------------------------------------------------------------------------
+def _degree(stride: int, z: bool, kind: str) -> float:
+    """Smem wavefronts per warp access / minimum, lanes (g = l/4, q = l%4)."""
+    counts = {}
+    for lane in range(32):
+        g, q = lane >> 2, lane & 3
+        if kind == "a":          # TSMM A fragment: element (row g, col q)
+            idx = g * stride + q
+        elif kind == "t":        # TSMTTSM A/B fragment: element (row q, col g)
+            idx = q * stride + g
+        elif z:                  # Z output: element (g, 2q) (e = 0 store)
+            idx = g * stride + 2 * q
+        elif stride % 2 == 0:    # D output, 16-byte store of (2q, 2q+1)
+            idx = (g * stride + 2 * q) // 2
+        else:                    # D output, 8-byte store
+            idx = g * stride + 2 * q
+        wide = z or (kind == "o" and stride % 2 == 0)
+        unit = idx % (8 if wide else 16)
+        counts[unit] = counts.get(unit, 0) + 1
+    minimum = 4 if (z or (kind == "o" and stride % 2 == 0)) else 2
+    return max(counts.values()) / minimum
+
+
+def pick_stride(w: int, z: bool, kind: str) -> int:
+    if (w * (2 if z else 1)) % 2:
+        return w  # odd-width D rows are not 16-byte multiples: dense, one bulk copy
+    best = None
+    for st in range(w, w + 9):
+        if st != w and ((st * (2 if z else 1)) % 2):
+            continue  # padded rows must stay 16-byte aligned (bulk copies)
+        key = (_degree(st, z, kind), st)
+        if best is None or key < best:
+            best = key
+    return best[1]
+
+
+def tsmm_mma_default(M: int, N: int, z: bool) -> dict:
+    S = 2 if z else 1
+    MK, NB = cdiv(M, 4), cdiv(N, 8)
+    AP, NOP = pick_stride(M, z, "a"), pick_stride(N, z, "o")
+    NCP = 8 * NB + 4 if z else (8 * NB if (8 * NB) % 16 == 8 else 8 * NB + 8)
+    wr0 = max(1, min(4, 16 // (NB * S)))
+    for NW in (8, 4):
+        for WR in sorted({wr0, max(1, wr0 // 2), 1}, reverse=True):
+            rpp = 8 * WR * NW
+            R = rpp * max(1, round(16384 / (rpp * AP * S * 8)))
+            smem = 256 + 8 * (MK * 4 * NCP * S + NW * 8 * WR * NOP * S + 3 * R * AP * S)
+            if smem <= 200 * 1024:
+                return dict(WR=WR, AP=AP, NOP=NOP, NT=(NW + 1) * 32, R=R, stages=4, ctas=2, impl=1)
+    return dict(WR=1, AP=AP, NOP=NOP, NT=160, R=32, stages=2, ctas=1, impl=1)
+
+
+def tsmm_pick(M: int, N: int, z: bool) -> dict:
+    if M * N >= 32 and N >= 4:
+        return tsmm_mma_default(M, N, z)
+    return tsmm_default(M, N, z)
