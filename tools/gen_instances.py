@@ -366,10 +366,13 @@ def candidates(op: str, M: int, N: int, z: bool) -> list:
                         continue
                     if NW > 16:
                         break
+                    pads = [False] + ([True] if min(M, N) * S * 8 >= 384 else [])
                     for tgt in (16384, 32768):
-                        out.append(dict(MT=WM, NTL=WN, NT=(NW + 1) * 32,
-                                        R=_rows(4 * k, row, tgt), impl=1,
-                                        AP=pick_stride(M, z, "t"), BP=pick_stride(N, z, "t")))
+                        for pad in pads:
+                            out.append(dict(MT=WM, NTL=WN, NT=(NW + 1) * 32,
+                                            R=_rows(4 * k, row, tgt), impl=1,
+                                            AP=pick_stride(M, z, "t", pad),
+                                            BP=pick_stride(N, z, "t", pad)))
     else:
         acc_max = 16 if z else 32
         NTL = 1
@@ -452,9 +455,14 @@ def _degree(stride: int, z: bool, kind: str) -> float:
     return max(counts.values()) / minimum
 
 
-def pick_stride(w: int, z: bool, kind: str) -> int:
-    if (w * (2 if z else 1)) % 2:
-        return w  # odd-width D rows are not 16-byte multiples: dense, one bulk copy
+def pick_stride(w: int, z: bool, kind: str, pad: bool = False) -> int:
+    """Conflict-minimising smem row stride for a width-w operand.  Padding
+    means one bulk copy per row, which the TMA engine cannot sustain for small
+    rows (r01 run 8: TSMTTSM D M=16 fell to 10 % of roofline), so the default
+    layout is dense (pad=False); padded strides are autotuning candidates for
+    wide rows only."""
+    if not pad or (w * (2 if z else 1)) % 2:
+        return w  # dense: one bulk copy per chunk (odd-width D rows cannot be padded)
     best = None
     for st in range(w, w + 9):
         if st != w and ((st * (2 if z else 1)) % 2):
