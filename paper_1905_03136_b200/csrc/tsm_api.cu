@@ -3,6 +3,8 @@
 // Host side of SURVEY.md §8(a) rows T0 / S0 ("plan / dispatch"): pick the
 // (M,N,type) instantiation and its launch parameters, validate, launch on the
 // caller's stream.  No device memory is allocated here; no host sync.
+#include <cuda.h>  // CUtensorMap types only (the encoder is resolved through the runtime)
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -58,6 +60,36 @@ tsm_status dev_info(int device, DevInfo* out) {
   return TSM_SUCCESS;
 }
 
+// ---- TMA tensor maps ----
+// cuTensorMapEncodeTiled is a driver entry point; resolving it through the
+// runtime (cudaGetDriverEntryPoint) keeps libtsm free of a libcuda link.
+static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+static std::once_flag g_encode_once;
+
+// 2-D map of a row-major rows x width (doubles) operand: 16-double (128-byte)
+// boxes of box_rows rows, 128-byte swizzle, zero fill past the last row.
+tsm_status make_tmap(TmaDesc* out, const void* base, long long rows, int width, int box_rows) {
+  std::call_once(g_encode_once, [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  });
+  if (!g_encode) return fail(TSM_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  static_assert(sizeof(TmaDesc) == sizeof(CUtensorMap), "TmaDesc must mirror CUtensorMap");
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(width), static_cast<cuuint64_t>(rows)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(width) * 8};
+  cuuint32_t box[2] = {16, static_cast<cuuint32_t>(box_rows)};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = g_encode(reinterpret_cast<CUtensorMap*>(out), CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2,
+                        const_cast<void*>(base), dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(TSM_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string(r) + ")");
+  return TSM_SUCCESS;
+}
+
 // RAII: make `device` current for the duration of a call.
 struct DeviceGuard {
   int prev = -1;
@@ -82,14 +114,25 @@ size_t smem_bytes(const KernelEntry& k, int stages) {
       long long need = std::max<long long>(stages * pstage, cells + k.NT);
       return static_cast<size_t>(256 + need * 8);
     }
+    if (k.impl == 2) {  // DMMA + TMA: 16-double boxes per row, ring aligned to 1024 bytes
+      const long long boxes = (k.M * S + 15) / 16 + (k.N * S + 15) / 16;
+      const long long tstage = static_cast<long long>(k.R) * boxes * 16;
+      long long need = std::max<long long>(stages * tstage, cells + k.NT);
+      return static_cast<size_t>(256 + 1024 + need * 8);
+    }
     long long need = std::max<long long>(stages * stage, std::max<long long>(cells, k.NT));
     return static_cast<size_t>(128 + need * 8);
   }
-  if (k.impl == 1) {  // DMMA TSMM: p0 = WR, p1 = AP, p2 = NOP (must match TsmmMmaCfg)
+  if (k.impl >= 1) {  // DMMA TSMM: p0 = WR, p1 = AP, p2 = NOP (must match TsmmMmaCfg)
     const long long MK = (k.M + 3) / 4, NB = (k.N + 7) / 8;
     const long long NCP = S == 2 ? 8 * NB + 4 : ((8 * NB) % 16 == 8 ? 8 * NB : 8 * NB + 8);
     const long long NW = k.NT / 32 - 1;
     const long long cd = ((MK * 4 * NCP * S + 15) / 16) * 16;
+    if (k.impl == 2) {  // TMA: swizzled boxes, staging and ring 1024-byte aligned
+      const long long od = NW * 8 * k.p0 * ((k.N * S + 15) / 16) * 16;
+      const long long ad = static_cast<long long>(k.R) * ((k.M * S + 15) / 16) * 16;
+      return static_cast<size_t>(256 + cd * 8 + 1024 + od * 8 + 1024 + stages * ad * 8);
+    }
     const long long od = ((NW * 8 * k.p0 * k.p2 * S + 15) / 16) * 16;
     return static_cast<size_t>(256 + (cd + od + stages * static_cast<long long>(k.R) * k.p1 * S) * 8);
   }
@@ -178,8 +221,28 @@ static tsm_status validate_config(const KernelEntry& e) {
   if (e.R < 2 || e.R % 2) return bad("rows_per_chunk must be even and >= 2");
   if (e.stages < 2 || e.stages > 16) return bad("stages must be in [2, 16]");
   if (e.ctas_per_sm < 1) return bad("ctas_per_sm must be >= 1");
-  if (e.impl != 0 && e.impl != 1) return bad("kernel must be 0 (DFMA tile) or 1 (DMMA)");
-  if (e.op == KIND_TSMTTSM && e.impl == 1) {
+  if (e.impl < 0 || e.impl > 2) return bad("kernel must be 0 (DFMA tile), 1 (DMMA) or 2 (DMMA + TMA)");
+  if (e.impl == 2 && e.op == KIND_TSMM) {
+    const int S = e.dt == TSM_Z ? 2 : 1;
+    if ((e.M * S) % 2 || (e.N * S) % 2 || e.M * S < 16 || e.N * S < 16)
+      return bad("kernel 2 needs 16-byte rows of >= 128 bytes (M*S, N*S even and >= 16)");
+    const int NW = e.NT / 32 - 1;
+    if (NW < 1) return bad("DMMA TSMM needs at least one consumer warp (threads >= 64)");
+    if (e.p0 < 1 || e.p0 > 8) return bad("WR (row blocks per warp) must be in [1, 8]");
+    if (e.R % 8 || e.R > 256 || e.R % (8 * e.p0 * NW))
+      return bad("kernel 2 needs rows_per_chunk <= 256, a multiple of 8*WR*consumer warps");
+  } else if (e.impl == 2) {
+    const int S = e.dt == TSM_Z ? 2 : 1;
+    if ((e.M * S) % 2 || (e.N * S) % 2 || e.M * S < 16 || e.N * S < 16)
+      return bad("kernel 2 needs 16-byte rows of >= 128 bytes (M*S, N*S even and >= 16)");
+    if (e.R % 8 || e.R > 256) return bad("kernel 2 needs rows_per_chunk a multiple of 8, <= 256");
+    const int MB = (e.M + 7) / 8, NB = (e.N + 7) / 8;
+    if (e.p0 < 1 || e.p1 < 1 || e.p0 > MB || e.p1 > NB) return bad("WM, WN must be in [1, ceil(M/8)], [1, ceil(N/8)]");
+    const int WT = ((MB + e.p0 - 1) / e.p0) * ((NB + e.p1 - 1) / e.p1);
+    const int NW = e.NT / 32 - 1;
+    if (NW < WT || NW % WT) return bad("threads/32 - 1 consumer warps must be a multiple of the warp tiles");
+    if (e.R % (4 * (NW / WT))) return bad("rows_per_chunk must be a multiple of 4 * row slots");
+  } else if (e.op == KIND_TSMTTSM && e.impl == 1) {
     const int MB = (e.M + 7) / 8, NB = (e.N + 7) / 8;
     if (e.p0 < 1 || e.p1 < 1 || e.p0 > MB || e.p1 > NB) return bad("WM, WN must be in [1, ceil(M/8)], [1, ceil(N/8)]");
     const int WT = ((MB + e.p0 - 1) / e.p0) * ((NB + e.p1 - 1) / e.p1);
@@ -295,7 +358,7 @@ tsm_status tsm_plan_create_config(tsm_plan* out, tsm_op op, tsm_dtype dtype, int
   e.p1 = cfg->p1;
   e.impl = cfg->kernel;
   e.p2 = (op == TSM_OP_TSMTTSM && e.impl == 0) ? 0 : cfg->p2;
-  e.p3 = (op == TSM_OP_TSMTTSM && e.impl == 1) ? cfg->p3 : 0;
+  e.p3 = (op == TSM_OP_TSMTTSM && e.impl >= 1) ? cfg->p3 : 0;
   e.stages = cfg->stages;
   e.ctas_per_sm = cfg->ctas_per_sm;
   tsm_status st = validate_config(e);
@@ -338,7 +401,10 @@ struct Geometry {
 Geometry geometry(const tsm_plan_s* p, long long K) {
   Geometry g;
   const long long K_even = K & ~1LL;
-  g.nchunks = (K_even + p->k->R - 1) / p->k->R;
+  // TMA kernels cover all K rows (the tensor copy zero-fills past K); the
+  // bulk-copy kernels cover the even part and treat an odd last row apart.
+  const long long Kc = p->k->impl == 2 ? K : K_even;
+  g.nchunks = (Kc + p->k->R - 1) / p->k->R;
   const long long gmax = static_cast<long long>(p->sms) * p->ctas_per_sm;
   g.grid = static_cast<int>(std::max<long long>(1, std::min(gmax, g.nchunks)));
   if (p->op == TSM_OP_TSMTTSM) {
@@ -402,6 +468,12 @@ tsm_status launch_tsmttsm(const tsm_plan_s* p, int dt, long long K, const void* 
   a.nchunks = g.nchunks;
   a.stages = p->stages;
   a.nfin = g.nfin;
+  if (p->k->impl == 2 && K > 0) {
+    const int S = dt == TSM_Z ? 2 : 1;
+    tsm_status st = make_tmap(&a.tmA, A, K, p->M * S, p->k->R);
+    if (st == TSM_SUCCESS) st = make_tmap(&a.tmB, B, K, p->N * S, p->k->R);
+    if (st != TSM_SUCCESS) return st;
+  }
   void* args[] = {&a};
   cudaError_t e = cudaLaunchKernel(p->k->func, dim3(g.grid), dim3(p->k->NT), args, p->smem,
                                    static_cast<cudaStream_t>(stream));
@@ -434,6 +506,12 @@ tsm_status launch_tsmm(const tsm_plan_s* p, int dt, long long K, const void* A, 
   a.K = K;
   a.nchunks = g.nchunks;
   a.stages = p->stages;
+  if (p->k->impl == 2) {
+    const int S = dt == TSM_Z ? 2 : 1;
+    tsm_status st = make_tmap(&a.tmA, A, K, p->M * S, p->k->R);
+    if (st == TSM_SUCCESS) st = make_tmap(&a.tmB, B, K, p->N * S, 8 * p->k->p0);
+    if (st != TSM_SUCCESS) return st;
+  }
   void* args[] = {&a};
   cudaError_t e = cudaLaunchKernel(p->k->func, dim3(g.grid), dim3(p->k->NT), args, p->smem,
                                    static_cast<cudaStream_t>(stream));
@@ -470,14 +548,15 @@ tsm_status tsm_plan_describe(tsm_plan p, int64_t K, char* buf, size_t len) {
   const Geometry g = geometry(p, K < 0 ? 0 : K);
   const KernelEntry* k = p->k;
   char tmp[512];
-  if (p->op == TSM_OP_TSMTTSM && k->impl == 1)
+  if (p->op == TSM_OP_TSMTTSM && k->impl >= 1)
     snprintf(tmp, sizeof tmp,
              "{\"op\":\"tsmttsm\",\"dtype\":\"%c\",\"M\":%d,\"N\":%d,\"WM\":%d,\"WN\":%d,"
              "\"AP\":%d,\"BP\":%d,\"threads\":%d,\"rows_per_chunk\":%d,\"stages\":%d,"
              "\"ctas_per_sm\":%d,\"smem\":%zu,\"grid\":%d,\"nchunks\":%lld,\"nfin\":%d,\"jit\":%s,"
-             "\"kernel\":\"dmma\"}",
+             "\"kernel\":\"%s\"}",
              p->dt ? 'z' : 'd', p->M, p->N, k->p0, k->p1, k->p2, k->p3, k->NT, k->R, p->stages,
-             p->ctas_per_sm, p->smem, g.grid, g.nchunks, g.nfin, p->jit ? "true" : "false");
+             p->ctas_per_sm, p->smem, g.grid, g.nchunks, g.nfin, p->jit ? "true" : "false",
+             k->impl == 2 ? "dmma+tma" : "dmma");
   else if (p->op == TSM_OP_TSMTTSM)
     snprintf(tmp, sizeof tmp,
              "{\"op\":\"tsmttsm\",\"dtype\":\"%c\",\"M\":%d,\"N\":%d,\"MT\":%d,\"NTL\":%d,"
@@ -494,7 +573,7 @@ tsm_status tsm_plan_describe(tsm_plan p, int64_t K, char* buf, size_t len) {
              "\"smem\":%zu,\"grid\":%d,\"nchunks\":%lld,\"jit\":%s,\"kernel\":\"%s\"}",
              p->dt ? 'z' : 'd', p->M, p->N, k->p0, k->p1, k->p2, k->NT, k->R, p->stages,
              p->ctas_per_sm, p->smem, g.grid, g.nchunks, p->jit ? "true" : "false",
-             k->impl ? "dmma(p0=WR,p1=AP,p2=NOP)" : "dfma");
+             k->impl == 2 ? "dmma+tma(p0=WR)" : (k->impl ? "dmma(p0=WR,p1=AP,p2=NOP)" : "dfma"));
   snprintf(buf, len, "%s", tmp);
   return TSM_SUCCESS;
 }

@@ -176,7 +176,7 @@ static tsm_status allreduce_impl(tsm_plan p, tsm_comm c, int dt, int64_t K, cons
   tsm_status st = tsm::launch_tsmttsm(p, dt, K, A, B, C, ws, ws_bytes - extra, stream, true);
   if (st != TSM_SUCCESS) return st;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  if (c->nranks == 1) return TSM_SUCCESS;
+  // (a 1-rank communicator still goes through NCCL: same code path at any size)
   if (c->flags & TSM_COMM_DETERMINISTIC) {
     // gather region: 256-byte aligned, after the local workspace
     size_t off = (local + 255) & ~static_cast<size_t>(255);
@@ -209,11 +209,9 @@ static tsm_status bcast_impl(tsm_plan p, tsm_comm c, int dt, int root, int64_t K
   if (tsm::plan_op(p) != TSM_OP_TSMM || tsm::plan_dt(p) != dt)
     return fail(TSM_ERR_INVALID_VALUE, "plan op/dtype does not match the call");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  if (c->nranks > 1) {
-    ncclResult_t r = g_nccl.Broadcast(C, C, static_cast<size_t>(tsm::plan_cells(p)), kNcclFloat64,
-                                      root, c->comm, s);
-    if (r != 0) return nccl_fail(r, "ncclBroadcast");
-  }
+  ncclResult_t r = g_nccl.Broadcast(C, C, static_cast<size_t>(tsm::plan_cells(p)), kNcclFloat64,
+                                    root, c->comm, s);
+  if (r != 0) return nccl_fail(r, "ncclBroadcast");
   return tsm::launch_tsmm(p, dt, K, A, C, B, stream, true);
 }
 

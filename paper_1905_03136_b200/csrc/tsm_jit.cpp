@@ -38,15 +38,17 @@ std::map<std::string, const KernelEntry*> g_jit_index;
 std::string cfg_type(const KernelEntry& e) {
   std::ostringstream os;
   const char* z = e.dt ? "true" : "false";
-  if (e.op == KIND_TSMTTSM && e.impl == 1)
+  if (e.op == KIND_TSMTTSM && e.impl >= 1)
     os << "tsm::TsmttsmMmaCfg<" << e.M << ", " << e.N << ", " << z << ", " << e.p0 << ", " << e.p1
-       << ", " << (e.NT / 32 - 1) << ", " << e.R << ", " << e.p2 << ", " << e.p3 << ">";
+       << ", " << (e.NT / 32 - 1) << ", " << e.R << ", " << e.p2 << ", " << e.p3 << ", "
+       << (e.impl == 2 ? "true" : "false") << ">";
   else if (e.op == KIND_TSMTTSM)
     os << "tsm::TsmttsmCfg<" << e.M << ", " << e.N << ", " << z << ", " << e.p0 << ", " << e.p1
        << ", " << e.NT << ", " << e.R << ">";
-  else if (e.impl == 1)
+  else if (e.impl >= 1)
     os << "tsm::TsmmMmaCfg<" << e.M << ", " << e.N << ", " << z << ", " << e.p0 << ", "
-       << (e.NT / 32 - 1) << ", " << e.R << ", " << e.p1 << ", " << e.p2 << ">";
+       << (e.NT / 32 - 1) << ", " << e.R << ", " << e.p1 << ", " << e.p2 << ", "
+       << (e.impl == 2 ? "true" : "false") << ">";
   else
     os << "tsm::TsmmCfg<" << e.M << ", " << e.N << ", " << z << ", " << e.p0 << ", " << e.p1
        << ", " << e.p2 << ", " << e.NT << ", " << e.R << ">";
@@ -54,8 +56,8 @@ std::string cfg_type(const KernelEntry& e) {
 }
 
 std::string kernel_name(const KernelEntry& e) {
-  const char* fn = e.op == KIND_TSMM ? (e.impl == 1 ? "tsm::tsmm_mma_kernel<" : "tsm::tsmm_kernel<")
-                   : (e.impl == 1 ? "tsm::tsmttsm_mma_kernel<" : "tsm::tsmttsm_kernel<");
+  const char* fn = e.op == KIND_TSMM ? (e.impl >= 1 ? "tsm::tsmm_mma_kernel<" : "tsm::tsmm_kernel<")
+                   : (e.impl >= 1 ? "tsm::tsmttsm_mma_kernel<" : "tsm::tsmttsm_kernel<");
   return std::string(fn) + cfg_type(e) + ">";
 }
 

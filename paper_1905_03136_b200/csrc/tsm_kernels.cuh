@@ -129,17 +129,49 @@ struct WsLayout {
   static constexpr int kCounterBytes = 256;  // u32 ticket, u32 done, padding
 };
 
+// --------------------------------------------------------------------------
+// TMA tensor copies (cp.async.bulk.tensor.2d, SASS UTMALDG / UTMASTG).
+// A row-major K x W (doubles) operand is described by a 2-D tensor map
+// (host: cuTensorMapEncodeTiled) with 16-double (128-byte) boxes of R rows and
+// the 128-byte swizzle: inside each 1024-byte atom the 16-byte chunk c of row
+// r lands at chunk c ^ (r & 7), so the column-wise fragment reads of the
+// DMMA kernels hit the minimum number of smem wavefronts.  Rows beyond K are
+// zero-filled by the TMA unit (no tail code).
+// --------------------------------------------------------------------------
+struct alignas(64) TmaDesc {
+  unsigned long long raw[16];  // CUtensorMap (opaque, 128 bytes)
+};
+__device__ __forceinline__ void tma_load_2d(void* dst, const TmaDesc* desc, int x, int y, u64* bar,
+                                            u64 policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(dst)),
+      "l"(desc), "r"(x), "r"(y), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ void tma_store_2d(const TmaDesc* desc, int x, int y, const void* src) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                   desc),
+               "r"(x), "r"(y), "r"(smem_u32(src))
+               : "memory");
+}
+// offset (doubles) of element (r, c), c < 16, inside a 128B-swizzled box region
+__device__ __forceinline__ int swz128(int r, int c) {
+  return r * 16 + ((((c >> 1) ^ r) & 7) << 1) + (c & 1);
+}
+
 // ==========================================================================
 // TSMTTSM
 // ==========================================================================
 struct TsmttsmArgs {
+  TmaDesc tmA, tmB;    // tensor maps (TMA kernels only)
   const double* A;     // K x M (x2 doubles for Z), row-major
   const double* B;     // K x N
   double* C;           // M x N
   double* partials;    // gridDim.x x (M*N*S) doubles
   u32* counters;       // [0] ticket, [1] done
   long long K;         // rows
-  long long nchunks;   // ceil(K_even / R)
+  long long nchunks;   // ceil(K_even / R)  (TMA kernels: ceil(K / R))
   int stages;          // smem ring depth
   int nfin;            // finisher blocks of the grid reduction
 };
@@ -448,11 +480,19 @@ __device__ __forceinline__ void mbar_arrive(u64* bar) {
 // stride = 8 mod 16 words for D, 4 mod 8 16-byte units for Z) makes the
 // fragment loads (4 rows x 8 consecutive elements) hit the minimum number of
 // smem wavefronts; the producer then issues one bulk copy per row.
-template <int M_, int N_, bool Z_, int WM_, int WN_, int NW_, int R_, int AP_ = M_, int BP_ = N_>
+// TMA = true: A and B arrive by 2-D tensor copies into 128B-swizzled boxes
+// (AP, BP ignored; requires M*S and N*S even and >= 16 doubles).
+template <int M_, int N_, bool Z_, int WM_, int WN_, int NW_, int R_, int AP_ = M_, int BP_ = N_,
+          bool TMA_ = false>
 struct TsmttsmMmaCfg {
-  static constexpr int M = M_, N = N_, WM = WM_, WN = WN_, NW = NW_, R = R_, AP = AP_, BP = BP_;
-  static constexpr bool Z = Z_;
+  static constexpr int M = M_, N = N_, WM = WM_, WN = WN_, NW = NW_, R = R_;
+  static constexpr bool Z = Z_, TMA = TMA_;
   static constexpr int S = Z ? 2 : 1;
+  static constexpr int NBA = (M * S + 15) / 16, NBB = (N * S + 15) / 16;  // 16-double boxes
+  static constexpr int AP = TMA ? NBA * 16 / S : AP_, BP = TMA ? NBB * 16 / S : BP_;
+  static_assert(!TMA || ((M * S) % 2 == 0 && (N * S) % 2 == 0 && M * S >= 16 && N * S >= 16),
+                "TMA tensor path: 16-byte rows of >= 128 bytes");
+  static_assert(!TMA || R % 8 == 0, "TMA swizzle atoms are 8 rows");
   static constexpr int MB = (M + 7) / 8, NB = (N + 7) / 8;      // 8x8 blocks of C
   static constexpr int WTM = (MB + WM - 1) / WM, WTN = (NB + WN - 1) / WN;
   static constexpr int WT = WTM * WTN;                          // warp tiles covering C
@@ -468,14 +508,17 @@ struct TsmttsmMmaCfg {
 };
 
 template <class Cfg>
-__global__ void __launch_bounds__(Cfg::NT) tsmttsm_mma_kernel(const TsmttsmArgs p) {
+__global__ void __launch_bounds__(Cfg::NT) tsmttsm_mma_kernel(const __grid_constant__ TsmttsmArgs p) {
   constexpr int M = Cfg::M, N = Cfg::N, S = Cfg::S, R = Cfg::R, NW = Cfg::NW;
   constexpr int WM = Cfg::WM, WN = Cfg::WN, WTM = Cfg::WTM, MB = Cfg::MB, NB = Cfg::NB;
   constexpr int WT = Cfg::WT, RS = Cfg::RS, CELLS = Cfg::CELLS, AP = Cfg::AP, BP = Cfg::BP;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   u64* full = reinterpret_cast<u64*>(smem_raw);
   u64* empty = full + 16;
-  double* ring = reinterpret_cast<double*>(smem_raw + 256);
+  // ring: 1024-byte aligned for the 128B-swizzle atoms of the TMA boxes
+  double* ring = reinterpret_cast<double*>(
+      Cfg::TMA ? ((reinterpret_cast<u64>(smem_raw) + 256 + 1023) & ~1023ull)
+               : reinterpret_cast<u64>(smem_raw) + 256);
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
@@ -508,8 +551,19 @@ __global__ void __launch_bounds__(Cfg::NT) tsmttsm_mma_kernel(const TsmttsmArgs 
   const int wt = warp % WT;
   const int wm = wt % WTM, wn = wt / WTM;
 
+  // offset (doubles) of element (row r, column x) of an operand of width W
+  // elements: dense row stride `st`, or the swizzled TMA boxes
+  auto off = [&](int r, int x, int st) -> int {
+    if constexpr (Cfg::TMA) {
+      const int c = x * S;  // first double of the element
+      return (c >> 4) * (R * 16) + swz128(r, c & 15);
+    } else {
+      return (r * st + x) * S;
+    }
+  };
+
   // one k-step: rows k0..k0+3 of the stage (row strides ap, bp elements), or
-  // of global memory for the odd tail row (strides M, N)
+  // of global memory for the odd tail row (strides M, N; non-TMA only)
   auto kstep = [&](const double* __restrict__ sA, const double* __restrict__ sB, int k0, int rows,
                    int ap, int bp) {
     const bool rv = (k0 + q) < rows;
@@ -518,12 +572,12 @@ __global__ void __launch_bounds__(Cfg::NT) tsmttsm_mma_kernel(const TsmttsmArgs 
 #pragma unroll
       for (int i = 0; i < WM; i++) {
         const int m = (wm * WM + i) * 8 + g;
-        a[i] = (rv && m < M) ? sA[(k0 + q) * ap + m] : 0.0;
+        a[i] = (rv && m < M) ? sA[off(k0 + q, m, ap)] : 0.0;
       }
 #pragma unroll
       for (int j = 0; j < WN; j++) {
         const int n = (wn * WN + j) * 8 + g;
-        b[j] = (rv && n < N) ? sB[(k0 + q) * bp + n] : 0.0;
+        b[j] = (rv && n < N) ? sB[off(k0 + q, n, bp)] : 0.0;
       }
 #pragma unroll
       for (int i = 0; i < WM; i++)
@@ -531,18 +585,18 @@ __global__ void __launch_bounds__(Cfg::NT) tsmttsm_mma_kernel(const TsmttsmArgs 
         for (int j = 0; j < WN; j++)
           if ((wm * WM + i) < MB && (wn * WN + j) < NB) dmma(acc[i][j][0][0], acc[i][j][0][1], a[i], b[j]);
     } else {
-      const double2* sA2 = reinterpret_cast<const double2*>(sA);
-      const double2* sB2 = reinterpret_cast<const double2*>(sB);
       double2 a[WM], b[WN];
 #pragma unroll
       for (int i = 0; i < WM; i++) {
         const int m = (wm * WM + i) * 8 + g;
-        a[i] = (rv && m < M) ? sA2[(k0 + q) * ap + m] : make_double2(0.0, 0.0);
+        a[i] = (rv && m < M) ? *reinterpret_cast<const double2*>(sA + off(k0 + q, m, ap))
+                             : make_double2(0.0, 0.0);
       }
 #pragma unroll
       for (int j = 0; j < WN; j++) {
         const int n = (wn * WN + j) * 8 + g;
-        b[j] = (rv && n < N) ? sB2[(k0 + q) * bp + n] : make_double2(0.0, 0.0);
+        b[j] = (rv && n < N) ? *reinterpret_cast<const double2*>(sB + off(k0 + q, n, bp))
+                             : make_double2(0.0, 0.0);
       }
 #pragma unroll
       for (int i = 0; i < WM; i++) {
@@ -560,7 +614,7 @@ __global__ void __launch_bounds__(Cfg::NT) tsmttsm_mma_kernel(const TsmttsmArgs 
   };
 
   if (warp == NW) {
-    // ---------------- producer warp: bulk copies into the ring ----------------
+    // ---------------- producer warp: bulk / tensor copies into the ring ----------------
     const u64 pol = policy_evict_first();
     int it = 0;
     for (long long c = blockIdx.x; c < p.nchunks; c += G, it++) {
@@ -568,22 +622,33 @@ __global__ void __launch_bounds__(Cfg::NT) tsmttsm_mma_kernel(const TsmttsmArgs 
       if (it >= stages && lane == 0) mbar_wait(&empty[s], static_cast<u32>(((it / stages) - 1) & 1));
       __syncwarp();
       const long long r0 = c * R;
-      const int rows = static_cast<int>((K_even - r0 < R) ? (K_even - r0) : R);
       double* dA = ring + static_cast<long long>(s) * Cfg::STAGE_DOUBLES;
       double* dB = dA + R * AP * S;
-      if (lane == 0) mbar_arrive_expect_tx(&full[s], static_cast<u32>(rows * (M + N) * S * 8));
-      __syncwarp();
-      if constexpr (AP == M) {
-        if (lane == 0) bulk_g2s(dA, p.A + r0 * M * S, static_cast<u32>(rows * M * S * 8), &full[s], pol);
+      if constexpr (Cfg::TMA) {
+        // whole boxes (rows past K are zero-filled and still counted)
+        if (lane == 0) {
+          mbar_arrive_expect_tx(&full[s], static_cast<u32>((Cfg::NBA + Cfg::NBB) * R * 128));
+          for (int b = 0; b < Cfg::NBA; b++)
+            tma_load_2d(dA + b * R * 16, &p.tmA, b * 16, static_cast<int>(r0), &full[s], pol);
+          for (int b = 0; b < Cfg::NBB; b++)
+            tma_load_2d(dB + b * R * 16, &p.tmB, b * 16, static_cast<int>(r0), &full[s], pol);
+        }
       } else {
-        for (int r = lane; r < rows; r += 32)
-          bulk_g2s(dA + r * AP * S, p.A + (r0 + r) * M * S, static_cast<u32>(M * S * 8), &full[s], pol);
-      }
-      if constexpr (BP == N) {
-        if (lane == 0) bulk_g2s(dB, p.B + r0 * N * S, static_cast<u32>(rows * N * S * 8), &full[s], pol);
-      } else {
-        for (int r = lane; r < rows; r += 32)
-          bulk_g2s(dB + r * BP * S, p.B + (r0 + r) * N * S, static_cast<u32>(N * S * 8), &full[s], pol);
+        const int rows = static_cast<int>((K_even - r0 < R) ? (K_even - r0) : R);
+        if (lane == 0) mbar_arrive_expect_tx(&full[s], static_cast<u32>(rows * (M + N) * S * 8));
+        __syncwarp();
+        if constexpr (AP == M) {
+          if (lane == 0) bulk_g2s(dA, p.A + r0 * M * S, static_cast<u32>(rows * M * S * 8), &full[s], pol);
+        } else {
+          for (int r = lane; r < rows; r += 32)
+            bulk_g2s(dA + r * AP * S, p.A + (r0 + r) * M * S, static_cast<u32>(M * S * 8), &full[s], pol);
+        }
+        if constexpr (BP == N) {
+          if (lane == 0) bulk_g2s(dB, p.B + r0 * N * S, static_cast<u32>(rows * N * S * 8), &full[s], pol);
+        } else {
+          for (int r = lane; r < rows; r += 32)
+            bulk_g2s(dB + r * BP * S, p.B + (r0 + r) * N * S, static_cast<u32>(N * S * 8), &full[s], pol);
+        }
       }
     }
   } else {
@@ -595,7 +660,7 @@ __global__ void __launch_bounds__(Cfg::NT) tsmttsm_mma_kernel(const TsmttsmArgs 
       const double* sA = ring + static_cast<long long>(s) * Cfg::STAGE_DOUBLES;
       const double* sB = sA + R * AP * S;
       const long long r0 = c * R;
-      const int rows = static_cast<int>((K_even - r0 < R) ? (K_even - r0) : R);
+      const int rows = Cfg::TMA ? R : static_cast<int>((K_even - r0 < R) ? (K_even - r0) : R);
       if (rows == R) {
 #pragma unroll 2
         for (int k0 = slot * 4; k0 < R; k0 += RS * 4) kstep(sA, sB, k0, R, AP, BP);
@@ -606,8 +671,10 @@ __global__ void __launch_bounds__(Cfg::NT) tsmttsm_mma_kernel(const TsmttsmArgs 
       if (lane == 0) mbar_arrive(&empty[s]);
     }
     // odd last row: a k-step whose rows 1..3 are zero, from global memory
-    if ((K & 1) && blockIdx.x == 0 && slot == 0)
-      kstep(p.A + (K - 1) * M * S, p.B + (K - 1) * N * S, 0, 1, M, N);
+    if constexpr (!Cfg::TMA) {
+      if ((K & 1) && blockIdx.x == 0 && slot == 0)
+        kstep(p.A + (K - 1) * M * S, p.B + (K - 1) * N * S, 0, 1, M, N);
+    }
   }
   __syncthreads();  // ring idle: every issued chunk was consumed
 
@@ -644,11 +711,12 @@ __global__ void __launch_bounds__(Cfg::NT) tsmttsm_mma_kernel(const TsmttsmArgs 
 // TSMM
 // ==========================================================================
 struct TsmmArgs {
+  TmaDesc tmA, tmB;   // tensor maps (TMA kernels only): A loads, B stores
   const double* A;    // K x M
   const double* C;    // M x N
   double* B;          // K x N
   long long K;
-  long long nchunks;  // ceil(K_even / R)
+  long long nchunks;  // ceil(K_even / R)  (TMA kernels: ceil(K / R))
   int stages;
 };
 
@@ -861,13 +929,21 @@ __global__ void __launch_bounds__(Cfg::NT) tsmm_kernel(const TsmmArgs p) {
 // padded).  Row strides are chosen (tools/gen_instances.py) so fragment loads
 // and accumulator stores hit the minimum number of smem wavefronts; padded A
 // rows are filled by one cp.async.bulk per row from the producer warp.
-template <int M_, int N_, bool Z_, int WR_, int NW_, int R_, int AP_, int NOP_>
+// TMA = true: A arrives by 2-D tensor copies into 128B-swizzled 16-double
+// boxes (conflict-free fragments, rows past K zero-filled) and every warp
+// writes its output rows into swizzled staging boxes that one TMA tensor store
+// per box moves to B (rows past K are clipped by the TMA unit).  AP / NOP are
+// ignored; requires M*S and N*S even and >= 16 doubles.
+template <int M_, int N_, bool Z_, int WR_, int NW_, int R_, int AP_, int NOP_, bool TMA_ = false>
 struct TsmmMmaCfg {
-  static constexpr int M = M_, N = N_, WR = WR_, NW = NW_, R = R_, AP = AP_, NOP = NOP_;
-  static constexpr bool Z = Z_;
+  static constexpr int M = M_, N = N_, WR = WR_, NW = NW_, R = R_;
+  static constexpr bool Z = Z_, TMA = TMA_;
   static constexpr int S = Z ? 2 : 1;
   static constexpr int MK = (M + 3) / 4;  // k-steps over m
   static constexpr int NB = (N + 7) / 8;  // 8-column blocks
+  static constexpr int NBA = (M * S + 15) / 16, NBO = (N * S + 15) / 16;  // TMA boxes per row
+  static constexpr int AP = TMA ? NBA * 16 / S : AP_;
+  static constexpr int NOP = TMA ? NBO * 16 / S : NOP_;
   // C row stride (elements): D = 8 mod 16 words, Z = 4 mod 8 16-byte units
   static constexpr int NCP = Z ? (8 * NB + 4) : ((8 * NB) % 16 == 8 ? 8 * NB : 8 * NB + 8);
   static constexpr int RW = 8 * WR;        // rows per warp per pass
@@ -883,10 +959,13 @@ struct TsmmMmaCfg {
                 "padded A rows: 16-byte aligned rows of 16-byte multiple size");
   static_assert(NOP == N || ((NOP * S) % 2 == 0 && (N * S) % 2 == 0),
                 "padded output rows: 16-byte aligned rows of 16-byte multiple size");
+  static_assert(!TMA || ((M * S) % 2 == 0 && (N * S) % 2 == 0 && M * S >= 16 && N * S >= 16),
+                "TMA tensor path: 16-byte rows of >= 128 bytes");
+  static_assert(!TMA || (R % 8 == 0 && R <= 256 && RW <= 256), "TMA box rows");
 };
 
 template <class Cfg>
-__global__ void __launch_bounds__(Cfg::NT) tsmm_mma_kernel(const TsmmArgs p) {
+__global__ void __launch_bounds__(Cfg::NT) tsmm_mma_kernel(const __grid_constant__ TsmmArgs p) {
   constexpr int M = Cfg::M, N = Cfg::N, S = Cfg::S, R = Cfg::R, NW = Cfg::NW, WR = Cfg::WR;
   constexpr int AP = Cfg::AP, NOP = Cfg::NOP, MK = Cfg::MK, NB = Cfg::NB, NCP = Cfg::NCP;
   constexpr int RW = Cfg::RW, RPP = Cfg::RPP;
@@ -894,14 +973,18 @@ __global__ void __launch_bounds__(Cfg::NT) tsmm_mma_kernel(const TsmmArgs p) {
   u64* full = reinterpret_cast<u64*>(smem_raw);
   u64* empty = full + 16;
   double* sC = reinterpret_cast<double*>(smem_raw + 256);
-  double* sOut = sC + ((Cfg::C_DOUBLES + 15) / 16) * 16;
-  double* ring = sOut + ((NW * Cfg::OUT_DOUBLES + 15) / 16) * 16;
+  // staging and ring start on 1024-byte boundaries (128B swizzle atoms)
+  const u64 after_c = reinterpret_cast<u64>(sC + ((Cfg::C_DOUBLES + 15) / 16) * 16);
+  double* sOut = reinterpret_cast<double*>(Cfg::TMA ? ((after_c + 1023) & ~1023ull) : after_c);
+  const u64 after_o = reinterpret_cast<u64>(sOut + ((NW * Cfg::OUT_DOUBLES + 15) / 16) * 16);
+  double* ring = reinterpret_cast<double*>(Cfg::TMA ? ((after_o + 1023) & ~1023ull) : after_o);
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, q = lane & 3;
   const long long K = p.K;
   const long long K_even = K & ~1LL;
+  const long long Kc = Cfg::TMA ? K : K_even;
   const int G = gridDim.x;
   const int stages = p.stages;
 
@@ -930,15 +1013,23 @@ __global__ void __launch_bounds__(Cfg::NT) tsmm_mma_kernel(const TsmmArgs p) {
       if (it >= stages && lane == 0) mbar_wait(&empty[s], static_cast<u32>(((it / stages) - 1) & 1));
       __syncwarp();
       const long long r0 = c * R;
-      const int rows = static_cast<int>((K_even - r0 < R) ? (K_even - r0) : R);
       double* dA = ring + static_cast<long long>(s) * Cfg::STAGE_DOUBLES;
-      if (lane == 0) mbar_arrive_expect_tx(&full[s], static_cast<u32>(rows * M * S * 8));
-      __syncwarp();
-      if constexpr (AP == M) {
-        if (lane == 0) bulk_g2s(dA, p.A + r0 * M * S, static_cast<u32>(rows * M * S * 8), &full[s], pol);
+      if constexpr (Cfg::TMA) {
+        if (lane == 0) {
+          mbar_arrive_expect_tx(&full[s], static_cast<u32>(Cfg::NBA * R * 128));
+          for (int b = 0; b < Cfg::NBA; b++)
+            tma_load_2d(dA + b * R * 16, &p.tmA, b * 16, static_cast<int>(r0), &full[s], pol);
+        }
       } else {
-        for (int r = lane; r < rows; r += 32)
-          bulk_g2s(dA + r * AP * S, p.A + (r0 + r) * M * S, static_cast<u32>(M * S * 8), &full[s], pol);
+        const int rows = static_cast<int>((K_even - r0 < R) ? (K_even - r0) : R);
+        if (lane == 0) mbar_arrive_expect_tx(&full[s], static_cast<u32>(rows * M * S * 8));
+        __syncwarp();
+        if constexpr (AP == M) {
+          if (lane == 0) bulk_g2s(dA, p.A + r0 * M * S, static_cast<u32>(rows * M * S * 8), &full[s], pol);
+        } else {
+          for (int r = lane; r < rows; r += 32)
+            bulk_g2s(dA + r * AP * S, p.A + (r0 + r) * M * S, static_cast<u32>(M * S * 8), &full[s], pol);
+        }
       }
     }
   } else {
@@ -954,13 +1045,26 @@ __global__ void __launch_bounds__(Cfg::NT) tsmm_mma_kernel(const TsmmArgs p) {
 #pragma unroll
           for (int z = 0; z < S; z++) creg[ks][j][z] = sC[((4 * ks + q) * NCP + 8 * j + g) * S + z];
     }
+    // offset (doubles) of element (row r, column x): dense / padded rows, or swizzled boxes
+    auto aoff = [&](int r, int x) -> int {
+      if constexpr (Cfg::TMA)
+        return ((x * S) >> 4) * (R * 16) + swz128(r, (x * S) & 15);
+      else
+        return (r * AP + x) * S;
+    };
+    auto ooff = [&](int r, int x) -> int {  // output staging (rows of this warp)
+      if constexpr (Cfg::TMA)
+        return ((x * S) >> 4) * (RW * 16) + swz128(r, (x * S) & 15);
+      else
+        return (r * NOP + x) * S;
+    };
     int it = 0;
     for (long long c = blockIdx.x; c < p.nchunks; c += G, it++) {
       const int s = it % stages;
       mbar_wait(&full[s], static_cast<u32>((it / stages) & 1));
       const double* sA = ring + static_cast<long long>(s) * Cfg::STAGE_DOUBLES;
       const long long r0 = c * R;
-      const int rows = static_cast<int>((K_even - r0 < R) ? (K_even - r0) : R);
+      const int rows = static_cast<int>((Kc - r0 < R) ? (Kc - r0) : R);
 #pragma unroll 1
       for (int pr = 0; pr < rows; pr += RPP) {
         const int wr0 = pr + warp * RW;
@@ -981,7 +1085,7 @@ __global__ void __launch_bounds__(Cfg::NT) tsmm_mma_kernel(const TsmmArgs p) {
           for (int i = 0; i < WR; i++) {
             const int r = wr0 + 8 * i + g;
 #pragma unroll
-            for (int z = 0; z < S; z++) a[i][z] = mv ? sA[(r * AP + m) * S + z] : 0.0;
+            for (int z = 0; z < S; z++) a[i][z] = mv ? sA[aoff(r, m) + z] : 0.0;
           }
           double cf[NB][S];
 #pragma unroll
@@ -1018,10 +1122,11 @@ __global__ void __launch_bounds__(Cfg::NT) tsmm_mma_kernel(const TsmmArgs p) {
 #pragma unroll
           for (int j = 0; j < NB; j++) {
             const int n = 8 * j + 2 * q;
-            if constexpr (!Cfg::Z && NOP % 2 == 0) {
-              // 16-byte store; NOP = 2 mod 4 keeps a warp's stores conflict-free
-              double* dst = stg + (8 * i + g) * NOP + n;
-              if (n + 1 < N)
+            const int rr = 8 * i + g;
+            if constexpr (!Cfg::Z && (Cfg::TMA || NOP % 2 == 0)) {
+              // 16-byte store (conflict-free: NOP = 2 mod 4, or swizzled boxes)
+              double* dst = stg + ooff(rr, n);
+              if (n + 1 < N || (Cfg::TMA && n < NOP))
                 *reinterpret_cast<double2*>(dst) = make_double2(acc[i][j][0][0], acc[i][j][0][1]);
               else if (n < N)
                 dst[0] = acc[i][j][0][0];
@@ -1029,8 +1134,12 @@ __global__ void __launch_bounds__(Cfg::NT) tsmm_mma_kernel(const TsmmArgs p) {
 #pragma unroll
               for (int e = 0; e < 2; e++) {
                 if (n + e < N) {
-#pragma unroll
-                  for (int z = 0; z < S; z++) stg[((8 * i + g) * NOP + n + e) * S + z] = acc[i][j][z][e];
+                  if constexpr (Cfg::Z) {
+                    *reinterpret_cast<double2*>(stg + ooff(rr, n + e)) =
+                        make_double2(acc[i][j][0][e], acc[i][j][1][e]);
+                  } else {
+                    stg[ooff(rr, n + e)] = acc[i][j][0][e];
+                  }
                 }
               }
             }
@@ -1038,7 +1147,13 @@ __global__ void __launch_bounds__(Cfg::NT) tsmm_mma_kernel(const TsmmArgs p) {
         fence_proxy_async_smem();
         __syncwarp();
         const int nr = (rows - wr0 < RW) ? rows - wr0 : RW;
-        if constexpr (NOP == N) {
+        if constexpr (Cfg::TMA) {
+          if (lane == 0) {
+            for (int b = 0; b < Cfg::NBO; b++)
+              tma_store_2d(&p.tmB, b * 16, static_cast<int>(r0 + wr0), stg + b * RW * 16);
+            bulk_commit();
+          }
+        } else if constexpr (NOP == N) {
           if (lane == 0) {
             bulk_s2g(p.B + (r0 + wr0) * N * S, stg, static_cast<u32>(nr * N * S * 8));
             bulk_commit();
@@ -1052,8 +1167,8 @@ __global__ void __launch_bounds__(Cfg::NT) tsmm_mma_kernel(const TsmmArgs p) {
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
     }
-    // Odd last row (K odd): warp 0 of block 0, plain fma from global A, smem C.
-    if ((K & 1) && blockIdx.x == 0 && warp == 0) {
+    // Odd last row (K odd, bulk-copy kernels): warp 0 of block 0, plain fma.
+    if (!Cfg::TMA && (K & 1) && blockIdx.x == 0 && warp == 0) {
       const double* a = p.A + (K - 1) * M * S;
       for (int n = lane; n < N; n += 32) {
         if constexpr (!Cfg::Z) {
@@ -1074,3 +1189,4 @@ __global__ void __launch_bounds__(Cfg::NT) tsmm_mma_kernel(const TsmmArgs p) {
 }
 
 }  // namespace tsm
+

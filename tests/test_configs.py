@@ -64,10 +64,16 @@ def test_candidates_valid(tsm, shape):
 
 def test_invalid_config_rejected_before_cuda(tsm):
     good = gi.to_tsm_config("tsmttsm", gi.tsmttsm_mma_default(64, 64, False), 3, 1)
+    assert good["kernel"] == 2  # DMMA + TMA tensor copies
     assert _status(tsm, "tsmttsm", "d", 64, 64, good) == 5
-    for k, v in [("rows_per_chunk", 30), ("threads", 100), ("p2", 63), ("kernel", 3)]:
+    for k, v in [("rows_per_chunk", 30), ("rows_per_chunk", 12), ("threads", 100), ("kernel", 3)]:
         bad = dict(good, **{k: v})
         assert _status(tsm, "tsmttsm", "d", 64, 64, bad) == 1, k
+    dense = dict(good, kernel=1)  # DMMA with bulk copies: p2/p3 are smem strides
+    assert _status(tsm, "tsmttsm", "d", 64, 64, dense) == 5
+    assert _status(tsm, "tsmttsm", "d", 64, 64, dict(dense, p2=63)) == 1
+    # TMA needs 16-byte rows of >= 128 bytes
+    assert _status(tsm, "tsmttsm", "d", 12, 64, dict(good, p0=1, p1=1, threads=32 * 9)) == 1
     # odd-width D rows cannot be padded (not 16-byte multiples)
     assert _status(tsm, "tsmttsm", "d", 63, 64, dict(good, p2=66)) == 1
 

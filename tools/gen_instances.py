@@ -109,10 +109,23 @@ def tsmttsm_mma_default(M: int, N: int, z: bool) -> dict:
     RS = NW // WT
     S = 2 if z else 1
     row_bytes = (M + N) * 8 * S
+    if tma_ok(M, N, z):
+        # 2-D TMA boxes of 16 doubles, 128B swizzle (conflict-free fragments)
+        tb = (cdiv(M * S, 16) + cdiv(N * S, 16)) * 128
+        step = max(8, 4 * RS)
+        step = step if step % 8 == 0 else 2 * step
+        R = min(256, max(step, (24576 // tb) // step * step))
+        return dict(MT=WM, NTL=WN, NT=(NW + 1) * 32, R=R, stages=4, ctas=2, impl=2, AP=M, BP=N)
     step = 4 * RS
     R = max(step, (24576 // row_bytes) // step * step)
     return dict(MT=WM, NTL=WN, NT=(NW + 1) * 32, R=R, stages=4, ctas=2, impl=1,
                 AP=pick_stride(M, z, "t"), BP=pick_stride(N, z, "t"))
+
+
+def tma_ok(M: int, N: int, z: bool) -> bool:
+    """2-D tensor maps need 16-byte global row strides; boxes are 16 doubles."""
+    S = 2 if z else 1
+    return (M * S) % 2 == 0 and (N * S) % 2 == 0 and M * S >= 16 and N * S >= 16
 
 
 def tsmttsm_pick(M: int, N: int, z: bool) -> dict:
@@ -159,7 +172,7 @@ def tsmm_default(M: int, N: int, z: bool) -> dict:
 
 
 def _tsmm_p(c: dict) -> tuple:
-    if c.get("impl", 0) == 1:
+    if c.get("impl", 0) >= 1:
         return (c["WR"], c["AP"], c["NOP"])
     return (c["NTL"], c["MSPLIT"], c["U"])
 
@@ -190,32 +203,34 @@ def resolve(op: str, M: int, N: int, z: bool, tuned: dict | None) -> dict:
         if tuned.get("impl", 0) != cfg.get("impl", 0):
             cfg = {k: v for k, v in cfg.items() if k in ("stages", "ctas")}
         cfg.update(tuned)
-    if op == "tsmttsm" and cfg.get("impl", 0) == 1 and "AP" not in cfg:
+    if op == "tsmttsm" and cfg.get("impl", 0) >= 1 and "AP" not in cfg:
         cfg["AP"], cfg["BP"] = pick_stride(M, z, "t"), pick_stride(N, z, "t")
     return cfg
 
 
 def cfg_type(op, dt, M, N, c) -> str:
     z = "true" if dt == "z" else "false"
-    if op == "tsmttsm" and c.get("impl", 0) == 1:
+    if op == "tsmttsm" and c.get("impl", 0) >= 1:
+        tma = "true" if c["impl"] == 2 else "false"
         return (f"tsm::TsmttsmMmaCfg<{M}, {N}, {z}, {c['MT']}, {c['NTL']}, {c['NT'] // 32 - 1}, "
-                f"{c['R']}, {c.get('AP', M)}, {c.get('BP', N)}>")
+                f"{c['R']}, {c.get('AP', M)}, {c.get('BP', N)}, {tma}>")
     if op == "tsmttsm":
         return f"tsm::TsmttsmCfg<{M}, {N}, {z}, {c['MT']}, {c['NTL']}, {c['NT']}, {c['R']}>"
-    if c.get("impl", 0) == 1:
+    if c.get("impl", 0) >= 1:
+        tma = "true" if c["impl"] == 2 else "false"
         return (f"tsm::TsmmMmaCfg<{M}, {N}, {z}, {c['WR']}, {c['NT'] // 32 - 1}, {c['R']}, "
-                f"{c['AP']}, {c['NOP']}>")
+                f"{c['AP']}, {c['NOP']}, {tma}>")
     return f"tsm::TsmmCfg<{M}, {N}, {z}, {c['NTL']}, {c['MSPLIT']}, {c['U']}, {c['NT']}, {c['R']}>"
 
 
 def entry_init(op, dt, M, N, c) -> str:
     t = cfg_type(op, dt, M, N, c)
     if op == "tsmttsm":
-        kn = "tsmttsm_mma_kernel" if c.get("impl", 0) == 1 else "tsmttsm_kernel"
+        kn = "tsmttsm_mma_kernel" if c.get("impl", 0) >= 1 else "tsmttsm_kernel"
         fn = f"(const void*)&tsm::{kn}<{t}>"
         kind = "tsm::KIND_TSMTTSM"
     else:
-        kn = "tsmm_mma_kernel" if c.get("impl", 0) == 1 else "tsmm_kernel"
+        kn = "tsmm_mma_kernel" if c.get("impl", 0) >= 1 else "tsmm_kernel"
         fn = f"(const void*)&tsm::{kn}<{t}>"
         kind = "tsm::KIND_TSMM"
     p = params4(op, M, N, c)
@@ -226,7 +241,7 @@ def entry_init(op, dt, M, N, c) -> str:
 def params4(op: str, M: int, N: int, c: dict) -> tuple:
     """(p0, p1, p2, p3) of the registry entry / tsm_config for a gen-style cfg."""
     if op == "tsmttsm":
-        if c.get("impl", 0) == 1:
+        if c.get("impl", 0) >= 1:
             return (c["MT"], c["NTL"], c.get("AP", M), c.get("BP", N))
         return (c["MT"], c["NTL"], 0, 0)
     return _tsmm_p(c) + (0,)
@@ -373,6 +388,12 @@ def candidates(op: str, M: int, N: int, z: bool) -> list:
                                             R=_rows(4 * k, row, tgt), impl=1,
                                             AP=pick_stride(M, z, "t", pad),
                                             BP=pick_stride(N, z, "t", pad)))
+                        if tma_ok(M, N, z):  # 2-D TMA boxes, 128B swizzle
+                            tb = (cdiv(M * S, 16) + cdiv(N * S, 16)) * 128
+                            step = 4 * k if (4 * k) % 8 == 0 else 8 * k
+                            Rt = min(256 // step * step, max(step, (tgt // tb) // step * step))
+                            out.append(dict(MT=WM, NTL=WN, NT=(NW + 1) * 32, R=Rt, impl=2,
+                                            AP=M, BP=N))
     else:
         acc_max = 16 if z else 32
         NTL = 1
@@ -407,6 +428,10 @@ def candidates(op: str, M: int, N: int, z: bool) -> list:
                 for tgt in (12288, 24576):
                     R = rpp * max(1, round(tgt / (rpp * d["AP"] * S_ * 8)))
                     out.append(dict(WR=WR, AP=d["AP"], NOP=d["NOP"], NT=(NW + 1) * 32, R=R, impl=1))
+                    if tma_ok(M, N, z) and rpp <= 256:
+                        ab = cdiv(M * S_, 16) * 128
+                        Rt = rpp * max(1, min(256 // rpp, round(tgt / (rpp * ab))))
+                        out.append(dict(WR=WR, AP=M, NOP=N, NT=(NW + 1) * 32, R=Rt, impl=2))
     # dedupe
     seen, uniq = set(), []
     for c in out:
@@ -419,7 +444,7 @@ def candidates(op: str, M: int, N: int, z: bool) -> list:
 
 def to_tsm_config(op: str, c: dict, stages: int, ctas: int) -> dict:
     """gen-style cfg -> tsm_config field dict (include/libtsm.h)."""
-    if op == "tsmttsm" and c.get("impl", 0) == 1:
+    if op == "tsmttsm" and c.get("impl", 0) >= 1:
         p = (c["MT"], c["NTL"], c["AP"], c["BP"])
     elif op == "tsmttsm":
         p = (c["MT"], c["NTL"], 0, 0)
@@ -479,9 +504,19 @@ def tsmm_mma_default(M: int, N: int, z: bool) -> dict:
     AP, NOP = pick_stride(M, z, "a"), pick_stride(N, z, "o")
     NCP = 8 * NB + 4 if z else (8 * NB if (8 * NB) % 16 == 8 else 8 * NB + 8)
     wr0 = max(1, min(4, 16 // (NB * S)))
+    tma = tma_ok(M, N, z)
     for NW in (8, 4):
         for WR in sorted({wr0, max(1, wr0 // 2), 1}, reverse=True):
             rpp = 8 * WR * NW
+            if tma:
+                if rpp > 256:
+                    continue
+                ab, ob = cdiv(M * S, 16) * 128, cdiv(N * S, 16) * 128
+                R = rpp * max(1, min(256 // rpp, round(16384 / (rpp * ab))))
+                smem = 2560 + 8 * MK * 4 * NCP * S + NW * 8 * WR * ob + 3 * R * ab
+                if smem <= 200 * 1024:
+                    return dict(WR=WR, AP=M, NOP=N, NT=(NW + 1) * 32, R=R, stages=4, ctas=2, impl=2)
+                continue
             R = rpp * max(1, round(16384 / (rpp * AP * S * 8)))
             smem = 256 + 8 * (MK * 4 * NCP * S + NW * 8 * WR * NOP * S + 3 * R * AP * S)
             if smem <= 200 * 1024:
