@@ -72,14 +72,18 @@ def build(jobs: int | None = None, verbose: bool = True) -> str:
     jobs = jobs or max(1, os.cpu_count() or 1)
     with cf.ThreadPoolExecutor(jobs) as ex:
         objs = list(ex.map(_compile, srcs))
+    keep = set(os.path.basename(o) for o in objs)
+    for f in os.listdir(OBJ):  # drop stale objects of earlier source versions
+        if f.endswith(".o") and f not in keep:
+            os.remove(os.path.join(OBJ, f))
     stamp = hashlib.sha1("".join(objs).encode()).hexdigest()[:16]
     stamp_file = os.path.join(OBJ, "libtsm.stamp")
     if os.path.exists(LIB) and os.path.exists(stamp_file) and open(stamp_file).read() == stamp:
         return LIB
     tmp = LIB + f".tmp{os.getpid()}"
     cmd = [NVCC, *ARCH, "-shared", "-Xcompiler", "-fPIC", "-cudart", "static", "-o", tmp, *objs,
-           "-L/usr/local/cuda/lib64", "-lnvrtc_static", "-lnvrtc-builtins_static",
-           "-lnvptxcompiler_static", "-ldl", "-lpthread", "-lrt"]
+           "-L/usr/local/cuda/lib64", "-lnvrtc", "-Xlinker", "-rpath=/usr/local/cuda/lib64",
+           "-ldl", "-lpthread", "-lrt"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stderr}")

@@ -123,6 +123,12 @@ size_t smem_bytes(const KernelEntry& k, int stages) {
     long long need = std::max<long long>(stages * stage, std::max<long long>(cells, k.NT));
     return static_cast<size_t>(128 + need * 8);
   }
+  if (k.impl == 3) {  // C-stationary DMMA TSMM: p0 = NBW, p1 = WR (must match TsmmCstCfg)
+    const long long NW = k.NT / 32 - 1;
+    const long long OB = k.p0 * 8 * S / 16, RW = 8 * k.p1;
+    const long long ad = static_cast<long long>(k.R) * ((k.M * S + 15) / 16) * 16;
+    return static_cast<size_t>(256 + 1024 + (NW * OB * RW * 16 + stages * ad) * 8);
+  }
   if (k.impl >= 1) {  // DMMA TSMM: p0 = WR, p1 = AP, p2 = NOP (must match TsmmMmaCfg)
     const long long MK = (k.M + 3) / 4, NB = (k.N + 7) / 8;
     const long long NCP = S == 2 ? 8 * NB + 4 : ((8 * NB) % 16 == 8 ? 8 * NB : 8 * NB + 8);
@@ -221,8 +227,20 @@ static tsm_status validate_config(const KernelEntry& e) {
   if (e.R < 2 || e.R % 2) return bad("rows_per_chunk must be even and >= 2");
   if (e.stages < 2 || e.stages > 16) return bad("stages must be in [2, 16]");
   if (e.ctas_per_sm < 1) return bad("ctas_per_sm must be >= 1");
-  if (e.impl < 0 || e.impl > 2) return bad("kernel must be 0 (DFMA tile), 1 (DMMA) or 2 (DMMA + TMA)");
-  if (e.impl == 2 && e.op == KIND_TSMM) {
+  if (e.impl < 0 || e.impl > 3) return bad("kernel must be 0 (DFMA), 1 (DMMA), 2 (DMMA + TMA), 3 (TSMM C-stationary)");
+  if (e.impl == 3) {
+    const int S = e.dt == TSM_Z ? 2 : 1;
+    if (e.op != KIND_TSMM) return bad("kernel 3 (C-stationary DMMA) is a TSMM kernel");
+    if ((e.M * S) % 2 || (e.N * S) % 2 || e.M * S < 16 || e.N * S < 16)
+      return bad("kernel 3 needs 16-byte rows of >= 128 bytes (M*S, N*S even and >= 16)");
+    const int NB = (e.N + 7) / 8, NW = e.NT / 32 - 1;
+    if (e.p0 < 1 || e.p0 > NB || (e.p0 * 8 * S) % 16) return bad("NBW must be in [1, ceil(N/8)] with 8*NBW*S a multiple of 16");
+    const int NG = (NB + e.p0 - 1) / e.p0;
+    if (NW < NG || NW % NG) return bad("consumer warps must be a multiple of the column groups");
+    if (e.p1 < 1 || 8 * e.p1 > 256) return bad("WR must be in [1, 32]");
+    const int RPP = 8 * e.p1 * (NW / NG);
+    if (e.R % RPP || e.R % 8 || e.R > 256) return bad("rows_per_chunk <= 256, a multiple of 8 and of the rows per pass");
+  } else if (e.impl == 2 && e.op == KIND_TSMM) {
     const int S = e.dt == TSM_Z ? 2 : 1;
     if ((e.M * S) % 2 || (e.N * S) % 2 || e.M * S < 16 || e.N * S < 16)
       return bad("kernel 2 needs 16-byte rows of >= 128 bytes (M*S, N*S even and >= 16)");
@@ -403,7 +421,7 @@ Geometry geometry(const tsm_plan_s* p, long long K) {
   const long long K_even = K & ~1LL;
   // TMA kernels cover all K rows (the tensor copy zero-fills past K); the
   // bulk-copy kernels cover the even part and treat an odd last row apart.
-  const long long Kc = p->k->impl == 2 ? K : K_even;
+  const long long Kc = p->k->impl >= 2 ? K : K_even;
   g.nchunks = (Kc + p->k->R - 1) / p->k->R;
   const long long gmax = static_cast<long long>(p->sms) * p->ctas_per_sm;
   g.grid = static_cast<int>(std::max<long long>(1, std::min(gmax, g.nchunks)));
@@ -506,10 +524,11 @@ tsm_status launch_tsmm(const tsm_plan_s* p, int dt, long long K, const void* A, 
   a.K = K;
   a.nchunks = g.nchunks;
   a.stages = p->stages;
-  if (p->k->impl == 2) {
+  if (p->k->impl >= 2) {  // B store boxes: 8*WR rows (WR = p0 for kernel 2, p1 for kernel 3)
     const int S = dt == TSM_Z ? 2 : 1;
+    const int wr = p->k->impl == 3 ? p->k->p1 : p->k->p0;
     tsm_status st = make_tmap(&a.tmA, A, K, p->M * S, p->k->R);
-    if (st == TSM_SUCCESS) st = make_tmap(&a.tmB, B, K, p->N * S, 8 * p->k->p0);
+    if (st == TSM_SUCCESS) st = make_tmap(&a.tmB, B, K, p->N * S, 8 * wr);
     if (st != TSM_SUCCESS) return st;
   }
   void* args[] = {&a};
@@ -573,7 +592,9 @@ tsm_status tsm_plan_describe(tsm_plan p, int64_t K, char* buf, size_t len) {
              "\"smem\":%zu,\"grid\":%d,\"nchunks\":%lld,\"jit\":%s,\"kernel\":\"%s\"}",
              p->dt ? 'z' : 'd', p->M, p->N, k->p0, k->p1, k->p2, k->NT, k->R, p->stages,
              p->ctas_per_sm, p->smem, g.grid, g.nchunks, p->jit ? "true" : "false",
-             k->impl == 2 ? "dmma+tma(p0=WR)" : (k->impl ? "dmma(p0=WR,p1=AP,p2=NOP)" : "dfma"));
+             k->impl == 3   ? "dmma-cstationary+tma(p0=NBW,p1=WR)"
+             : k->impl == 2 ? "dmma+tma(p0=WR)"
+                            : (k->impl ? "dmma(p0=WR,p1=AP,p2=NOP)" : "dfma"));
   snprintf(buf, len, "%s", tmp);
   return TSM_SUCCESS;
 }

@@ -45,6 +45,9 @@ std::string cfg_type(const KernelEntry& e) {
   else if (e.op == KIND_TSMTTSM)
     os << "tsm::TsmttsmCfg<" << e.M << ", " << e.N << ", " << z << ", " << e.p0 << ", " << e.p1
        << ", " << e.NT << ", " << e.R << ">";
+  else if (e.impl == 3)
+    os << "tsm::TsmmCstCfg<" << e.M << ", " << e.N << ", " << z << ", " << e.p0 << ", " << e.p1
+       << ", " << (e.NT / 32 - 1) << ", " << e.R << ">";
   else if (e.impl >= 1)
     os << "tsm::TsmmMmaCfg<" << e.M << ", " << e.N << ", " << z << ", " << e.p0 << ", "
        << (e.NT / 32 - 1) << ", " << e.R << ", " << e.p1 << ", " << e.p2 << ", "
@@ -56,7 +59,8 @@ std::string cfg_type(const KernelEntry& e) {
 }
 
 std::string kernel_name(const KernelEntry& e) {
-  const char* fn = e.op == KIND_TSMM ? (e.impl >= 1 ? "tsm::tsmm_mma_kernel<" : "tsm::tsmm_kernel<")
+  const char* fn = e.op == KIND_TSMM ? (e.impl == 3 ? "tsm::tsmm_cst_kernel<"
+                                        : e.impl >= 1 ? "tsm::tsmm_mma_kernel<" : "tsm::tsmm_kernel<")
                    : (e.impl >= 1 ? "tsm::tsmttsm_mma_kernel<" : "tsm::tsmttsm_kernel<");
   return std::string(fn) + cfg_type(e) + ">";
 }

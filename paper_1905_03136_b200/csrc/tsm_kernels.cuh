@@ -124,6 +124,22 @@ __device__ __forceinline__ void zfma(double& re, double& im, double ar, double a
   im = fma(ai, br, im);
 }
 
+// Position in the smem ring: stage index s, mbarrier phase parity ph of that
+// stage's current use, and how many times the ring wrapped (incremental, so
+// the hot loops carry no integer division by the run-time stage count).
+struct Ring {
+  int s = 0;
+  u32 ph = 0;
+  int round = 0;
+  __device__ __forceinline__ void next(int stages) {
+    if (++s == stages) {
+      s = 0;
+      ph ^= 1u;
+      round++;
+    }
+  }
+};
+
 // Workspace layout shared by host and device code.
 struct WsLayout {
   static constexpr int kCounterBytes = 256;  // u32 ticket, u32 done, padding
@@ -380,10 +396,10 @@ __global__ void __launch_bounds__(Cfg::NT) tsmttsm_kernel(const TsmttsmArgs p) {
 #pragma unroll
       for (int q = 0; q < S; q++) acc[i][j][q] = 0.0;
 
-  int it = 0;
-  for (long long c = blockIdx.x; c < p.nchunks; c += G, it++) {
-    const int s = it % stages;
-    mbar_wait(&full[s], static_cast<u32>((it / stages) & 1));
+  Ring ring_it;
+  for (long long c = blockIdx.x; c < p.nchunks; c += G, ring_it.next(stages)) {
+    const int s = ring_it.s;
+    mbar_wait(&full[s], ring_it.ph);
     const double* sA = ring + static_cast<long long>(s) * Cfg::STAGE_DOUBLES;
     const double* sB = sA + R * M * S;
     const long long r0 = c * R;
@@ -616,10 +632,10 @@ __global__ void __launch_bounds__(Cfg::NT) tsmttsm_mma_kernel(const __grid_const
   if (warp == NW) {
     // ---------------- producer warp: bulk / tensor copies into the ring ----------------
     const u64 pol = policy_evict_first();
-    int it = 0;
-    for (long long c = blockIdx.x; c < p.nchunks; c += G, it++) {
-      const int s = it % stages;
-      if (it >= stages && lane == 0) mbar_wait(&empty[s], static_cast<u32>(((it / stages) - 1) & 1));
+    Ring ring_it;
+    for (long long c = blockIdx.x; c < p.nchunks; c += G, ring_it.next(stages)) {
+      const int s = ring_it.s;
+      if (ring_it.round > 0 && lane == 0) mbar_wait(&empty[s], ring_it.ph ^ 1u);
       __syncwarp();
       const long long r0 = c * R;
       double* dA = ring + static_cast<long long>(s) * Cfg::STAGE_DOUBLES;
@@ -653,10 +669,10 @@ __global__ void __launch_bounds__(Cfg::NT) tsmttsm_mma_kernel(const __grid_const
     }
   } else {
     // ---------------- consumer warps ----------------
-    int it = 0;
-    for (long long c = blockIdx.x; c < p.nchunks; c += G, it++) {
-      const int s = it % stages;
-      mbar_wait(&full[s], static_cast<u32>((it / stages) & 1));
+    Ring ring_it;
+    for (long long c = blockIdx.x; c < p.nchunks; c += G, ring_it.next(stages)) {
+      const int s = ring_it.s;
+      mbar_wait(&full[s], ring_it.ph);
       const double* sA = ring + static_cast<long long>(s) * Cfg::STAGE_DOUBLES;
       const double* sB = sA + R * AP * S;
       const long long r0 = c * R;
@@ -868,11 +884,11 @@ __global__ void __launch_bounds__(Cfg::NT) tsmm_kernel(const TsmmArgs p) {
     }
   };
 
-  int it = 0;
+  Ring ring_it;
   int pass = 0;  // global pass counter -> output buffer parity
-  for (long long c = blockIdx.x; c < p.nchunks; c += G, it++) {
-    const int s = it % stages;
-    mbar_wait(&full[s], static_cast<u32>((it / stages) & 1));
+  for (long long c = blockIdx.x; c < p.nchunks; c += G, ring_it.next(stages)) {
+    const int s = ring_it.s;
+    mbar_wait(&full[s], ring_it.ph);
     const double* sA = ring + static_cast<long long>(s) * Cfg::A_STAGE_DOUBLES;
     const long long r0 = c * R;
     const int rows = static_cast<int>((K_even - r0 < R) ? (K_even - r0) : R);
@@ -1007,10 +1023,10 @@ __global__ void __launch_bounds__(Cfg::NT) tsmm_mma_kernel(const __grid_constant
   if (warp == NW) {
     // ---------------- producer warp ----------------
     const u64 pol = policy_evict_first();
-    int it = 0;
-    for (long long c = blockIdx.x; c < p.nchunks; c += G, it++) {
-      const int s = it % stages;
-      if (it >= stages && lane == 0) mbar_wait(&empty[s], static_cast<u32>(((it / stages) - 1) & 1));
+    Ring ring_it;
+    for (long long c = blockIdx.x; c < p.nchunks; c += G, ring_it.next(stages)) {
+      const int s = ring_it.s;
+      if (ring_it.round > 0 && lane == 0) mbar_wait(&empty[s], ring_it.ph ^ 1u);
       __syncwarp();
       const long long r0 = c * R;
       double* dA = ring + static_cast<long long>(s) * Cfg::STAGE_DOUBLES;
@@ -1058,10 +1074,10 @@ __global__ void __launch_bounds__(Cfg::NT) tsmm_mma_kernel(const __grid_constant
       else
         return (r * NOP + x) * S;
     };
-    int it = 0;
-    for (long long c = blockIdx.x; c < p.nchunks; c += G, it++) {
-      const int s = it % stages;
-      mbar_wait(&full[s], static_cast<u32>((it / stages) & 1));
+    Ring ring_it;
+    for (long long c = blockIdx.x; c < p.nchunks; c += G, ring_it.next(stages)) {
+      const int s = ring_it.s;
+      mbar_wait(&full[s], ring_it.ph);
       const double* sA = ring + static_cast<long long>(s) * Cfg::STAGE_DOUBLES;
       const long long r0 = c * R;
       const int rows = static_cast<int>((Kc - r0 < R) ? (Kc - r0) : R);
@@ -1188,5 +1204,179 @@ __global__ void __launch_bounds__(Cfg::NT) tsmm_mma_kernel(const __grid_constant
   }
 }
 
-}  // namespace tsm
+// --------------------------------------------------------------------------
+// TSMM, "C-stationary" DMMA kernel (impl 3).  The N columns of B are split
+// into NG column groups of NBW 8-column blocks; a consumer warp serves one
+// column group and keeps ITS slice of C as MMA-B fragments in registers for
+// the whole kernel (MK x NBW fragments: the paper's "C in registers",
+// PAPER.md:701-703, made affordable by distributing C over warps).  Per
+// k-step a warp loads only A fragments (128B-swizzled TMA boxes:
+// conflict-free) for WR row blocks and issues WR*NBW DMMAs.  Each warp writes
+// its (8*WR rows x 8*NBW columns) tile to a private swizzled staging box and
+// stores it with one TMA tensor store per 16-double box -- no cross-warp
+// barrier; rows past K and columns past N are clipped by the TMA unit.
+// Requires the TMA conditions (M*S, N*S even and >= 16) and 8*NBW*S a
+// multiple of 16 doubles (whole output boxes per warp).
+// --------------------------------------------------------------------------
+template <int M_, int N_, bool Z_, int NBW_, int WR_, int NW_, int R_>
+struct TsmmCstCfg {
+  static constexpr int M = M_, N = N_, NBW = NBW_, WR = WR_, NW = NW_, R = R_;
+  static constexpr bool Z = Z_;
+  static constexpr int S = Z ? 2 : 1;
+  static constexpr int MK = (M + 3) / 4;            // k-steps over m
+  static constexpr int NB = (N + 7) / 8;            // 8-column blocks of B
+  static constexpr int NG = (NB + NBW - 1) / NBW;   // column groups
+  static constexpr int RG = NW / NG;                // warps per column group
+  static constexpr int RW = 8 * WR;                 // rows per warp per pass
+  static constexpr int RPP = RW * RG;               // rows per pass
+  static constexpr int NBA = (M * S + 15) / 16;     // A boxes per row
+  static constexpr int OB = NBW * 8 * S / 16;       // output boxes per warp
+  static constexpr int NT = (NW + 1) * 32;
+  static constexpr int STAGE_DOUBLES = R * NBA * 16;
+  static constexpr int OUT_DOUBLES = OB * RW * 16;  // per warp
+  static_assert(NW % NG == 0 && RG >= 1, "consumer warps must be a multiple of the column groups");
+  static_assert((NBW * 8 * S) % 16 == 0, "a warp's columns must fill whole 16-double boxes");
+  static_assert((M * S) % 2 == 0 && (N * S) % 2 == 0 && M * S >= 16 && N * S >= 16,
+                "TMA tensor path: 16-byte rows of >= 128 bytes");
+  static_assert(R % RPP == 0 && R % 8 == 0 && R <= 256 && RW <= 256, "TMA box rows");
+};
 
+template <class Cfg>
+__global__ void __launch_bounds__(Cfg::NT) tsmm_cst_kernel(const __grid_constant__ TsmmArgs p) {
+  constexpr int M = Cfg::M, N = Cfg::N, S = Cfg::S, R = Cfg::R, NW = Cfg::NW, WR = Cfg::WR;
+  constexpr int MK = Cfg::MK, NB = Cfg::NB, NBW = Cfg::NBW, NG = Cfg::NG, RW = Cfg::RW;
+  constexpr int RPP = Cfg::RPP, OB = Cfg::OB;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  u64* full = reinterpret_cast<u64*>(smem_raw);
+  u64* empty = full + 16;
+  double* sOut = reinterpret_cast<double*>((reinterpret_cast<u64>(smem_raw) + 256 + 1023) & ~1023ull);
+  double* ring = sOut + NW * Cfg::OUT_DOUBLES;  // multiple of 1024 bytes
+
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, q = lane & 3;
+  const long long K = p.K;
+  const int G = gridDim.x;
+  const int stages = p.stages;
+
+  if (tid == 0) {
+    for (int s = 0; s < stages; s++) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NW);
+    }
+    fence_mbar_init();
+    fence_proxy_async_smem();
+  }
+  __syncthreads();
+
+  if (warp == NW) {
+    // ---------------- producer warp: TMA boxes of A ----------------
+    if (lane == 0) {
+      const u64 pol = policy_evict_first();
+      Ring ring_it;
+      for (long long c = blockIdx.x; c < p.nchunks; c += G, ring_it.next(stages)) {
+        const int s = ring_it.s;
+        if (ring_it.round > 0) mbar_wait(&empty[s], ring_it.ph ^ 1u);
+        double* dA = ring + static_cast<long long>(s) * Cfg::STAGE_DOUBLES;
+        mbar_arrive_expect_tx(&full[s], static_cast<u32>(Cfg::NBA * R * 128));
+        for (int b = 0; b < Cfg::NBA; b++)
+          tma_load_2d(dA + b * R * 16, &p.tmA, b * 16, static_cast<int>(c * R), &full[s], pol);
+      }
+    }
+  } else {
+    // ---------------- consumer warps ----------------
+    const int cg = warp % NG, rg = warp / NG;
+    const int nb0 = cg * NBW;  // first 8-column block of this warp
+    double* stg = sOut + warp * Cfg::OUT_DOUBLES;
+    // this warp's C slice as MMA-B fragments: lane holds C[4ks+q][8(nb0+j)+g]
+    double cf[MK][NBW][S];
+#pragma unroll
+    for (int ks = 0; ks < MK; ks++)
+#pragma unroll
+      for (int j = 0; j < NBW; j++) {
+        const int m = 4 * ks + q, n = 8 * (nb0 + j) + g;
+#pragma unroll
+        for (int z = 0; z < S; z++) cf[ks][j][z] = (m < M && n < N) ? __ldg(&p.C[(m * N + n) * S + z]) : 0.0;
+      }
+    auto aoff = [&](int r, int x) -> int {  // element (row r, column x) of the A stage
+      return ((x * S) >> 4) * (R * 16) + swz128(r, (x * S) & 15);
+    };
+    Ring ring_it;
+    for (long long c = blockIdx.x; c < p.nchunks; c += G, ring_it.next(stages)) {
+      const int s = ring_it.s;
+      mbar_wait(&full[s], ring_it.ph);
+      const double* sA = ring + static_cast<long long>(s) * Cfg::STAGE_DOUBLES;
+      const long long r0 = c * R;
+      const int rows = static_cast<int>((K - r0 < R) ? (K - r0) : R);
+#pragma unroll 1
+      for (int pr = 0; pr < rows; pr += RPP) {
+        const int wr0 = pr + rg * RW;
+        if (wr0 >= rows) break;
+        double acc[WR][NBW][S][2];
+#pragma unroll
+        for (int i = 0; i < WR; i++)
+#pragma unroll
+          for (int j = 0; j < NBW; j++)
+#pragma unroll
+            for (int z = 0; z < S; z++) acc[i][j][z][0] = acc[i][j][z][1] = 0.0;
+#pragma unroll
+        for (int ks = 0; ks < MK; ks++) {
+          const int m = 4 * ks + q;
+          const bool mv = (4 * ks + 4 <= M) || (m < M);
+#pragma unroll
+          for (int i = 0; i < WR; i++) {
+            const int r = wr0 + 8 * i + g;
+            if constexpr (!Cfg::Z) {
+              const double a = mv ? sA[aoff(r, m)] : 0.0;
+#pragma unroll
+              for (int j = 0; j < NBW; j++) dmma(acc[i][j][0][0], acc[i][j][0][1], a, cf[ks][j][0]);
+            } else {
+              const double2 a = mv ? *reinterpret_cast<const double2*>(sA + aoff(r, m)) : make_double2(0.0, 0.0);
+              const double nai = -a.y;
+#pragma unroll
+              for (int j = 0; j < NBW; j++) {
+                dmma(acc[i][j][0][0], acc[i][j][0][1], a.x, cf[ks][j][0]);  // re += ar cr
+                dmma(acc[i][j][0][0], acc[i][j][0][1], nai, cf[ks][j][1]);  // re -= ai ci
+                dmma(acc[i][j][1][0], acc[i][j][1][1], a.x, cf[ks][j][1]);  // im += ar ci
+                dmma(acc[i][j][1][0], acc[i][j][1][1], a.y, cf[ks][j][0]);  // im += ai cr
+              }
+            }
+          }
+        }
+        // registers -> private swizzled staging -> TMA tensor stores
+        if (lane == 0) bulk_wait_read<0>();
+        __syncwarp();
+#pragma unroll
+        for (int i = 0; i < WR; i++)
+#pragma unroll
+          for (int j = 0; j < NBW; j++) {
+            const int rr = 8 * i + g;
+            if constexpr (!Cfg::Z) {
+              const int c0 = 8 * j + 2 * q;  // column within the warp's tile (doubles)
+              *reinterpret_cast<double2*>(stg + (c0 >> 4) * (RW * 16) + swz128(rr, c0 & 15)) =
+                  make_double2(acc[i][j][0][0], acc[i][j][0][1]);
+            } else {
+#pragma unroll
+              for (int e = 0; e < 2; e++) {
+                const int c0 = 2 * (8 * j + 2 * q + e);
+                *reinterpret_cast<double2*>(stg + (c0 >> 4) * (RW * 16) + swz128(rr, c0 & 15)) =
+                    make_double2(acc[i][j][0][e], acc[i][j][1][e]);
+              }
+            }
+          }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0 && nb0 < NB) {
+          for (int b = 0; b < OB; b++)
+            tma_store_2d(&p.tmB, nb0 * 8 * S + b * 16, static_cast<int>(r0 + wr0), stg + b * RW * 16);
+          bulk_commit();
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+    }
+    if (lane == 0) bulk_wait_all();
+  }
+}
+
+}  // namespace tsm

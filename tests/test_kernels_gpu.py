@@ -1,0 +1,92 @@
+"""Every kernel family, forced through explicit configurations (the autotuner's
+search space), against the oracle on ragged K -- so a variant that the tuned
+table does not currently pick is still proven correct before it can be picked.
+
+  TSMTTSM: 0 register-tile DFMA, 1 DMMA bulk copies, 2 DMMA + TMA tensor maps
+  TSMM:    0 DFMA, 1 DMMA bulk copies, 2 DMMA + TMA, 3 C-stationary DMMA + TMA
+"""
+import os
+import sys
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import tsminputs as ti
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, os.path.join(ROOT, "tools"))
+import gen_instances as gi  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+SHAPES = [(64, 64), (48, 16), (16, 40), (32, 32), (24, 24), (8, 8), (33, 17), (3, 5)]
+K_LIST = [1, 7, 4099, 65537]
+
+
+@pytest.fixture(scope="module")
+def tsm():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    from paper_1905_03136_b200 import binding
+    return binding
+
+
+def per_impl(tsm, op, M, N, z):
+    """First candidate of each kernel family for this shape that fits the
+    device (some candidates exceed shared memory; the autotuner skips those)."""
+    seen = {}
+    for c in gi.candidates(op, M, N, z):
+        impl = c.get("impl", 0)
+        if impl in seen:
+            continue
+        try:
+            seen[impl] = (c, tsm.Plan(op, "z" if z else "d", M, N, 0,
+                                      config=gi.to_tsm_config(op, c, 3, 2)))
+        except tsm.TsmError as e:
+            if e.status != 2:  # only TSM_ERR_UNSUPPORTED (resources) may be skipped
+                raise
+    return seen
+
+
+@pytest.mark.parametrize("cplx", [False, True], ids=["D", "Z"])
+@pytest.mark.parametrize("M,N", SHAPES)
+def test_every_family(tsm, M, N, cplx):
+    dt = "z" if cplx else "d"
+    for op in ("tsmttsm", "tsmm"):
+        fams = per_impl(tsm, op, M, N, cplx)
+        assert fams
+        for impl, (c, plan) in sorted(fams.items()):
+            assert plan.config()["kernel"] == impl
+            for K in K_LIST:
+                A = ti.matrix(K, M, "A", complex_=cplx, seed=K)
+                if op == "tsmttsm":
+                    B = ti.matrix(K, N, "B", complex_=cplx, seed=K)
+                    got = tsm.tsmttsm(torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda(), plan=plan)
+                    ref, bound = oracle.tsmttsm(A, B)
+                    tol = 1e-12
+                else:
+                    Cm = ti.matrix(M, N, "C", complex_=cplx, seed=K)
+                    got = tsm.tsmm(torch.from_numpy(A).cuda(), torch.from_numpy(Cm).cuda(), plan=plan)
+                    ref, bound = oracle.tsmm(A, Cm)
+                    tol = 1e-13
+                torch.cuda.synchronize()
+                r, wi, _ = oracle.max_err_ratio(got.cpu().numpy(), ref, bound)
+                assert r <= tol, (op, dt, M, N, impl, c, K, r, wi)
+
+
+@pytest.mark.parametrize("cplx", [False, True], ids=["D", "Z"])
+def test_cstationary_int_bitwise(tsm, cplx):
+    M, N, K = 64, 48, 100001
+    dt = "z" if cplx else "d"
+    cands = gi.tsmm_cst_configs(M, N, cplx)
+    assert cands
+    A = ti.matrix(K, M, "A", complex_=cplx, mode="int")
+    Cm = ti.matrix(M, N, "C", complex_=cplx, mode="int")
+    ref, _ = oracle.tsmm(A, Cm)
+    for c in cands[:: max(1, len(cands) // 4)]:
+        plan = tsm.Plan("tsmm", dt, M, N, 0, config=gi.to_tsm_config("tsmm", c, 3, 1))
+        got = tsm.tsmm(torch.from_numpy(A).cuda(), torch.from_numpy(Cm).cuda(), plan=plan)
+        torch.cuda.synchronize()
+        assert np.array_equal(got.cpu().numpy(), ref), c

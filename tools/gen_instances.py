@@ -92,8 +92,8 @@ def tsmttsm_mma_default(M: int, N: int, z: bool) -> dict:
     MB, NB = cdiv(M, 8), cdiv(N, 8)
     wmax = 8 if z else 16  # WM*WN blocks per warp
     best = None
-    for WM in range(1, min(MB, 4) + 1):
-        for WN in range(1, min(NB, 4) + 1):
+    for WM in range(1, min(MB, 8) + 1):
+        for WN in range(1, min(NB, 8) + 1):
             if WM * WN > wmax:
                 continue
             if cdiv(MB, WM) * cdiv(NB, WN) > 16:
@@ -172,6 +172,8 @@ def tsmm_default(M: int, N: int, z: bool) -> dict:
 
 
 def _tsmm_p(c: dict) -> tuple:
+    if c.get("impl", 0) == 3:
+        return (c["NBW"], c["WR"], 0)
     if c.get("impl", 0) >= 1:
         return (c["WR"], c["AP"], c["NOP"])
     return (c["NTL"], c["MSPLIT"], c["U"])
@@ -216,6 +218,8 @@ def cfg_type(op, dt, M, N, c) -> str:
                 f"{c['R']}, {c.get('AP', M)}, {c.get('BP', N)}, {tma}>")
     if op == "tsmttsm":
         return f"tsm::TsmttsmCfg<{M}, {N}, {z}, {c['MT']}, {c['NTL']}, {c['NT']}, {c['R']}>"
+    if c.get("impl", 0) == 3:
+        return f"tsm::TsmmCstCfg<{M}, {N}, {z}, {c['NBW']}, {c['WR']}, {c['NT'] // 32 - 1}, {c['R']}>"
     if c.get("impl", 0) >= 1:
         tma = "true" if c["impl"] == 2 else "false"
         return (f"tsm::TsmmMmaCfg<{M}, {N}, {z}, {c['WR']}, {c['NT'] // 32 - 1}, {c['R']}, "
@@ -230,7 +234,8 @@ def entry_init(op, dt, M, N, c) -> str:
         fn = f"(const void*)&tsm::{kn}<{t}>"
         kind = "tsm::KIND_TSMTTSM"
     else:
-        kn = "tsmm_mma_kernel" if c.get("impl", 0) >= 1 else "tsmm_kernel"
+        kn = {3: "tsmm_cst_kernel", 2: "tsmm_mma_kernel", 1: "tsmm_mma_kernel"}.get(
+            c.get("impl", 0), "tsmm_kernel")
         fn = f"(const void*)&tsm::{kn}<{t}>"
         kind = "tsm::KIND_TSMM"
     p = params4(op, M, N, c)
@@ -366,14 +371,14 @@ def candidates(op: str, M: int, N: int, z: bool) -> list:
             MB, NB = cdiv(M, 8), cdiv(N, 8)
             wmax = 8 if z else 16
             wt = []
-            for WM in range(1, min(MB, 4) + 1):
-                for WN in range(1, min(NB, 4) + 1):
+            for WM in range(1, min(MB, 8) + 1):
+                for WN in range(1, min(NB, 8) + 1):
                     if WM * WN > wmax or cdiv(MB, WM) * cdiv(NB, WN) > 16:
                         continue
                     bal = cdiv(MB, WM) * WM * cdiv(NB, WN) * WN / (MB * NB)
                     wt.append((bal * (1 + 0.5 * (WM + WN) / (WM * WN)), WM, WN))
             wt.sort()
-            for (_, WM, WN) in wt[:3]:
+            for (_, WM, WN) in wt[:4]:
                 WT = cdiv(MB, WM) * cdiv(NB, WN)
                 for k in (1, 2, 4, 8):
                     NW = WT * k
@@ -416,6 +421,8 @@ def candidates(op: str, M: int, N: int, z: bool) -> list:
                         out.append(dict(NTL=NTL, MSPLIT=MS, U=U, NT=NT, R=R, impl=0))
                         break
                 MS *= 2
+    if op == "tsmm":
+        out.extend(tsmm_cst_configs(M, N, z))
     if op == "tsmm" and N >= 2:
         d = tsmm_mma_default(M, N, z)
         S_ = 2 if z else 1
@@ -528,3 +535,32 @@ def tsmm_pick(M: int, N: int, z: bool) -> dict:
     if M * N >= 32 and N >= 4:
         return tsmm_mma_default(M, N, z)
     return tsmm_default(M, N, z)
+
+
+def tsmm_cst_configs(M: int, N: int, z: bool) -> list:
+    """C-stationary DMMA TSMM candidates: NBW column blocks per warp such that
+    the warp's C slice (MK x NBW fragments) fits in <= 48 registers-doubles."""
+    if not tma_ok(M, N, z):
+        return []
+    S = 2 if z else 1
+    MK, NB = cdiv(M, 4), cdiv(N, 8)
+    out = []
+    for NBW in range(1, NB + 1):
+        if (NBW * 8 * S) % 16 or MK * NBW * S > 48:
+            continue
+        NG = cdiv(NB, NBW)
+        for RG in (1, 2, 4):
+            NW = NG * RG
+            if NW > 16 or NW < 2:
+                continue
+            for WR in (1, 2, 4):
+                if WR * NBW * 2 * S > 32:
+                    continue
+                rpp = 8 * WR * RG
+                if rpp > 256:
+                    continue
+                ab = cdiv(M * S, 16) * 128
+                for tgt in (16384, 32768):
+                    R = rpp * max(1, min(256 // rpp, round(tgt / (rpp * ab))))
+                    out.append(dict(NBW=NBW, WR=WR, NT=(NW + 1) * 32, R=R, impl=3))
+    return out
