@@ -188,6 +188,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--deterministic", action="store_true")
+    ap.add_argument("--force-comm", action="store_true",
+                    help="use the NCCL process group + libtsm comm path even with one rank")
     ap.add_argument("--report", default="", help="write the per-kernel table (JSON) here")
     args = ap.parse_args()
 
@@ -206,7 +208,12 @@ def main():
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
+    dist_on = world > 1 or args.force_comm
+    if dist_on:
+        if "RANK" not in os.environ:  # single process without torchrun (--force-comm)
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29517")
+            os.environ.update(RANK="0", WORLD_SIZE="1", LOCAL_RANK="0")
         dist.init_process_group("nccl", device_id=dev)
         comm = tsm.Comm(rank, world, local, deterministic=args.deterministic)
     else:
@@ -289,7 +296,7 @@ def main():
     clocks = ClockSampler(local)
     clocks.start()
     time.sleep(0.4)
-    if world > 1:
+    if dist_on:
         dist.barrier()
     torch.cuda.synchronize()
     t0 = torch.cuda.Event(enable_timing=True)
@@ -299,11 +306,11 @@ def main():
         step(evs[s])
     t1.record(stream)
     torch.cuda.synchronize()
-    if world > 1:
+    if dist_on:
         dist.barrier()
     clk = clocks.stop()
     total_ms = t0.elapsed_time(t1)
-    if world > 1:
+    if dist_on:
         tt = torch.tensor([total_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         total_ms = float(tt.item())
@@ -398,7 +405,7 @@ def main():
 
         e2e_step()
         torch.cuda.synchronize()
-        if world > 1:
+        if dist_on:
             dist.barrier()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
@@ -408,7 +415,7 @@ def main():
         e1.record(stream)
         torch.cuda.synchronize()
         e_ms = e0.elapsed_time(e1) / args.e2e_steps
-        if world > 1:
+        if dist_on:
             tt = torch.tensor([e_ms], dtype=torch.float64, device=dev)
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             e_ms = float(tt.item())

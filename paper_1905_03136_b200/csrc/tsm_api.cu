@@ -228,6 +228,15 @@ static tsm_status validate_config(const KernelEntry& e) {
   if (e.stages < 2 || e.stages > 16) return bad("stages must be in [2, 16]");
   if (e.ctas_per_sm < 1) return bad("ctas_per_sm must be >= 1");
   if (e.impl < 0 || e.impl > 3) return bad("kernel must be 0 (DFMA), 1 (DMMA), 2 (DMMA + TMA), 3 (TSMM C-stationary)");
+  if (e.edge) {
+    if (e.op != KIND_TSMTTSM || (e.impl != 1 && e.impl != 2))
+      return bad("the edge flag (kernel | 16) applies to the DMMA TSMTTSM kernels 1 and 2");
+    if (e.M < 8 || e.N < 8 || (e.M % 8 == 0 && e.N % 8 == 0))
+      return bad("edge mode needs M, N >= 8 and a width that is not a multiple of 8");
+    const int S = e.dt == TSM_Z ? 2 : 1;
+    const int E = e.M * e.N - (e.M / 8) * 8 * (e.N / 8) * 8;
+    if ((E + 31) / 32 * S > 32) return bad("edge too large for one DFMA warp (<= 32 cells per lane)");
+  }
   if (e.impl == 3) {
     const int S = e.dt == TSM_Z ? 2 : 1;
     if (e.op != KIND_TSMM) return bad("kernel 3 (C-stationary DMMA) is a TSMM kernel");
@@ -254,17 +263,17 @@ static tsm_status validate_config(const KernelEntry& e) {
     if ((e.M * S) % 2 || (e.N * S) % 2 || e.M * S < 16 || e.N * S < 16)
       return bad("kernel 2 needs 16-byte rows of >= 128 bytes (M*S, N*S even and >= 16)");
     if (e.R % 8 || e.R > 256) return bad("kernel 2 needs rows_per_chunk a multiple of 8, <= 256");
-    const int MB = (e.M + 7) / 8, NB = (e.N + 7) / 8;
+    const int MB = e.edge ? e.M / 8 : (e.M + 7) / 8, NB = e.edge ? e.N / 8 : (e.N + 7) / 8;
     if (e.p0 < 1 || e.p1 < 1 || e.p0 > MB || e.p1 > NB) return bad("WM, WN must be in [1, ceil(M/8)], [1, ceil(N/8)]");
     const int WT = ((MB + e.p0 - 1) / e.p0) * ((NB + e.p1 - 1) / e.p1);
-    const int NW = e.NT / 32 - 1;
+    const int NW = e.NT / 32 - 1 - e.edge;
     if (NW < WT || NW % WT) return bad("threads/32 - 1 consumer warps must be a multiple of the warp tiles");
     if (e.R % (4 * (NW / WT))) return bad("rows_per_chunk must be a multiple of 4 * row slots");
   } else if (e.op == KIND_TSMTTSM && e.impl == 1) {
-    const int MB = (e.M + 7) / 8, NB = (e.N + 7) / 8;
+    const int MB = e.edge ? e.M / 8 : (e.M + 7) / 8, NB = e.edge ? e.N / 8 : (e.N + 7) / 8;
     if (e.p0 < 1 || e.p1 < 1 || e.p0 > MB || e.p1 > NB) return bad("WM, WN must be in [1, ceil(M/8)], [1, ceil(N/8)]");
     const int WT = ((MB + e.p0 - 1) / e.p0) * ((NB + e.p1 - 1) / e.p1);
-    const int NW = e.NT / 32 - 1;
+    const int NW = e.NT / 32 - 1 - e.edge;
     if (NW < WT || NW % WT) return bad("threads/32 - 1 consumer warps must be a multiple of the warp tiles");
     if (e.R % 4) return bad("rows_per_chunk must be a multiple of 4 for the DMMA kernel");
     const int S = e.dt == TSM_Z ? 2 : 1;
@@ -374,7 +383,8 @@ tsm_status tsm_plan_create_config(tsm_plan* out, tsm_op op, tsm_dtype dtype, int
   e.R = cfg->rows_per_chunk;
   e.p0 = cfg->p0;
   e.p1 = cfg->p1;
-  e.impl = cfg->kernel;
+  e.impl = cfg->kernel & 15;
+  e.edge = (cfg->kernel >> 4) & 1;
   e.p2 = (op == TSM_OP_TSMTTSM && e.impl == 0) ? 0 : cfg->p2;
   e.p3 = (op == TSM_OP_TSMTTSM && e.impl >= 1) ? cfg->p3 : 0;
   e.stages = cfg->stages;
@@ -392,7 +402,7 @@ tsm_status tsm_plan_get_config(tsm_plan p, tsm_config* cfg) {
   cfg->p1 = p->k->p1;
   cfg->p2 = p->k->p2;
   cfg->p3 = p->k->p3;
-  cfg->kernel = p->k->impl;
+  cfg->kernel = p->k->impl | (p->k->edge << 4);
   cfg->stages = p->stages;
   cfg->ctas_per_sm = p->ctas_per_sm;
   return TSM_SUCCESS;
@@ -575,7 +585,8 @@ tsm_status tsm_plan_describe(tsm_plan p, int64_t K, char* buf, size_t len) {
              "\"kernel\":\"%s\"}",
              p->dt ? 'z' : 'd', p->M, p->N, k->p0, k->p1, k->p2, k->p3, k->NT, k->R, p->stages,
              p->ctas_per_sm, p->smem, g.grid, g.nchunks, g.nfin, p->jit ? "true" : "false",
-             k->impl == 2 ? "dmma+tma" : "dmma");
+             k->impl == 2 ? (k->edge ? "dmma+tma+dfma-edge" : "dmma+tma")
+                          : (k->edge ? "dmma+dfma-edge" : "dmma"));
   else if (p->op == TSM_OP_TSMTTSM)
     snprintf(tmp, sizeof tmp,
              "{\"op\":\"tsmttsm\",\"dtype\":\"%c\",\"M\":%d,\"N\":%d,\"MT\":%d,\"NTL\":%d,"

@@ -498,22 +498,31 @@ __device__ __forceinline__ void mbar_arrive(u64* bar) {
 // smem wavefronts; the producer then issues one bulk copy per row.
 // TMA = true: A and B arrive by 2-D tensor copies into 128B-swizzled boxes
 // (AP, BP ignored; requires M*S and N*S even and >= 16 doubles).
+// EDGE = true: DMMA covers only the 8-aligned core MC x NC of C
+// (MC = 8*floor(M/8)); one extra consumer warp computes the E = M*N - MC*NC
+// edge cells with DFMA (worth it when M or N is just above a multiple of 8,
+// where 8x8 blocks would waste up to (ceil8(M)/M)^2 of the DMMA work).
 template <int M_, int N_, bool Z_, int WM_, int WN_, int NW_, int R_, int AP_ = M_, int BP_ = N_,
-          bool TMA_ = false>
+          bool TMA_ = false, bool EDGE_ = false>
 struct TsmttsmMmaCfg {
   static constexpr int M = M_, N = N_, WM = WM_, WN = WN_, NW = NW_, R = R_;
-  static constexpr bool Z = Z_, TMA = TMA_;
+  static constexpr bool Z = Z_, TMA = TMA_, EDGE = EDGE_;
   static constexpr int S = Z ? 2 : 1;
   static constexpr int NBA = (M * S + 15) / 16, NBB = (N * S + 15) / 16;  // 16-double boxes
   static constexpr int AP = TMA ? NBA * 16 / S : AP_, BP = TMA ? NBB * 16 / S : BP_;
   static_assert(!TMA || ((M * S) % 2 == 0 && (N * S) % 2 == 0 && M * S >= 16 && N * S >= 16),
                 "TMA tensor path: 16-byte rows of >= 128 bytes");
   static_assert(!TMA || R % 8 == 0, "TMA swizzle atoms are 8 rows");
-  static constexpr int MB = (M + 7) / 8, NB = (N + 7) / 8;      // 8x8 blocks of C
+  static constexpr int MC = EDGE ? (M / 8) * 8 : M, NC = EDGE ? (N / 8) * 8 : N;  // DMMA core
+  static constexpr int MB = (MC + 7) / 8, NB = (NC + 7) / 8;   // 8x8 blocks of the core
+  static constexpr int E = M * N - MC * NC;                    // edge cells (DFMA warp)
+  static constexpr int TE = (E + 31) / 32;                     // edge cells per lane
+  static constexpr int NE = EDGE ? 1 : 0;                      // edge warps
+  static_assert(!EDGE || (MB >= 1 && NB >= 1 && E > 0), "edge mode needs a core and an edge");
   static constexpr int WTM = (MB + WM - 1) / WM, WTN = (NB + WN - 1) / WN;
   static constexpr int WT = WTM * WTN;                          // warp tiles covering C
   static constexpr int RS = NW / WT;                            // row slots (k-step groups)
-  static constexpr int NT = (NW + 1) * 32;                      // + producer warp
+  static constexpr int NT = (NW + NE + 1) * 32;                 // + edge + producer warp
   static constexpr int CELLS = M * N * S;
   static constexpr int STAGE_DOUBLES = R * (AP + BP) * S;
   static_assert(NW % WT == 0 && RS >= 1, "consumer warps must be a multiple of the warp tiles");
@@ -547,7 +556,7 @@ __global__ void __launch_bounds__(Cfg::NT) tsmttsm_mma_kernel(const __grid_const
   if (tid == 0) {
     for (int s = 0; s < stages; s++) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], NW);
+      mbar_init(&empty[s], NW + Cfg::NE);  // consumer + edge warps release a stage
     }
     fence_mbar_init();
     fence_proxy_async_smem();
@@ -629,7 +638,49 @@ __global__ void __launch_bounds__(Cfg::NT) tsmttsm_mma_kernel(const __grid_const
     }
   };
 
-  if (warp == NW) {
+  // edge cells (EDGE mode): lane owns cells e = lane + 32 t of the strip
+  // {m >= MC} x [0, N)  followed by  [0, MC) x {n >= NC}
+  constexpr int TE = Cfg::EDGE ? Cfg::TE : 1;
+  double eacc[TE][S];
+  int em[TE], en[TE];
+  if constexpr (Cfg::EDGE) {
+    constexpr int MR = M - Cfg::MC, NR = (N - Cfg::NC) > 0 ? (N - Cfg::NC) : 1;
+#pragma unroll
+    for (int t = 0; t < TE; t++) {
+      const int e = lane + 32 * t;
+      if (e < MR * N) {
+        em[t] = Cfg::MC + e / N;
+        en[t] = e % N;
+      } else {
+        const int e2 = e - MR * N;
+        em[t] = e2 / NR;
+        en[t] = Cfg::NC + e2 % NR;
+      }
+      if (e >= Cfg::E) em[t] = -1;  // no cell
+#pragma unroll
+      for (int z = 0; z < S; z++) eacc[t][z] = 0.0;
+    }
+  }
+  // DFMA over rows [0, rows) of a stage (or of global memory: the odd tail row)
+  auto edge_rows = [&](const double* __restrict__ sA, const double* __restrict__ sB, int rows, int ap,
+                       int bp) {
+#pragma unroll 2
+    for (int r = 0; r < rows; r++) {
+#pragma unroll
+      for (int t = 0; t < TE; t++) {
+        if (em[t] < 0) continue;
+        if constexpr (!Cfg::Z) {
+          eacc[t][0] = fma(sA[off(r, em[t], ap)], sB[off(r, en[t], bp)], eacc[t][0]);
+        } else {
+          const double2 a = *reinterpret_cast<const double2*>(sA + off(r, em[t], ap));
+          const double2 b = *reinterpret_cast<const double2*>(sB + off(r, en[t], bp));
+          zfma(eacc[t][0], eacc[t][1], a.x, a.y, b.x, b.y);
+        }
+      }
+    }
+  };
+
+  if (warp == NW + Cfg::NE) {
     // ---------------- producer warp: bulk / tensor copies into the ring ----------------
     const u64 pol = policy_evict_first();
     Ring ring_it;
@@ -666,6 +717,22 @@ __global__ void __launch_bounds__(Cfg::NT) tsmttsm_mma_kernel(const __grid_const
             bulk_g2s(dB + r * BP * S, p.B + (r0 + r) * N * S, static_cast<u32>(N * S * 8), &full[s], pol);
         }
       }
+    }
+  } else if (Cfg::EDGE && warp == NW) {
+    // ---------------- edge warp: DFMA on the cells outside the DMMA core ----------------
+    Ring ring_it;
+    for (long long c = blockIdx.x; c < p.nchunks; c += G, ring_it.next(stages)) {
+      const int s = ring_it.s;
+      mbar_wait(&full[s], ring_it.ph);
+      const double* sA = ring + static_cast<long long>(s) * Cfg::STAGE_DOUBLES;
+      const double* sB = sA + R * AP * S;
+      const long long r0 = c * R;
+      edge_rows(sA, sB, Cfg::TMA ? R : static_cast<int>((K_even - r0 < R) ? (K_even - r0) : R), AP, BP);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+    }
+    if constexpr (!Cfg::TMA) {
+      if ((K & 1) && blockIdx.x == 0) edge_rows(p.A + (K - 1) * M * S, p.B + (K - 1) * N * S, 1, M, N);
     }
   } else {
     // ---------------- consumer warps ----------------
@@ -716,6 +783,16 @@ __global__ void __launch_bounds__(Cfg::NT) tsmttsm_mma_kernel(const __grid_const
             }
           }
         }
+      }
+    }
+    if constexpr (Cfg::EDGE) {  // edge cells are disjoint from the core: written once
+      if (warp == NW && sl == 0) {
+#pragma unroll
+        for (int t = 0; t < TE; t++)
+          if (em[t] >= 0) {
+#pragma unroll
+            for (int z = 0; z < S; z++) sP[(em[t] * N + en[t]) * S + z] = eacc[t][z];
+          }
       }
     }
     __syncthreads();

@@ -17,7 +17,9 @@ struct KernelEntry {
   int p0, p1, p2, p3;  // DMMA TSMTTSM: WM, WN, AP, BP; DMMA TSMM: WR, AP, NOP, -
   int stages;        // default pipeline depth
   int ctas_per_sm;   // target resident CTAs per SM (clipped by occupancy)
-  int impl;          // 0 = register-tile DFMA kernel, 1 = DMMA (mma.sync m8n8k4 f64) kernel
+  int impl;          // 0 = register-tile DFMA kernel, 1 = DMMA (mma.sync m8n8k4 f64) kernel,
+                     // 2 = DMMA + TMA tensor copies, 3 = C-stationary DMMA TSMM
+  int edge;          // DMMA TSMTTSM: DFMA edge warp for the cells outside the 8-aligned core
 };
 
 struct KernelTable {

@@ -90,3 +90,32 @@ def test_cstationary_int_bitwise(tsm, cplx):
         got = tsm.tsmm(torch.from_numpy(A).cuda(), torch.from_numpy(Cm).cuda(), plan=plan)
         torch.cuda.synchronize()
         assert np.array_equal(got.cpu().numpy(), ref), c
+
+
+@pytest.mark.parametrize("cplx", [False, True], ids=["D", "Z"])
+@pytest.mark.parametrize("M,N", [(49, 49), (33, 17), (17, 33), (57, 58), (9, 10)])
+def test_dmma_edge_warp(tsm, M, N, cplx):
+    """DMMA core + DFMA edge warp (kernel | 16): every edge candidate family."""
+    dt = "z" if cplx else "d"
+    cands = gi.edge_candidates(M, N, cplx)
+    assert cands
+    picked = {}
+    for c in cands:
+        picked.setdefault(c["impl"], c)
+    for impl, c in picked.items():
+        plan = tsm.Plan("tsmttsm", dt, M, N, 0, config=gi.to_tsm_config("tsmttsm", c, 3, 2))
+        assert plan.config()["kernel"] == impl | 16
+        assert "edge" in plan.describe(1000)["kernel"]
+        for K in (1, 7, 4099, 65537):
+            A = ti.matrix(K, M, "A", complex_=cplx, seed=K + 1)
+            B = ti.matrix(K, N, "B", complex_=cplx, seed=K + 2)
+            got = tsm.tsmttsm(torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda(), plan=plan)
+            torch.cuda.synchronize()
+            ref, bound = oracle.tsmttsm(A, B)
+            r, wi, _ = oracle.max_err_ratio(got.cpu().numpy(), ref, bound)
+            assert r <= 1e-12, (M, N, impl, c, K, r, wi)
+        Ai = ti.matrix(70001, M, "A", complex_=cplx, mode="int")
+        Bi = ti.matrix(70001, N, "B", complex_=cplx, mode="int")
+        got = tsm.tsmttsm(torch.from_numpy(Ai).cuda(), torch.from_numpy(Bi).cuda(), plan=plan)
+        torch.cuda.synchronize()
+        assert np.array_equal(got.cpu().numpy(), oracle.tsmttsm(Ai, Bi)[0])

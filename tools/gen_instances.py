@@ -122,6 +122,45 @@ def tsmttsm_mma_default(M: int, N: int, z: bool) -> dict:
                 AP=pick_stride(M, z, "t"), BP=pick_stride(N, z, "t"))
 
 
+def edge_candidates(M: int, N: int, z: bool) -> list:
+    """DMMA on the 8-aligned core + one DFMA edge warp (EDGE=1), for widths
+    just above a multiple of 8 (M % 8 or N % 8 in 1..3)."""
+    if M < 8 or N < 8 or (M % 8 not in (1, 2, 3) and N % 8 not in (1, 2, 3)):
+        return []
+    S = 2 if z else 1
+    E = M * N - (M // 8) * 8 * (N // 8) * 8
+    if cdiv(E, 32) * S > 32:
+        return []
+    MB, NB = M // 8, N // 8
+    wmax = 8 if z else 16
+    wt = []
+    for WM in range(1, min(MB, 8) + 1):
+        for WN in range(1, min(NB, 8) + 1):
+            if WM * WN > wmax or cdiv(MB, WM) * cdiv(NB, WN) > 16:
+                continue
+            bal = cdiv(MB, WM) * WM * cdiv(NB, WN) * WN / (MB * NB)
+            wt.append((bal * (1 + 0.5 * (WM + WN) / (WM * WN)), WM, WN))
+    wt.sort()
+    out = []
+    row = (M + N) * 8 * S
+    for (_, WM, WN) in wt[:3]:
+        WT = cdiv(MB, WM) * cdiv(NB, WN)
+        for k in (1, 2, 4):
+            NW = WT * k
+            if NW > 16 or NW < 2:
+                continue
+            for tgt in (16384, 32768):
+                out.append(dict(MT=WM, NTL=WN, NT=(NW + 2) * 32, R=_rows(4 * k, row, tgt), impl=1,
+                                AP=M, BP=N, EDGE=1))
+                if tma_ok(M, N, z):
+                    tb = (cdiv(M * S, 16) + cdiv(N * S, 16)) * 128
+                    step = 4 * k if (4 * k) % 8 == 0 else 8 * k
+                    Rt = min(256 // step * step, max(step, (tgt // tb) // step * step))
+                    out.append(dict(MT=WM, NTL=WN, NT=(NW + 2) * 32, R=Rt, impl=2, AP=M, BP=N,
+                                    EDGE=1))
+    return out
+
+
 def tma_ok(M: int, N: int, z: bool) -> bool:
     """2-D tensor maps need 16-byte global row strides; boxes are 16 doubles."""
     S = 2 if z else 1
@@ -214,8 +253,9 @@ def cfg_type(op, dt, M, N, c) -> str:
     z = "true" if dt == "z" else "false"
     if op == "tsmttsm" and c.get("impl", 0) >= 1:
         tma = "true" if c["impl"] == 2 else "false"
-        return (f"tsm::TsmttsmMmaCfg<{M}, {N}, {z}, {c['MT']}, {c['NTL']}, {c['NT'] // 32 - 1}, "
-                f"{c['R']}, {c.get('AP', M)}, {c.get('BP', N)}, {tma}>")
+        edge = c.get("EDGE", 0)
+        return (f"tsm::TsmttsmMmaCfg<{M}, {N}, {z}, {c['MT']}, {c['NTL']}, {c['NT'] // 32 - 1 - edge}, "
+                f"{c['R']}, {c.get('AP', M)}, {c.get('BP', N)}, {tma}, {'true' if edge else 'false'}>")
     if op == "tsmttsm":
         return f"tsm::TsmttsmCfg<{M}, {N}, {z}, {c['MT']}, {c['NTL']}, {c['NT']}, {c['R']}>"
     if c.get("impl", 0) == 3:
@@ -240,7 +280,8 @@ def entry_init(op, dt, M, N, c) -> str:
         kind = "tsm::KIND_TSMM"
     p = params4(op, M, N, c)
     return (f"  {{{kind}, {1 if dt == 'z' else 0}, {M}, {N}, {fn}, {c['NT']}, {c['R']}, "
-            f"{p[0]}, {p[1]}, {p[2]}, {p[3]}, {c['stages']}, {c['ctas']}, {c.get('impl', 0)}}},")
+            f"{p[0]}, {p[1]}, {p[2]}, {p[3]}, {c['stages']}, {c['ctas']}, {c.get('impl', 0)}, "
+            f"{c.get('EDGE', 0)}}},")
 
 
 def params4(op: str, M: int, N: int, c: dict) -> tuple:
@@ -306,7 +347,8 @@ def main(per_file: int = 12) -> int:
                     p = params4(op, M, N, c)
                     lines.append(f"  {{{0 if op == 'tsmttsm' else 1}, {1 if dt == 'z' else 0}, {M}, {N}, "
                                  f"nullptr, {c['NT']}, {c['R']}, {p[0]}, {p[1]}, {p[2]}, {p[3]}, "
-                                 f"{c['stages']}, {c['ctas']}, {c.get('impl', 0)}}},")
+                                 f"{c['stages']}, {c['ctas']}, {c.get('impl', 0)}, "
+                                 f"{c.get('EDGE', 0)}}},")
     lines += ["};", "}  // namespace tsm", ""]
     _write(os.path.join(GEN, "params_gen.cpp"), "\n".join(lines))
 
@@ -399,6 +441,7 @@ def candidates(op: str, M: int, N: int, z: bool) -> list:
                             Rt = min(256 // step * step, max(step, (tgt // tb) // step * step))
                             out.append(dict(MT=WM, NTL=WN, NT=(NW + 1) * 32, R=Rt, impl=2,
                                             AP=M, BP=N))
+            out.extend(edge_candidates(M, N, z))
     else:
         acc_max = 16 if z else 32
         NTL = 1
@@ -458,7 +501,7 @@ def to_tsm_config(op: str, c: dict, stages: int, ctas: int) -> dict:
     else:
         p = _tsmm_p(c) + (0,)
     return dict(threads=c["NT"], rows_per_chunk=c["R"], p0=p[0], p1=p[1], p2=p[2], p3=p[3],
-                stages=stages, ctas_per_sm=ctas, kernel=c.get("impl", 0))
+                stages=stages, ctas_per_sm=ctas, kernel=c.get("impl", 0) | (c.get("EDGE", 0) << 4))
 
 
 # ---------------------------------------------------------------------------
