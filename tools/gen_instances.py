@@ -429,7 +429,9 @@ def candidates(op: str, M: int, N: int, z: bool) -> list:
                     if NW > 16:
                         break
                     pads = [False] + ([True] if min(M, N) * S * 8 >= 384 else [])
-                    for tgt in (16384, 32768):
+                    # big stages (64 KB, run with 2-3 stages) give each warp more
+                    # k-steps per mbarrier round trip
+                    for tgt in (16384, 32768, 65536):
                         for pad in pads:
                             out.append(dict(MT=WM, NTL=WN, NT=(NW + 1) * 32,
                                             R=_rows(4 * k, row, tgt), impl=1,
