@@ -43,6 +43,18 @@ def peaks():
         return 6.65e12, "fallback"
 
 
+def bench_config(args, widths, world):
+    """The workload description shared by the libtsm arm and the reference arm."""
+    z = args.dtype == "z"
+    return {"workload": f"configs[1] sweep: {'Z' if z else 'D'} M=N {widths[0]}..{widths[-1]}, "
+                        "tsmttsm then tsmm per step",
+            "K_per_gpu": args.K, "widths": f"{widths[0]}..{widths[-1]}",
+            "l2": "inputs > L2 (>=268 MB per kernel), no flush",
+            "parallelism": f"K-sharded x{world}" if world > 1 else "single GPU",
+            "collectives": ("allgather+rank-order sum" if args.deterministic else "nccl allreduce")
+                           + " of C, nccl broadcast of C" if world > 1 else "none"}
+
+
 def sizes(op, M, N, K, z):
     s = 16 if z else 8
     byts = s * (K * M + K * N + M * N)
@@ -160,8 +172,7 @@ def run_reference(args, rank, world):
             "warmup": args.warmup, "ms_per_step": 1e3 * tt / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "impl": "reference",
-            "config": {"workload": f"{args.dtype.upper()} M=N 1..64 sweep, tsmttsm then tsmm",
-                       "K": K, "widths": "1..64"},
+            "config": bench_config(args, widths, world),
             "cpu_baseline": {"value": v, "unit": "GB/s", "cores": cores, "kind": "oracle",
                              "sample": sample},
             "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -360,14 +371,7 @@ def main():
             "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms_step,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
-            "config": {"workload": f"configs[1] sweep: {'Z' if z else 'D'} M=N "
-                                   f"{widths[0]}..{widths[-1]}, tsmttsm then tsmm per step",
-                       "K_per_gpu": K, "widths": f"{widths[0]}..{widths[-1]}",
-                       "l2": "inputs > L2 (>=268 MB per kernel), no flush",
-                       "parallelism": f"K-sharded x{world}" if world > 1 else "single GPU",
-                       "collectives": ("allgather+rank-order sum" if args.deterministic else
-                                       "nccl allreduce") + " of C, nccl broadcast of C"
-                       if world > 1 else "none"},
+            "config": bench_config(args, widths, world),
             "roofline": roofline,
             "roofline_step": {"frac": roof_sum / (tot_k * 1e-3),
                               "min_frac": min(r["frac"] for r in rows),
@@ -391,17 +395,47 @@ def main():
             d2h += (K * M + M * M) * hA.element_size()
             e2e_bytes += sizes("tsmttsm", M, M, K, z)[0] + sizes("tsmm", M, M, K, z)[0]
 
+        # PCIe is full duplex: width i+1's H2D (s_in) overlaps width i's kernels
+        # (compute stream) and width i-1's D2H (s_out); device buffers are
+        # double-buffered (two halves of the K x 64 buffers) with events
+        # guarding reuse.
+        s_in = torch.cuda.Stream(dev)
+        s_out = torch.cuda.Stream(dev)
+        half = K * (maxw // 2) if 2 * mw <= maxw else 0
+        nbuf = 2 if half else 1
+
         def e2e_step():
-            for M in e2w:
-                dA = Abuf[: K * M].view(K, M)
-                dB = Bbuf[: K * M].view(K, M)
-                dA.copy_(hA[: K * M].view(K, M), non_blocking=True)
-                dB.copy_(hB[: K * M].view(K, M), non_blocking=True)
+            ev_in, ev_comp, ev_out = {}, {}, {}
+            s_in.wait_stream(stream)  # previous step's kernels are done with the buffers
+            s_out.wait_stream(stream)
+            for i, M in enumerate(e2w):
+                off = (i % nbuf) * half
+                dA = Abuf[off: off + K * M].view(K, M)
+                dB = Bbuf[off: off + K * M].view(K, M)
+                dO = Obuf[off: off + K * M].view(K, M)
+                with torch.cuda.stream(s_in):
+                    if i >= nbuf:  # the kernels of width i-nbuf have finished reading this buffer
+                        s_in.wait_event(ev_comp[i - nbuf])
+                    dA.copy_(hA[: K * M].view(K, M), non_blocking=True)
+                    dB.copy_(hB[: K * M].view(K, M), non_blocking=True)
+                    ev_in[i] = torch.cuda.Event()
+                    ev_in[i].record(s_in)
+                stream.wait_event(ev_in[i])
+                if i >= nbuf:  # D2H of width i-nbuf has read this buffer of Obuf
+                    stream.wait_event(ev_out[i - nbuf])
                 C = tsm.tsmttsm(dA, dB, out=Cs[M], plan=plans[("tsmttsm", M)]) if comm is None \
                     else tsm.tsmttsm_allreduce(comm, dA, dB, out=Cs[M])
-                O = tsm.tsmm(dA, C, out=Obuf[: K * M].view(K, M), plan=plans[("tsmm", M)])
-                hC[M].copy_(C, non_blocking=True)
-                hO[: K * M].view(K, M).copy_(O, non_blocking=True)
+                O = tsm.tsmm(dA, C, out=dO, plan=plans[("tsmm", M)])
+                ev_comp[i] = torch.cuda.Event()
+                ev_comp[i].record(stream)
+                with torch.cuda.stream(s_out):
+                    s_out.wait_event(ev_comp[i])
+                    hC[M].copy_(C, non_blocking=True)
+                    hO[: K * M].view(K, M).copy_(O, non_blocking=True)
+                    ev_out[i] = torch.cuda.Event()
+                    ev_out[i].record(s_out)
+            stream.wait_stream(s_in)
+            stream.wait_stream(s_out)
 
         e2e_step()
         torch.cuda.synchronize()
@@ -423,8 +457,9 @@ def main():
                        "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                        "widths": e2w, "ms_per_step": e_ms,
                        "note": "pinned host A,B -> device, tsmttsm + tsmm via the public API, "
-                               "C and B' -> pinned host; bytes counted as the kernels' "
-                               "algorithmic bytes (same metric as value)"}
+                               "C and B' -> pinned host; H2D / kernels / D2H of consecutive "
+                               "widths overlap on three streams (PCIe full duplex); bytes "
+                               "counted as the kernels' algorithmic bytes (same metric as value)"}
         del hA, hB, hO
 
     # ---------------- cpu baseline (rank 0, N=1 only) ----------------
