@@ -171,6 +171,12 @@ __device__ __forceinline__ void tma_store_2d(const TmaDesc* desc, int x, int y, 
                "r"(x), "r"(y), "r"(smem_u32(src))
                : "memory");
 }
+// Byte offset o' >= o such that base + o' is 1024-byte aligned in the shared
+// window (computed from the shared address, applied as pointer arithmetic).
+__device__ __forceinline__ int align1024(const void* base, int o) {
+  const u32 a = smem_u32(base) + static_cast<u32>(o);
+  return o + static_cast<int>((1024u - (a & 1023u)) & 1023u);
+}
 // offset (doubles) of element (r, c), c < 16, inside a 128B-swizzled box region
 __device__ __forceinline__ int swz128(int r, int c) {
   return r * 16 + ((((c >> 1) ^ r) & 7) << 1) + (c & 1);
@@ -540,10 +546,10 @@ __global__ void __launch_bounds__(Cfg::NT) tsmttsm_mma_kernel(const __grid_const
   extern __shared__ __align__(128) unsigned char smem_raw[];
   u64* full = reinterpret_cast<u64*>(smem_raw);
   u64* empty = full + 16;
-  // ring: 1024-byte aligned for the 128B-swizzle atoms of the TMA boxes
-  double* ring = reinterpret_cast<double*>(
-      Cfg::TMA ? ((reinterpret_cast<u64>(smem_raw) + 256 + 1023) & ~1023ull)
-               : reinterpret_cast<u64>(smem_raw) + 256);
+  // ring: 1024-byte aligned for the 128B-swizzle atoms of the TMA boxes.
+  // Pointer arithmetic on smem_raw (never an integer round trip) keeps the
+  // shared address space visible to the compiler: fragment loads stay LDS.
+  double* ring = reinterpret_cast<double*>(smem_raw + (Cfg::TMA ? align1024(smem_raw, 256) : 256));
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
@@ -1067,10 +1073,11 @@ __global__ void __launch_bounds__(Cfg::NT) tsmm_mma_kernel(const __grid_constant
   u64* empty = full + 16;
   double* sC = reinterpret_cast<double*>(smem_raw + 256);
   // staging and ring start on 1024-byte boundaries (128B swizzle atoms)
-  const u64 after_c = reinterpret_cast<u64>(sC + ((Cfg::C_DOUBLES + 15) / 16) * 16);
-  double* sOut = reinterpret_cast<double*>(Cfg::TMA ? ((after_c + 1023) & ~1023ull) : after_c);
-  const u64 after_o = reinterpret_cast<u64>(sOut + ((NW * Cfg::OUT_DOUBLES + 15) / 16) * 16);
-  double* ring = reinterpret_cast<double*>(Cfg::TMA ? ((after_o + 1023) & ~1023ull) : after_o);
+  const int after_c = 256 + ((Cfg::C_DOUBLES + 15) / 16) * 16 * 8;  // byte offsets
+  double* sOut = reinterpret_cast<double*>(smem_raw + (Cfg::TMA ? align1024(smem_raw, after_c) : after_c));
+  unsigned char* after_o = reinterpret_cast<unsigned char*>(sOut + ((NW * Cfg::OUT_DOUBLES + 15) / 16) * 16);
+  double* ring = reinterpret_cast<double*>(
+      after_o + (Cfg::TMA ? align1024(after_o, 0) : 0));
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
@@ -1326,7 +1333,7 @@ __global__ void __launch_bounds__(Cfg::NT) tsmm_cst_kernel(const __grid_constant
   extern __shared__ __align__(128) unsigned char smem_raw[];
   u64* full = reinterpret_cast<u64*>(smem_raw);
   u64* empty = full + 16;
-  double* sOut = reinterpret_cast<double*>((reinterpret_cast<u64>(smem_raw) + 256 + 1023) & ~1023ull);
+  double* sOut = reinterpret_cast<double*>(smem_raw + align1024(smem_raw, 256));
   double* ring = sOut + NW * Cfg::OUT_DOUBLES;  // multiple of 1024 bytes
 
   const int tid = threadIdx.x;
