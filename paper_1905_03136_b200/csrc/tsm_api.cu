@@ -228,7 +228,15 @@ static tsm_status validate_config(const KernelEntry& e) {
   if (e.stages < 2 || e.stages > 16) return bad("stages must be in [2, 16]");
   if (e.ctas_per_sm < 1) return bad("ctas_per_sm must be >= 1");
   if (e.impl < 0 || e.impl > 3) return bad("kernel must be 0 (DFMA), 1 (DMMA), 2 (DMMA + TMA), 3 (TSMM C-stationary)");
-  if (e.edge) {
+  if (e.edge & 2) {  // paired 16-byte fragment loads
+    if (e.op != KIND_TSMTTSM || (e.impl != 1 && e.impl != 2) || e.dt != TSM_D)
+      return bad("the pair flag (kernel | 32) applies to the real DMMA TSMTTSM kernels 1 and 2");
+    if (e.p0 % 2 || e.p1 % 2) return bad("the pair flag needs even WM and WN");
+    if (e.impl == 1 && (e.p2 % 2 || e.p3 % 2 || e.M % 2 || e.N % 2))
+      return bad("the pair flag needs even smem strides (and even M, N for kernel 1)");
+    if (e.edge & 1) return bad("the pair and edge flags are exclusive");
+  }
+  if (e.edge & 1) {
     if (e.op != KIND_TSMTTSM || (e.impl != 1 && e.impl != 2))
       return bad("the edge flag (kernel | 16) applies to the DMMA TSMTTSM kernels 1 and 2");
     if (e.M < 8 || e.N < 8 || (e.M % 8 == 0 && e.N % 8 == 0))
@@ -263,17 +271,23 @@ static tsm_status validate_config(const KernelEntry& e) {
     if ((e.M * S) % 2 || (e.N * S) % 2 || e.M * S < 16 || e.N * S < 16)
       return bad("kernel 2 needs 16-byte rows of >= 128 bytes (M*S, N*S even and >= 16)");
     if (e.R % 8 || e.R > 256) return bad("kernel 2 needs rows_per_chunk a multiple of 8, <= 256");
-    const int MB = e.edge ? e.M / 8 : (e.M + 7) / 8, NB = e.edge ? e.N / 8 : (e.N + 7) / 8;
+    const int ed = e.edge & 1;
+    const int pr = e.edge & 2;  // pair mode: 8x8 blocks in whole 16-wide pairs
+    const int MB = ed ? e.M / 8 : pr ? 2 * ((e.M + 15) / 16) : (e.M + 7) / 8;
+    const int NB = ed ? e.N / 8 : pr ? 2 * ((e.N + 15) / 16) : (e.N + 7) / 8;
     if (e.p0 < 1 || e.p1 < 1 || e.p0 > MB || e.p1 > NB) return bad("WM, WN must be in [1, ceil(M/8)], [1, ceil(N/8)]");
     const int WT = ((MB + e.p0 - 1) / e.p0) * ((NB + e.p1 - 1) / e.p1);
-    const int NW = e.NT / 32 - 1 - e.edge;
+    const int NW = e.NT / 32 - 1 - ed;
     if (NW < WT || NW % WT) return bad("threads/32 - 1 consumer warps must be a multiple of the warp tiles");
     if (e.R % (4 * (NW / WT))) return bad("rows_per_chunk must be a multiple of 4 * row slots");
   } else if (e.op == KIND_TSMTTSM && e.impl == 1) {
-    const int MB = e.edge ? e.M / 8 : (e.M + 7) / 8, NB = e.edge ? e.N / 8 : (e.N + 7) / 8;
+    const int ed = e.edge & 1;
+    const int pr = e.edge & 2;  // pair mode: 8x8 blocks in whole 16-wide pairs
+    const int MB = ed ? e.M / 8 : pr ? 2 * ((e.M + 15) / 16) : (e.M + 7) / 8;
+    const int NB = ed ? e.N / 8 : pr ? 2 * ((e.N + 15) / 16) : (e.N + 7) / 8;
     if (e.p0 < 1 || e.p1 < 1 || e.p0 > MB || e.p1 > NB) return bad("WM, WN must be in [1, ceil(M/8)], [1, ceil(N/8)]");
     const int WT = ((MB + e.p0 - 1) / e.p0) * ((NB + e.p1 - 1) / e.p1);
-    const int NW = e.NT / 32 - 1 - e.edge;
+    const int NW = e.NT / 32 - 1 - ed;
     if (NW < WT || NW % WT) return bad("threads/32 - 1 consumer warps must be a multiple of the warp tiles");
     if (e.R % 4) return bad("rows_per_chunk must be a multiple of 4 for the DMMA kernel");
     const int S = e.dt == TSM_Z ? 2 : 1;
@@ -384,7 +398,7 @@ tsm_status tsm_plan_create_config(tsm_plan* out, tsm_op op, tsm_dtype dtype, int
   e.p0 = cfg->p0;
   e.p1 = cfg->p1;
   e.impl = cfg->kernel & 15;
-  e.edge = (cfg->kernel >> 4) & 1;
+  e.edge = (cfg->kernel >> 4) & 3;
   e.p2 = (op == TSM_OP_TSMTTSM && e.impl == 0) ? 0 : cfg->p2;
   e.p3 = (op == TSM_OP_TSMTTSM && e.impl >= 1) ? cfg->p3 : 0;
   e.stages = cfg->stages;
@@ -585,8 +599,8 @@ tsm_status tsm_plan_describe(tsm_plan p, int64_t K, char* buf, size_t len) {
              "\"kernel\":\"%s\"}",
              p->dt ? 'z' : 'd', p->M, p->N, k->p0, k->p1, k->p2, k->p3, k->NT, k->R, p->stages,
              p->ctas_per_sm, p->smem, g.grid, g.nchunks, g.nfin, p->jit ? "true" : "false",
-             k->impl == 2 ? (k->edge ? "dmma+tma+dfma-edge" : "dmma+tma")
-                          : (k->edge ? "dmma+dfma-edge" : "dmma"));
+             k->impl == 2 ? ((k->edge & 1) ? "dmma+tma+dfma-edge" : (k->edge & 2) ? "dmma+tma+pair" : "dmma+tma")
+                          : ((k->edge & 1) ? "dmma+dfma-edge" : (k->edge & 2) ? "dmma+pair" : "dmma"));
   else if (p->op == TSM_OP_TSMTTSM)
     snprintf(tmp, sizeof tmp,
              "{\"op\":\"tsmttsm\",\"dtype\":\"%c\",\"M\":%d,\"N\":%d,\"MT\":%d,\"NTL\":%d,"

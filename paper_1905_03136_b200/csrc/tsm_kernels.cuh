@@ -508,11 +508,16 @@ __device__ __forceinline__ void mbar_arrive(u64* bar) {
 // (MC = 8*floor(M/8)); one extra consumer warp computes the E = M*N - MC*NC
 // edge cells with DFMA (worth it when M or N is just above a multiple of 8,
 // where 8x8 blocks would waste up to (ceil8(M)/M)^2 of the DMMA work).
+// PAIR = true (D only): blocks are used in pairs covering 16 consecutive m (n);
+// block 2p holds the even, block 2p+1 the odd rows (columns) of the pair, so
+// one 16-byte LDS.128 per lane feeds both fragments (half the load
+// instructions of one LDS.64 per fragment).
 template <int M_, int N_, bool Z_, int WM_, int WN_, int NW_, int R_, int AP_ = M_, int BP_ = N_,
-          bool TMA_ = false, bool EDGE_ = false>
+          bool TMA_ = false, bool EDGE_ = false, bool PAIR_ = false>
 struct TsmttsmMmaCfg {
   static constexpr int M = M_, N = N_, WM = WM_, WN = WN_, NW = NW_, R = R_;
-  static constexpr bool Z = Z_, TMA = TMA_, EDGE = EDGE_;
+  static constexpr bool Z = Z_, TMA = TMA_, EDGE = EDGE_, PAIR = PAIR_;
+  static_assert(!PAIR || (!Z_ && !EDGE_ && WM_ % 2 == 0 && WN_ % 2 == 0), "pairs: real, even tiles, no edge");
   static constexpr int S = Z ? 2 : 1;
   static constexpr int NBA = (M * S + 15) / 16, NBB = (N * S + 15) / 16;  // 16-double boxes
   static constexpr int AP = TMA ? NBA * 16 / S : AP_, BP = TMA ? NBB * 16 / S : BP_;
@@ -520,7 +525,9 @@ struct TsmttsmMmaCfg {
                 "TMA tensor path: 16-byte rows of >= 128 bytes");
   static_assert(!TMA || R % 8 == 0, "TMA swizzle atoms are 8 rows");
   static constexpr int MC = EDGE ? (M / 8) * 8 : M, NC = EDGE ? (N / 8) * 8 : N;  // DMMA core
-  static constexpr int MB = (MC + 7) / 8, NB = (NC + 7) / 8;   // 8x8 blocks of the core
+  // 8x8 blocks of the core (pair mode: whole 16-wide pairs)
+  static constexpr int MB = PAIR ? 2 * ((MC + 15) / 16) : (MC + 7) / 8;
+  static constexpr int NB = PAIR ? 2 * ((NC + 15) / 16) : (NC + 7) / 8;
   static constexpr int E = M * N - MC * NC;                    // edge cells (DFMA warp)
   static constexpr int TE = (E + 31) / 32;                     // edge cells per lane
   static constexpr int NE = EDGE ? 1 : 0;                      // edge warps
@@ -554,6 +561,11 @@ __global__ void __launch_bounds__(Cfg::NT) tsmttsm_mma_kernel(const __grid_const
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, q = lane & 3;
+  // pair mode: lane g loads the 16-byte granule pc(g) of its 16-row band.  Under the
+  // 128B swizzle (TMA) the granules of rows k0..k0+3 are XORed with the row, and
+  // pc(g) = g/2 + 4(g%2) makes the 8 lanes of each LDS.128 phase hit 8 distinct
+  // granules; the dense layout (padded stride) needs the identity.
+  auto pc = [](int x) { return Cfg::TMA ? ((x >> 1) | ((x & 1) << 2)) : x; };
   const long long K = p.K;
   const long long K_even = K & ~1LL;
   const int G = gridDim.x;
@@ -600,15 +612,41 @@ __global__ void __launch_bounds__(Cfg::NT) tsmttsm_mma_kernel(const __grid_const
     const bool rv = (k0 + q) < rows;
     if constexpr (!Cfg::Z) {
       double a[WM], b[WN];
+      if constexpr (Cfg::PAIR) {
+        // one 16-byte load per lane: (m, m+1) -> fragments of blocks 2p, 2p+1
 #pragma unroll
-      for (int i = 0; i < WM; i++) {
-        const int m = (wm * WM + i) * 8 + g;
-        a[i] = (rv && m < M) ? sA[off(k0 + q, m, ap)] : 0.0;
-      }
+        for (int ip = 0; ip < WM / 2; ip++) {
+          const int m = (wm * WM + 2 * ip) * 8 + 2 * pc(g);
+          double2 v = make_double2(0.0, 0.0);
+          if (rv && m + 1 < M)
+            v = *reinterpret_cast<const double2*>(sA + off(k0 + q, m, ap));
+          else if (rv && m < M)
+            v.x = sA[off(k0 + q, m, ap)];
+          a[2 * ip] = v.x;
+          a[2 * ip + 1] = v.y;
+        }
 #pragma unroll
-      for (int j = 0; j < WN; j++) {
-        const int n = (wn * WN + j) * 8 + g;
-        b[j] = (rv && n < N) ? sB[off(k0 + q, n, bp)] : 0.0;
+        for (int jp = 0; jp < WN / 2; jp++) {
+          const int n = (wn * WN + 2 * jp) * 8 + 2 * pc(g);
+          double2 v = make_double2(0.0, 0.0);
+          if (rv && n + 1 < N)
+            v = *reinterpret_cast<const double2*>(sB + off(k0 + q, n, bp));
+          else if (rv && n < N)
+            v.x = sB[off(k0 + q, n, bp)];
+          b[2 * jp] = v.x;
+          b[2 * jp + 1] = v.y;
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < WM; i++) {
+          const int m = (wm * WM + i) * 8 + g;
+          a[i] = (rv && m < M) ? sA[off(k0 + q, m, ap)] : 0.0;
+        }
+#pragma unroll
+        for (int j = 0; j < WN; j++) {
+          const int n = (wn * WN + j) * 8 + g;
+          b[j] = (rv && n < N) ? sB[off(k0 + q, n, bp)] : 0.0;
+        }
       }
 #pragma unroll
       for (int i = 0; i < WM; i++)
@@ -774,12 +812,14 @@ __global__ void __launch_bounds__(Cfg::NT) tsmttsm_mma_kernel(const __grid_const
     if (warp < NW && slot == sl) {
 #pragma unroll
       for (int i = 0; i < WM; i++) {
-        const int m = (wm * WM + i) * 8 + g;
+        // pair mode: blocks 2p / 2p+1 hold the even / odd rows of a 16-row band
+        const int m = Cfg::PAIR ? (wm * WM + (i & ~1)) * 8 + 2 * pc(g) + (i & 1) : (wm * WM + i) * 8 + g;
 #pragma unroll
         for (int j = 0; j < WN; j++) {
 #pragma unroll
           for (int e = 0; e < 2; e++) {
-            const int n = (wn * WN + j) * 8 + 2 * q + e;
+            const int n = Cfg::PAIR ? (wn * WN + (j & ~1)) * 8 + 2 * pc(2 * q + e) + (j & 1)
+                                    : (wn * WN + j) * 8 + 2 * q + e;
             if (m < M && n < N && (wm * WM + i) < MB && (wn * WN + j) < NB) {
 #pragma unroll
               for (int z = 0; z < S; z++) {

@@ -19,7 +19,8 @@ struct KernelEntry {
   int ctas_per_sm;   // target resident CTAs per SM (clipped by occupancy)
   int impl;          // 0 = register-tile DFMA kernel, 1 = DMMA (mma.sync m8n8k4 f64) kernel,
                      // 2 = DMMA + TMA tensor copies, 3 = C-stationary DMMA TSMM
-  int edge;          // DMMA TSMTTSM: DFMA edge warp for the cells outside the 8-aligned core
+  int edge;          // DMMA TSMTTSM flags: bit 0 = DFMA edge warp for the cells outside the
+                     // 8-aligned core, bit 1 = paired 16-byte fragment loads
 };
 
 struct KernelTable {

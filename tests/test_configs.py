@@ -91,3 +91,33 @@ def test_conflict_model_pins():
     assert gi._degree(gi.pick_stride(64, False, "a", pad=True), False, "a") == 1.0
     # odd widths stay dense (rows are not 16-byte multiples)
     assert gi.pick_stride(63, False, "a", pad=True) == 63 and gi.pick_stride(33, False, "t", pad=True) == 33
+
+
+def _lds128_worst(addr):
+    """Max lanes on one 16-byte bank group within an LDS.128 phase (8 lanes)."""
+    worst = 0
+    for ph in range(4):
+        cnt = {}
+        for lane in range(8 * ph, 8 * ph + 8):
+            gran = (addr(lane >> 2, lane & 3) * 8 // 16) % 8
+            cnt[gran] = cnt.get(gran, 0) + 1
+        worst = max(worst, max(cnt.values()))
+    return worst
+
+
+def test_pair_layouts_conflict_free():
+    # padded dense strides: rows 32 B apart modulo 128 -> one granule per lane
+    for w in (16, 20, 32, 40, 48, 56, 64):
+        st = gi.pair_stride(w)
+        assert st >= w and st % 2 == 0
+        assert _lds128_worst(lambda g, q: q * st + 2 * g) == 1, w
+    assert _lds128_worst(lambda g, q: q * 64 + 2 * g) == 4  # dense stride 64: 4-way
+
+    # 128B swizzle (TMA boxes): granule (c/2 ^ row) -- identity lanes conflict 2-way,
+    # the kernel's permutation pc(g) = g/2 + 4(g%2) is conflict-free for every k0
+    def swz(r, c):
+        return r * 16 + ((((c >> 1) ^ r) & 7) << 1) + (c & 1)
+
+    for k0 in (0, 4, 8, 12):
+        assert _lds128_worst(lambda g, q: swz(k0 + q, 2 * g)) == 2
+        assert _lds128_worst(lambda g, q: swz(k0 + q, 2 * ((g >> 1) | ((g & 1) << 2)))) == 1

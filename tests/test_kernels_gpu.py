@@ -119,3 +119,38 @@ def test_dmma_edge_warp(tsm, M, N, cplx):
         got = tsm.tsmttsm(torch.from_numpy(Ai).cuda(), torch.from_numpy(Bi).cuda(), plan=plan)
         torch.cuda.synchronize()
         assert np.array_equal(got.cpu().numpy(), oracle.tsmttsm(Ai, Bi)[0])
+
+
+@pytest.mark.parametrize("M,N", [(64, 64), (48, 16), (40, 40), (34, 18), (16, 16), (62, 50), (20, 64)])
+def test_dmma_pair_loads(tsm, M, N):
+    """Real DMMA TSMTTSM with paired 16-byte fragment loads (kernel | 32):
+    bulk-copy (padded conflict-free strides) and TMA (swizzle-permuted lanes)
+    variants, ragged K and an integer-valued bitwise check of the C-cell mapping."""
+    cands = gi.pair_candidates(M, N, False)
+    assert cands
+    picked = {}
+    for c in cands:
+        picked.setdefault((c["impl"], c["NT"]), c)
+    assert {i for i, _ in picked} >= ({2} if M % 2 == 0 else set())
+    for (impl, _), c in sorted(picked.items()):
+        try:
+            plan = tsm.Plan("tsmttsm", "d", M, N, 0, config=gi.to_tsm_config("tsmttsm", c, 3, 1))
+        except tsm.TsmError as e:
+            if e.status != 2:
+                raise
+            continue
+        assert plan.config()["kernel"] == impl | 32
+        assert "pair" in plan.describe(1000)["kernel"]
+        for K in (1, 6, 4099, 65537):
+            A = ti.matrix(K, M, "A", seed=K + 3)
+            B = ti.matrix(K, N, "B", seed=K + 4)
+            got = tsm.tsmttsm(torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda(), plan=plan)
+            torch.cuda.synchronize()
+            ref, bound = oracle.tsmttsm(A, B)
+            r, wi, _ = oracle.max_err_ratio(got.cpu().numpy(), ref, bound)
+            assert r <= 1e-12, (M, N, impl, c, K, r, wi)
+        Ai = ti.matrix(70001, M, "A", mode="int")
+        Bi = ti.matrix(70001, N, "B", mode="int")
+        got = tsm.tsmttsm(torch.from_numpy(Ai).cuda(), torch.from_numpy(Bi).cuda(), plan=plan)
+        torch.cuda.synchronize()
+        assert np.array_equal(got.cpu().numpy(), oracle.tsmttsm(Ai, Bi)[0]), c

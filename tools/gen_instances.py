@@ -161,6 +161,53 @@ def edge_candidates(M: int, N: int, z: bool) -> list:
     return out
 
 
+def pair_stride(w: int) -> int:
+    """Smallest even smem stride >= w whose 4 fragment rows start 32 bytes
+    apart modulo 128: the 8 lanes of each LDS.128 phase then read 8 distinct
+    16-byte granules (conflict-free paired loads without the swizzle)."""
+    st = w
+    while st % 16 not in (4, 12):
+        st += 1
+    return st
+
+
+def pair_candidates(M: int, N: int, z: bool) -> list:
+    """Real DMMA TSMTTSM with paired fragment loads (PAIR=1): each lane loads
+    rows (m, m+1) with one 16-byte LDS feeding two 8x8 blocks, halving the
+    fragment load instructions per DMMA.  Needs even WM, WN."""
+    if z or M < 16 or N < 16:
+        return []
+    MB, NB = 2 * cdiv(M, 16), 2 * cdiv(N, 16)
+    wt = []
+    for WM in range(2, min(MB, 8) + 1, 2):
+        for WN in range(2, min(NB, 8) + 1, 2):
+            if WM * WN > 16 or cdiv(MB, WM) * cdiv(NB, WN) > 16:
+                continue
+            bal = cdiv(MB, WM) * WM * cdiv(NB, WN) * WN * 64 / (M * N)
+            wt.append((bal * (1 + 0.5 * (WM + WN) / (WM * WN)), WM, WN))
+    wt.sort()
+    out = []
+    row = (M + N) * 8
+    for (_, WM, WN) in wt[:3]:
+        WT = cdiv(MB, WM) * cdiv(NB, WN)
+        for k in (1, 2, 4, 8):
+            NW = WT * k
+            if NW > 16:
+                break
+            if NW < 4 and WT * k * 2 <= 16:
+                continue
+            for tgt in (16384, 32768, 65536):
+                if M % 2 == 0 and N % 2 == 0:  # conflict-free strides (row copies if padded)
+                    out.append(dict(MT=WM, NTL=WN, NT=(NW + 1) * 32, R=_rows(4 * k, row, tgt), impl=1,
+                                    AP=pair_stride(M), BP=pair_stride(N), PAIR=1))
+                if tma_ok(M, N, z):
+                    tb = (cdiv(M, 16) + cdiv(N, 16)) * 128
+                    step = 4 * k if (4 * k) % 8 == 0 else 8 * k
+                    Rt = min(256 // step * step, max(step, (tgt // tb) // step * step))
+                    out.append(dict(MT=WM, NTL=WN, NT=(NW + 1) * 32, R=Rt, impl=2, AP=M, BP=N, PAIR=1))
+    return out
+
+
 def tma_ok(M: int, N: int, z: bool) -> bool:
     """2-D tensor maps need 16-byte global row strides; boxes are 16 doubles."""
     S = 2 if z else 1
@@ -254,8 +301,10 @@ def cfg_type(op, dt, M, N, c) -> str:
     if op == "tsmttsm" and c.get("impl", 0) >= 1:
         tma = "true" if c["impl"] == 2 else "false"
         edge = c.get("EDGE", 0)
+        pair = "true" if c.get("PAIR", 0) else "false"
         return (f"tsm::TsmttsmMmaCfg<{M}, {N}, {z}, {c['MT']}, {c['NTL']}, {c['NT'] // 32 - 1 - edge}, "
-                f"{c['R']}, {c.get('AP', M)}, {c.get('BP', N)}, {tma}, {'true' if edge else 'false'}>")
+                f"{c['R']}, {c.get('AP', M)}, {c.get('BP', N)}, {tma}, {'true' if edge else 'false'}, "
+                f"{pair}>")
     if op == "tsmttsm":
         return f"tsm::TsmttsmCfg<{M}, {N}, {z}, {c['MT']}, {c['NTL']}, {c['NT']}, {c['R']}>"
     if c.get("impl", 0) == 3:
@@ -281,7 +330,13 @@ def entry_init(op, dt, M, N, c) -> str:
     p = params4(op, M, N, c)
     return (f"  {{{kind}, {1 if dt == 'z' else 0}, {M}, {N}, {fn}, {c['NT']}, {c['R']}, "
             f"{p[0]}, {p[1]}, {p[2]}, {p[3]}, {c['stages']}, {c['ctas']}, {c.get('impl', 0)}, "
-            f"{c.get('EDGE', 0)}}},")
+            f"{flags(c)}}},")
+
+
+def flags(c: dict) -> int:
+    """KernelEntry.edge / tsm_config.kernel >> 4: bit 0 DFMA edge warp, bit 1
+    paired 16-byte fragment loads."""
+    return c.get("EDGE", 0) | (c.get("PAIR", 0) << 1)
 
 
 def params4(op: str, M: int, N: int, c: dict) -> tuple:
@@ -348,7 +403,7 @@ def main(per_file: int = 12) -> int:
                     lines.append(f"  {{{0 if op == 'tsmttsm' else 1}, {1 if dt == 'z' else 0}, {M}, {N}, "
                                  f"nullptr, {c['NT']}, {c['R']}, {p[0]}, {p[1]}, {p[2]}, {p[3]}, "
                                  f"{c['stages']}, {c['ctas']}, {c.get('impl', 0)}, "
-                                 f"{c.get('EDGE', 0)}}},")
+                                 f"{flags(c)}}},")
     lines += ["};", "}  // namespace tsm", ""]
     _write(os.path.join(GEN, "params_gen.cpp"), "\n".join(lines))
 
@@ -367,9 +422,6 @@ def _write(path: str, src: str) -> None:
         with open(path, "w") as f:
             f.write(src)
 
-
-if __name__ == "__main__":
-    sys.exit(main())
 
 
 # ---------------------------------------------------------------------------
@@ -444,6 +496,7 @@ def candidates(op: str, M: int, N: int, z: bool) -> list:
                             out.append(dict(MT=WM, NTL=WN, NT=(NW + 1) * 32, R=Rt, impl=2,
                                             AP=M, BP=N))
             out.extend(edge_candidates(M, N, z))
+            out.extend(pair_candidates(M, N, z))
     else:
         acc_max = 16 if z else 32
         NTL = 1
@@ -503,7 +556,7 @@ def to_tsm_config(op: str, c: dict, stages: int, ctas: int) -> dict:
     else:
         p = _tsmm_p(c) + (0,)
     return dict(threads=c["NT"], rows_per_chunk=c["R"], p0=p[0], p1=p[1], p2=p[2], p3=p[3],
-                stages=stages, ctas_per_sm=ctas, kernel=c.get("impl", 0) | (c.get("EDGE", 0) << 4))
+                stages=stages, ctas_per_sm=ctas, kernel=c.get("impl", 0) | (flags(c) << 4))
 
 
 # ---------------------------------------------------------------------------
@@ -609,3 +662,7 @@ def tsmm_cst_configs(M: int, N: int, z: bool) -> list:
                     R = rpp * max(1, min(256 // rpp, round(tgt / (rpp * ab))))
                     out.append(dict(NBW=NBW, WR=WR, NT=(NW + 1) * 32, R=R, impl=3))
     return out
+
+
+if __name__ == "__main__":
+    sys.exit(main())
