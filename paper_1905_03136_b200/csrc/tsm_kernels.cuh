@@ -1122,6 +1122,8 @@ __global__ void __launch_bounds__(Cfg::NT) tsmm_mma_kernel(const __grid_constant
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, q = lane & 3;
+  // swizzled (TMA) boxes: MMA row g <-> A/B row rho(g), conflict-free (see tsmm_cst_kernel)
+  const int rho = Cfg::TMA ? ((((g & 1) << 2) | (g & 2) | (g >> 2)) ^ (g & 1)) : g;
   const long long K = p.K;
   const long long K_even = K & ~1LL;
   const long long Kc = Cfg::TMA ? K : K_even;
@@ -1223,7 +1225,7 @@ __global__ void __launch_bounds__(Cfg::NT) tsmm_mma_kernel(const __grid_constant
           double a[WR][S];
 #pragma unroll
           for (int i = 0; i < WR; i++) {
-            const int r = wr0 + 8 * i + g;
+            const int r = wr0 + 8 * i + rho;
 #pragma unroll
             for (int z = 0; z < S; z++) a[i][z] = mv ? sA[aoff(r, m) + z] : 0.0;
           }
@@ -1262,7 +1264,7 @@ __global__ void __launch_bounds__(Cfg::NT) tsmm_mma_kernel(const __grid_constant
 #pragma unroll
           for (int j = 0; j < NB; j++) {
             const int n = 8 * j + 2 * q;
-            const int rr = 8 * i + g;
+            const int rr = 8 * i + rho;
             if constexpr (!Cfg::Z && (Cfg::TMA || NOP % 2 == 0)) {
               // 16-byte store (conflict-free: NOP = 2 mod 4, or swizzled boxes)
               double* dst = stg + ooff(rr, n);
@@ -1411,6 +1413,11 @@ __global__ void __launch_bounds__(Cfg::NT) tsmm_cst_kernel(const __grid_constant
     // ---------------- consumer warps ----------------
     const int cg = warp % NG, rg = warp / NG;
     const int nb0 = cg * NBW;  // first 8-column block of this warp
+    // MMA row g of a block is A/B row rho(g) = bitrev3(g) ^ (g & 1) =
+    // [0,5,2,7,1,4,3,6]: under the 128B swizzle the A fragment loads (D: 16
+    // lanes per 8-byte phase, Z: 8 lanes per 16-byte phase) and the 16-byte
+    // staging stores then touch distinct banks (identity rows: 2-way conflicts).
+    const int rho = ((((g & 1) << 2) | (g & 2) | (g >> 2)) ^ (g & 1));
     double* stg = sOut + warp * Cfg::OUT_DOUBLES;
     // this warp's C slice as MMA-B fragments: lane holds C[4ks+q][8(nb0+j)+g]
     double cf[MK][NBW][S];
@@ -1449,7 +1456,7 @@ __global__ void __launch_bounds__(Cfg::NT) tsmm_cst_kernel(const __grid_constant
           const bool mv = (4 * ks + 4 <= M) || (m < M);
 #pragma unroll
           for (int i = 0; i < WR; i++) {
-            const int r = wr0 + 8 * i + g;
+            const int r = wr0 + 8 * i + rho;
             if constexpr (!Cfg::Z) {
               const double a = mv ? sA[aoff(r, m)] : 0.0;
 #pragma unroll
@@ -1474,7 +1481,7 @@ __global__ void __launch_bounds__(Cfg::NT) tsmm_cst_kernel(const __grid_constant
         for (int i = 0; i < WR; i++)
 #pragma unroll
           for (int j = 0; j < NBW; j++) {
-            const int rr = 8 * i + g;
+            const int rr = 8 * i + rho;
             if constexpr (!Cfg::Z) {
               const int c0 = 8 * j + 2 * q;  // column within the warp's tile (doubles)
               *reinterpret_cast<double2*>(stg + (c0 >> 4) * (RW * 16) + swz128(rr, c0 & 15)) =

@@ -121,3 +121,33 @@ def test_pair_layouts_conflict_free():
     for k0 in (0, 4, 8, 12):
         assert _lds128_worst(lambda g, q: swz(k0 + q, 2 * g)) == 2
         assert _lds128_worst(lambda g, q: swz(k0 + q, 2 * ((g >> 1) | ((g & 1) << 2)))) == 1
+
+
+def test_cstationary_row_permutation_conflict_free():
+    # C-stationary TSMM: MMA row g <-> A/B row rho(g) under the 128B swizzle
+    def swz(r, c):
+        return r * 16 + ((((c >> 1) ^ r) & 7) << 1) + (c & 1)
+
+    def worst(addr, lanes_per, unit):
+        w = 0
+        for ph in range(32 // lanes_per):
+            cnt = {}
+            for lane in range(lanes_per * ph, lanes_per * ph + lanes_per):
+                u = unit(addr(lane >> 2, lane & 3))
+                cnt[u] = cnt.get(u, 0) + 1
+            w = max(w, max(cnt.values()))
+        return w
+
+    rho = [0, 5, 2, 7, 1, 4, 3, 6]  # tsm_kernels.cuh tsmm_cst_kernel
+    assert sorted(rho) == list(range(8))
+    u8, u16 = (lambda d: d % 16), (lambda d: (d // 2) % 8)
+    checks = [(lambda p, g, q, ks: swz(p[g], (4 * ks + q) & 15), 16, u8, 16),       # D A loads
+              (lambda p, g, q, j: swz(p[g], (8 * j + 2 * q) & 15), 8, u16, 2),      # D stores
+              (lambda p, g, q, ks: swz(p[g], (2 * (4 * ks + q)) & 15), 8, u16, 8),  # Z A loads
+              (lambda p, g, q, c: swz(p[g], (2 * (8 * (c >> 1) + 2 * q + (c & 1))) & 15), 8, u16, 4)]
+    ident = list(range(8))
+    got_id, got_rho = [], []
+    for f, lp, u, nv in checks:
+        got_id.append(max(worst(lambda g, q: f(ident, g, q, v), lp, u) for v in range(nv)))
+        got_rho.append(max(worst(lambda g, q: f(rho, g, q, v), lp, u) for v in range(nv)))
+    assert got_id == [2, 2, 2, 1] and got_rho == [1, 1, 1, 1]
