@@ -502,6 +502,45 @@ __device__ __forceinline__ void mbar_arrive(u64* bar) {
 // stride = 8 mod 16 words for D, 4 mod 8 16-byte units for Z) makes the
 // fragment loads (4 rows x 8 consecutive elements) hit the minimum number of
 // smem wavefronts; the producer then issues one bulk copy per row.
+// Shared-memory wavefronts of one fragment load over a dense operand of row
+// stride `st` elements when the 4 rows of a k-step are d apart (rows d*q,
+// lanes g = 0..7 read consecutive elements; m-offsets shift every lane alike).
+// D: LDS.64, two 16-lane phases of 8-byte units; paired D: LDS.128 (g reads
+// elements 2g, 2g+1), four 8-lane phases of 16-byte units; Z: LDS.128 of one
+// complex element.  Returns the worst lanes-per-unit count (1 = conflict-free).
+constexpr int frag_conflict(int st, int d, bool z, bool pair) {
+  int worst = 0;
+  const int lanes = (z || pair) ? 8 : 16, units = (z || pair) ? 8 : 16;
+  for (int ph = 0; ph < 32 / lanes; ph++) {
+    int cnt[16] = {};
+    for (int l = ph * lanes; l < ph * lanes + lanes; l++) {
+      const int g = l >> 2, q = l & 3;
+      const int e = d * q * st + (pair ? 2 * g : g);  // element index (complex for Z)
+      const int u = z ? e % units : pair ? (e / 2) % units : e % units;
+      if (++cnt[u] > worst) worst = cnt[u];
+    }
+  }
+  return worst;
+}
+
+// Row spacing d of the k-step rows for a dense layout: the d in {1, 2, 4} (with
+// R a multiple of the 4d-row atom) with the fewest conflicts on A and B.
+// Rows are assigned per 4d-row atom: k-step t reads rows
+// (t/d)*4d + t%d + d*q, so odd strides (d = 4) and strides = 2 mod 4 (d = 2)
+// become conflict-free without padding; strides = 0 mod 8 cannot.
+constexpr int pick_kdist(int ap, int bp, bool z, bool pair, int r) {
+  int best = 1, bc = 1 << 20;
+  for (int d = 1; d <= 4; d *= 2) {
+    if (r % (4 * d)) continue;
+    const int c = frag_conflict(ap, d, z, pair) + frag_conflict(bp, d, z, pair);
+    if (c < bc) {
+      bc = c;
+      best = d;
+    }
+  }
+  return best;
+}
+
 // TMA = true: A and B arrive by 2-D tensor copies into 128B-swizzled boxes
 // (AP, BP ignored; requires M*S and N*S even and >= 16 doubles).
 // EDGE = true: DMMA covers only the 8-aligned core MC x NC of C
@@ -538,6 +577,9 @@ struct TsmttsmMmaCfg {
   static constexpr int NT = (NW + NE + 1) * 32;                 // + edge + producer warp
   static constexpr int CELLS = M * N * S;
   static constexpr int STAGE_DOUBLES = R * (AP + BP) * S;
+  // k-step row spacing (see pick_kdist); the 128B swizzle needs rows 2 apart
+  static constexpr int KD = TMA ? 2 : pick_kdist(AP, BP, Z, PAIR, R);
+  static_assert(R % (4 * KD) == 0, "rows per chunk: whole k-step atoms");
   static_assert(NW % WT == 0 && RS >= 1, "consumer warps must be a multiple of the warp tiles");
   static_assert(R % 4 == 0, "R must be a multiple of the k-step (4 rows)");
   static_assert(WM <= MB && WN <= NB, "warp tile larger than C");
@@ -561,11 +603,6 @@ __global__ void __launch_bounds__(Cfg::NT) tsmttsm_mma_kernel(const __grid_const
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, q = lane & 3;
-  // pair mode: lane g loads the 16-byte granule pc(g) of its 16-row band.  Under the
-  // 128B swizzle (TMA) the granules of rows k0..k0+3 are XORed with the row, and
-  // pc(g) = g/2 + 4(g%2) makes the 8 lanes of each LDS.128 phase hit 8 distinct
-  // granules; the dense layout (padded stride) needs the identity.
-  auto pc = [](int x) { return Cfg::TMA ? ((x >> 1) | ((x & 1) << 2)) : x; };
   const long long K = p.K;
   const long long K_even = K & ~1LL;
   const int G = gridDim.x;
@@ -605,34 +642,41 @@ __global__ void __launch_bounds__(Cfg::NT) tsmttsm_mma_kernel(const __grid_const
     }
   };
 
-  // one k-step: rows k0..k0+3 of the stage (row strides ap, bp elements), or
-  // of global memory for the odd tail row (strides M, N; non-TMA only)
+  // one k-step: 4 rows of the stage (row strides ap, bp elements), or of global
+  // memory for the odd tail row (strides M, N; non-TMA only).  K-step k0 (t = k0/4)
+  // reads rows (t/KD)*4KD + t%KD + KD*q: rows KD apart, chosen so that every
+  // fragment load hits distinct banks (swizzled TMA boxes: KD = 2 puts the 4
+  // rows in different swizzle phases; dense rows: see pick_kdist).  The sum over
+  // k is unchanged: A and B fragments of a lane always read the same row, and
+  // the k-steps of a 4KD-row atom visit each of its rows once.
   auto kstep = [&](const double* __restrict__ sA, const double* __restrict__ sB, int k0, int rows,
                    int ap, int bp) {
-    const bool rv = (k0 + q) < rows;
+    constexpr int KD = Cfg::KD;
+    const int kr = (k0 & ~(4 * KD - 1)) + ((k0 >> 2) & (KD - 1)) + KD * q;
+    const bool rv = kr < rows;
     if constexpr (!Cfg::Z) {
       double a[WM], b[WN];
       if constexpr (Cfg::PAIR) {
         // one 16-byte load per lane: (m, m+1) -> fragments of blocks 2p, 2p+1
 #pragma unroll
         for (int ip = 0; ip < WM / 2; ip++) {
-          const int m = (wm * WM + 2 * ip) * 8 + 2 * pc(g);
+          const int m = (wm * WM + 2 * ip) * 8 + 2 * g;
           double2 v = make_double2(0.0, 0.0);
           if (rv && m + 1 < M)
-            v = *reinterpret_cast<const double2*>(sA + off(k0 + q, m, ap));
+            v = *reinterpret_cast<const double2*>(sA + off(kr, m, ap));
           else if (rv && m < M)
-            v.x = sA[off(k0 + q, m, ap)];
+            v.x = sA[off(kr, m, ap)];
           a[2 * ip] = v.x;
           a[2 * ip + 1] = v.y;
         }
 #pragma unroll
         for (int jp = 0; jp < WN / 2; jp++) {
-          const int n = (wn * WN + 2 * jp) * 8 + 2 * pc(g);
+          const int n = (wn * WN + 2 * jp) * 8 + 2 * g;
           double2 v = make_double2(0.0, 0.0);
           if (rv && n + 1 < N)
-            v = *reinterpret_cast<const double2*>(sB + off(k0 + q, n, bp));
+            v = *reinterpret_cast<const double2*>(sB + off(kr, n, bp));
           else if (rv && n < N)
-            v.x = sB[off(k0 + q, n, bp)];
+            v.x = sB[off(kr, n, bp)];
           b[2 * jp] = v.x;
           b[2 * jp + 1] = v.y;
         }
@@ -640,12 +684,12 @@ __global__ void __launch_bounds__(Cfg::NT) tsmttsm_mma_kernel(const __grid_const
 #pragma unroll
         for (int i = 0; i < WM; i++) {
           const int m = (wm * WM + i) * 8 + g;
-          a[i] = (rv && m < M) ? sA[off(k0 + q, m, ap)] : 0.0;
+          a[i] = (rv && m < M) ? sA[off(kr, m, ap)] : 0.0;
         }
 #pragma unroll
         for (int j = 0; j < WN; j++) {
           const int n = (wn * WN + j) * 8 + g;
-          b[j] = (rv && n < N) ? sB[off(k0 + q, n, bp)] : 0.0;
+          b[j] = (rv && n < N) ? sB[off(kr, n, bp)] : 0.0;
         }
       }
 #pragma unroll
@@ -658,13 +702,13 @@ __global__ void __launch_bounds__(Cfg::NT) tsmttsm_mma_kernel(const __grid_const
 #pragma unroll
       for (int i = 0; i < WM; i++) {
         const int m = (wm * WM + i) * 8 + g;
-        a[i] = (rv && m < M) ? *reinterpret_cast<const double2*>(sA + off(k0 + q, m, ap))
+        a[i] = (rv && m < M) ? *reinterpret_cast<const double2*>(sA + off(kr, m, ap))
                              : make_double2(0.0, 0.0);
       }
 #pragma unroll
       for (int j = 0; j < WN; j++) {
         const int n = (wn * WN + j) * 8 + g;
-        b[j] = (rv && n < N) ? *reinterpret_cast<const double2*>(sB + off(k0 + q, n, bp))
+        b[j] = (rv && n < N) ? *reinterpret_cast<const double2*>(sB + off(kr, n, bp))
                              : make_double2(0.0, 0.0);
       }
 #pragma unroll
@@ -791,8 +835,9 @@ __global__ void __launch_bounds__(Cfg::NT) tsmttsm_mma_kernel(const __grid_const
       if (rows == R) {
 #pragma unroll 2
         for (int k0 = slot * 4; k0 < R; k0 += RS * 4) kstep(sA, sB, k0, R, AP, BP);
-      } else {
-        for (int k0 = slot * 4; k0 < rows; k0 += RS * 4) kstep(sA, sB, k0, rows, AP, BP);
+      } else {  // partial chunk: every k-step of the atoms that hold rows < rows
+        const int kend = (rows + 4 * Cfg::KD - 1) & ~(4 * Cfg::KD - 1);
+        for (int k0 = slot * 4; k0 < kend; k0 += RS * 4) kstep(sA, sB, k0, rows, AP, BP);
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
@@ -813,12 +858,12 @@ __global__ void __launch_bounds__(Cfg::NT) tsmttsm_mma_kernel(const __grid_const
 #pragma unroll
       for (int i = 0; i < WM; i++) {
         // pair mode: blocks 2p / 2p+1 hold the even / odd rows of a 16-row band
-        const int m = Cfg::PAIR ? (wm * WM + (i & ~1)) * 8 + 2 * pc(g) + (i & 1) : (wm * WM + i) * 8 + g;
+        const int m = Cfg::PAIR ? (wm * WM + (i & ~1)) * 8 + 2 * g + (i & 1) : (wm * WM + i) * 8 + g;
 #pragma unroll
         for (int j = 0; j < WN; j++) {
 #pragma unroll
           for (int e = 0; e < 2; e++) {
-            const int n = Cfg::PAIR ? (wn * WN + (j & ~1)) * 8 + 2 * pc(2 * q + e) + (j & 1)
+            const int n = Cfg::PAIR ? (wn * WN + (j & ~1)) * 8 + 2 * (2 * q + e) + (j & 1)
                                     : (wn * WN + j) * 8 + 2 * q + e;
             if (m < M && n < N && (wm * WM + i) < MB && (wn * WN + j) < NB) {
 #pragma unroll

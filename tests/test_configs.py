@@ -113,14 +113,35 @@ def test_pair_layouts_conflict_free():
         assert _lds128_worst(lambda g, q: q * st + 2 * g) == 1, w
     assert _lds128_worst(lambda g, q: q * 64 + 2 * g) == 4  # dense stride 64: 4-way
 
-    # 128B swizzle (TMA boxes): granule (c/2 ^ row) -- identity lanes conflict 2-way,
-    # the kernel's permutation pc(g) = g/2 + 4(g%2) is conflict-free for every k0
+    # 128B swizzle (TMA boxes): granule (c/2 ^ row).  Contiguous k-step rows
+    # conflict 2-way; the kernel's row remap (k0 & ~7) + (k0/4 % 2) + 2q is
+    # conflict-free for paired D (LDS.128), plain D (LDS.64) and Z (LDS.128)
     def swz(r, c):
         return r * 16 + ((((c >> 1) ^ r) & 7) << 1) + (c & 1)
 
-    for k0 in (0, 4, 8, 12):
-        assert _lds128_worst(lambda g, q: swz(k0 + q, 2 * g)) == 2
-        assert _lds128_worst(lambda g, q: swz(k0 + q, 2 * ((g >> 1) | ((g & 1) << 2)))) == 1
+    def remap(k0, q):
+        return (k0 & ~7) + ((k0 >> 2) & 1) + 2 * q
+
+    def worst64(addr):  # LDS.64: two 16-lane phases, 8-byte units
+        w = 0
+        for h in range(2):
+            cnt = {}
+            for lane in range(16 * h, 16 * h + 16):
+                u = addr(lane >> 2, lane & 3) % 16
+                cnt[u] = cnt.get(u, 0) + 1
+            w = max(w, max(cnt.values()))
+        return w
+
+    for k0 in range(0, 32, 4):
+        for m0 in (0, 8, 16, 24):
+            assert _lds128_worst(lambda g, q: swz(k0 + q, (2 * m0 + 2 * g) % 16)) == 2
+            assert _lds128_worst(lambda g, q: swz(remap(k0, q), (2 * m0 + 2 * g) % 16)) == 1
+            assert worst64(lambda g, q: swz(k0 + q, (m0 + g) % 16)) == 2
+            assert worst64(lambda g, q: swz(remap(k0, q), (m0 + g) % 16)) == 1
+            assert _lds128_worst(lambda g, q: swz(k0 + q, (2 * (m0 + g)) % 16)) == 2  # Z
+            assert _lds128_worst(lambda g, q: swz(remap(k0, q), (2 * (m0 + g)) % 16)) == 1
+    # the remap visits every row of an 8-row atom once per two k-steps
+    assert sorted(remap(k0, q) for k0 in (0, 4) for q in range(4)) == list(range(8))
 
 
 def test_cstationary_row_permutation_conflict_free():
@@ -151,3 +172,29 @@ def test_cstationary_row_permutation_conflict_free():
         got_id.append(max(worst(lambda g, q: f(ident, g, q, v), lp, u) for v in range(nv)))
         got_rho.append(max(worst(lambda g, q: f(rho, g, q, v), lp, u) for v in range(nv)))
     assert got_id == [2, 2, 2, 1] and got_rho == [1, 1, 1, 1]
+
+
+def test_dense_kstep_row_spacing():
+    """Dense (bulk-copy) layouts: k-step rows d apart (tsm_kernels.cuh
+    pick_kdist) -- odd strides need d = 4, strides = 2 mod 4 need d = 2,
+    strides = 4 mod 8 are conflict-free contiguously, 0 mod 8 never."""
+    def lds64(st, d):
+        w = 0
+        for h in range(2):
+            cnt = {}
+            for lane in range(16 * h, 16 * h + 16):
+                u = (d * (lane & 3) * st + (lane >> 2)) % 16
+                cnt[u] = cnt.get(u, 0) + 1
+            w = max(w, max(cnt.values()))
+        return w
+
+    for st in range(8, 72):
+        best = min(lds64(st, d) for d in (1, 2, 4))
+        if st % 2:
+            assert lds64(st, 4) == 1 and lds64(st, 1) >= 2, st
+        elif st % 4 == 2:
+            assert lds64(st, 2) == 1, st
+        elif st % 8 == 4:
+            assert lds64(st, 1) == 1, st
+        else:
+            assert best >= 2, st

@@ -124,7 +124,7 @@ def test_dmma_edge_warp(tsm, M, N, cplx):
 @pytest.mark.parametrize("M,N", [(64, 64), (48, 16), (40, 40), (34, 18), (16, 16), (62, 50), (20, 64)])
 def test_dmma_pair_loads(tsm, M, N):
     """Real DMMA TSMTTSM with paired 16-byte fragment loads (kernel | 32):
-    bulk-copy (padded conflict-free strides) and TMA (swizzle-permuted lanes)
+    bulk-copy (padded conflict-free strides) and TMA (swizzle-aware k-row remap)
     variants, ragged K and an integer-valued bitwise check of the C-cell mapping."""
     cands = gi.pair_candidates(M, N, False)
     assert cands

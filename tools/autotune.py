@@ -53,6 +53,10 @@ def main():
     ap.add_argument("--jobs", type=int, default=min(32, os.cpu_count() or 8))
     ap.add_argument("--out", default=os.path.join(ROOT, "tune", "b200.json"))
     ap.add_argument("--time-budget", type=float, default=0, help="stop after this many seconds")
+    ap.add_argument("--filter", default="", help="python expression on a candidate dict c, e.g. "
+                    "\"c.get('PAIR')\" -- only matching candidates are timed")
+    ap.add_argument("--keep-better", action="store_true",
+                    help="keep the stored entry when it is faster than this run's best")
     a = ap.parse_args()
     t_start = time.time()
     shapes = parse_shapes(a)
@@ -85,6 +89,10 @@ def main():
                     break
                 key = f"{op}_{dt}_{M}_{N}"
                 cands = gi.candidates(op, M, N, z)
+                if a.filter:
+                    cands = [c for c in cands if eval(a.filter, {}, {"c": c})]  # noqa: S307
+                    if not cands:
+                        continue
                 A = Abuf[: K * M].view(K, M)
                 if op == "tsmttsm":
                     B = Bbuf[: K * N].view(K, N)
@@ -160,6 +168,9 @@ def main():
                 cfg["stages"] = got["stages"]
                 cfg["ctas"] = got["ctas_per_sm"]
                 prev = db["entries"].get(key)
+                if a.keep_better and prev and prev["ms"] <= t:
+                    print(f"{key}: kept stored {prev['ms']:.4f} ms (this run {t:.4f} ms {cfg})", flush=True)
+                    continue
                 db["entries"][key] = {"cfg": cfg, "ms": t, "frac": roof / (t * 1e-3),
                                       "candidates": len(res), "default_ms": None}
                 print(f"{key}: best {t:.4f} ms ({100 * roof / (t * 1e-3):.1f}% roof) "

@@ -198,8 +198,12 @@ def pair_candidates(M: int, N: int, z: bool) -> list:
                 continue
             for tgt in (16384, 32768, 65536):
                 if M % 2 == 0 and N % 2 == 0:  # conflict-free strides (row copies if padded)
-                    out.append(dict(MT=WM, NTL=WN, NT=(NW + 1) * 32, R=_rows(4 * k, row, tgt), impl=1,
+                    Rp = _rows(16 * k, row, tgt)  # whole 16-row k-step atoms (kernel KD <= 4)
+                    out.append(dict(MT=WM, NTL=WN, NT=(NW + 1) * 32, R=Rp, impl=1,
                                     AP=pair_stride(M), BP=pair_stride(N), PAIR=1))
+                    if M % 8 and N % 8 and (M % 4 == N % 4):  # dense rows, spaced k-steps
+                        out.append(dict(MT=WM, NTL=WN, NT=(NW + 1) * 32, R=Rp, impl=1,
+                                        AP=M, BP=N, PAIR=1))
                 if tma_ok(M, N, z):
                     tb = (cdiv(M, 16) + cdiv(N, 16)) * 128
                     step = 4 * k if (4 * k) % 8 == 0 else 8 * k
