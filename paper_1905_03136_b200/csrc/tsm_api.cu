@@ -244,6 +244,8 @@ static tsm_status validate_config(const KernelEntry& e) {
     const int S = e.dt == TSM_Z ? 2 : 1;
     const int E = e.M * e.N - (e.M / 8) * 8 * (e.N / 8) * 8;
     if ((E + 31) / 32 * S > 32) return bad("edge too large for one DFMA warp (<= 32 cells per lane)");
+  } else if (e.edge & 12) {
+    return bad("edge warp count bits (kernel bits 6-7) need the edge flag (kernel | 16)");
   }
   if (e.impl == 3) {
     const int S = e.dt == TSM_Z ? 2 : 1;
@@ -271,7 +273,7 @@ static tsm_status validate_config(const KernelEntry& e) {
     if ((e.M * S) % 2 || (e.N * S) % 2 || e.M * S < 16 || e.N * S < 16)
       return bad("kernel 2 needs 16-byte rows of >= 128 bytes (M*S, N*S even and >= 16)");
     if (e.R % 8 || e.R > 256) return bad("kernel 2 needs rows_per_chunk a multiple of 8, <= 256");
-    const int ed = e.edge & 1;
+    const int ed = edge_warps(e.edge);
     const int pr = e.edge & 2;  // pair mode: 8x8 blocks in whole 16-wide pairs
     const int MB = ed ? e.M / 8 : pr ? 2 * ((e.M + 15) / 16) : (e.M + 7) / 8;
     const int NB = ed ? e.N / 8 : pr ? 2 * ((e.N + 15) / 16) : (e.N + 7) / 8;
@@ -281,7 +283,7 @@ static tsm_status validate_config(const KernelEntry& e) {
     if (NW < WT || NW % WT) return bad("threads/32 - 1 consumer warps must be a multiple of the warp tiles");
     if (e.R % (4 * (NW / WT))) return bad("rows_per_chunk must be a multiple of 4 * row slots");
   } else if (e.op == KIND_TSMTTSM && e.impl == 1) {
-    const int ed = e.edge & 1;
+    const int ed = edge_warps(e.edge);
     const int pr = e.edge & 2;  // pair mode: 8x8 blocks in whole 16-wide pairs
     const int MB = ed ? e.M / 8 : pr ? 2 * ((e.M + 15) / 16) : (e.M + 7) / 8;
     const int NB = ed ? e.N / 8 : pr ? 2 * ((e.N + 15) / 16) : (e.N + 7) / 8;
@@ -398,7 +400,7 @@ tsm_status tsm_plan_create_config(tsm_plan* out, tsm_op op, tsm_dtype dtype, int
   e.p0 = cfg->p0;
   e.p1 = cfg->p1;
   e.impl = cfg->kernel & 15;
-  e.edge = (cfg->kernel >> 4) & 3;
+  e.edge = (cfg->kernel >> 4) & 15;
   e.p2 = (op == TSM_OP_TSMTTSM && e.impl == 0) ? 0 : cfg->p2;
   e.p3 = (op == TSM_OP_TSMTTSM && e.impl >= 1) ? cfg->p3 : 0;
   e.stages = cfg->stages;

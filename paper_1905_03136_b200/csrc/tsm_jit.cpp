@@ -40,8 +40,8 @@ std::string cfg_type(const KernelEntry& e) {
   const char* z = e.dt ? "true" : "false";
   if (e.op == KIND_TSMTTSM && e.impl >= 1)
     os << "tsm::TsmttsmMmaCfg<" << e.M << ", " << e.N << ", " << z << ", " << e.p0 << ", " << e.p1
-       << ", " << (e.NT / 32 - 1 - (e.edge & 1)) << ", " << e.R << ", " << e.p2 << ", " << e.p3 << ", "
-       << (e.impl == 2 ? "true" : "false") << ", " << ((e.edge & 1) ? "true" : "false") << ", "
+       << ", " << (e.NT / 32 - 1 - edge_warps(e.edge)) << ", " << e.R << ", " << e.p2 << ", " << e.p3 << ", "
+       << (e.impl == 2 ? "true" : "false") << ", " << edge_warps(e.edge) << ", "
        << ((e.edge & 2) ? "true" : "false") << ">";
   else if (e.op == KIND_TSMTTSM)
     os << "tsm::TsmttsmCfg<" << e.M << ", " << e.N << ", " << z << ", " << e.p0 << ", " << e.p1

@@ -552,10 +552,10 @@ constexpr int pick_kdist(int ap, int bp, bool z, bool pair, int r) {
 // one 16-byte LDS.128 per lane feeds both fragments (half the load
 // instructions of one LDS.64 per fragment).
 template <int M_, int N_, bool Z_, int WM_, int WN_, int NW_, int R_, int AP_ = M_, int BP_ = N_,
-          bool TMA_ = false, bool EDGE_ = false, bool PAIR_ = false>
+          bool TMA_ = false, int EDGE_ = 0, bool PAIR_ = false>
 struct TsmttsmMmaCfg {
   static constexpr int M = M_, N = N_, WM = WM_, WN = WN_, NW = NW_, R = R_;
-  static constexpr bool Z = Z_, TMA = TMA_, EDGE = EDGE_, PAIR = PAIR_;
+  static constexpr bool Z = Z_, TMA = TMA_, EDGE = EDGE_ > 0, PAIR = PAIR_;
   static_assert(!PAIR || (!Z_ && !EDGE_ && WM_ % 2 == 0 && WN_ % 2 == 0), "pairs: real, even tiles, no edge");
   static constexpr int S = Z ? 2 : 1;
   static constexpr int NBA = (M * S + 15) / 16, NBB = (N * S + 15) / 16;  // 16-double boxes
@@ -569,7 +569,8 @@ struct TsmttsmMmaCfg {
   static constexpr int NB = PAIR ? 2 * ((NC + 15) / 16) : (NC + 7) / 8;
   static constexpr int E = M * N - MC * NC;                    // edge cells (DFMA warp)
   static constexpr int TE = (E + 31) / 32;                     // edge cells per lane
-  static constexpr int NE = EDGE ? 1 : 0;                      // edge warps
+  static constexpr int NE = EDGE_;                             // edge warps (split the rows)
+  static_assert(NE >= 0 && NE <= 4, "0..4 edge warps");
   static_assert(!EDGE || (MB >= 1 && NB >= 1 && E > 0), "edge mode needs a core and an edge");
   static constexpr int WTM = (MB + WM - 1) / WM, WTN = (NB + WN - 1) / WN;
   static constexpr int WT = WTM * WTN;                          // warp tiles covering C
@@ -750,10 +751,10 @@ __global__ void __launch_bounds__(Cfg::NT) tsmttsm_mma_kernel(const __grid_const
     }
   }
   // DFMA over rows [0, rows) of a stage (or of global memory: the odd tail row)
-  auto edge_rows = [&](const double* __restrict__ sA, const double* __restrict__ sB, int rows, int ap,
-                       int bp) {
+  auto edge_rows = [&](const double* __restrict__ sA, const double* __restrict__ sB, int r_begin, int rows,
+                       int ap, int bp) {
 #pragma unroll 2
-    for (int r = 0; r < rows; r++) {
+    for (int r = r_begin; r < rows; r += Cfg::NE) {
 #pragma unroll
       for (int t = 0; t < TE; t++) {
         if (em[t] < 0) continue;
@@ -806,8 +807,10 @@ __global__ void __launch_bounds__(Cfg::NT) tsmttsm_mma_kernel(const __grid_const
         }
       }
     }
-  } else if (Cfg::EDGE && warp == NW) {
-    // ---------------- edge warp: DFMA on the cells outside the DMMA core ----------------
+  } else if (Cfg::EDGE && warp < NW + Cfg::NE) {
+    // ---------------- edge warps: DFMA on the cells outside the DMMA core ----------------
+    // (edge warp ew takes rows ew, ew + NE, ... of every chunk)
+    const int ew = warp - NW;
     Ring ring_it;
     for (long long c = blockIdx.x; c < p.nchunks; c += G, ring_it.next(stages)) {
       const int s = ring_it.s;
@@ -815,12 +818,13 @@ __global__ void __launch_bounds__(Cfg::NT) tsmttsm_mma_kernel(const __grid_const
       const double* sA = ring + static_cast<long long>(s) * Cfg::STAGE_DOUBLES;
       const double* sB = sA + R * AP * S;
       const long long r0 = c * R;
-      edge_rows(sA, sB, Cfg::TMA ? R : static_cast<int>((K_even - r0 < R) ? (K_even - r0) : R), AP, BP);
+      edge_rows(sA, sB, ew, Cfg::TMA ? R : static_cast<int>((K_even - r0 < R) ? (K_even - r0) : R), AP, BP);
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
     }
     if constexpr (!Cfg::TMA) {
-      if ((K & 1) && blockIdx.x == 0) edge_rows(p.A + (K - 1) * M * S, p.B + (K - 1) * N * S, 1, M, N);
+      if ((K & 1) && blockIdx.x == 0 && ew == 0)
+        edge_rows(p.A + (K - 1) * M * S, p.B + (K - 1) * N * S, 0, 1, M, N);
     }
   } else {
     // ---------------- consumer warps ----------------
@@ -853,7 +857,7 @@ __global__ void __launch_bounds__(Cfg::NT) tsmttsm_mma_kernel(const __grid_const
   // ---- T3: block partial, slot by slot in slot order ----
   double* sP = ring;
 #pragma unroll 1
-  for (int sl = 0; sl < RS; sl++) {
+  for (int sl = 0; sl < (RS > Cfg::NE ? RS : Cfg::NE); sl++) {
     if (warp < NW && slot == sl) {
 #pragma unroll
       for (int i = 0; i < WM; i++) {
@@ -876,13 +880,16 @@ __global__ void __launch_bounds__(Cfg::NT) tsmttsm_mma_kernel(const __grid_const
         }
       }
     }
-    if constexpr (Cfg::EDGE) {  // edge cells are disjoint from the core: written once
-      if (warp == NW && sl == 0) {
+    if constexpr (Cfg::EDGE) {  // edge cells are disjoint from the core; edge warps in order
+      if (warp == NW + sl && sl < Cfg::NE) {
 #pragma unroll
         for (int t = 0; t < TE; t++)
           if (em[t] >= 0) {
 #pragma unroll
-            for (int z = 0; z < S; z++) sP[(em[t] * N + en[t]) * S + z] = eacc[t][z];
+            for (int z = 0; z < S; z++) {
+              const int idx = (em[t] * N + en[t]) * S + z;
+              sP[idx] = (sl == 0) ? eacc[t][z] : sP[idx] + eacc[t][z];
+            }
           }
       }
     }

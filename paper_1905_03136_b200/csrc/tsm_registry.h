@@ -19,9 +19,13 @@ struct KernelEntry {
   int ctas_per_sm;   // target resident CTAs per SM (clipped by occupancy)
   int impl;          // 0 = register-tile DFMA kernel, 1 = DMMA (mma.sync m8n8k4 f64) kernel,
                      // 2 = DMMA + TMA tensor copies, 3 = C-stationary DMMA TSMM
-  int edge;          // DMMA TSMTTSM flags: bit 0 = DFMA edge warp for the cells outside the
-                     // 8-aligned core, bit 1 = paired 16-byte fragment loads
+  int edge;          // DMMA TSMTTSM flags: bit 0 = DFMA edge warps for the cells outside the
+                     // 8-aligned core, bit 1 = paired 16-byte fragment loads, bits 2-3 =
+                     // edge warps - 1 (tsm_config.kernel bits 4..7)
 };
+
+// number of DFMA edge warps encoded in KernelEntry::edge
+inline int edge_warps(int flags) { return (flags & 1) ? 1 + ((flags >> 2) & 3) : 0; }
 
 struct KernelTable {
   const KernelEntry* entries;

@@ -95,16 +95,16 @@ def test_cstationary_int_bitwise(tsm, cplx):
 @pytest.mark.parametrize("cplx", [False, True], ids=["D", "Z"])
 @pytest.mark.parametrize("M,N", [(49, 49), (33, 17), (17, 33), (57, 58), (9, 10)])
 def test_dmma_edge_warp(tsm, M, N, cplx):
-    """DMMA core + DFMA edge warp (kernel | 16): every edge candidate family."""
+    """DMMA core + DFMA edge warps (kernel | 16, warp count in bits 6-7): every edge candidate family."""
     dt = "z" if cplx else "d"
     cands = gi.edge_candidates(M, N, cplx)
     assert cands
     picked = {}
     for c in cands:
-        picked.setdefault(c["impl"], c)
-    for impl, c in picked.items():
+        picked.setdefault((c["impl"], c["EDGE"]), c)  # 1, 2, 4 edge warps
+    for (impl, _), c in picked.items():
         plan = tsm.Plan("tsmttsm", dt, M, N, 0, config=gi.to_tsm_config("tsmttsm", c, 3, 2))
-        assert plan.config()["kernel"] == impl | 16
+        assert plan.config()["kernel"] == impl | (gi.flags(c) << 4)
         assert "edge" in plan.describe(1000)["kernel"]
         for K in (1, 7, 4099, 65537):
             A = ti.matrix(K, M, "A", complex_=cplx, seed=K + 1)

@@ -149,15 +149,19 @@ def edge_candidates(M: int, N: int, z: bool) -> list:
             NW = WT * k
             if NW > 16 or NW < 2:
                 continue
-            for tgt in (16384, 32768):
-                out.append(dict(MT=WM, NTL=WN, NT=(NW + 2) * 32, R=_rows(4 * k, row, tgt), impl=1,
-                                AP=M, BP=N, EDGE=1))
-                if tma_ok(M, N, z):
-                    tb = (cdiv(M * S, 16) + cdiv(N * S, 16)) * 128
-                    step = 4 * k if (4 * k) % 8 == 0 else 8 * k
-                    Rt = min(256 // step * step, max(step, (tgt // tb) // step * step))
-                    out.append(dict(MT=WM, NTL=WN, NT=(NW + 2) * 32, R=Rt, impl=2, AP=M, BP=N,
-                                    EDGE=1))
+            for ne in (1, 2, 4):  # edge warps split the rows of a chunk
+                if NW + ne + 1 > 32:
+                    continue
+                for tgt in (16384, 32768):
+                    Rd = _rows(16 * k, row, tgt)  # whole k-step atoms for any row spacing
+                    out.append(dict(MT=WM, NTL=WN, NT=(NW + ne + 1) * 32, R=Rd, impl=1,
+                                    AP=M, BP=N, EDGE=ne))
+                    if tma_ok(M, N, z):
+                        tb = (cdiv(M * S, 16) + cdiv(N * S, 16)) * 128
+                        step = 4 * k if (4 * k) % 8 == 0 else 8 * k
+                        Rt = min(256 // step * step, max(step, (tgt // tb) // step * step))
+                        out.append(dict(MT=WM, NTL=WN, NT=(NW + ne + 1) * 32, R=Rt, impl=2, AP=M, BP=N,
+                                        EDGE=ne))
     return out
 
 
@@ -307,8 +311,7 @@ def cfg_type(op, dt, M, N, c) -> str:
         edge = c.get("EDGE", 0)
         pair = "true" if c.get("PAIR", 0) else "false"
         return (f"tsm::TsmttsmMmaCfg<{M}, {N}, {z}, {c['MT']}, {c['NTL']}, {c['NT'] // 32 - 1 - edge}, "
-                f"{c['R']}, {c.get('AP', M)}, {c.get('BP', N)}, {tma}, {'true' if edge else 'false'}, "
-                f"{pair}>")
+                f"{c['R']}, {c.get('AP', M)}, {c.get('BP', N)}, {tma}, {edge}, {pair}>")
     if op == "tsmttsm":
         return f"tsm::TsmttsmCfg<{M}, {N}, {z}, {c['MT']}, {c['NTL']}, {c['NT']}, {c['R']}>"
     if c.get("impl", 0) == 3:
@@ -338,9 +341,10 @@ def entry_init(op, dt, M, N, c) -> str:
 
 
 def flags(c: dict) -> int:
-    """KernelEntry.edge / tsm_config.kernel >> 4: bit 0 DFMA edge warp, bit 1
-    paired 16-byte fragment loads."""
-    return c.get("EDGE", 0) | (c.get("PAIR", 0) << 1)
+    """KernelEntry.edge / tsm_config.kernel >> 4: bit 0 DFMA edge warps, bit 1
+    paired 16-byte fragment loads, bits 2-3 edge warps - 1 (EDGE = edge warp count)."""
+    e = c.get("EDGE", 0)
+    return (1 if e else 0) | (c.get("PAIR", 0) << 1) | (((e - 1) & 3) << 2 if e else 0)
 
 
 def params4(op: str, M: int, N: int, c: dict) -> tuple:
