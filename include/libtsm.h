@@ -120,7 +120,18 @@ typedef struct tsm_config {
                           p3 = BP smem row strides (elements) of A and B (= M, N: dense);
                           rows_per_chunk a multiple of 4.
                  TSMM:    p0 = WR 8-row blocks per warp, p1 = AP smem row stride of A,
-                          p2 = NOP smem row stride of the output staging. */
+                          p2 = NOP smem row stride of the output staging.
+                 2 = DMMA with 2-D TMA tensor copies (M*S, N*S even and >= 16).
+                 3 = TSMM only: C-stationary DMMA (p0 = NBW 8-column blocks per warp,
+                     p1 = WR 8-row blocks per warp; TMA conditions as 2).
+                 Flags (OR-ed in, DMMA TSMTTSM kernels 1/2 unless noted):
+                   16  DFMA edge warps for the cells outside the 8-aligned core;
+                       bits 6-7 = edge warps - 1 (1..4 warps splitting the rows);
+                   32  paired 16-byte fragment loads (D, even p0/p1);
+                   256 complex-as-real (Z; TSMTTSM 1/2, TSMM 3): the real kernel runs
+                       on the interleaved (re, im) view -- A, B as real K x 2M, K x 2N --
+                       and p0..p3, threads, rows refer to that 2M x 2N real problem.
+                 Invalid combinations return TSM_ERR_INVALID_VALUE. */
   int p3;
 } tsm_config;
 

@@ -104,11 +104,14 @@ struct DeviceGuard {
   }
 };
 
-size_t smem_bytes(const KernelEntry& k, int stages) {
+size_t smem_bytes(const KernelEntry& kin, int stages) {
+  // complex-as-real kernels run the real kernel on 2M x 2N (and keep the real
+  // product plus its complex combination in smem at the end: 1.5x the cells)
+  const KernelEntry k = real_view(kin);
   const long long S = k.dt == TSM_Z ? 2 : 1;
   if (k.op == KIND_TSMTTSM) {
     const long long stage = static_cast<long long>(k.R) * (k.M + k.N) * S;
-    const long long cells = static_cast<long long>(k.M) * k.N * S;
+    const long long cells = static_cast<long long>(k.M) * k.N * S * (zr_flag(kin.edge) ? 3 : 2) / 2;
     if (k.impl == 1) {  // DMMA kernel: 2 x 16 mbarriers, ring (padded rows); partial + scratch
       const long long pstage = static_cast<long long>(k.R) * (k.p2 + k.p3) * S;
       long long need = std::max<long long>(stages * pstage, cells + k.NT);
@@ -221,7 +224,19 @@ static bool is_pow2(int x) { return x > 0 && (x & (x - 1)) == 0; }
 
 // Mirror of the static_asserts of TsmttsmCfg / TsmmCfg, so a bad explicit
 // configuration is rejected with a clear message before any compilation.
-static tsm_status validate_config(const KernelEntry& e) {
+static tsm_status validate_config_real(const KernelEntry& e);
+
+static tsm_status validate_config(const KernelEntry& ein) {
+  auto bad = [](const std::string& w) { return fail(TSM_ERR_INVALID_VALUE, "bad config: " + w); };
+  if (zr_flag(ein.edge)) {  // complex computed by the real kernel on the interleaved 2M x 2N view
+    if (ein.dt != TSM_Z) return bad("the complex-as-real flag (kernel | 256) needs dtype Z");
+    if (!((ein.op == KIND_TSMTTSM && (ein.impl == 1 || ein.impl == 2)) || (ein.op == KIND_TSMM && ein.impl == 3)))
+      return bad("complex-as-real applies to DMMA TSMTTSM kernels 1, 2 and TSMM kernel 3");
+  }
+  return validate_config_real(real_view(ein));
+}
+
+static tsm_status validate_config_real(const KernelEntry& e) {
   auto bad = [](const std::string& w) { return fail(TSM_ERR_INVALID_VALUE, "bad config: " + w); };
   if (e.NT < 32 || e.NT > 1024 || e.NT % 32) return bad("threads must be a multiple of 32 in [32, 1024]");
   if (e.R < 2 || e.R % 2) return bad("rows_per_chunk must be even and >= 2");
@@ -400,7 +415,7 @@ tsm_status tsm_plan_create_config(tsm_plan* out, tsm_op op, tsm_dtype dtype, int
   e.p0 = cfg->p0;
   e.p1 = cfg->p1;
   e.impl = cfg->kernel & 15;
-  e.edge = (cfg->kernel >> 4) & 15;
+  e.edge = (cfg->kernel >> 4) & 31;
   e.p2 = (op == TSM_OP_TSMTTSM && e.impl == 0) ? 0 : cfg->p2;
   e.p3 = (op == TSM_OP_TSMTTSM && e.impl >= 1) ? cfg->p3 : 0;
   e.stages = cfg->stages;
@@ -593,6 +608,19 @@ tsm_status tsm_plan_describe(tsm_plan p, int64_t K, char* buf, size_t len) {
   const Geometry g = geometry(p, K < 0 ? 0 : K);
   const KernelEntry* k = p->k;
   char tmp[512];
+  std::string kname;
+  if (p->op == TSM_OP_TSMTTSM && k->impl >= 1) {
+    kname = k->impl == 2 ? "dmma+tma" : "dmma";
+    if (k->edge & 1) kname += "+dfma-edge" + (edge_warps(k->edge) > 1 ? "x" + std::to_string(edge_warps(k->edge)) : "");
+    if (k->edge & 2) kname += "+pair";
+  } else if (p->op == TSM_OP_TSMTTSM) {
+    kname = k->impl ? "dmma" : "dfma";
+  } else {
+    kname = k->impl == 3   ? "dmma-cstationary+tma(p0=NBW,p1=WR)"
+            : k->impl == 2 ? "dmma+tma(p0=WR)"
+                           : (k->impl ? "dmma(p0=WR,p1=AP,p2=NOP)" : "dfma");
+  }
+  if (zr_flag(k->edge)) kname += "+complex-as-real(2Mx2N)";
   if (p->op == TSM_OP_TSMTTSM && k->impl >= 1)
     snprintf(tmp, sizeof tmp,
              "{\"op\":\"tsmttsm\",\"dtype\":\"%c\",\"M\":%d,\"N\":%d,\"WM\":%d,\"WN\":%d,"
@@ -600,9 +628,7 @@ tsm_status tsm_plan_describe(tsm_plan p, int64_t K, char* buf, size_t len) {
              "\"ctas_per_sm\":%d,\"smem\":%zu,\"grid\":%d,\"nchunks\":%lld,\"nfin\":%d,\"jit\":%s,"
              "\"kernel\":\"%s\"}",
              p->dt ? 'z' : 'd', p->M, p->N, k->p0, k->p1, k->p2, k->p3, k->NT, k->R, p->stages,
-             p->ctas_per_sm, p->smem, g.grid, g.nchunks, g.nfin, p->jit ? "true" : "false",
-             k->impl == 2 ? ((k->edge & 1) ? "dmma+tma+dfma-edge" : (k->edge & 2) ? "dmma+tma+pair" : "dmma+tma")
-                          : ((k->edge & 1) ? "dmma+dfma-edge" : (k->edge & 2) ? "dmma+pair" : "dmma"));
+             p->ctas_per_sm, p->smem, g.grid, g.nchunks, g.nfin, p->jit ? "true" : "false", kname.c_str());
   else if (p->op == TSM_OP_TSMTTSM)
     snprintf(tmp, sizeof tmp,
              "{\"op\":\"tsmttsm\",\"dtype\":\"%c\",\"M\":%d,\"N\":%d,\"MT\":%d,\"NTL\":%d,"
@@ -611,17 +637,14 @@ tsm_status tsm_plan_describe(tsm_plan p, int64_t K, char* buf, size_t len) {
              "\"kernel\":\"%s\"}",
              p->dt ? 'z' : 'd', p->M, p->N, k->p0, k->p1, (p->M + k->p0 - 1) / k->p0,
              (p->N + k->p1 - 1) / k->p1, k->NT, k->R, p->stages, p->ctas_per_sm, p->smem, g.grid,
-             g.nchunks, g.nfin, p->jit ? "true" : "false", k->impl ? "dmma" : "dfma");
+             g.nchunks, g.nfin, p->jit ? "true" : "false", kname.c_str());
   else
     snprintf(tmp, sizeof tmp,
              "{\"op\":\"tsmm\",\"dtype\":\"%c\",\"M\":%d,\"N\":%d,\"NTL\":%d,\"MSPLIT\":%d,"
              "\"U\":%d,\"threads\":%d,\"rows_per_chunk\":%d,\"stages\":%d,\"ctas_per_sm\":%d,"
              "\"smem\":%zu,\"grid\":%d,\"nchunks\":%lld,\"jit\":%s,\"kernel\":\"%s\"}",
              p->dt ? 'z' : 'd', p->M, p->N, k->p0, k->p1, k->p2, k->NT, k->R, p->stages,
-             p->ctas_per_sm, p->smem, g.grid, g.nchunks, p->jit ? "true" : "false",
-             k->impl == 3   ? "dmma-cstationary+tma(p0=NBW,p1=WR)"
-             : k->impl == 2 ? "dmma+tma(p0=WR)"
-                            : (k->impl ? "dmma(p0=WR,p1=AP,p2=NOP)" : "dfma"));
+             p->ctas_per_sm, p->smem, g.grid, g.nchunks, p->jit ? "true" : "false", kname.c_str());
   snprintf(buf, len, "%s", tmp);
   return TSM_SUCCESS;
 }

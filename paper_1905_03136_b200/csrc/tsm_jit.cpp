@@ -35,20 +35,23 @@ std::mutex g_jit_mu;
 std::deque<KernelEntry> g_jit_entries;  // stable addresses
 std::map<std::string, const KernelEntry*> g_jit_index;
 
-std::string cfg_type(const KernelEntry& e) {
+std::string cfg_type(const KernelEntry& ein) {
+  // complex-as-real entries instantiate the real kernel on 2M x 2N with ZR = true
+  const KernelEntry e = real_view(ein);
+  const char* zr = zr_flag(ein.edge) ? "true" : "false";
   std::ostringstream os;
   const char* z = e.dt ? "true" : "false";
   if (e.op == KIND_TSMTTSM && e.impl >= 1)
     os << "tsm::TsmttsmMmaCfg<" << e.M << ", " << e.N << ", " << z << ", " << e.p0 << ", " << e.p1
        << ", " << (e.NT / 32 - 1 - edge_warps(e.edge)) << ", " << e.R << ", " << e.p2 << ", " << e.p3 << ", "
        << (e.impl == 2 ? "true" : "false") << ", " << edge_warps(e.edge) << ", "
-       << ((e.edge & 2) ? "true" : "false") << ">";
+       << ((e.edge & 2) ? "true" : "false") << ", " << zr << ">";
   else if (e.op == KIND_TSMTTSM)
     os << "tsm::TsmttsmCfg<" << e.M << ", " << e.N << ", " << z << ", " << e.p0 << ", " << e.p1
        << ", " << e.NT << ", " << e.R << ">";
   else if (e.impl == 3)
     os << "tsm::TsmmCstCfg<" << e.M << ", " << e.N << ", " << z << ", " << e.p0 << ", " << e.p1
-       << ", " << (e.NT / 32 - 1) << ", " << e.R << ">";
+       << ", " << (e.NT / 32 - 1) << ", " << e.R << ", " << zr << ">";
   else if (e.impl >= 1)
     os << "tsm::TsmmMmaCfg<" << e.M << ", " << e.N << ", " << z << ", " << e.p0 << ", "
        << (e.NT / 32 - 1) << ", " << e.R << ", " << e.p1 << ", " << e.p2 << ", "

@@ -552,10 +552,11 @@ constexpr int pick_kdist(int ap, int bp, bool z, bool pair, int r) {
 // one 16-byte LDS.128 per lane feeds both fragments (half the load
 // instructions of one LDS.64 per fragment).
 template <int M_, int N_, bool Z_, int WM_, int WN_, int NW_, int R_, int AP_ = M_, int BP_ = N_,
-          bool TMA_ = false, int EDGE_ = 0, bool PAIR_ = false>
+          bool TMA_ = false, int EDGE_ = 0, bool PAIR_ = false, bool ZR_ = false>
 struct TsmttsmMmaCfg {
   static constexpr int M = M_, N = N_, WM = WM_, WN = WN_, NW = NW_, R = R_;
-  static constexpr bool Z = Z_, TMA = TMA_, EDGE = EDGE_ > 0, PAIR = PAIR_;
+  static constexpr bool Z = Z_, TMA = TMA_, EDGE = EDGE_ > 0, PAIR = PAIR_, ZR = ZR_;
+  static_assert(!ZR || (!Z_ && M_ % 2 == 0 && N_ % 2 == 0), "complex-as-real: real kernel on 2M x 2N");
   static_assert(!PAIR || (!Z_ && !EDGE_ && WM_ % 2 == 0 && WN_ % 2 == 0), "pairs: real, even tiles, no edge");
   static constexpr int S = Z ? 2 : 1;
   static constexpr int NBA = (M * S + 15) / 16, NBB = (N * S + 15) / 16;  // 16-double boxes
@@ -577,6 +578,7 @@ struct TsmttsmMmaCfg {
   static constexpr int RS = NW / WT;                            // row slots (k-step groups)
   static constexpr int NT = (NW + NE + 1) * 32;                 // + edge + producer warp
   static constexpr int CELLS = M * N * S;
+  static constexpr int OUT_CELLS = ZR ? CELLS / 2 : CELLS;  // doubles of the block partial
   static constexpr int STAGE_DOUBLES = R * (AP + BP) * S;
   // k-step row spacing (see pick_kdist); the 128B swizzle needs rows 2 apart
   static constexpr int KD = TMA ? 2 : pick_kdist(AP, BP, Z, PAIR, R);
@@ -895,7 +897,21 @@ __global__ void __launch_bounds__(Cfg::NT) tsmttsm_mma_kernel(const __grid_const
     }
     __syncthreads();
   }
-  grid_reduce<Cfg::NT, CELLS>(p, sP, ring + CELLS);
+  if constexpr (Cfg::ZR) {
+    // complex C from the real product P = Ar^T Br of the interleaved (re, im)
+    // columns: C[m][n] = (P[2m][2n] - P[2m+1][2n+1]) + i (P[2m][2n+1] + P[2m+1][2n])
+    constexpr int NZ = N / 2, MNZ = (M / 2) * NZ;
+    double* sQ = ring + CELLS;
+    for (int idx = tid; idx < MNZ; idx += Cfg::NT) {
+      const int m = 2 * (idx / NZ), n = 2 * (idx % NZ);
+      sQ[2 * idx] = sP[m * N + n] - sP[(m + 1) * N + n + 1];
+      sQ[2 * idx + 1] = sP[m * N + n + 1] + sP[(m + 1) * N + n];
+    }
+    __syncthreads();
+    grid_reduce<Cfg::NT, Cfg::OUT_CELLS>(p, sQ, sQ + Cfg::OUT_CELLS);
+  } else {
+    grid_reduce<Cfg::NT, CELLS>(p, sP, ring + CELLS);
+  }
 }
 
 // ==========================================================================
@@ -1396,10 +1412,11 @@ __global__ void __launch_bounds__(Cfg::NT) tsmm_mma_kernel(const __grid_constant
 // Requires the TMA conditions (M*S, N*S even and >= 16) and 8*NBW*S a
 // multiple of 16 doubles (whole output boxes per warp).
 // --------------------------------------------------------------------------
-template <int M_, int N_, bool Z_, int NBW_, int WR_, int NW_, int R_>
+template <int M_, int N_, bool Z_, int NBW_, int WR_, int NW_, int R_, bool ZR_ = false>
 struct TsmmCstCfg {
   static constexpr int M = M_, N = N_, NBW = NBW_, WR = WR_, NW = NW_, R = R_;
-  static constexpr bool Z = Z_;
+  static constexpr bool Z = Z_, ZR = ZR_;
+  static_assert(!ZR || (!Z_ && M_ % 2 == 0 && N_ % 2 == 0), "complex-as-real: real kernel on 2M x 2N");
   static constexpr int S = Z ? 2 : 1;
   static constexpr int MK = (M + 3) / 4;            // k-steps over m
   static constexpr int NB = (N + 7) / 8;            // 8-column blocks of B
@@ -1478,8 +1495,20 @@ __global__ void __launch_bounds__(Cfg::NT) tsmm_cst_kernel(const __grid_constant
 #pragma unroll
       for (int j = 0; j < NBW; j++) {
         const int m = 4 * ks + q, n = 8 * (nb0 + j) + g;
+        if constexpr (Cfg::ZR) {
+          // complex C as the real 2M x 2N matrix C' with B_real = A_real C':
+          // C'[2m][2n] = C'[2m+1][2n+1] = Re c, C'[2m][2n+1] = Im c, C'[2m+1][2n] = -Im c
+          double v = 0.0;
+          if (m < M && n < N) {
+            const double* c2 = p.C + ((m >> 1) * (N >> 1) + (n >> 1)) * 2;
+            const double re = __ldg(c2), im = __ldg(c2 + 1);
+            v = ((m & 1) == (n & 1)) ? re : ((m & 1) ? -im : im);
+          }
+          cf[ks][j][0] = v;
+        } else {
 #pragma unroll
-        for (int z = 0; z < S; z++) cf[ks][j][z] = (m < M && n < N) ? __ldg(&p.C[(m * N + n) * S + z]) : 0.0;
+          for (int z = 0; z < S; z++) cf[ks][j][z] = (m < M && n < N) ? __ldg(&p.C[(m * N + n) * S + z]) : 0.0;
+        }
       }
     auto aoff = [&](int r, int x) -> int {  // element (row r, column x) of the A stage
       return ((x * S) >> 4) * (R * 16) + swz128(r, (x * S) & 15);

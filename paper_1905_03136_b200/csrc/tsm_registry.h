@@ -21,11 +21,28 @@ struct KernelEntry {
                      // 2 = DMMA + TMA tensor copies, 3 = C-stationary DMMA TSMM
   int edge;          // DMMA TSMTTSM flags: bit 0 = DFMA edge warps for the cells outside the
                      // 8-aligned core, bit 1 = paired 16-byte fragment loads, bits 2-3 =
-                     // edge warps - 1 (tsm_config.kernel bits 4..7)
+                     // edge warps - 1, bit 4 = complex-as-real (tsm_config.kernel bits 4..8)
 };
 
 // number of DFMA edge warps encoded in KernelEntry::edge
 inline int edge_warps(int flags) { return (flags & 1) ? 1 + ((flags >> 2) & 3) : 0; }
+
+// bit 4: complex (Z) computed by the real kernel on the interleaved view -- A, B
+// as real K x 2M, K x 2N; TSMTTSM combines the 2M x 2N real product, TSMM uses
+// the real 2M x 2N image of C (tsm_kernels.cuh ZR)
+inline bool zr_flag(int flags) { return (flags & 16) != 0; }
+
+// the real problem a complex-as-real entry runs (identity otherwise)
+inline KernelEntry real_view(const KernelEntry& k) {
+  KernelEntry v = k;
+  if (zr_flag(k.edge)) {
+    v.M = 2 * k.M;
+    v.N = 2 * k.N;
+    v.dt = 0;
+    v.edge = k.edge & ~16;
+  }
+  return v;
+}
 
 struct KernelTable {
   const KernelEntry* entries;

@@ -154,3 +154,55 @@ def test_dmma_pair_loads(tsm, M, N):
         got = tsm.tsmttsm(torch.from_numpy(Ai).cuda(), torch.from_numpy(Bi).cuda(), plan=plan)
         torch.cuda.synchronize()
         assert np.array_equal(got.cpu().numpy(), oracle.tsmttsm(Ai, Bi)[0]), c
+
+
+@pytest.mark.parametrize("op", ["tsmttsm", "tsmm"])
+@pytest.mark.parametrize("M,N", [(17, 17), (9, 12), (33, 20), (8, 8), (25, 25), (40, 48)])
+def test_complex_as_real(tsm, op, M, N):
+    """Z through the real kernels on the interleaved 2M x 2N view (kernel | 256):
+    every family the generator offers (TMA / bulk, pair, edge), ragged K, and
+    integer-valued inputs bit-exact against the oracle."""
+    cands = gi.zr_candidates(op, M, N)
+    if not cands:
+        pytest.skip("no complex-as-real candidate for this shape")
+    picked = {}
+    for c in cands:
+        picked.setdefault((c.get("impl"), c.get("PAIR", 0), c.get("EDGE", 0)), c)
+    ran = 0
+    for key, c in sorted(picked.items()):
+        try:
+            plan = tsm.Plan(op, "z", M, N, 0, config=gi.to_tsm_config(op, c, 3, 1))
+        except tsm.TsmError as e:
+            if e.status != 2:
+                raise
+            continue
+        assert plan.config()["kernel"] & 256
+        assert "complex-as-real" in plan.describe(1000)["kernel"]
+        ran += 1
+        for K in (1, 5, 4099, 65537):
+            A = ti.matrix(K, M, "A", complex_=True, seed=K + 11)
+            if op == "tsmttsm":
+                B = ti.matrix(K, N, "B", complex_=True, seed=K + 12)
+                got = tsm.tsmttsm(torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda(), plan=plan)
+                ref, bound = oracle.tsmttsm(A, B)
+                tol = 1e-12
+            else:
+                Cm = ti.matrix(M, N, "C", complex_=True, seed=K + 13)
+                got = tsm.tsmm(torch.from_numpy(A).cuda(), torch.from_numpy(Cm).cuda(), plan=plan)
+                ref, bound = oracle.tsmm(A, Cm)
+                tol = 1e-13
+            torch.cuda.synchronize()
+            r, wi, _ = oracle.max_err_ratio(got.cpu().numpy(), ref, bound)
+            assert r <= tol, (op, M, N, key, c, K, r, wi)
+        Ai = ti.matrix(30001, M, "A", complex_=True, mode="int")
+        if op == "tsmttsm":
+            Bi = ti.matrix(30001, N, "B", complex_=True, mode="int")
+            got = tsm.tsmttsm(torch.from_numpy(Ai).cuda(), torch.from_numpy(Bi).cuda(), plan=plan)
+            ref = oracle.tsmttsm(Ai, Bi)[0]
+        else:
+            Ci = ti.matrix(M, N, "C", complex_=True, mode="int")
+            got = tsm.tsmm(torch.from_numpy(Ai).cuda(), torch.from_numpy(Ci).cuda(), plan=plan)
+            ref = oracle.tsmm(Ai, Ci)[0]
+        torch.cuda.synchronize()
+        assert np.array_equal(got.cpu().numpy(), ref), (key, c)
+    assert ran

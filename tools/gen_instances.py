@@ -305,17 +305,20 @@ def resolve(op: str, M: int, N: int, z: bool, tuned: dict | None) -> dict:
 
 
 def cfg_type(op, dt, M, N, c) -> str:
+    zr = "true" if c.get("ZR", 0) else "false"
+    if c.get("ZR", 0):  # complex-as-real: the real kernel on the interleaved 2M x 2N view
+        M, N, dt = 2 * M, 2 * N, "d"
     z = "true" if dt == "z" else "false"
     if op == "tsmttsm" and c.get("impl", 0) >= 1:
         tma = "true" if c["impl"] == 2 else "false"
         edge = c.get("EDGE", 0)
         pair = "true" if c.get("PAIR", 0) else "false"
         return (f"tsm::TsmttsmMmaCfg<{M}, {N}, {z}, {c['MT']}, {c['NTL']}, {c['NT'] // 32 - 1 - edge}, "
-                f"{c['R']}, {c.get('AP', M)}, {c.get('BP', N)}, {tma}, {edge}, {pair}>")
+                f"{c['R']}, {c.get('AP', M)}, {c.get('BP', N)}, {tma}, {edge}, {pair}, {zr}>")
     if op == "tsmttsm":
         return f"tsm::TsmttsmCfg<{M}, {N}, {z}, {c['MT']}, {c['NTL']}, {c['NT']}, {c['R']}>"
     if c.get("impl", 0) == 3:
-        return f"tsm::TsmmCstCfg<{M}, {N}, {z}, {c['NBW']}, {c['WR']}, {c['NT'] // 32 - 1}, {c['R']}>"
+        return f"tsm::TsmmCstCfg<{M}, {N}, {z}, {c['NBW']}, {c['WR']}, {c['NT'] // 32 - 1}, {c['R']}, {zr}>"
     if c.get("impl", 0) >= 1:
         tma = "true" if c["impl"] == 2 else "false"
         return (f"tsm::TsmmMmaCfg<{M}, {N}, {z}, {c['WR']}, {c['NT'] // 32 - 1}, {c['R']}, "
@@ -342,13 +345,17 @@ def entry_init(op, dt, M, N, c) -> str:
 
 def flags(c: dict) -> int:
     """KernelEntry.edge / tsm_config.kernel >> 4: bit 0 DFMA edge warps, bit 1
-    paired 16-byte fragment loads, bits 2-3 edge warps - 1 (EDGE = edge warp count)."""
+    paired 16-byte fragment loads, bits 2-3 edge warps - 1 (EDGE = edge warp count),
+    bit 4 complex-as-real (ZR)."""
     e = c.get("EDGE", 0)
-    return (1 if e else 0) | (c.get("PAIR", 0) << 1) | (((e - 1) & 3) << 2 if e else 0)
+    return ((1 if e else 0) | (c.get("PAIR", 0) << 1) | (((e - 1) & 3) << 2 if e else 0)
+            | (c.get("ZR", 0) << 4))
 
 
 def params4(op: str, M: int, N: int, c: dict) -> tuple:
     """(p0, p1, p2, p3) of the registry entry / tsm_config for a gen-style cfg."""
+    if c.get("ZR", 0):
+        M, N = 2 * M, 2 * N
     if op == "tsmttsm":
         if c.get("impl", 0) >= 1:
             return (c["MT"], c["NTL"], c.get("AP", M), c.get("BP", N))
@@ -529,6 +536,8 @@ def candidates(op: str, M: int, N: int, z: bool) -> list:
                 MS *= 2
     if op == "tsmm":
         out.extend(tsmm_cst_configs(M, N, z))
+    if z:
+        out.extend(zr_candidates(op, M, N))
     if op == "tsmm" and N >= 2:
         d = tsmm_mma_default(M, N, z)
         S_ = 2 if z else 1
@@ -553,6 +562,21 @@ def candidates(op: str, M: int, N: int, z: bool) -> list:
             seen.add(k)
             uniq.append(c)
     return uniq
+
+
+def zr_candidates(op: str, M: int, N: int) -> list:
+    """Complex-as-real (ZR=1): the real DMMA kernels on the interleaved 2M x 2N
+    view (A, B as real K x 2M, K x 2N).  Flops and bytes equal the complex
+    kernel's; 8x8 blocks pad 2M instead of M (Z 17: 40/34 instead of 24/17)."""
+    if op == "tsmttsm":
+        if min(M, N) < 4:
+            return []
+        base = [c for c in candidates("tsmttsm", 2 * M, 2 * N, False) if c.get("impl", 0) in (1, 2)]
+    else:
+        if 2 * M < 16 or 2 * N < 16:
+            return []
+        base = tsmm_cst_configs(2 * M, 2 * N, False)
+    return [dict(c, ZR=1) for c in base]
 
 
 def to_tsm_config(op: str, c: dict, stages: int, ctas: int) -> dict:
