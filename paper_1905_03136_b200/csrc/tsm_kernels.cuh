@@ -127,6 +127,12 @@ __device__ __forceinline__ void zfma(double& re, double& im, double ar, double a
 // Position in the smem ring: stage index s, mbarrier phase parity ph of that
 // stage's current use, and how many times the ring wrapped (incremental, so
 // the hot loops carry no integer division by the run-time stage count).
+// compile-time int as a value (dispatching generic lambdas on a constant)
+template <int V>
+struct IC {
+  static constexpr int value = V;
+};
+
 struct Ring {
   int s = 0;
   u32 ph = 0;
@@ -652,8 +658,12 @@ __global__ void __launch_bounds__(Cfg::NT) tsmttsm_mma_kernel(const __grid_const
   // rows in different swizzle phases; dense rows: see pick_kdist).  The sum over
   // k is unchanged: A and B fragments of a lane always read the same row, and
   // the k-steps of a 4KD-row atom visit each of its rows once.
-  auto kstep = [&](const double* __restrict__ sA, const double* __restrict__ sB, int k0, int rows,
-                   int ap, int bp) {
+  // cm, cn (IC<.>): accumulator blocks of this warp's tile that lie inside C --
+  // compile-time, so partial tiles issue no predicated-off DMMAs (which still
+  // occupy the tensor pipe: ncu r19, D 40 ran 30 block-slots for 25 blocks).
+  auto kstep = [&](auto cm, auto cn, const double* __restrict__ sA, const double* __restrict__ sB, int k0,
+                   int rows, int ap, int bp) {
+    constexpr int CM = decltype(cm)::value, CN = decltype(cn)::value;
     constexpr int KD = Cfg::KD;
     const int kr = (k0 & ~(4 * KD - 1)) + ((k0 >> 2) & (KD - 1)) + KD * q;
     const bool rv = kr < rows;
@@ -662,7 +672,7 @@ __global__ void __launch_bounds__(Cfg::NT) tsmttsm_mma_kernel(const __grid_const
       if constexpr (Cfg::PAIR) {
         // one 16-byte load per lane: (m, m+1) -> fragments of blocks 2p, 2p+1
 #pragma unroll
-        for (int ip = 0; ip < WM / 2; ip++) {
+        for (int ip = 0; ip < CM / 2; ip++) {
           const int m = (wm * WM + 2 * ip) * 8 + 2 * g;
           double2 v = make_double2(0.0, 0.0);
           if (rv && m + 1 < M)
@@ -673,7 +683,7 @@ __global__ void __launch_bounds__(Cfg::NT) tsmttsm_mma_kernel(const __grid_const
           a[2 * ip + 1] = v.y;
         }
 #pragma unroll
-        for (int jp = 0; jp < WN / 2; jp++) {
+        for (int jp = 0; jp < CN / 2; jp++) {
           const int n = (wn * WN + 2 * jp) * 8 + 2 * g;
           double2 v = make_double2(0.0, 0.0);
           if (rv && n + 1 < N)
@@ -685,41 +695,39 @@ __global__ void __launch_bounds__(Cfg::NT) tsmttsm_mma_kernel(const __grid_const
         }
       } else {
 #pragma unroll
-        for (int i = 0; i < WM; i++) {
+        for (int i = 0; i < CM; i++) {
           const int m = (wm * WM + i) * 8 + g;
           a[i] = (rv && m < M) ? sA[off(kr, m, ap)] : 0.0;
         }
 #pragma unroll
-        for (int j = 0; j < WN; j++) {
+        for (int j = 0; j < CN; j++) {
           const int n = (wn * WN + j) * 8 + g;
           b[j] = (rv && n < N) ? sB[off(kr, n, bp)] : 0.0;
         }
       }
 #pragma unroll
-      for (int i = 0; i < WM; i++)
+      for (int i = 0; i < CM; i++)
 #pragma unroll
-        for (int j = 0; j < WN; j++)
-          if ((wm * WM + i) < MB && (wn * WN + j) < NB) dmma(acc[i][j][0][0], acc[i][j][0][1], a[i], b[j]);
+        for (int j = 0; j < CN; j++) dmma(acc[i][j][0][0], acc[i][j][0][1], a[i], b[j]);
     } else {
       double2 a[WM], b[WN];
 #pragma unroll
-      for (int i = 0; i < WM; i++) {
+      for (int i = 0; i < CM; i++) {
         const int m = (wm * WM + i) * 8 + g;
         a[i] = (rv && m < M) ? *reinterpret_cast<const double2*>(sA + off(kr, m, ap))
                              : make_double2(0.0, 0.0);
       }
 #pragma unroll
-      for (int j = 0; j < WN; j++) {
+      for (int j = 0; j < CN; j++) {
         const int n = (wn * WN + j) * 8 + g;
         b[j] = (rv && n < N) ? *reinterpret_cast<const double2*>(sB + off(kr, n, bp))
                              : make_double2(0.0, 0.0);
       }
 #pragma unroll
-      for (int i = 0; i < WM; i++) {
+      for (int i = 0; i < CM; i++) {
         const double nai = -a[i].y;
 #pragma unroll
-        for (int j = 0; j < WN; j++)
-          if ((wm * WM + i) < MB && (wn * WN + j) < NB) {
+        for (int j = 0; j < CN; j++) {
             dmma(acc[i][j][0][0], acc[i][j][0][1], a[i].x, b[j].x);  // re += ar br
             dmma(acc[i][j][0][0], acc[i][j][0][1], nai, b[j].y);     // re -= ai bi
             dmma(acc[i][j][1][0], acc[i][j][1][1], a[i].x, b[j].y);  // im += ar bi
@@ -830,29 +838,42 @@ __global__ void __launch_bounds__(Cfg::NT) tsmttsm_mma_kernel(const __grid_const
     }
   } else {
     // ---------------- consumer warps ----------------
-    Ring ring_it;
-    for (long long c = blockIdx.x; c < p.nchunks; c += G, ring_it.next(stages)) {
-      const int s = ring_it.s;
-      mbar_wait(&full[s], ring_it.ph);
-      const double* sA = ring + static_cast<long long>(s) * Cfg::STAGE_DOUBLES;
-      const double* sB = sA + R * AP * S;
-      const long long r0 = c * R;
-      const int rows = Cfg::TMA ? R : static_cast<int>((K_even - r0 < R) ? (K_even - r0) : R);
-      if (rows == R) {
+    auto consume = [&](auto cm, auto cn) {
+      Ring ring_it;
+      for (long long c = blockIdx.x; c < p.nchunks; c += G, ring_it.next(stages)) {
+        const int s = ring_it.s;
+        mbar_wait(&full[s], ring_it.ph);
+        const double* sA = ring + static_cast<long long>(s) * Cfg::STAGE_DOUBLES;
+        const double* sB = sA + R * AP * S;
+        const long long r0 = c * R;
+        const int rows = Cfg::TMA ? R : static_cast<int>((K_even - r0 < R) ? (K_even - r0) : R);
+        if (rows == R) {
 #pragma unroll 2
-        for (int k0 = slot * 4; k0 < R; k0 += RS * 4) kstep(sA, sB, k0, R, AP, BP);
-      } else {  // partial chunk: every k-step of the atoms that hold rows < rows
-        const int kend = (rows + 4 * Cfg::KD - 1) & ~(4 * Cfg::KD - 1);
-        for (int k0 = slot * 4; k0 < kend; k0 += RS * 4) kstep(sA, sB, k0, rows, AP, BP);
+          for (int k0 = slot * 4; k0 < R; k0 += RS * 4) kstep(cm, cn, sA, sB, k0, R, AP, BP);
+        } else {  // partial chunk: every k-step of the atoms that hold rows < rows
+          const int kend = (rows + 4 * Cfg::KD - 1) & ~(4 * Cfg::KD - 1);
+          for (int k0 = slot * 4; k0 < kend; k0 += RS * 4) kstep(cm, cn, sA, sB, k0, rows, AP, BP);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[s]);
-    }
-    // odd last row: a k-step whose rows 1..3 are zero, from global memory
-    if constexpr (!Cfg::TMA) {
-      if ((K & 1) && blockIdx.x == 0 && slot == 0)
-        kstep(p.A + (K - 1) * M * S, p.B + (K - 1) * N * S, 0, 1, M, N);
-    }
+      // odd last row: a k-step whose rows 1..3 are zero, from global memory
+      if constexpr (!Cfg::TMA) {
+        if ((K & 1) && blockIdx.x == 0 && slot == 0)
+          kstep(cm, cn, p.A + (K - 1) * M * S, p.B + (K - 1) * N * S, 0, 1, M, N);
+      }
+    };
+    // warp-uniform dispatch on whether this warp's tile is the last (partial) one
+    constexpr int RM = MB - (WTM - 1) * WM, RN = NB - (Cfg::WTN - 1) * WN;  // blocks in C
+    const bool lm = (wm == WTM - 1), ln = (wn == Cfg::WTN - 1);
+    if (lm && ln)
+      consume(IC<RM>{}, IC<RN>{});
+    else if (lm)
+      consume(IC<RM>{}, IC<WN>{});
+    else if (ln)
+      consume(IC<WM>{}, IC<RN>{});
+    else
+      consume(IC<WM>{}, IC<WN>{});
   }
   __syncthreads();  // ring idle: every issued chunk was consumed
 
@@ -1513,80 +1534,90 @@ __global__ void __launch_bounds__(Cfg::NT) tsmm_cst_kernel(const __grid_constant
     auto aoff = [&](int r, int x) -> int {  // element (row r, column x) of the A stage
       return ((x * S) >> 4) * (R * 16) + swz128(r, (x * S) & 15);
     };
-    Ring ring_it;
-    for (long long c = blockIdx.x; c < p.nchunks; c += G, ring_it.next(stages)) {
-      const int s = ring_it.s;
-      mbar_wait(&full[s], ring_it.ph);
-      const double* sA = ring + static_cast<long long>(s) * Cfg::STAGE_DOUBLES;
-      const long long r0 = c * R;
-      const int rows = static_cast<int>((K - r0 < R) ? (K - r0) : R);
-#pragma unroll 1
-      for (int pr = 0; pr < rows; pr += RPP) {
-        const int wr0 = pr + rg * RW;
-        if (wr0 >= rows) break;
-        double acc[WR][NBW][S][2];
-#pragma unroll
-        for (int i = 0; i < WR; i++)
-#pragma unroll
-          for (int j = 0; j < NBW; j++)
-#pragma unroll
-            for (int z = 0; z < S; z++) acc[i][j][z][0] = acc[i][j][z][1] = 0.0;
-#pragma unroll
-        for (int ks = 0; ks < MK; ks++) {
-          const int m = 4 * ks + q;
-          const bool mv = (4 * ks + 4 <= M) || (m < M);
-#pragma unroll
-          for (int i = 0; i < WR; i++) {
-            const int r = wr0 + 8 * i + rho;
-            if constexpr (!Cfg::Z) {
-              const double a = mv ? sA[aoff(r, m)] : 0.0;
-#pragma unroll
-              for (int j = 0; j < NBW; j++) dmma(acc[i][j][0][0], acc[i][j][0][1], a, cf[ks][j][0]);
-            } else {
-              const double2 a = mv ? *reinterpret_cast<const double2*>(sA + aoff(r, m)) : make_double2(0.0, 0.0);
-              const double nai = -a.y;
-#pragma unroll
-              for (int j = 0; j < NBW; j++) {
-                dmma(acc[i][j][0][0], acc[i][j][0][1], a.x, cf[ks][j][0]);  // re += ar cr
-                dmma(acc[i][j][0][0], acc[i][j][0][1], nai, cf[ks][j][1]);  // re -= ai ci
-                dmma(acc[i][j][1][0], acc[i][j][1][1], a.x, cf[ks][j][1]);  // im += ar ci
-                dmma(acc[i][j][1][0], acc[i][j][1][1], a.y, cf[ks][j][0]);  // im += ai cr
+    // blocks of this warp's column group inside C (the last group may be
+    // partial): compile-time, so no DMMA is issued for columns past N
+    auto consume = [&](auto nbv) {
+      constexpr int NBV = decltype(nbv)::value;
+      Ring ring_it;
+      for (long long c = blockIdx.x; c < p.nchunks; c += G, ring_it.next(stages)) {
+        const int s = ring_it.s;
+        mbar_wait(&full[s], ring_it.ph);
+        const double* sA = ring + static_cast<long long>(s) * Cfg::STAGE_DOUBLES;
+        const long long r0 = c * R;
+        const int rows = static_cast<int>((K - r0 < R) ? (K - r0) : R);
+  #pragma unroll 1
+        for (int pr = 0; pr < rows; pr += RPP) {
+          const int wr0 = pr + rg * RW;
+          if (wr0 >= rows) break;
+          double acc[WR][NBW][S][2];
+  #pragma unroll
+          for (int i = 0; i < WR; i++)
+  #pragma unroll
+            for (int j = 0; j < NBW; j++)
+  #pragma unroll
+              for (int z = 0; z < S; z++) acc[i][j][z][0] = acc[i][j][z][1] = 0.0;
+  #pragma unroll
+          for (int ks = 0; ks < MK; ks++) {
+            const int m = 4 * ks + q;
+            const bool mv = (4 * ks + 4 <= M) || (m < M);
+  #pragma unroll
+            for (int i = 0; i < WR; i++) {
+              const int r = wr0 + 8 * i + rho;
+              if constexpr (!Cfg::Z) {
+                const double a = mv ? sA[aoff(r, m)] : 0.0;
+  #pragma unroll
+                for (int j = 0; j < NBV; j++) dmma(acc[i][j][0][0], acc[i][j][0][1], a, cf[ks][j][0]);
+              } else {
+                const double2 a = mv ? *reinterpret_cast<const double2*>(sA + aoff(r, m)) : make_double2(0.0, 0.0);
+                const double nai = -a.y;
+  #pragma unroll
+                for (int j = 0; j < NBV; j++) {
+                  dmma(acc[i][j][0][0], acc[i][j][0][1], a.x, cf[ks][j][0]);  // re += ar cr
+                  dmma(acc[i][j][0][0], acc[i][j][0][1], nai, cf[ks][j][1]);  // re -= ai ci
+                  dmma(acc[i][j][1][0], acc[i][j][1][1], a.x, cf[ks][j][1]);  // im += ar ci
+                  dmma(acc[i][j][1][0], acc[i][j][1][1], a.y, cf[ks][j][0]);  // im += ai cr
+                }
               }
             }
           }
-        }
-        // registers -> private swizzled staging -> TMA tensor stores
-        if (lane == 0) bulk_wait_read<0>();
-        __syncwarp();
-#pragma unroll
-        for (int i = 0; i < WR; i++)
-#pragma unroll
-          for (int j = 0; j < NBW; j++) {
-            const int rr = 8 * i + rho;
-            if constexpr (!Cfg::Z) {
-              const int c0 = 8 * j + 2 * q;  // column within the warp's tile (doubles)
-              *reinterpret_cast<double2*>(stg + (c0 >> 4) * (RW * 16) + swz128(rr, c0 & 15)) =
-                  make_double2(acc[i][j][0][0], acc[i][j][0][1]);
-            } else {
-#pragma unroll
-              for (int e = 0; e < 2; e++) {
-                const int c0 = 2 * (8 * j + 2 * q + e);
+          // registers -> private swizzled staging -> TMA tensor stores
+          if (lane == 0) bulk_wait_read<0>();
+          __syncwarp();
+  #pragma unroll
+          for (int i = 0; i < WR; i++)
+  #pragma unroll
+            for (int j = 0; j < NBV; j++) {  // blocks past N: clipped by the TMA store
+              const int rr = 8 * i + rho;
+              if constexpr (!Cfg::Z) {
+                const int c0 = 8 * j + 2 * q;  // column within the warp's tile (doubles)
                 *reinterpret_cast<double2*>(stg + (c0 >> 4) * (RW * 16) + swz128(rr, c0 & 15)) =
-                    make_double2(acc[i][j][0][e], acc[i][j][1][e]);
+                    make_double2(acc[i][j][0][0], acc[i][j][0][1]);
+              } else {
+  #pragma unroll
+                for (int e = 0; e < 2; e++) {
+                  const int c0 = 2 * (8 * j + 2 * q + e);
+                  *reinterpret_cast<double2*>(stg + (c0 >> 4) * (RW * 16) + swz128(rr, c0 & 15)) =
+                      make_double2(acc[i][j][0][e], acc[i][j][1][e]);
+                }
               }
             }
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0 && nb0 < NB) {
+            for (int b = 0; b < OB; b++)
+              tma_store_2d(&p.tmB, nb0 * 8 * S + b * 16, static_cast<int>(r0 + wr0), stg + b * RW * 16);
+            bulk_commit();
           }
-        fence_proxy_async_smem();
-        __syncwarp();
-        if (lane == 0 && nb0 < NB) {
-          for (int b = 0; b < OB; b++)
-            tma_store_2d(&p.tmB, nb0 * 8 * S + b * 16, static_cast<int>(r0 + wr0), stg + b * RW * 16);
-          bulk_commit();
         }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[s]);
-    }
+    };
+    constexpr int NBL = NB - (NG - 1) * NBW;
+    if (cg == NG - 1)
+      consume(IC<NBL>{});
+    else
+      consume(IC<NBW>{});
     if (lane == 0) bulk_wait_all();
   }
 }
