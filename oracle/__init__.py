@@ -11,7 +11,10 @@ Definitions (PAPER.md is the authority):
     -- PAPER.md:64-68 (op definitions), PAPER.md:342-349 (Listing 1).
   * TSMM ``B = A C``, ``B[k][n] = sum_m A[k][m] C[m][n]``
     -- PAPER.md:64-68, PAPER.md:372-375 (reduction along the short M axis).
-  * Z = complex128, plain (non-conjugating) transpose -- DESIGN.md reading R1.
+  * Z = complex128, plain (non-conjugating) transpose -- DESIGN.md reading R1;
+    ``conj=True`` gives the conjugate variants of NEXT row N2 (A^H B, A conj(C)).
+  * TSMM update ``B <- alpha A C + beta B`` -- NEXT row N1, the classical
+    Gram-Schmidt step of PAPER.md:108-112 (alpha = -1, beta = 1).
 
 Every function returns ``(result, bound)`` where ``bound`` is the north-star
 tolerance scale ``|A|^T |B|`` (TSMTTSM) or ``|A||C|`` (TSMM).
@@ -50,10 +53,16 @@ def _load():
     if _lib is None:
         lib = ctypes.CDLL(build())
         dp = ctypes.POINTER(ctypes.c_double)
-        for name in ("oracle_tsmttsm_d", "oracle_tsmttsm_z", "oracle_tsmm_d", "oracle_tsmm_z"):
+        for name in ("oracle_tsmttsm_d", "oracle_tsmttsm_z", "oracle_tsmttsm_zc", "oracle_tsmm_d",
+                     "oracle_tsmm_z"):
             f = getattr(lib, name)
             f.argtypes = [ctypes.c_int64, ctypes.c_int, ctypes.c_int, dp, dp, dp, dp]
             f.restype = None
+        d, i = ctypes.c_double, ctypes.c_int
+        lib.oracle_tsmm_update_d.argtypes = [ctypes.c_int64, i, i, d, dp, dp, d, dp, dp]
+        lib.oracle_tsmm_update_d.restype = None
+        lib.oracle_tsmm_update_z.argtypes = [ctypes.c_int64, i, i, d, d, dp, dp, d, d, dp, dp, i]
+        lib.oracle_tsmm_update_z.restype = None
         lib.oracle_max_err_ratio.argtypes = [ctypes.c_int64, ctypes.c_int, dp, dp, dp,
                                              ctypes.POINTER(ctypes.c_int64), dp]
         lib.oracle_max_err_ratio.restype = ctypes.c_double
@@ -82,9 +91,12 @@ def set_num_threads(n: int) -> None:
     _load().oracle_set_num_threads(int(n))
 
 
-def tsmttsm(A: np.ndarray, B: np.ndarray):
-    """C = A^T B (plain transpose).  A: K x M, B: K x N -> (C M x N, bound M x N)."""
+def tsmttsm(A: np.ndarray, B: np.ndarray, conj: bool = False):
+    """C = A^T B (plain transpose; conj=True: A^H B, complex only -- NEXT N2).
+    A: K x M, B: K x N -> (C M x N, bound M x N)."""
     is_c = np.iscomplexobj(A)
+    if conj and not is_c:
+        raise ValueError("conj applies to complex inputs")
     A = _prep(A, is_c)
     B = _prep(B, is_c)
     K, M = A.shape
@@ -93,7 +105,7 @@ def tsmttsm(A: np.ndarray, B: np.ndarray):
         raise ValueError("A and B must have the same row count K")
     C = np.zeros((M, N), dtype=A.dtype)
     bound = np.zeros((M, N), dtype=np.float64)
-    f = _load().oracle_tsmttsm_z if is_c else _load().oracle_tsmttsm_d
+    f = (_load().oracle_tsmttsm_zc if conj else _load().oracle_tsmttsm_z) if is_c else _load().oracle_tsmttsm_d
     f(K, M, N, _ptr(A), _ptr(B), _ptr(C), _ptr(bound))
     return C, bound
 
@@ -112,6 +124,33 @@ def tsmm(A: np.ndarray, C: np.ndarray):
     f = _load().oracle_tsmm_z if is_c else _load().oracle_tsmm_d
     f(K, M, N, _ptr(A), _ptr(C), _ptr(B), _ptr(bound))
     return B, bound
+
+
+def tsmm_update(A: np.ndarray, C: np.ndarray, B: np.ndarray, alpha, beta, conj: bool = False):
+    """B_new = alpha * A C + beta * B (conj=True: A conj(C), complex only) --
+    NEXT N1, the classical Gram-Schmidt update of PAPER.md:108-112 (alpha=-1,
+    beta=1).  B is not modified.  -> (B_new K x N, bound K x N)."""
+    is_c = np.iscomplexobj(A)
+    if conj and not is_c:
+        raise ValueError("conj applies to complex inputs")
+    A = _prep(A, is_c)
+    C = _prep(C, is_c)
+    out = _prep(np.array(B, copy=True), is_c)
+    K, M = A.shape
+    M2, N = C.shape
+    if M != M2 or out.shape != (K, N):
+        raise ValueError("shape mismatch")
+    bound = np.zeros((K, N), dtype=np.float64)
+    lib = _load()
+    if is_c:
+        al, be = complex(alpha), complex(beta)
+        lib.oracle_tsmm_update_z(K, M, N, ctypes.c_double(al.real), ctypes.c_double(al.imag), _ptr(A), _ptr(C),
+                                 ctypes.c_double(be.real), ctypes.c_double(be.imag), _ptr(out), _ptr(bound),
+                                 int(conj))
+    else:
+        lib.oracle_tsmm_update_d(K, M, N, ctypes.c_double(float(alpha)), _ptr(A), _ptr(C),
+                                 ctypes.c_double(float(beta)), _ptr(out), _ptr(bound))
+    return out, bound
 
 
 def max_err_ratio(got: np.ndarray, ref: np.ndarray, bound: np.ndarray):

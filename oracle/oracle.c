@@ -141,10 +141,13 @@ void oracle_tsmttsm_d(int64_t K, int M, int N, const double *A, const double *B,
 }
 
 /* ------------------------------------------------------------------------ */
-/* TSMTTSM, complex double (interleaved re,im).  Plain transpose, no conj.   */
+/* TSMTTSM, complex double (interleaved re,im).  Plain transpose (R1); with  */
+/* conj = 1 the conjugate transpose C = A^H B (NEXT row N2: the complex      */
+/* Gram-Schmidt use of PAPER.md:108-112 needs A^H): conj(a) = ar - i ai is   */
+/* substituted for a, i.e. ai -> -ai in the same 4 fmas.                     */
 /* ------------------------------------------------------------------------ */
-void oracle_tsmttsm_z(int64_t K, int M, int N, const double *A, const double *B,
-                      double *C, double *bound) {
+static void tsmttsm_z_impl(int64_t K, int M, int N, const double *A, const double *B,
+                           double *C, double *bound, int conj) {
   const int64_t MN = (int64_t)M * N;
   const int64_t nblk = (K + ORACLE_BLOCK - 1) / ORACLE_BLOCK;
   /* per block: re sum, re comp, im sum, im comp, bound */
@@ -166,7 +169,7 @@ void oracle_tsmttsm_z(int64_t K, int M, int N, const double *A, const double *B,
         for (int64_t k = c0; k < c1; k++) {
           const double *a = A + 2 * k * M, *bb = B + 2 * k * N;
           for (int m = 0; m < M; m++) {
-            const double ar = a[2 * m], ai = a[2 * m + 1];
+            const double ar = a[2 * m], ai = conj ? -a[2 * m + 1] : a[2 * m + 1];
             const double am = hypot(ar, ai);
             for (int n = 0; n < N; n++) {
               const double br = bb[2 * n], bi = bb[2 * n + 1];
@@ -206,6 +209,17 @@ void oracle_tsmttsm_z(int64_t K, int M, int N, const double *A, const double *B,
     if (bound) bound[i] = bd;
   }
   free(bs);
+}
+
+void oracle_tsmttsm_z(int64_t K, int M, int N, const double *A, const double *B,
+                      double *C, double *bound) {
+  tsmttsm_z_impl(K, M, N, A, B, C, bound, 0);
+}
+
+/* C = A^H B */
+void oracle_tsmttsm_zc(int64_t K, int M, int N, const double *A, const double *B,
+                       double *C, double *bound) {
+  tsmttsm_z_impl(K, M, N, A, B, C, bound, 1);
 }
 
 /* ------------------------------------------------------------------------ */
@@ -249,6 +263,70 @@ void oracle_tsmm_z(int64_t K, int M, int N, const double *A, const double *C,
       B[2 * (k * N + n)] = re;
       B[2 * (k * N + n) + 1] = im;
       if (bound) bound[k * N + n] = bd;
+    }
+  }
+}
+
+/* ------------------------------------------------------------------------ */
+/* TSMM update (NEXT row N1): B <- alpha * (A C) + beta * B.  PAPER.md:108-112: */
+/* "both the TSMTTSM (A^T B) and TSMM (A C) occur in classical Gram-Schmidt   */
+/* orthogonalization of a number of vectors represented by B against an       */
+/* orthogonal basis A" -- the projection step is B <- B - A (A^T B), i.e.      */
+/* alpha = -1, beta = 1.  Per (k, n): s = serial fma chain over m (as in       */
+/* oracle_tsmm_*), then out = fma(alpha, s, beta * b_old) (D), and the complex */
+/* products alpha*s + beta*b written out the same way (Z).  conj_c = 1 uses   */
+/* conj(C) (N2).  bound = |alpha| sum_m |a||c| + |beta| |b_old|.               */
+/* ------------------------------------------------------------------------ */
+void oracle_tsmm_update_d(int64_t K, int M, int N, double alpha, const double *A,
+                          const double *C, double beta, double *B, double *bound) {
+#pragma omp parallel for schedule(static)
+  for (int64_t k = 0; k < K; k++) {
+    const double *a = A + k * M;
+    for (int n = 0; n < N; n++) {
+      double s = 0, bd = 0;
+      for (int m = 0; m < M; m++) {
+        s = fma(a[m], C[m * N + n], s);
+        bd += fabs(a[m]) * fabs(C[m * N + n]);
+      }
+      const double b = B[k * N + n];
+      B[k * N + n] = fma(alpha, s, beta * b);
+      if (bound) bound[k * N + n] = fabs(alpha) * bd + fabs(beta) * fabs(b);
+    }
+  }
+}
+
+void oracle_tsmm_update_z(int64_t K, int M, int N, double alpha_re, double alpha_im,
+                          const double *A, const double *C, double beta_re, double beta_im,
+                          double *B, double *bound, int conj_c) {
+#pragma omp parallel for schedule(static)
+  for (int64_t k = 0; k < K; k++) {
+    const double *a = A + 2 * k * M;
+    for (int n = 0; n < N; n++) {
+      double re = 0, im = 0, bd = 0;
+      for (int m = 0; m < M; m++) {
+        const double ar = a[2 * m], ai = a[2 * m + 1];
+        const double cr = C[2 * (m * N + n)];
+        const double ci = conj_c ? -C[2 * (m * N + n) + 1] : C[2 * (m * N + n) + 1];
+        re = fma(ar, cr, re);
+        re = fma(-ai, ci, re);
+        im = fma(ar, ci, im);
+        im = fma(ai, cr, im);
+        bd += hypot(ar, ai) * hypot(cr, ci);
+      }
+      double *b = B + 2 * (k * N + n);
+      const double br = b[0], bi = b[1];
+      /* alpha * s + beta * b, each complex product as two fma chains */
+      double orr = beta_re * br;
+      orr = fma(-beta_im, bi, orr);
+      orr = fma(alpha_re, re, orr);
+      orr = fma(-alpha_im, im, orr);
+      double oi = beta_re * bi;
+      oi = fma(beta_im, br, oi);
+      oi = fma(alpha_re, im, oi);
+      oi = fma(alpha_im, re, oi);
+      b[0] = orr;
+      b[1] = oi;
+      if (bound) bound[k * N + n] = hypot(alpha_re, alpha_im) * bd + hypot(beta_re, beta_im) * hypot(br, bi);
     }
   }
 }

@@ -330,3 +330,108 @@ def test_generator_ranges():
     z = ti.matrix(3, 2, "C", complex_=True, seed=5)
     flat = ti.raw_values(12, 5, "C", "fp")
     assert np.array_equal(z.reshape(-1).view(np.float64), flat)
+
+
+# --------------------------------------------------------------------------- #
+# NEXT rows N1 (TSMM update / Gram-Schmidt step) and N2 (conjugate variants)   #
+# --------------------------------------------------------------------------- #
+def _z(a):
+    a = np.array(a, dtype=np.float64)
+    return np.ascontiguousarray(a[..., 0] + 1j * a[..., 1])
+
+
+def test_conj_hand_z_2x2(golden):
+    g = golden("hand_z_2x2_tsmttsm_conj.json")
+    C, bound = oracle.tsmttsm(g["A"], g["B"], conj=True)
+    assert np.array_equal(C, g["C"])
+    # the bound is conjugation-invariant (|conj a| = |a|)
+    assert np.array_equal(bound, oracle.tsmttsm(g["A"], g["B"])[1])
+
+
+def test_conj_i_times_i():
+    # conj(i) * i = 1 (the plain transpose gives -1)
+    C, _ = oracle.tsmttsm(np.array([[1j]]), np.array([[1j]]), conj=True)
+    assert C[0, 0] == 1 + 0j
+
+
+@pytest.mark.parametrize("K,M", [(4096, 64), (64, 33)])
+def test_conj_walsh(K, M):
+    # (1+i) Walsh: A^H A = |1+i|^2 K I = 2K I exactly (plain: 2iK I)
+    Az = (1 + 1j) * ti.walsh(K, M)
+    C, _ = oracle.tsmttsm(Az, Az, conj=True)
+    assert np.array_equal(C, 2 * K * np.eye(M))
+
+
+def test_conj_int_exact():
+    # integer mode: exact, equals conj(A)^T B computed in exact int64 arithmetic
+    K, M, N = 3001, 5, 4
+    A = ti.matrix(K, M, "A", complex_=True, mode="int")
+    B = ti.matrix(K, N, "B", complex_=True, mode="int")
+    C, _ = oracle.tsmttsm(A, B, conj=True)
+    ar, ai, br, bi = (_int64(x) for x in (A.real, A.imag, B.real, B.imag))
+    re = ar.T @ br + ai.T @ bi
+    im = ar.T @ bi - ai.T @ br
+    assert np.array_equal(C, re.astype(np.float64) + 1j * im.astype(np.float64))
+
+
+def test_update_hand(golden):
+    g = golden("hand_tsmm_update.json")
+    d = g["d"]
+    out, bound = oracle.tsmm_update(np.array(d["A"], float), np.array(d["C"], float), np.array(d["B"], float),
+                                    d["alpha"], d["beta"])
+    assert np.array_equal(out, np.array(d["out"], float))
+    assert np.array_equal(bound, [[2 * 3 + 3 * 10], [2 * 4 + 3 * 4]])
+    z = g["z_conj"]
+    out, _ = oracle.tsmm_update(_z(z["A"]), _z(z["C"]), _z(z["B"]), complex(*z["alpha"]), complex(*z["beta"]),
+                                conj=True)
+    assert np.array_equal(out, _z(z["out"]))
+
+
+@pytest.mark.parametrize("cplx", [False, True])
+def test_update_reduces_to_tsmm(cplx):
+    # alpha = 1, beta = 0: exactly the TSMM oracle (fma(1, s, 0) = s)
+    K, M, N = 777, 9, 6
+    A = ti.matrix(K, M, "A", complex_=cplx)
+    Cm = ti.matrix(M, N, "C", complex_=cplx)
+    B0 = ti.matrix(K, N, "B", complex_=cplx)
+    out, _ = oracle.tsmm_update(A, Cm, B0, 1, 0)
+    ref, _ = oracle.tsmm(A, Cm)
+    assert np.array_equal(out, ref)
+
+
+@pytest.mark.parametrize("cplx", [False, True])
+def test_update_int_exact(cplx):
+    # integer mode: B_new = alpha A C + beta B exactly (int64 arithmetic)
+    K, M, N = 2000, 7, 5
+    A = ti.matrix(K, M, "A", complex_=cplx, mode="int")
+    Cm = ti.matrix(M, N, "C", complex_=cplx, mode="int")
+    B0 = ti.matrix(K, N, "B", complex_=cplx, mode="int")
+    alpha, beta = (-3, 2) if not cplx else (-3 + 1j, 2 - 2j)
+    out, _ = oracle.tsmm_update(A, Cm, B0, alpha, beta)
+    if cplx:
+        ac = (_int64(A.real) @ _int64(Cm.real) - _int64(A.imag) @ _int64(Cm.imag)) + \
+            1j * (_int64(A.real) @ _int64(Cm.imag) + _int64(A.imag) @ _int64(Cm.real))
+    else:
+        ac = _int64(A) @ _int64(Cm)
+    assert np.array_equal(out, alpha * ac + beta * B0)
+
+
+@pytest.mark.parametrize("cplx", [False, True])
+def test_gram_schmidt_projection_exact(cplx):
+    # classical Gram-Schmidt of B against an orthonormal A:
+    # C = A^T B (A^H B for Z), B' = B - A C  =>  A^T B' = 0.  With the scaled
+    # Walsh basis (entries +-2^-j, K = 4^j) and integer B every product and
+    # sum is a dyadic rational within 53 bits: the projection is exact.
+    j = 6
+    K, M, N = 4 ** j, 16, 5
+    A = ti.walsh(K, M, scale=2.0 ** -j)
+    B = ti.matrix(K, N, "B", complex_=cplx, mode="int")
+    if cplx:
+        A = 1j * A  # unit-modulus phase: A^H A = I (the plain transpose gives -I)
+    C, _ = oracle.tsmttsm(A, B, conj=cplx)
+    Bp, _ = oracle.tsmm_update(A, C, B, -1, 1)
+    R, _ = oracle.tsmttsm(A, Bp, conj=cplx)
+    assert np.count_nonzero(R) == 0
+    # and the update removed exactly the projection A C
+    AC, _ = oracle.tsmm(A, C)
+    assert np.array_equal(Bp, B - AC)
