@@ -147,6 +147,20 @@ tsm_status tsm_plan_create_config(tsm_plan *out, tsm_op op, tsm_dtype dtype, int
 /* The configuration a plan resolved to (stages/ctas after clipping). */
 tsm_status tsm_plan_get_config(tsm_plan p, tsm_config *cfg);
 
+/* Plan flags.
+ *   TSM_FLAG_CONJ  Z plans only.  TSMTTSM: C = A^H B (conjugate transpose of A,
+ *                  what complex classical Gram-Schmidt against a basis A needs,
+ *                  PAPER.md:108-112).  TSMM: B = A conj(C).  Same kernels: the
+ *                  sign of Im(A) / Im(C) is flipped on load (exact). */
+#define TSM_FLAG_CONJ 1u
+
+/* tsm_plan_create / tsm_plan_create_config with flags: cfg == NULL selects the
+ * tuned default configuration.  TSM_ERR_INVALID_VALUE for unknown flags or
+ * TSM_FLAG_CONJ on a D plan. */
+tsm_status tsm_plan_create_ex(tsm_plan *out, tsm_op op, tsm_dtype dtype, int M, int N, int device,
+                              const tsm_config *cfg, unsigned flags);
+tsm_status tsm_plan_get_flags(tsm_plan p, unsigned *flags);
+
 /* Bytes of device workspace a TSMTTSM call with K rows needs (partials of the
  * fixed-order grid reduction plus 2 counter words); 0 for TSMM plans.
  * The first 256 bytes hold counters that MUST be zero before the first use of
@@ -184,6 +198,42 @@ tsm_status tsmm_d(tsm_plan p, int64_t K, const double *A, const double *C, doubl
                   tsm_stream stream);
 tsm_status tsmm_z(tsm_plan p, int64_t K, const tsm_zcomplex *A, const tsm_zcomplex *C,
                   tsm_zcomplex *B, tsm_stream stream);
+
+/* ------------------------------------------------------------------------ */
+/* TSMM update  B <- alpha * A C + beta * B   (SURVEY.md §8(f) NEXT row N1;  */
+/* the TSMM step of classical Gram-Schmidt: B -= A C is    */
+/* alpha = -1, beta = 1).  One pass over A and B:                            */
+/*   beta = 0: B = alpha A C, written like tsmm_* (B is not read);            */
+/*   beta = 1: the kernels add alpha A C into B with bulk / TMA reduce-add    */
+/*             (cp.reduce.async.bulk .add.f64: B is read and written by the   */
+/*             memory system, one rounding per element);                      */
+/*   other beta: B is first scaled by beta (one extra pass over B), then as 1.*/
+/* alpha multiplies C once per block (alpha = 1 leaves C bit-exact).  A plan */
+/* with TSM_FLAG_CONJ uses conj(C).  Errors as tsmm_*.                        */
+/* ------------------------------------------------------------------------ */
+tsm_status tsmm_update_d(tsm_plan p, int64_t K, double alpha, const double *A, const double *C,
+                         double beta, double *B, tsm_stream stream);
+tsm_status tsmm_update_z(tsm_plan p, int64_t K, tsm_zcomplex alpha, const tsm_zcomplex *A,
+                         const tsm_zcomplex *C, tsm_zcomplex beta, tsm_zcomplex *B,
+                         tsm_stream stream);
+
+/* ------------------------------------------------------------------------ */
+/* One block classical Gram-Schmidt projection (NEXT row N1) */
+/* of the K x N block vector B against the K x M basis A:                    */
+/*   C = A^T B        (p_tt: TSMTTSM plan (M, N); Z: create it with          */
+/*                     TSM_FLAG_CONJ for A^H B),                              */
+/*   B <- B - A C     (p_mm: TSMM plan (M, N), tsmm_update with alpha = -1,   */
+/*                     beta = 1).                                             */
+/* comm != NULL: K is this rank's K_local and C is summed over ranks (as      */
+/* tsmttsm_allreduce_*) before the update; ws then needs the extra bytes of   */
+/* tsm_comm_workspace_extra_bytes.  C (M x N, device) holds the coefficients  */
+/* on return.                                                                 */
+/* ------------------------------------------------------------------------ */
+tsm_status tsm_cgs_step_d(tsm_plan p_tt, tsm_plan p_mm, tsm_comm comm, int64_t K, const double *A,
+                          double *B, double *C, void *ws, size_t ws_bytes, tsm_stream stream);
+tsm_status tsm_cgs_step_z(tsm_plan p_tt, tsm_plan p_mm, tsm_comm comm, int64_t K,
+                          const tsm_zcomplex *A, tsm_zcomplex *B, tsm_zcomplex *C, void *ws,
+                          size_t ws_bytes, tsm_stream stream);
 
 /* ------------------------------------------------------------------------ */
 /* Device input generator (same counter-based generator as  */

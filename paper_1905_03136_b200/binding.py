@@ -24,6 +24,7 @@ STATUS = {0: "TSM_SUCCESS", 1: "TSM_ERR_INVALID_VALUE", 2: "TSM_ERR_UNSUPPORTED"
 OP = {"tsmttsm": 0, "tsmm": 1}
 DTYPE = {"d": 0, "z": 1}
 TSM_COMM_DETERMINISTIC = 1
+TSM_FLAG_CONJ = 1
 MAT_ID = {"A": 1, "B": 2, "C": 3}
 
 # exported symbols declared in include/libtsm.h (checked by tests/test_abi.py)
@@ -33,8 +34,14 @@ EXPORTS = [
     "tsmttsm_d", "tsmttsm_z", "tsmm_d", "tsmm_z", "tsm_fill", "tsm_l2_flush",
     "tsm_comm_unique_id", "tsm_comm_init", "tsm_comm_destroy", "tsm_comm_workspace_extra_bytes",
     "tsmttsm_allreduce_d", "tsmttsm_allreduce_z", "tsmm_bcast_d", "tsmm_bcast_z",
-    "tsm_build_info",
+    "tsm_build_info", "tsm_plan_create_ex", "tsm_plan_get_flags", "tsmm_update_d", "tsmm_update_z",
+    "tsm_cgs_step_d", "tsm_cgs_step_z",
 ]
+
+
+class ZComplex(ctypes.Structure):
+    """tsm_zcomplex (include/libtsm.h), passed by value."""
+    _fields_ = [("re", ctypes.c_double), ("im", ctypes.c_double)]
 
 
 class TsmConfig(ctypes.Structure):
@@ -84,6 +91,12 @@ def _load():
         "tsmm_bcast_d": [P, P, I, I64, VP, VP, VP, VP],
         "tsmm_bcast_z": [P, P, I, I64, VP, VP, VP, VP],
         "tsm_build_info": [],
+        "tsm_plan_create_ex": [ctypes.POINTER(P), I, I, I, I, I, ctypes.POINTER(TsmConfig), ctypes.c_uint],
+        "tsm_plan_get_flags": [P, ctypes.POINTER(ctypes.c_uint)],
+        "tsmm_update_d": [P, I64, ctypes.c_double, VP, VP, ctypes.c_double, VP, VP],
+        "tsmm_update_z": [P, I64, ZComplex, VP, VP, ZComplex, VP, VP],
+        "tsm_cgs_step_d": [P, P, P, I64, VP, VP, VP, VP, SZ, VP],
+        "tsm_cgs_step_z": [P, P, P, I64, VP, VP, VP, VP, SZ, VP],
     }
     for name, args in sig.items():
         f = getattr(lib, name)
@@ -117,6 +130,40 @@ def tsm_plan_create_config(op: str, dtype: str, M: int, N: int, device: int, cfg
     check(lib.tsm_plan_create_config(ctypes.byref(h), OP[op], DTYPE[dtype], M, N, device,
                                      ctypes.byref(c)), f"tsm_plan_create_config({op},{dtype},{M},{N})")
     return h.value
+
+
+def tsm_plan_create_ex(op: str, dtype: str, M: int, N: int, device: int, cfg: dict | None,
+                       flags: int) -> int:
+    h = ctypes.c_void_p()
+    c = TsmConfig(**cfg) if cfg is not None else None
+    check(lib.tsm_plan_create_ex(ctypes.byref(h), OP[op], DTYPE[dtype], M, N, device,
+                                 ctypes.byref(c) if c is not None else None, flags),
+          f"tsm_plan_create_ex({op},{dtype},{M},{N},flags={flags})")
+    return h.value
+
+
+def tsm_plan_get_flags(plan: int) -> int:
+    f = ctypes.c_uint()
+    check(lib.tsm_plan_get_flags(plan, ctypes.byref(f)), "tsm_plan_get_flags")
+    return f.value
+
+
+def tsmm_update_d(plan, K, alpha, A, C, beta, B, stream):
+    check(lib.tsmm_update_d(plan, K, float(alpha), A, C, float(beta), B, stream), "tsmm_update_d")
+
+
+def tsmm_update_z(plan, K, alpha, A, C, beta, B, stream):
+    a, b = complex(alpha), complex(beta)
+    check(lib.tsmm_update_z(plan, K, ZComplex(a.real, a.imag), A, C, ZComplex(b.real, b.imag), B, stream),
+          "tsmm_update_z")
+
+
+def tsm_cgs_step_d(p_tt, p_mm, comm, K, A, B, C, ws, ws_bytes, stream):
+    check(lib.tsm_cgs_step_d(p_tt, p_mm, comm, K, A, B, C, ws, ws_bytes, stream), "tsm_cgs_step_d")
+
+
+def tsm_cgs_step_z(p_tt, p_mm, comm, K, A, B, C, ws, ws_bytes, stream):
+    check(lib.tsm_cgs_step_z(p_tt, p_mm, comm, K, A, B, C, ws, ws_bytes, stream), "tsm_cgs_step_z")
 
 
 def tsm_plan_get_config(plan: int) -> dict:
@@ -185,10 +232,14 @@ class Plan:
     """Owning wrapper of a tsm_plan handle."""
 
     def __init__(self, op: str, dtype: str, M: int, N: int, device: int = 0,
-                 config: dict | None = None):
+                 config: dict | None = None, conj: bool = False):
+        """conj=True (Z only, TSM_FLAG_CONJ): TSMTTSM C = A^H B, TSMM B = A conj(C)."""
         self.op, self.dtype, self.M, self.N, self.device = op, dtype, M, N, device
+        self.conj = conj
         self.handle = None
-        if config is None:
+        if conj:
+            self.handle = tsm_plan_create_ex(op, dtype, M, N, device, config, TSM_FLAG_CONJ)
+        elif config is None:
             self.handle = tsm_plan_create(op, dtype, M, N, device)
         else:
             self.handle = tsm_plan_create_config(op, dtype, M, N, device, config)
@@ -210,12 +261,12 @@ class Plan:
             self.handle = None
 
 
-def get_plan(op: str, dtype: str, M: int, N: int, device: int) -> Plan:
-    key = (op, dtype, M, N, device)
+def get_plan(op: str, dtype: str, M: int, N: int, device: int, conj: bool = False) -> Plan:
+    key = (op, dtype, M, N, device, conj)
     with _mu:
         p = _plans.get(key)
         if p is None:
-            p = Plan(op, dtype, M, N, device)
+            p = Plan(op, dtype, M, N, device, conj=conj)
             _plans[key] = p
     return p
 
@@ -255,8 +306,9 @@ def workspace(plan: Plan, K: int, stream: int, min_bytes: int = 0):
     return buf
 
 
-def tsmttsm(A, B, out=None, plan: Plan | None = None):
-    """C = A^T B (plain transpose) for torch CUDA tensors A (K x M), B (K x N)."""
+def tsmttsm(A, B, out=None, plan: Plan | None = None, conj: bool = False):
+    """C = A^T B (plain transpose; conj=True: A^H B, Z only) for torch CUDA
+    tensors A (K x M), B (K x N)."""
     torch = _torch()
     _check_cuda(A, B)
     dt = _dtype_code(A)
@@ -265,7 +317,7 @@ def tsmttsm(A, B, out=None, plan: Plan | None = None):
     K, M = A.shape
     N = B.shape[1]
     dev = A.device.index
-    plan = plan or get_plan("tsmttsm", dt, M, N, dev)
+    plan = plan or get_plan("tsmttsm", dt, M, N, dev, conj)
     C = out if out is not None else torch.empty((M, N), dtype=A.dtype, device=A.device)
     _check_cuda(C)
     stream = torch.cuda.current_stream(A.device).cuda_stream
@@ -292,6 +344,53 @@ def tsmm(A, C, out=None, plan: Plan | None = None):
     f = tsmm_z if dt == "z" else tsmm_d
     f(plan.handle, K, A.data_ptr(), C.data_ptr(), B.data_ptr(), stream)
     return B
+
+
+def tsmm_update(A, C, B, alpha=1.0, beta=0.0, plan: Plan | None = None, conj: bool = False):
+    """In place B <- alpha * A C + beta * B (NEXT N1; conj: A conj(C), Z only).
+    Returns B."""
+    torch = _torch()
+    _check_cuda(A, C, B)
+    dt = _dtype_code(A)
+    if C.dtype != A.dtype or B.dtype != A.dtype or A.dim() != 2 or C.dim() != 2 or B.dim() != 2 \
+            or A.shape[1] != C.shape[0] or B.shape != (A.shape[0], C.shape[1]):
+        raise ValueError("A (K x M), C (M x N), B (K x N): shapes / dtypes do not match")
+    K, M = A.shape
+    N = C.shape[1]
+    plan = plan or get_plan("tsmm", dt, M, N, A.device.index, conj)
+    stream = torch.cuda.current_stream(A.device).cuda_stream
+    f = tsmm_update_z if dt == "z" else tsmm_update_d
+    f(plan.handle, K, alpha, A.data_ptr(), C.data_ptr(), beta, B.data_ptr(), stream)
+    return B
+
+
+def cgs_step(A, B, C=None, p_tt: Plan | None = None, p_mm: Plan | None = None, comm=None):
+    """One block classical Gram-Schmidt projection of B (K x N) against the
+    basis A (K x M), in place: C = A^T B (A^H B for Z), then
+    B <- B - A C.  comm: a Comm (K = this rank's rows; C summed over ranks).
+    Returns C."""
+    torch = _torch()
+    _check_cuda(A, B)
+    dt = _dtype_code(A)
+    K, M = A.shape
+    N = B.shape[1]
+    dev = A.device.index
+    p_tt = p_tt or get_plan("tsmttsm", dt, M, N, dev, dt == "z")
+    p_mm = p_mm or get_plan("tsmm", dt, M, N, dev)
+    C = C if C is not None else torch.empty((M, N), dtype=A.dtype, device=A.device)
+    _check_cuda(C)
+    stream = torch.cuda.current_stream(A.device).cuda_stream
+    extra = 0
+    if comm is not None:
+        n = ctypes.c_size_t()
+        check(lib.tsm_comm_workspace_extra_bytes(comm.handle, p_tt.handle, ctypes.byref(n)),
+              "tsm_comm_workspace_extra_bytes")
+        extra = n.value
+    ws = workspace(p_tt, K, stream, p_tt.workspace_bytes(K) + extra)
+    f = tsm_cgs_step_z if dt == "z" else tsm_cgs_step_d
+    f(p_tt.handle, p_mm.handle, comm.handle if comm is not None else None, K, A.data_ptr(), B.data_ptr(),
+      C.data_ptr(), ws.data_ptr(), ws.numel(), stream)
+    return C
 
 
 def fill(t, mat: str, seed: int, mode: str = "fp", start: int = 0):

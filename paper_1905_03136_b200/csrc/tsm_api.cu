@@ -178,6 +178,20 @@ __global__ void fill_kernel(double* __restrict__ dst, long long n, u64 base, int
   }
 }
 
+// B *= beta (tsmm_update with beta not in {0, 1}); z: complex beta on (re, im) pairs
+__global__ void scale_kernel(double* __restrict__ b, long long n, double br, double bi, int z) {
+  const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n; i += stride) {
+    if (z) {
+      const double re = b[2 * i], im = b[2 * i + 1];
+      b[2 * i] = br * re - bi * im;
+      b[2 * i + 1] = br * im + bi * re;
+    } else {
+      b[i] *= br;
+    }
+  }
+}
+
 __global__ void l2_flush_kernel(double4* __restrict__ dst, long long n4) {
   long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
   const long long st = static_cast<long long>(gridDim.x) * blockDim.x;
@@ -196,6 +210,7 @@ struct tsm_plan_s {
   int ctas_per_sm;
   size_t smem;
   bool jit;  // kernel compiled at run time by NVRTC (shape/config outside the AOT set)
+  unsigned flags = 0;  // TSM_FLAG_CONJ
 };
 
 extern "C" {
@@ -425,6 +440,25 @@ tsm_status tsm_plan_create_config(tsm_plan* out, tsm_op op, tsm_dtype dtype, int
   return make_plan(out, e, device, true);
 }
 
+tsm_status tsm_plan_create_ex(tsm_plan* out, tsm_op op, tsm_dtype dtype, int M, int N, int device,
+                              const tsm_config* cfg, unsigned flags) {
+  if (!out) return fail(TSM_ERR_INVALID_VALUE, "out == NULL");
+  *out = nullptr;
+  if (flags & ~TSM_FLAG_CONJ) return fail(TSM_ERR_INVALID_VALUE, "unknown plan flags");
+  if ((flags & TSM_FLAG_CONJ) && dtype != TSM_Z)
+    return fail(TSM_ERR_INVALID_VALUE, "TSM_FLAG_CONJ applies to Z plans");
+  tsm_status st = cfg ? tsm_plan_create_config(out, op, dtype, M, N, device, cfg)
+                      : tsm_plan_create(out, op, dtype, M, N, device);
+  if (st == TSM_SUCCESS) (*out)->flags = flags;
+  return st;
+}
+
+tsm_status tsm_plan_get_flags(tsm_plan p, unsigned* flags) {
+  if (!p || !flags) return fail(TSM_ERR_INVALID_VALUE, "null argument");
+  *flags = p->flags;
+  return TSM_SUCCESS;
+}
+
 tsm_status tsm_plan_get_config(tsm_plan p, tsm_config* cfg) {
   if (!p || !cfg) return fail(TSM_ERR_INVALID_VALUE, "null argument");
   cfg->threads = p->k->NT;
@@ -527,6 +561,7 @@ tsm_status launch_tsmttsm(const tsm_plan_s* p, int dt, long long K, const void* 
   a.nchunks = g.nchunks;
   a.stages = p->stages;
   a.nfin = g.nfin;
+  a.conj = (p->flags & TSM_FLAG_CONJ) ? (1ull << 63) : 0ull;
   if (p->k->impl == 2 && K > 0) {
     const int S = dt == TSM_Z ? 2 : 1;
     tsm_status st = make_tmap(&a.tmA, A, K, p->M * S, p->k->R);
@@ -541,7 +576,7 @@ tsm_status launch_tsmttsm(const tsm_plan_s* p, int dt, long long K, const void* 
 }
 
 tsm_status launch_tsmm(const tsm_plan_s* p, int dt, long long K, const void* A, const void* C,
-                       void* B, void* stream, bool allow_k0) {
+                       void* B, void* stream, bool allow_k0, const TsmmMode* mode) {
   if (!p) return fail(TSM_ERR_INVALID_VALUE, "plan == NULL");
   if (p->op != TSM_OP_TSMM || p->dt != dt)
     return fail(TSM_ERR_INVALID_VALUE, "plan op/dtype does not match the call");
@@ -565,6 +600,12 @@ tsm_status launch_tsmm(const tsm_plan_s* p, int dt, long long K, const void* A, 
   a.K = K;
   a.nchunks = g.nchunks;
   a.stages = p->stages;
+  const TsmmMode dflt;
+  if (!mode) mode = &dflt;
+  a.reduce = mode->reduce;
+  a.alpha_re = mode->alpha_re;
+  a.alpha_im = dt == TSM_Z ? mode->alpha_im : 0.0;
+  a.conj = (p->flags & TSM_FLAG_CONJ) ? (1ull << 63) : 0ull;
   if (p->k->impl >= 2) {  // B store boxes: 8*WR rows (WR = p0 for kernel 2, p1 for kernel 3)
     const int S = dt == TSM_Z ? 2 : 1;
     const int wr = p->k->impl == 3 ? p->k->p1 : p->k->p0;
@@ -579,10 +620,44 @@ tsm_status launch_tsmm(const tsm_plan_s* p, int dt, long long K, const void* A, 
   return TSM_SUCCESS;
 }
 
+tsm_status launch_tsmm_update(const tsm_plan_s* p, int dt, long long K, double ar, double ai,
+                              const void* A, const void* C, double br, double bi, void* B,
+                              void* stream, bool allow_k0) {
+  if (!p) return fail(TSM_ERR_INVALID_VALUE, "plan == NULL");
+  if (dt == TSM_D) ai = bi = 0.0;
+  const bool beta0 = br == 0.0 && bi == 0.0, beta1 = br == 1.0 && bi == 0.0;
+  if (!beta0 && !beta1 && K > 0) {
+    // validate everything first (same checks as the TSMM launch), then scale B
+    if (p->op != TSM_OP_TSMM || p->dt != dt)
+      return fail(TSM_ERR_INVALID_VALUE, "plan op/dtype does not match the call");
+    if (!A || !B || !C) return fail(TSM_ERR_INVALID_VALUE, "null pointer");
+    if (misaligned(A) || misaligned(B) || misaligned(C))
+      return fail(TSM_ERR_MISALIGNED, "A, B and C must be 16-byte aligned");
+    DeviceGuard dg(p->device);
+    if (dg.err != cudaSuccess) return cuda_fail(dg.err, "cudaSetDevice");
+    DevInfo di;
+    tsm_status st = dev_info(p->device, &di);
+    if (st != TSM_SUCCESS) return st;
+    const long long n = K * p->N;
+    const int grid = static_cast<int>(std::min<long long>((n + 255) / 256, di.sms * 8LL));
+    scale_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(static_cast<double*>(B), n, br, bi,
+                                                                      dt == TSM_Z);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "scale_kernel launch");
+  }
+  TsmmMode m;
+  m.alpha_re = ar;
+  m.alpha_im = ai;
+  m.reduce = beta0 ? 0 : 1;
+  return launch_tsmm(p, dt, K, A, C, B, stream, allow_k0, &m);
+}
+
 int plan_device(const tsm_plan_s* p) { return p->device; }
 int plan_cells(const tsm_plan_s* p) { return p->M * p->N * (p->dt == TSM_Z ? 2 : 1); }
 int plan_op(const tsm_plan_s* p) { return p->op; }
 int plan_dt(const tsm_plan_s* p) { return p->dt; }
+int plan_M(const tsm_plan_s* p) { return p->M; }
+int plan_N(const tsm_plan_s* p) { return p->N; }
 
 }  // namespace tsm
 
@@ -664,6 +739,15 @@ tsm_status tsmm_d(tsm_plan p, int64_t K, const double* A, const double* C, doubl
 tsm_status tsmm_z(tsm_plan p, int64_t K, const tsm_zcomplex* A, const tsm_zcomplex* C,
                   tsm_zcomplex* B, tsm_stream stream) {
   return launch_tsmm(p, TSM_Z, K, A, C, B, stream, false);
+}
+
+tsm_status tsmm_update_d(tsm_plan p, int64_t K, double alpha, const double* A, const double* C,
+                         double beta, double* B, tsm_stream stream) {
+  return launch_tsmm_update(p, TSM_D, K, alpha, 0.0, A, C, beta, 0.0, B, stream, false);
+}
+tsm_status tsmm_update_z(tsm_plan p, int64_t K, tsm_zcomplex alpha, const tsm_zcomplex* A,
+                         const tsm_zcomplex* C, tsm_zcomplex beta, tsm_zcomplex* B, tsm_stream stream) {
+  return launch_tsmm_update(p, TSM_Z, K, alpha.re, alpha.im, A, C, beta.re, beta.im, B, stream, false);
 }
 
 tsm_status tsm_fill(double* dst, int64_t n, uint64_t seed, int mat_id, int mode, int64_t start,

@@ -224,4 +224,32 @@ tsm_status tsmm_bcast_z(tsm_plan p, tsm_comm c, int root, int64_t K_local, const
   return bcast_impl(p, c, TSM_Z, root, K_local, A, C, B, stream);
 }
 
+// One block classical Gram-Schmidt projection (NEXT row N1):
+// C = A^T B (A^H B with a TSM_FLAG_CONJ plan), summed over ranks when comm is
+// given, then B <- B - A C through the TSMM update path (reduce-add into B).
+static tsm_status cgs_impl(tsm_plan ptt, tsm_plan pmm, tsm_comm c, int dt, int64_t K, const void* A,
+                           void* B, void* C, void* ws, size_t ws_bytes, tsm_stream stream) {
+  if (!ptt || !pmm) return fail(TSM_ERR_INVALID_VALUE, "null plan");
+  if (tsm::plan_op(ptt) != TSM_OP_TSMTTSM || tsm::plan_op(pmm) != TSM_OP_TSMM)
+    return fail(TSM_ERR_INVALID_VALUE, "p_tt must be a TSMTTSM plan and p_mm a TSMM plan");
+  if (tsm::plan_dt(ptt) != dt || tsm::plan_dt(pmm) != dt)
+    return fail(TSM_ERR_INVALID_VALUE, "plan dtype does not match the call");
+  if (tsm::plan_M(ptt) != tsm::plan_M(pmm) || tsm::plan_N(ptt) != tsm::plan_N(pmm))
+    return fail(TSM_ERR_INVALID_VALUE, "p_tt and p_mm must have the same (M, N)");
+  tsm_status st = c ? allreduce_impl(ptt, c, dt, K, A, B, C, ws, ws_bytes, stream)
+                    : tsm::launch_tsmttsm(ptt, dt, K, A, B, C, ws, ws_bytes, stream, false);
+  if (st != TSM_SUCCESS) return st;
+  return tsm::launch_tsmm_update(pmm, dt, K, -1.0, 0.0, A, C, 1.0, 0.0, B, stream, c != nullptr);
+}
+
+tsm_status tsm_cgs_step_d(tsm_plan p_tt, tsm_plan p_mm, tsm_comm comm, int64_t K, const double* A,
+                          double* B, double* C, void* ws, size_t ws_bytes, tsm_stream stream) {
+  return cgs_impl(p_tt, p_mm, comm, TSM_D, K, A, B, C, ws, ws_bytes, stream);
+}
+tsm_status tsm_cgs_step_z(tsm_plan p_tt, tsm_plan p_mm, tsm_comm comm, int64_t K,
+                          const tsm_zcomplex* A, tsm_zcomplex* B, tsm_zcomplex* C, void* ws,
+                          size_t ws_bytes, tsm_stream stream) {
+  return cgs_impl(p_tt, p_mm, comm, TSM_Z, K, A, B, C, ws, ws_bytes, stream);
+}
+
 }  // extern "C"

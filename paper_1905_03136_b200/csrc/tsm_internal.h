@@ -23,13 +23,24 @@ tsm_status fail(tsm_status s, const std::string& why);
 // Launch paths (tsm_api.cu).  allow_k0: the sharded layer may pass K = 0.
 tsm_status launch_tsmttsm(const tsm_plan_s* p, int dt, long long K, const void* A, const void* B,
                           void* C, void* ws, size_t ws_bytes, void* stream, bool allow_k0);
+// TSMM output mode (NEXT N1): B = alpha A C (reduce = 0) or B += alpha A C (reduce = 1).
+struct TsmmMode {
+  double alpha_re = 1.0, alpha_im = 0.0;
+  int reduce = 0;
+};
 tsm_status launch_tsmm(const tsm_plan_s* p, int dt, long long K, const void* A, const void* C,
-                       void* B, void* stream, bool allow_k0);
+                       void* B, void* stream, bool allow_k0, const TsmmMode* mode = nullptr);
+// B <- alpha A C + beta B (tsmm_update_*): beta in {0, 1} in one pass, else B *= beta first.
+tsm_status launch_tsmm_update(const tsm_plan_s* p, int dt, long long K, double ar, double ai,
+                              const void* A, const void* C, double br, double bi, void* B,
+                              void* stream, bool allow_k0);
 size_t workspace_bytes(const tsm_plan_s* p, long long K);
 int plan_device(const tsm_plan_s* p);
 int plan_cells(const tsm_plan_s* p);  // doubles in C
 int plan_op(const tsm_plan_s* p);
 int plan_dt(const tsm_plan_s* p);
+int plan_M(const tsm_plan_s* p);
+int plan_N(const tsm_plan_s* p);
 
 // Fixed rank-order sum of nranks gathered partial C's (tsm_comm.cu).
 tsm_status rank_sum(const double* gathered, double* C, int nranks, int cells, void* stream);

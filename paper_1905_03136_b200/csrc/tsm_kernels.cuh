@@ -98,6 +98,13 @@ __device__ __forceinline__ void bulk_s2g(void* dst, const void* src, u32 bytes) 
                "r"(smem_u32(src)), "r"(bytes)
                : "memory");
 }
+// Shared -> global bulk reduce-add (f64, round-to-nearest; bulk-group completion):
+// dst[i] += src[i], done by the memory system (TSMM update with beta = 1).
+__device__ __forceinline__ void bulk_red_add(void* dst, const void* src, u32 bytes) {
+  asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f64 [%0], [%1], %2;" ::"l"(dst),
+               "r"(smem_u32(src)), "r"(bytes)
+               : "memory");
+}
 __device__ __forceinline__ void bulk_commit() {
   asm volatile("cp.async.bulk.commit_group;" ::: "memory");
 }
@@ -177,6 +184,18 @@ __device__ __forceinline__ void tma_store_2d(const TmaDesc* desc, int x, int y, 
                "r"(x), "r"(y), "r"(smem_u32(src))
                : "memory");
 }
+// Tensor reduce-add of a box (element type from the tensor map: f64).
+__device__ __forceinline__ void tma_red_add_2d(const TmaDesc* desc, int x, int y, const void* src) {
+  asm volatile("cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.tile.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                   desc),
+               "r"(x), "r"(y), "r"(smem_u32(src))
+               : "memory");
+}
+// x with its sign bit XORed with mask (0 or 1<<63): conjugation on the integer
+// pipe, exact, NaN-preserving.
+__device__ __forceinline__ double flip_sign(double x, u64 mask) {
+  return __longlong_as_double(__double_as_longlong(x) ^ static_cast<long long>(mask));
+}
 // Byte offset o' >= o such that base + o' is 1024-byte aligned in the shared
 // window (computed from the shared address, applied as pointer arithmetic).
 __device__ __forceinline__ int align1024(const void* base, int o) {
@@ -202,6 +221,7 @@ struct TsmttsmArgs {
   long long nchunks;   // ceil(K_even / R)  (TMA kernels: ceil(K / R))
   int stages;          // smem ring depth
   int nfin;            // finisher blocks of the grid reduction
+  u64 conj;            // Z: sign mask XORed into Im(A) -- 1<<63 gives C = A^H B (NEXT N2)
 };
 
 // M, N: widths.  Z: complex.  MT, NTL: tiles per row along m / n (powers of
@@ -228,7 +248,7 @@ struct TsmttsmCfg {
 template <class Cfg>
 __device__ __forceinline__ void tsmttsm_row(const double* __restrict__ ar,
                                             const double* __restrict__ br, int tm, int tn,
-                                            double (&c)[Cfg::TM][Cfg::TN][Cfg::S]) {
+                                            double (&c)[Cfg::TM][Cfg::TN][Cfg::S], u64 conj) {
   constexpr int TM = Cfg::TM, TN = Cfg::TN, MT = Cfg::MT, NTL = Cfg::NTL;
   constexpr int M = Cfg::M, N = Cfg::N;
   if constexpr (!Cfg::Z) {
@@ -273,6 +293,8 @@ __device__ __forceinline__ void tsmttsm_row(const double* __restrict__ ar,
       else
         b[j] = (n < N) ? br2[n] : make_double2(0.0, 0.0);
     }
+#pragma unroll
+    for (int i = 0; i < TM; i++) a[i].y = flip_sign(a[i].y, conj);
 #pragma unroll
     for (int i = 0; i < TM; i++)
 #pragma unroll
@@ -419,10 +441,10 @@ __global__ void __launch_bounds__(Cfg::NT) tsmttsm_kernel(const TsmttsmArgs p) {
     if (rows == R) {
 #pragma unroll 2
       for (int r = rs; r < R; r += RB)
-        tsmttsm_row<Cfg>(sA + r * M * S, sB + r * N * S, tm, tn, acc);
+        tsmttsm_row<Cfg>(sA + r * M * S, sB + r * N * S, tm, tn, acc, p.conj);
     } else {
       for (int r = rs; r < rows; r += RB)
-        tsmttsm_row<Cfg>(sA + r * M * S, sB + r * N * S, tm, tn, acc);
+        tsmttsm_row<Cfg>(sA + r * M * S, sB + r * N * S, tm, tn, acc, p.conj);
     }
     __syncthreads();  // stage s fully consumed by every thread
     if (tid == 0) {
@@ -432,7 +454,7 @@ __global__ void __launch_bounds__(Cfg::NT) tsmttsm_kernel(const TsmttsmArgs p) {
   }
   // Odd last row (K odd): block 0, slot 0 reads it straight from global.
   if ((K & 1) && blockIdx.x == 0 && rs == 0)
-    tsmttsm_row<Cfg>(p.A + (K - 1) * M * S, p.B + (K - 1) * N * S, tm, tn, acc);
+    tsmttsm_row<Cfg>(p.A + (K - 1) * M * S, p.B + (K - 1) * N * S, tm, tn, acc, p.conj);
 
   // ---- T3: block-level reduction (fixed order) ----
   // (a) butterfly over the row-slot lanes of a warp (same tile, TPR < 32).
@@ -725,6 +747,7 @@ __global__ void __launch_bounds__(Cfg::NT) tsmttsm_mma_kernel(const __grid_const
       }
 #pragma unroll
       for (int i = 0; i < CM; i++) {
+        a[i].y = flip_sign(a[i].y, p.conj);  // A^H B (N2)
         const double nai = -a[i].y;
 #pragma unroll
         for (int j = 0; j < CN; j++) {
@@ -773,7 +796,7 @@ __global__ void __launch_bounds__(Cfg::NT) tsmttsm_mma_kernel(const __grid_const
         } else {
           const double2 a = *reinterpret_cast<const double2*>(sA + off(r, em[t], ap));
           const double2 b = *reinterpret_cast<const double2*>(sB + off(r, en[t], bp));
-          zfma(eacc[t][0], eacc[t][1], a.x, a.y, b.x, b.y);
+          zfma(eacc[t][0], eacc[t][1], a.x, flip_sign(a.y, p.conj), b.x, b.y);
         }
       }
     }
@@ -920,13 +943,14 @@ __global__ void __launch_bounds__(Cfg::NT) tsmttsm_mma_kernel(const __grid_const
   }
   if constexpr (Cfg::ZR) {
     // complex C from the real product P = Ar^T Br of the interleaved (re, im)
-    // columns: C[m][n] = (P[2m][2n] - P[2m+1][2n+1]) + i (P[2m][2n+1] + P[2m+1][2n])
+    // columns: C[m][n] = (P[2m][2n] - P[2m+1][2n+1]) + i (P[2m][2n+1] + P[2m+1][2n]);
+    // A^H B (conj, N2) flips the sign of the Im(A) rows: + P[2m+1][2n+1], - P[2m+1][2n]
     constexpr int NZ = N / 2, MNZ = (M / 2) * NZ;
     double* sQ = ring + CELLS;
     for (int idx = tid; idx < MNZ; idx += Cfg::NT) {
       const int m = 2 * (idx / NZ), n = 2 * (idx % NZ);
-      sQ[2 * idx] = sP[m * N + n] - sP[(m + 1) * N + n + 1];
-      sQ[2 * idx + 1] = sP[m * N + n + 1] + sP[(m + 1) * N + n];
+      sQ[2 * idx] = sP[m * N + n] - flip_sign(sP[(m + 1) * N + n + 1], p.conj);
+      sQ[2 * idx + 1] = sP[m * N + n + 1] + flip_sign(sP[(m + 1) * N + n], p.conj);
     }
     __syncthreads();
     grid_reduce<Cfg::NT, Cfg::OUT_CELLS>(p, sQ, sQ + Cfg::OUT_CELLS);
@@ -946,7 +970,37 @@ struct TsmmArgs {
   long long K;
   long long nchunks;  // ceil(K_even / R)  (TMA kernels: ceil(K / R))
   int stages;
+  int reduce;         // 0: B = A C' (store); 1: B += A C' (bulk / TMA reduce-add; NEXT N1)
+  double alpha_re, alpha_im;  // C' = alpha * C (alpha = 1: C used as given, bit-exact)
+  u64 conj;           // Z: sign mask XORed into Im(C) -- 1<<63 uses conj(C) (NEXT N2)
 };
+
+// TSMM: the C the kernels multiply by, C' = alpha * (conj ? conj(c) : c).
+// alpha = 1 + 0i leaves C bit-exact (and NaN/Inf untouched).
+__device__ __forceinline__ void c_prime(const TsmmArgs& p, double& re, double& im) {
+  im = flip_sign(im, p.conj);
+  if (p.alpha_im == 0.0) {
+    re *= p.alpha_re;
+    im *= p.alpha_re;
+  } else {
+    const double r = p.alpha_re * re - p.alpha_im * im;
+    im = p.alpha_re * im + p.alpha_im * re;
+    re = r;
+  }
+}
+// B rows out of smem staging: store, or add into B (update mode)
+__device__ __forceinline__ void b_out_bulk(const TsmmArgs& p, void* dst, const void* src, u32 bytes) {
+  if (p.reduce)
+    bulk_red_add(dst, src, bytes);
+  else
+    bulk_s2g(dst, src, bytes);
+}
+__device__ __forceinline__ void b_out_tma(const TsmmArgs& p, int x, int y, const void* src) {
+  if (p.reduce)
+    tma_red_add_2d(&p.tmB, x, y, src);
+  else
+    tma_store_2d(&p.tmB, x, y, src);
+}
 
 // NTL: threads per row along n (interleaved columns), MSPLIT: lanes sharing
 // one output that split the m-sum (butterfly-combined), U: rows per thread per
@@ -999,8 +1053,17 @@ __global__ void __launch_bounds__(Cfg::NT) tsmm_kernel(const TsmmArgs p) {
     fence_mbar_init();
     fence_proxy_async_smem();
   }
-  // S1: stage C once per persistent block.
-  for (int i = tid; i < Cfg::C_DOUBLES; i += NT) sC[i] = __ldg(&p.C[i]);
+  // S1: stage C' = alpha * C (conj for N2) once per persistent block.
+  for (int i = tid; i < M * N; i += NT) {
+    if constexpr (Cfg::Z) {
+      double re = __ldg(&p.C[2 * i]), im = __ldg(&p.C[2 * i + 1]);
+      c_prime(p, re, im);
+      sC[2 * i] = re;
+      sC[2 * i + 1] = im;
+    } else {
+      sC[i] = p.alpha_re * __ldg(&p.C[i]);
+    }
+  }
   __syncthreads();
 
   u64 pol = 0;
@@ -1114,7 +1177,7 @@ __global__ void __launch_bounds__(Cfg::NT) tsmm_kernel(const TsmmArgs p) {
       __syncthreads();           // pass complete (and, on the last pass, stage s consumed)
       if (tid == 0) {
         const int prow = (rows - base < Cfg::ROWS_PER_PASS) ? rows - base : Cfg::ROWS_PER_PASS;
-        bulk_s2g(p.B + (r0 + base) * N * S, out, static_cast<u32>(prow * N * S * 8));
+        b_out_bulk(p, p.B + (r0 + base) * N * S, out, static_cast<u32>(prow * N * S * 8));
         bulk_commit();
       }
     }
@@ -1130,13 +1193,15 @@ __global__ void __launch_bounds__(Cfg::NT) tsmm_kernel(const TsmmArgs p) {
       if constexpr (!Cfg::Z) {
         double s0 = 0.0;
         for (int m = 0; m < M; m++) s0 = fma(a[m], sC[m * N + n], s0);
-        p.B[(K - 1) * N + n] = s0;
+        double* o = p.B + (K - 1) * N + n;
+        *o = p.reduce ? *o + s0 : s0;
       } else {
         double re = 0.0, im = 0.0;
         for (int m = 0; m < M; m++)
           zfma(re, im, a[2 * m], a[2 * m + 1], sC[2 * (m * N + n)], sC[2 * (m * N + n) + 1]);
-        p.B[2 * ((K - 1) * N + n)] = re;
-        p.B[2 * ((K - 1) * N + n) + 1] = im;
+        double* o = p.B + 2 * ((K - 1) * N + n);
+        o[0] = p.reduce ? o[0] + re : re;
+        o[1] = p.reduce ? o[1] + im : im;
       }
     }
   }
@@ -1227,11 +1292,17 @@ __global__ void __launch_bounds__(Cfg::NT) tsmm_mma_kernel(const __grid_constant
     fence_mbar_init();
     fence_proxy_async_smem();
   }
-  // S1: C -> smem once, zero padded to MK*4 rows x NCP columns
+  // S1: C' = alpha * C (conj for N2) -> smem once, zero padded to MK*4 rows x NCP columns
   for (int i = tid; i < MK * 4 * NCP; i += Cfg::NT) {
     const int m = i / NCP, n = i % NCP;
-#pragma unroll
-    for (int z = 0; z < S; z++) sC[i * S + z] = (m < M && n < N) ? __ldg(&p.C[(m * N + n) * S + z]) : 0.0;
+    double re = 0.0, im = 0.0;
+    if (m < M && n < N) {
+      re = __ldg(&p.C[(m * N + n) * S]);
+      if constexpr (Cfg::Z) im = __ldg(&p.C[(m * N + n) * S + 1]);
+      c_prime(p, re, im);
+    }
+    sC[i * S] = re;
+    if constexpr (Cfg::Z) sC[i * S + 1] = im;
   }
   __syncthreads();
 
@@ -1381,17 +1452,17 @@ __global__ void __launch_bounds__(Cfg::NT) tsmm_mma_kernel(const __grid_constant
         if constexpr (Cfg::TMA) {
           if (lane == 0) {
             for (int b = 0; b < Cfg::NBO; b++)
-              tma_store_2d(&p.tmB, b * 16, static_cast<int>(r0 + wr0), stg + b * RW * 16);
+              b_out_tma(p, b * 16, static_cast<int>(r0 + wr0), stg + b * RW * 16);
             bulk_commit();
           }
         } else if constexpr (NOP == N) {
           if (lane == 0) {
-            bulk_s2g(p.B + (r0 + wr0) * N * S, stg, static_cast<u32>(nr * N * S * 8));
+            b_out_bulk(p, p.B + (r0 + wr0) * N * S, stg, static_cast<u32>(nr * N * S * 8));
             bulk_commit();
           }
         } else {
           for (int r = lane; r < nr; r += 32)
-            bulk_s2g(p.B + (r0 + wr0 + r) * N * S, stg + r * NOP * S, static_cast<u32>(N * S * 8));
+            b_out_bulk(p, p.B + (r0 + wr0 + r) * N * S, stg + r * NOP * S, static_cast<u32>(N * S * 8));
           bulk_commit();
         }
       }
@@ -1405,13 +1476,15 @@ __global__ void __launch_bounds__(Cfg::NT) tsmm_mma_kernel(const __grid_constant
         if constexpr (!Cfg::Z) {
           double s0 = 0.0;
           for (int m = 0; m < M; m++) s0 = fma(a[m], sC[m * NCP + n], s0);
-          p.B[(K - 1) * N + n] = s0;
+          double* o = p.B + (K - 1) * N + n;
+          *o = p.reduce ? *o + s0 : s0;
         } else {
           double re = 0.0, im = 0.0;
           for (int m = 0; m < M; m++)
             zfma(re, im, a[2 * m], a[2 * m + 1], sC[2 * (m * NCP + n)], sC[2 * (m * NCP + n) + 1]);
-          p.B[2 * ((K - 1) * N + n)] = re;
-          p.B[2 * ((K - 1) * N + n) + 1] = im;
+          double* o = p.B + 2 * ((K - 1) * N + n);
+          o[0] = p.reduce ? o[0] + re : re;
+          o[1] = p.reduce ? o[1] + im : im;
         }
       }
     }
@@ -1522,13 +1595,19 @@ __global__ void __launch_bounds__(Cfg::NT) tsmm_cst_kernel(const __grid_constant
           double v = 0.0;
           if (m < M && n < N) {
             const double* c2 = p.C + ((m >> 1) * (N >> 1) + (n >> 1)) * 2;
-            const double re = __ldg(c2), im = __ldg(c2 + 1);
+            double re = __ldg(c2), im = __ldg(c2 + 1);
+            c_prime(p, re, im);
             v = ((m & 1) == (n & 1)) ? re : ((m & 1) ? -im : im);
           }
           cf[ks][j][0] = v;
         } else {
 #pragma unroll
           for (int z = 0; z < S; z++) cf[ks][j][z] = (m < M && n < N) ? __ldg(&p.C[(m * N + n) * S + z]) : 0.0;
+          if constexpr (Cfg::Z) {
+            c_prime(p, cf[ks][j][0], cf[ks][j][1]);
+          } else {
+            cf[ks][j][0] *= p.alpha_re;
+          }
         }
       }
     auto aoff = [&](int r, int x) -> int {  // element (row r, column x) of the A stage
@@ -1605,7 +1684,7 @@ __global__ void __launch_bounds__(Cfg::NT) tsmm_cst_kernel(const __grid_constant
           __syncwarp();
           if (lane == 0 && nb0 < NB) {
             for (int b = 0; b < OB; b++)
-              tma_store_2d(&p.tmB, nb0 * 8 * S + b * 16, static_cast<int>(r0 + wr0), stg + b * RW * 16);
+              b_out_tma(p, nb0 * 8 * S + b * 16, static_cast<int>(r0 + wr0), stg + b * RW * 16);
             bulk_commit();
           }
         }

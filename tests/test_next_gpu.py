@@ -1,0 +1,158 @@
+"""NEXT rows N1 / N2 on the GPU, against the oracle:
+
+  N2  conjugate variants: TSMTTSM C = A^H B and TSMM B = A conj(C) (plan flag
+      TSM_FLAG_CONJ) on every Z kernel family (DFMA, DMMA, DMMA+TMA, edge
+      warps, complex-as-real, C-stationary);
+  N1  TSMM update B <- alpha A C + beta B (bulk / TMA reduce-add for beta = 1,
+      a scaling pass first for other beta) on every TSMM family, and the
+      classical Gram-Schmidt step C = A^T B, B -= A C.
+"""
+import os
+import sys
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import tsminputs as ti
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, os.path.join(ROOT, "tools"))
+import gen_instances as gi  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def tsm():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    from paper_1905_03136_b200 import binding
+    return binding
+
+
+def families(tsm, op, M, N, z, conj=False):
+    """One plan per kernel family the generator offers for this shape."""
+    seen = {}
+    for c in gi.candidates(op, M, N, z):
+        key = (c.get("impl", 0), c.get("EDGE", 0) > 0, c.get("PAIR", 0), c.get("ZR", 0))
+        if key in seen:
+            continue
+        try:
+            seen[key] = (c, tsm.Plan(op, "z" if z else "d", M, N, 0, config=gi.to_tsm_config(op, c, 3, 1),
+                                     conj=conj))
+        except tsm.TsmError as e:
+            if e.status != 2:
+                raise
+    return seen
+
+
+def cu(x):
+    return torch.from_numpy(np.ascontiguousarray(x)).cuda()
+
+
+@pytest.mark.parametrize("M,N", [(3, 5), (8, 8), (17, 17), (24, 40), (33, 20), (64, 64)])
+def test_conj_tsmttsm_every_family(tsm, M, N):
+    fams = families(tsm, "tsmttsm", M, N, True, conj=True)
+    assert fams
+    for key, (c, plan) in sorted(fams.items()):
+        assert tsm.tsm_plan_get_flags(plan.handle) == tsm.TSM_FLAG_CONJ
+        for K in (1, 7, 4099, 65537):
+            A = ti.matrix(K, M, "A", complex_=True, seed=K + 21)
+            B = ti.matrix(K, N, "B", complex_=True, seed=K + 22)
+            got = tsm.tsmttsm(cu(A), cu(B), plan=plan)
+            torch.cuda.synchronize()
+            ref, bound = oracle.tsmttsm(A, B, conj=True)
+            r, wi, _ = oracle.max_err_ratio(got.cpu().numpy(), ref, bound)
+            assert r <= 1e-12, (M, N, key, c, K, r, wi)
+        Ai = ti.matrix(30001, M, "A", complex_=True, mode="int")
+        Bi = ti.matrix(30001, N, "B", complex_=True, mode="int")
+        got = tsm.tsmttsm(cu(Ai), cu(Bi), plan=plan)
+        torch.cuda.synchronize()
+        assert np.array_equal(got.cpu().numpy(), oracle.tsmttsm(Ai, Bi, conj=True)[0]), (key, c)
+
+
+def test_conj_flag_rules(tsm):
+    with pytest.raises(tsm.TsmError) as e:
+        tsm.Plan("tsmttsm", "d", 8, 8, 0, conj=True)
+    assert e.value.status == 1
+    h = tsm.ctypes.c_void_p()
+    assert tsm.lib.tsm_plan_create_ex(tsm.ctypes.byref(h), 0, 1, 8, 8, 0, None, 2) == 1  # unknown flag
+    # conj plan differs from the plain plan exactly by the sign of Im(A)
+    A = ti.matrix(1000, 9, "A", complex_=True, mode="int")
+    B = ti.matrix(1000, 4, "B", complex_=True, mode="int")
+    c1 = tsm.tsmttsm(cu(A), cu(B), conj=True).cpu().numpy()
+    c2 = tsm.tsmttsm(cu(np.conj(A)), cu(B)).cpu().numpy()
+    assert np.array_equal(c1, c2)
+
+
+UPD = [(1.0, 0.0), (-1.0, 1.0), (2.5, 0.5), (0.0, 1.0), (0.0, 0.0), (-0.75, -2.0)]
+UPDZ = [(1.0, 0.0), (-1.0, 1.0), (0.5 - 2j, 0.25j), (1j, -1.0)]
+
+
+@pytest.mark.parametrize("cplx", [False, True], ids=["D", "Z"])
+@pytest.mark.parametrize("M,N", [(1, 1), (5, 3), (16, 16), (32, 32), (41, 41), (64, 48), (24, 24)])
+def test_tsmm_update_every_family(tsm, M, N, cplx):
+    fams = families(tsm, "tsmm", M, N, cplx, conj=False)
+    assert fams
+    for conj in ([False, True] if cplx else [False]):
+        for key, (c, plan0) in sorted(fams.items()):
+            plan = tsm.Plan("tsmm", "z" if cplx else "d", M, N, 0, config=plan0.config(), conj=conj) \
+                if conj else plan0
+            for K, (alpha, beta) in zip((1, 6, 4099, 65537, 3, 20001), UPDZ * 2 if cplx else UPD):
+                A = ti.matrix(K, M, "A", complex_=cplx, seed=K + 31)
+                Cm = ti.matrix(M, N, "C", complex_=cplx, seed=K + 32)
+                B0 = ti.matrix(K, N, "B", complex_=cplx, seed=K + 33)
+                Bd = cu(B0)
+                tsm.tsmm_update(cu(A), cu(Cm), Bd, alpha, beta, plan=plan)
+                torch.cuda.synchronize()
+                ref, bound = oracle.tsmm_update(A, Cm, B0, alpha, beta, conj=conj)
+                r, wi, _ = oracle.max_err_ratio(Bd.cpu().numpy(), ref, bound)
+                assert r <= 1e-13, (M, N, key, conj, c, K, alpha, beta, r, wi)
+            # integer mode, the Gram-Schmidt coefficients: bit-exact
+            K = 50001
+            A = ti.matrix(K, M, "A", complex_=cplx, mode="int")
+            Cm = ti.matrix(M, N, "C", complex_=cplx, mode="int")
+            B0 = ti.matrix(K, N, "B", complex_=cplx, mode="int")
+            Bd = cu(B0)
+            tsm.tsmm_update(cu(A), cu(Cm), Bd, -1.0, 1.0, plan=plan)
+            torch.cuda.synchronize()
+            assert np.array_equal(Bd.cpu().numpy(), oracle.tsmm_update(A, Cm, B0, -1, 1, conj=conj)[0]), key
+
+
+@pytest.mark.parametrize("cplx", [False, True], ids=["D", "Z"])
+@pytest.mark.parametrize("M,N", [(16, 5), (32, 32), (8, 64), (64, 8)])
+def test_cgs_step_exact_projection(tsm, M, N, cplx):
+    # orthonormal scaled-Walsh basis (x i for Z) and integer B: the projection
+    # is exact, so A^T B' = 0 (A^H for Z) and B' equals the oracle bit for bit.
+    j = 7
+    K = 4 ** j
+    A = ti.walsh(K, M, scale=2.0 ** -j)
+    if cplx:
+        A = 1j * A
+    B0 = ti.matrix(K, N, "B", complex_=cplx, mode="int")
+    Ad, Bd = cu(A), cu(B0)
+    C = tsm.cgs_step(Ad, Bd)
+    torch.cuda.synchronize()
+    Cref, _ = oracle.tsmttsm(A, B0, conj=cplx)
+    assert np.array_equal(C.cpu().numpy(), Cref)
+    Bref, _ = oracle.tsmm_update(A, Cref, B0, -1, 1)
+    assert np.array_equal(Bd.cpu().numpy(), Bref)
+    R = tsm.tsmttsm(Ad, Bd, conj=cplx).cpu().numpy()
+    assert np.count_nonzero(R) == 0
+
+
+@pytest.mark.parametrize("cplx", [False, True], ids=["D", "Z"])
+def test_cgs_step_fp(tsm, cplx):
+    K, M, N = 1 << 20, 24, 12
+    A = ti.matrix(K, M, "A", complex_=cplx)
+    B0 = ti.matrix(K, N, "B", complex_=cplx)
+    Bd = cu(B0)
+    C = tsm.cgs_step(cu(A), Bd).cpu().numpy()
+    torch.cuda.synchronize()
+    Cref, cb = oracle.tsmttsm(A, B0, conj=cplx)
+    assert oracle.max_err_ratio(C, Cref, cb)[0] <= 1e-12
+    # the update is checked against the oracle applied to the GPU's C
+    Bref, bb = oracle.tsmm_update(A, C, B0, -1, 1)
+    assert oracle.max_err_ratio(Bd.cpu().numpy(), Bref, bb)[0] <= 1e-13

@@ -7,7 +7,13 @@
       roofline.traffic.
   ncu_summary.py launches <launches.csv> [--out profiles/...json]
       per-kernel totals / shares from a `--metrics gpu__time_duration.sum` list.
+  ncu_summary.py traffic <rep.ncu-rep> --traffic profiles/ncu_traffic.json
+      a `--metrics dram__bytes_read.sum,dram__bytes_write.sum,...` capture over
+      many shapes (tools/quick_time.py): dram read+write bytes per launch,
+      keyed like bench.py's roofline.kernel ("tsmm_d M=N=58"; median over the
+      launches of a shape), parsed from the template arguments in the names.
 """
+import re
 import argparse
 import csv
 import io
@@ -64,6 +70,42 @@ def full(a):
         json.dump(db, open(a.traffic, "w"), indent=1, sort_keys=True)
 
 
+def kernel_key(name: str):
+    """bench.py key of a libtsm kernel name (None for other kernels)."""
+    m = re.search(r"(tsmttsm|tsmm)\w*<\s*tsm::(\w+)Cfg<([^>]*)>", name) or \
+        re.search(r"(tsmttsm|tsmm)\w*<(\w+)Cfg<([^>]*)>", name)
+    if not m:
+        return None
+    op, fam, args = m.group(1), m.group(2), [x.strip() for x in m.group(3).split(",")]
+    M, N = int(args[0]), int(args[1])
+    z = args[2] in ("1", "true")
+    zr = (fam == "TsmttsmMma" and len(args) >= 13 and args[12] in ("1", "true")) or \
+         (fam == "TsmmCst" and len(args) >= 8 and args[7] in ("1", "true"))
+    if zr:
+        M, N, z = M // 2, N // 2, True
+    if M != N:
+        return f"{op}_{'z' if z else 'd'} M={M},N={N}"
+    return f"{op}_{'z' if z else 'd'} M=N={M}"
+
+
+def traffic(a):
+    hdr, units, rows = raw_rows(a.rep)
+    ik = hdr.index("Kernel Name")
+    i_r, i_w = hdr.index("dram__bytes_read.sum"), hdr.index("dram__bytes_write.sum")
+    per = {}
+    for r in rows:
+        key = kernel_key(r[ik])
+        if key is None:
+            continue
+        per.setdefault(key, []).append(to_bytes(r[i_r], units[i_r]) + to_bytes(r[i_w], units[i_w]))
+    db = json.load(open(a.traffic)) if os.path.exists(a.traffic) else {}
+    for k, v in per.items():
+        v.sort()
+        db[k] = v[len(v) // 2]
+    json.dump(db, open(a.traffic, "w"), indent=1, sort_keys=True)
+    print(f"{len(per)} kernels -> {a.traffic}")
+
+
 def launches(a):
     rows = list(csv.reader(open(a.csv)))
     start = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
@@ -96,11 +138,14 @@ def main():
     f.add_argument("rep")
     f.add_argument("--name", default="")
     f.add_argument("--traffic", default="")
+    t = sub.add_parser("traffic")
+    t.add_argument("rep")
+    t.add_argument("--traffic", required=True)
     l = sub.add_parser("launches")
     l.add_argument("csv")
     l.add_argument("--out", default="")
     a = ap.parse_args()
-    {"full": full, "launches": launches}[a.cmd](a)
+    {"full": full, "launches": launches, "traffic": traffic}[a.cmd](a)
 
 
 if __name__ == "__main__":
