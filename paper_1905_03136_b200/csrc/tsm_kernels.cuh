@@ -840,7 +840,7 @@ __global__ void __launch_bounds__(Cfg::NT) tsmttsm_mma_kernel(const __grid_const
         }
       }
     }
-  } else if (Cfg::EDGE && warp < NW + Cfg::NE) {
+  } else if (Cfg::EDGE && warp >= NW) {  // (warp < NW + NE: the producer is NW + NE)
     // ---------------- edge warps: DFMA on the cells outside the DMMA core ----------------
     // (edge warp ew takes rows ew, ew + NE, ... of every chunk)
     const int ew = warp - NW;
