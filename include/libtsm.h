@@ -124,6 +124,8 @@ typedef struct tsm_config {
                  2 = DMMA with 2-D TMA tensor copies (M*S, N*S even and >= 16).
                  3 = TSMM only: C-stationary DMMA (p0 = NBW 8-column blocks per warp,
                      p1 = WR 8-row blocks per warp; TMA conditions as 2).
+                 4 = TSMM only: C-stationary DMMA with bulk copies and shared
+                     per-row-group output staging (any width; p0 = NBW, p1 = WR).
                  Flags (OR-ed in, DMMA TSMTTSM kernels 1/2 unless noted):
                    16  DFMA edge warps for the cells outside the 8-aligned core;
                        bits 6-7 = edge warps - 1 (1..4 warps splitting the rows);

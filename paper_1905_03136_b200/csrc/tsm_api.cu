@@ -126,6 +126,12 @@ size_t smem_bytes(const KernelEntry& kin, int stages) {
     long long need = std::max<long long>(stages * stage, std::max<long long>(cells, k.NT));
     return static_cast<size_t>(128 + need * 8);
   }
+  if (k.impl == 4) {  // C-stationary DMMA TSMM, bulk copies: p0 = NBW, p1 = WR (TsmmCstbCfg)
+    const long long NW = k.NT / 32 - 1, NB = (k.N + 7) / 8, NG = (NB + k.p0 - 1) / k.p0, RG = NW / NG;
+    const long long outd = ((8LL * k.p1 * k.N * S + 15) / 16) * 16;
+    const long long stg = ((static_cast<long long>(k.R) * k.M * S + 15) / 16) * 16;
+    return static_cast<size_t>(256 + (RG * 2 * outd + stages * stg) * 8);
+  }
   if (k.impl == 3) {  // C-stationary DMMA TSMM: p0 = NBW, p1 = WR (must match TsmmCstCfg)
     const long long NW = k.NT / 32 - 1;
     const long long OB = k.p0 * 8 * S / 16, RW = 8 * k.p1;
@@ -257,7 +263,8 @@ static tsm_status validate_config_real(const KernelEntry& e) {
   if (e.R < 2 || e.R % 2) return bad("rows_per_chunk must be even and >= 2");
   if (e.stages < 2 || e.stages > 16) return bad("stages must be in [2, 16]");
   if (e.ctas_per_sm < 1) return bad("ctas_per_sm must be >= 1");
-  if (e.impl < 0 || e.impl > 3) return bad("kernel must be 0 (DFMA), 1 (DMMA), 2 (DMMA + TMA), 3 (TSMM C-stationary)");
+  if (e.impl < 0 || e.impl > 4)
+    return bad("kernel must be 0 (DFMA), 1 (DMMA), 2 (DMMA + TMA), 3 (TSMM C-stationary), 4 (TSMM C-stationary, bulk)");
   if (e.edge & 2) {  // paired 16-byte fragment loads
     if (e.op != KIND_TSMTTSM || (e.impl != 1 && e.impl != 2) || e.dt != TSM_D)
       return bad("the pair flag (kernel | 32) applies to the real DMMA TSMTTSM kernels 1 and 2");
@@ -277,7 +284,18 @@ static tsm_status validate_config_real(const KernelEntry& e) {
   } else if (e.edge & 12) {
     return bad("edge warp count bits (kernel bits 6-7) need the edge flag (kernel | 16)");
   }
-  if (e.impl == 3) {
+  if (e.impl == 4) {
+    if (e.op != KIND_TSMM) return bad("kernel 4 (C-stationary, bulk copies) is a TSMM kernel");
+    const int S = e.dt == TSM_Z ? 2 : 1;
+    const int NB = (e.N + 7) / 8, NW = e.NT / 32 - 1;
+    if (e.p0 < 1 || e.p0 > NB) return bad("NBW must be in [1, ceil(N/8)]");
+    const int NG = (NB + e.p0 - 1) / e.p0;
+    if (NW < NG || NW % NG || NW / NG > 15) return bad("consumer warps must be 1..15 row groups of the column groups");
+    if (e.p1 < 1 || e.p1 > 8) return bad("WR must be in [1, 8]");
+    if (((e.M + 3) / 4) * e.p0 * S > 64) return bad("C slice too large for registers (MK * NBW * S > 64)");
+    const int RPP = 8 * e.p1 * (NW / NG);
+    if (e.R % RPP || e.R % 2) return bad("rows_per_chunk must be even and a multiple of the rows per pass");
+  } else if (e.impl == 3) {
     const int S = e.dt == TSM_Z ? 2 : 1;
     if (e.op != KIND_TSMM) return bad("kernel 3 (C-stationary DMMA) is a TSMM kernel");
     if ((e.M * S) % 2 || (e.N * S) % 2 || e.M * S < 16 || e.N * S < 16)
@@ -496,7 +514,7 @@ Geometry geometry(const tsm_plan_s* p, long long K) {
   const long long K_even = K & ~1LL;
   // TMA kernels cover all K rows (the tensor copy zero-fills past K); the
   // bulk-copy kernels cover the even part and treat an odd last row apart.
-  const long long Kc = p->k->impl >= 2 ? K : K_even;
+  const long long Kc = (p->k->impl == 2 || p->k->impl == 3) ? K : K_even;  // TMA kernels
   g.nchunks = (Kc + p->k->R - 1) / p->k->R;
   const long long gmax = static_cast<long long>(p->sms) * p->ctas_per_sm;
   g.grid = static_cast<int>(std::max<long long>(1, std::min(gmax, g.nchunks)));
@@ -606,7 +624,7 @@ tsm_status launch_tsmm(const tsm_plan_s* p, int dt, long long K, const void* A, 
   a.alpha_re = mode->alpha_re;
   a.alpha_im = dt == TSM_Z ? mode->alpha_im : 0.0;
   a.conj = (p->flags & TSM_FLAG_CONJ) ? (1ull << 63) : 0ull;
-  if (p->k->impl >= 2) {  // B store boxes: 8*WR rows (WR = p0 for kernel 2, p1 for kernel 3)
+  if (p->k->impl == 2 || p->k->impl == 3) {  // B store boxes: 8*WR rows (WR = p0 for kernel 2, p1 for kernel 3)
     const int S = dt == TSM_Z ? 2 : 1;
     const int wr = p->k->impl == 3 ? p->k->p1 : p->k->p0;
     tsm_status st = make_tmap(&a.tmA, A, K, p->M * S, p->k->R);
@@ -691,7 +709,8 @@ tsm_status tsm_plan_describe(tsm_plan p, int64_t K, char* buf, size_t len) {
   } else if (p->op == TSM_OP_TSMTTSM) {
     kname = k->impl ? "dmma" : "dfma";
   } else {
-    kname = k->impl == 3   ? "dmma-cstationary+tma(p0=NBW,p1=WR)"
+    kname = k->impl == 4   ? "dmma-cstationary+bulk(p0=NBW,p1=WR)"
+            : k->impl == 3 ? "dmma-cstationary+tma(p0=NBW,p1=WR)"
             : k->impl == 2 ? "dmma+tma(p0=WR)"
                            : (k->impl ? "dmma(p0=WR,p1=AP,p2=NOP)" : "dfma");
   }

@@ -49,6 +49,9 @@ std::string cfg_type(const KernelEntry& ein) {
   else if (e.op == KIND_TSMTTSM)
     os << "tsm::TsmttsmCfg<" << e.M << ", " << e.N << ", " << z << ", " << e.p0 << ", " << e.p1
        << ", " << e.NT << ", " << e.R << ">";
+  else if (e.impl == 4)
+    os << "tsm::TsmmCstbCfg<" << e.M << ", " << e.N << ", " << z << ", " << e.p0 << ", " << e.p1
+       << ", " << (e.NT / 32 - 1) << ", " << e.R << ">";
   else if (e.impl == 3)
     os << "tsm::TsmmCstCfg<" << e.M << ", " << e.N << ", " << z << ", " << e.p0 << ", " << e.p1
        << ", " << (e.NT / 32 - 1) << ", " << e.R << ", " << zr << ">";
@@ -63,7 +66,8 @@ std::string cfg_type(const KernelEntry& ein) {
 }
 
 std::string kernel_name(const KernelEntry& e) {
-  const char* fn = e.op == KIND_TSMM ? (e.impl == 3 ? "tsm::tsmm_cst_kernel<"
+  const char* fn = e.op == KIND_TSMM ? (e.impl == 4   ? "tsm::tsmm_cstb_kernel<"
+                                        : e.impl == 3 ? "tsm::tsmm_cst_kernel<"
                                         : e.impl >= 1 ? "tsm::tsmm_mma_kernel<" : "tsm::tsmm_kernel<")
                    : (e.impl >= 1 ? "tsm::tsmttsm_mma_kernel<" : "tsm::tsmttsm_kernel<");
   return std::string(fn) + cfg_type(e) + ">";

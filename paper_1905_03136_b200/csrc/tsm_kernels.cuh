@@ -1701,4 +1701,202 @@ __global__ void __launch_bounds__(Cfg::NT) tsmm_cst_kernel(const __grid_constant
   }
 }
 
+// --------------------------------------------------------------------------
+// TSMM, C-stationary DMMA kernel with bulk copies (impl 4): the C-in-registers
+// design of impl 3 for widths the TMA tensor path cannot take (odd D widths:
+// rows are not 16-byte multiples; D widths < 16).  A arrives as one dense
+// bulk copy per chunk (row stride M).  The NG warps of a row group write their
+// column slices into a shared double-buffered staging block [RW rows][N], meet
+// at a named barrier (id 1 + row group), and one lane stores the RW contiguous
+// rows of B with a single bulk copy (or bulk reduce-add in update mode).
+// Before that barrier the issuing lane waits until its previous store has read
+// the other buffer, so a buffer is rewritten only after its store completed.
+// --------------------------------------------------------------------------
+template <int M_, int N_, bool Z_, int NBW_, int WR_, int NW_, int R_>
+struct TsmmCstbCfg {
+  static constexpr int M = M_, N = N_, NBW = NBW_, WR = WR_, NW = NW_, R = R_;
+  static constexpr bool Z = Z_;
+  static constexpr int S = Z ? 2 : 1;
+  static constexpr int MK = (M + 3) / 4;            // k-steps over m
+  static constexpr int NB = (N + 7) / 8;            // 8-column blocks of B
+  static constexpr int NG = (NB + NBW - 1) / NBW;   // column groups
+  static constexpr int RG = NW / NG;                // row groups (warps per column group)
+  static constexpr int RW = 8 * WR;                 // rows per row group per pass
+  static constexpr int RPP = RW * RG;               // rows per pass
+  static constexpr int NT = (NW + 1) * 32;
+  static constexpr int STAGE_DOUBLES = ((R * M * S + 15) / 16) * 16;
+  static constexpr int OUT_DOUBLES = ((RW * N * S + 15) / 16) * 16;  // one staging buffer
+  static_assert(NW % NG == 0 && RG >= 1 && RG <= 15, "consumer warps: a multiple of the column groups, <= 15 row groups");
+  static_assert(R % RPP == 0 && R % 2 == 0, "rows per chunk: whole passes");
+};
+
+template <class Cfg>
+__global__ void __launch_bounds__(Cfg::NT) tsmm_cstb_kernel(const __grid_constant__ TsmmArgs p) {
+  constexpr int M = Cfg::M, N = Cfg::N, S = Cfg::S, R = Cfg::R, NW = Cfg::NW, WR = Cfg::WR;
+  constexpr int MK = Cfg::MK, NB = Cfg::NB, NBW = Cfg::NBW, NG = Cfg::NG, RW = Cfg::RW;
+  constexpr int RPP = Cfg::RPP;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  u64* full = reinterpret_cast<u64*>(smem_raw);
+  u64* empty = full + 16;
+  double* stage_out = reinterpret_cast<double*>(smem_raw + 256);
+  double* ring = stage_out + Cfg::RG * 2 * Cfg::OUT_DOUBLES;
+
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, q = lane & 3;
+  const long long K = p.K;
+  const long long K_even = K & ~1LL;
+  const int G = gridDim.x;
+  const int stages = p.stages;
+
+  if (tid == 0) {
+    for (int s = 0; s < stages; s++) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NW);
+    }
+    fence_mbar_init();
+    fence_proxy_async_smem();
+  }
+  __syncthreads();
+
+  if (warp == NW) {
+    // ---------------- producer warp: one bulk copy per chunk of A ----------------
+    if (lane == 0) {
+      const u64 pol = policy_evict_first();
+      Ring ring_it;
+      for (long long c = blockIdx.x; c < p.nchunks; c += G, ring_it.next(stages)) {
+        const int s = ring_it.s;
+        if (ring_it.round > 0) mbar_wait(&empty[s], ring_it.ph ^ 1u);
+        const long long r0 = c * R;
+        const int rows = static_cast<int>((K_even - r0 < R) ? (K_even - r0) : R);
+        const u32 bytes = static_cast<u32>(rows * M * S * 8);
+        double* dA = ring + static_cast<long long>(s) * Cfg::STAGE_DOUBLES;
+        mbar_arrive_expect_tx(&full[s], bytes);
+        bulk_g2s(dA, p.A + r0 * M * S, bytes, &full[s], pol);
+      }
+    }
+  } else {
+    // ---------------- consumer warps ----------------
+    const int cg = warp % NG, rg = warp / NG;
+    const int nb0 = cg * NBW;
+    const bool issuer = (cg == 0 && lane == 0);
+    // this warp's C' slice as MMA-B fragments: lane holds C'[4ks+q][8(nb0+j)+g]
+    double cf[MK][NBW][S];
+#pragma unroll
+    for (int ks = 0; ks < MK; ks++)
+#pragma unroll
+      for (int j = 0; j < NBW; j++) {
+        const int m = 4 * ks + q, n = 8 * (nb0 + j) + g;
+        double re = 0.0, im = 0.0;
+        if (m < M && n < N) {
+          re = __ldg(&p.C[(m * N + n) * S]);
+          if constexpr (Cfg::Z) im = __ldg(&p.C[(m * N + n) * S + 1]);
+          c_prime(p, re, im);
+        }
+        cf[ks][j][0] = re;
+        if constexpr (Cfg::Z) cf[ks][j][S - 1] = im;
+      }
+    auto consume = [&](auto nbv) {
+      constexpr int NBV = decltype(nbv)::value;  // blocks of this column group inside C
+      int pass = 0;
+      Ring ring_it;
+      for (long long c = blockIdx.x; c < p.nchunks; c += G, ring_it.next(stages)) {
+        const int s = ring_it.s;
+        mbar_wait(&full[s], ring_it.ph);
+        const double* sA = ring + static_cast<long long>(s) * Cfg::STAGE_DOUBLES;
+        const long long r0 = c * R;
+        const int rows = static_cast<int>((K_even - r0 < R) ? (K_even - r0) : R);
+#pragma unroll 1
+        for (int pr = 0; pr < rows; pr += RPP) {
+          const int wr0 = pr + rg * RW;
+          if (wr0 >= rows) break;  // uniform across the row group
+          double acc[WR][NBW][S][2];
+#pragma unroll
+          for (int i = 0; i < WR; i++)
+#pragma unroll
+            for (int j = 0; j < NBW; j++)
+#pragma unroll
+              for (int z = 0; z < S; z++) acc[i][j][z][0] = acc[i][j][z][1] = 0.0;
+#pragma unroll
+          for (int ks = 0; ks < MK; ks++) {
+            const int m = 4 * ks + q;
+            const bool mv = (4 * ks + 4 <= M) || (m < M);
+#pragma unroll
+            for (int i = 0; i < WR; i++) {
+              const int r = wr0 + 8 * i + g;  // rows past `rows`: stale, never stored
+              if constexpr (!Cfg::Z) {
+                const double a = mv ? sA[r * M + m] : 0.0;
+#pragma unroll
+                for (int j = 0; j < NBV; j++) dmma(acc[i][j][0][0], acc[i][j][0][1], a, cf[ks][j][0]);
+              } else {
+                const double2 a = mv ? *reinterpret_cast<const double2*>(sA + (r * M + m) * 2)
+                                     : make_double2(0.0, 0.0);
+                const double nai = -a.y;
+#pragma unroll
+                for (int j = 0; j < NBV; j++) {
+                  dmma(acc[i][j][0][0], acc[i][j][0][1], a.x, cf[ks][j][0]);  // re += ar cr
+                  dmma(acc[i][j][0][0], acc[i][j][0][1], nai, cf[ks][j][1]);  // re -= ai ci
+                  dmma(acc[i][j][1][0], acc[i][j][1][1], a.x, cf[ks][j][1]);  // im += ar ci
+                  dmma(acc[i][j][1][0], acc[i][j][1][1], a.y, cf[ks][j][0]);  // im += ai cr
+                }
+              }
+            }
+          }
+          // registers -> this row group's staging buffer (pass & 1), dense [RW][N]
+          double* stg = stage_out + (rg * 2 + (pass & 1)) * Cfg::OUT_DOUBLES;
+#pragma unroll
+          for (int i = 0; i < WR; i++)
+#pragma unroll
+            for (int j = 0; j < NBV; j++)
+#pragma unroll
+              for (int e = 0; e < 2; e++) {
+                const int rr = 8 * i + g, n = 8 * (nb0 + j) + 2 * q + e;
+                if (n < N) {
+#pragma unroll
+                  for (int z = 0; z < S; z++) stg[(rr * N + n) * S + z] = acc[i][j][z][e];
+                }
+              }
+          fence_proxy_async_smem();
+          if (issuer) bulk_wait_read<0>();  // the previous pass's store has read the other buffer
+          asm volatile("bar.sync %0, %1;" ::"r"(1 + rg), "r"(NG * 32) : "memory");
+          if (issuer) {
+            const int nr = (rows - wr0 < RW) ? rows - wr0 : RW;
+            b_out_bulk(p, p.B + (r0 + wr0) * N * S, stg, static_cast<u32>(nr * N * S * 8));
+            bulk_commit();
+          }
+          pass++;
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+      }
+    };
+    constexpr int NBL = NB - (NG - 1) * NBW;
+    if (cg == NG - 1)
+      consume(IC<NBL>{});
+    else
+      consume(IC<NBW>{});
+    if (issuer) bulk_wait_all();
+    // Odd last row (K odd): warp 0 of block 0 from global A and C' (plain fma).
+    if ((K & 1) && blockIdx.x == 0 && warp == 0) {
+      const double* a = p.A + (K - 1) * M * S;
+      for (int n = lane; n < N; n += 32) {
+        double re = 0.0, im = 0.0;
+        for (int m = 0; m < M; m++) {
+          double cr = __ldg(&p.C[(m * N + n) * S]), ci = 0.0;
+          if constexpr (Cfg::Z) ci = __ldg(&p.C[(m * N + n) * S + 1]);
+          c_prime(p, cr, ci);
+          if constexpr (Cfg::Z) {
+            zfma(re, im, a[2 * m], a[2 * m + 1], cr, ci);
+          } else {
+            re = fma(a[m], cr, re);
+          }
+        }
+        double* o = p.B + ((K - 1) * N + n) * S;
+        o[0] = p.reduce ? o[0] + re : re;
+        if constexpr (Cfg::Z) o[1] = p.reduce ? o[1] + im : im;
+      }
+    }
+  }
+}
+
 }  // namespace tsm

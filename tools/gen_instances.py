@@ -266,7 +266,7 @@ def tsmm_default(M: int, N: int, z: bool) -> dict:
 
 
 def _tsmm_p(c: dict) -> tuple:
-    if c.get("impl", 0) == 3:
+    if c.get("impl", 0) in (3, 4):
         return (c["NBW"], c["WR"], 0)
     if c.get("impl", 0) >= 1:
         return (c["WR"], c["AP"], c["NOP"])
@@ -317,6 +317,8 @@ def cfg_type(op, dt, M, N, c) -> str:
                 f"{c['R']}, {c.get('AP', M)}, {c.get('BP', N)}, {tma}, {edge}, {pair}, {zr}>")
     if op == "tsmttsm":
         return f"tsm::TsmttsmCfg<{M}, {N}, {z}, {c['MT']}, {c['NTL']}, {c['NT']}, {c['R']}>"
+    if c.get("impl", 0) == 4:
+        return f"tsm::TsmmCstbCfg<{M}, {N}, {z}, {c['NBW']}, {c['WR']}, {c['NT'] // 32 - 1}, {c['R']}>"
     if c.get("impl", 0) == 3:
         return f"tsm::TsmmCstCfg<{M}, {N}, {z}, {c['NBW']}, {c['WR']}, {c['NT'] // 32 - 1}, {c['R']}, {zr}>"
     if c.get("impl", 0) >= 1:
@@ -333,7 +335,7 @@ def entry_init(op, dt, M, N, c) -> str:
         fn = f"(const void*)&tsm::{kn}<{t}>"
         kind = "tsm::KIND_TSMTTSM"
     else:
-        kn = {3: "tsmm_cst_kernel", 2: "tsmm_mma_kernel", 1: "tsmm_mma_kernel"}.get(
+        kn = {4: "tsmm_cstb_kernel", 3: "tsmm_cst_kernel", 2: "tsmm_mma_kernel", 1: "tsmm_mma_kernel"}.get(
             c.get("impl", 0), "tsmm_kernel")
         fn = f"(const void*)&tsm::{kn}<{t}>"
         kind = "tsm::KIND_TSMM"
@@ -536,6 +538,7 @@ def candidates(op: str, M: int, N: int, z: bool) -> list:
                 MS *= 2
     if op == "tsmm":
         out.extend(tsmm_cst_configs(M, N, z))
+        out.extend(tsmm_cstb_configs(M, N, z))
     if z:
         out.extend(zr_candidates(op, M, N))
     if op == "tsmm" and N >= 2:
@@ -693,6 +696,32 @@ def tsmm_cst_configs(M: int, N: int, z: bool) -> list:
                 for tgt in (16384, 32768):
                     R = rpp * max(1, min(256 // rpp, round(tgt / (rpp * ab))))
                     out.append(dict(NBW=NBW, WR=WR, NT=(NW + 1) * 32, R=R, impl=3))
+    return out
+
+
+def tsmm_cstb_configs(M: int, N: int, z: bool) -> list:
+    """C-stationary DMMA TSMM with bulk copies (impl 4): the widths the TMA
+    kernel 3 cannot take (rows not 16-byte multiples or < 128 bytes)."""
+    if tma_ok(M, N, z) or N < 2:
+        return []
+    S = 2 if z else 1
+    MK, NB = cdiv(M, 4), cdiv(N, 8)
+    out = []
+    for NBW in range(1, NB + 1):
+        if MK * NBW * S > 48:
+            continue
+        NG = cdiv(NB, NBW)
+        for RG in (1, 2, 4):
+            NW = NG * RG
+            if NW > 16 or NW < 2 or RG > 15:
+                continue
+            for WR in (1, 2, 4):
+                if WR * NBW * 2 * S > 32:
+                    continue
+                rpp = 8 * WR * RG
+                for tgt in (16384, 32768):
+                    R = rpp * max(1, round(tgt / (rpp * M * S * 8)))
+                    out.append(dict(NBW=NBW, WR=WR, NT=(NW + 1) * 32, R=R, impl=4))
     return out
 
 
