@@ -133,10 +133,12 @@ size_t smem_bytes(const KernelEntry& kin, int stages) {
     return static_cast<size_t>(256 + (RG * 2 * outd + stages * stg) * 8);
   }
   if (k.impl == 3) {  // C-stationary DMMA TSMM: p0 = NBW, p1 = WR (must match TsmmCstCfg)
-    const long long NW = k.NT / 32 - 1;
-    const long long OB = k.p0 * 8 * S / 16, RW = 8 * k.p1;
+    const long long NW = k.NT / 32 - 1, EC = (k.edge & 1) ? k.N % 8 : 0;
+    const long long NB = (k.N - EC + 7) / 8, NG = (NB + k.p0 - 1) / k.p0, NBL = NB - (NG - 1) * k.p0;
+    const long long OB = k.p0 * 8 * S / 16, OBL = ((8 * NBL + EC) * S + 15) / 16, RW = 8 * k.p1;
     const long long ad = static_cast<long long>(k.R) * ((k.M * S + 15) / 16) * 16;
-    return static_cast<size_t>(256 + 1024 + (NW * OB * RW * 16 + stages * ad) * 8);
+    const long long ce = ((((k.M + 3) / 4) * 4 * EC * S + 127) / 128) * 128;
+    return static_cast<size_t>(256 + ce * 8 + 1024 + (NW * std::max(OB, OBL) * RW * 16 + stages * ad) * 8);
   }
   if (k.impl >= 1) {  // DMMA TSMM: p0 = WR, p1 = AP, p2 = NOP (must match TsmmMmaCfg)
     const long long MK = (k.M + 3) / 4, NB = (k.N + 7) / 8;
@@ -273,7 +275,13 @@ static tsm_status validate_config_real(const KernelEntry& e) {
       return bad("the pair flag needs even smem strides (and even M, N for kernel 1)");
     if (e.edge & 1) return bad("the pair and edge flags are exclusive");
   }
-  if (e.edge & 1) {
+  if ((e.edge & 1) && e.op == KIND_TSMM) {  // C-stationary TSMM: DFMA edge columns
+    const int S = e.dt == TSM_Z ? 2 : 1;
+    if (e.impl != 3) return bad("edge columns (kernel | 16) apply to TSMM kernel 3");
+    if (e.edge & 14) return bad("TSMM edge columns take no other flag bits");
+    if (e.N < 8 || e.N % 8 == 0) return bad("edge columns need N >= 8 and N not a multiple of 8");
+    if (e.p1 * (e.N % 8) * S > 16) return bad("edge columns: WR * (N mod 8) * S must be <= 16");
+  } else if (e.edge & 1) {
     if (e.op != KIND_TSMTTSM || (e.impl != 1 && e.impl != 2))
       return bad("the edge flag (kernel | 16) applies to the DMMA TSMTTSM kernels 1 and 2");
     if (e.M < 8 || e.N < 8 || (e.M % 8 == 0 && e.N % 8 == 0))
@@ -300,7 +308,8 @@ static tsm_status validate_config_real(const KernelEntry& e) {
     if (e.op != KIND_TSMM) return bad("kernel 3 (C-stationary DMMA) is a TSMM kernel");
     if ((e.M * S) % 2 || (e.N * S) % 2 || e.M * S < 16 || e.N * S < 16)
       return bad("kernel 3 needs 16-byte rows of >= 128 bytes (M*S, N*S even and >= 16)");
-    const int NB = (e.N + 7) / 8, NW = e.NT / 32 - 1;
+    const int EC = (e.edge & 1) ? e.N % 8 : 0;  // DFMA edge columns
+    const int NB = (e.N - EC + 7) / 8, NW = e.NT / 32 - 1;
     if (e.p0 < 1 || e.p0 > NB || (e.p0 * 8 * S) % 16) return bad("NBW must be in [1, ceil(N/8)] with 8*NBW*S a multiple of 16");
     const int NG = (NB + e.p0 - 1) / e.p0;
     if (NW < NG || NW % NG) return bad("consumer warps must be a multiple of the column groups");
@@ -714,6 +723,7 @@ tsm_status tsm_plan_describe(tsm_plan p, int64_t K, char* buf, size_t len) {
             : k->impl == 2 ? "dmma+tma(p0=WR)"
                            : (k->impl ? "dmma(p0=WR,p1=AP,p2=NOP)" : "dfma");
   }
+  if (p->op == TSM_OP_TSMM && (k->edge & 1)) kname += "+dfma-edge-columns";
   if (zr_flag(k->edge)) kname += "+complex-as-real(2Mx2N)";
   if (p->op == TSM_OP_TSMTTSM && k->impl >= 1)
     snprintf(tmp, sizeof tmp,

@@ -54,7 +54,7 @@ std::string cfg_type(const KernelEntry& ein) {
        << ", " << (e.NT / 32 - 1) << ", " << e.R << ">";
   else if (e.impl == 3)
     os << "tsm::TsmmCstCfg<" << e.M << ", " << e.N << ", " << z << ", " << e.p0 << ", " << e.p1
-       << ", " << (e.NT / 32 - 1) << ", " << e.R << ", " << zr << ">";
+       << ", " << (e.NT / 32 - 1) << ", " << e.R << ", " << zr << ", " << ((e.edge & 1) ? e.N % 8 : 0) << ">";
   else if (e.impl >= 1)
     os << "tsm::TsmmMmaCfg<" << e.M << ", " << e.N << ", " << z << ", " << e.p0 << ", "
        << (e.NT / 32 - 1) << ", " << e.R << ", " << e.p1 << ", " << e.p2 << ", "

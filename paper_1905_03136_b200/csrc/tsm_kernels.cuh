@@ -1506,23 +1506,31 @@ __global__ void __launch_bounds__(Cfg::NT) tsmm_mma_kernel(const __grid_constant
 // Requires the TMA conditions (M*S, N*S even and >= 16) and 8*NBW*S a
 // multiple of 16 doubles (whole output boxes per warp).
 // --------------------------------------------------------------------------
-template <int M_, int N_, bool Z_, int NBW_, int WR_, int NW_, int R_, bool ZR_ = false>
+// EC > 0 ("edge columns", kernel | 16): the last EC = N mod 8 columns are
+// computed with DFMA by the warps of the last column group (each lane adds its
+// m = 4ks+q terms, a 4-lane butterfly finishes the sum) instead of padding a
+// whole 8-column DMMA block; C' of those columns is staged in smem.
+template <int M_, int N_, bool Z_, int NBW_, int WR_, int NW_, int R_, bool ZR_ = false, int EC_ = 0>
 struct TsmmCstCfg {
-  static constexpr int M = M_, N = N_, NBW = NBW_, WR = WR_, NW = NW_, R = R_;
+  static constexpr int M = M_, N = N_, NBW = NBW_, WR = WR_, NW = NW_, R = R_, EC = EC_;
   static constexpr bool Z = Z_, ZR = ZR_;
   static_assert(!ZR || (!Z_ && M_ % 2 == 0 && N_ % 2 == 0), "complex-as-real: real kernel on 2M x 2N");
+  static_assert(EC == 0 || (EC == N % 8 && N >= 8), "edge columns: EC = N mod 8, N >= 8");
   static constexpr int S = Z ? 2 : 1;
   static constexpr int MK = (M + 3) / 4;            // k-steps over m
-  static constexpr int NB = (N + 7) / 8;            // 8-column blocks of B
+  static constexpr int NB = (N - EC + 7) / 8;       // 8-column DMMA blocks of B
   static constexpr int NG = (NB + NBW - 1) / NBW;   // column groups
   static constexpr int RG = NW / NG;                // warps per column group
   static constexpr int RW = 8 * WR;                 // rows per warp per pass
   static constexpr int RPP = RW * RG;               // rows per pass
   static constexpr int NBA = (M * S + 15) / 16;     // A boxes per row
   static constexpr int OB = NBW * 8 * S / 16;       // output boxes per warp
+  static constexpr int NBL = NB - (NG - 1) * NBW;   // DMMA blocks of the last column group
+  static constexpr int OBL = ((8 * NBL + EC) * S + 15) / 16;  // its boxes (incl. edge columns)
   static constexpr int NT = (NW + 1) * 32;
   static constexpr int STAGE_DOUBLES = R * NBA * 16;
-  static constexpr int OUT_DOUBLES = OB * RW * 16;  // per warp
+  static constexpr int OUT_DOUBLES = (OB > OBL ? OB : OBL) * RW * 16;  // per warp
+  static constexpr int CE_DOUBLES = ((MK * 4 * EC * S + 127) / 128) * 128;  // edge C' in smem
   static_assert(NW % NG == 0 && RG >= 1, "consumer warps must be a multiple of the column groups");
   static_assert((NBW * 8 * S) % 16 == 0, "a warp's columns must fill whole 16-double boxes");
   static_assert((M * S) % 2 == 0 && (N * S) % 2 == 0 && M * S >= 16 && N * S >= 16,
@@ -1534,11 +1542,12 @@ template <class Cfg>
 __global__ void __launch_bounds__(Cfg::NT) tsmm_cst_kernel(const __grid_constant__ TsmmArgs p) {
   constexpr int M = Cfg::M, N = Cfg::N, S = Cfg::S, R = Cfg::R, NW = Cfg::NW, WR = Cfg::WR;
   constexpr int MK = Cfg::MK, NB = Cfg::NB, NBW = Cfg::NBW, NG = Cfg::NG, RW = Cfg::RW;
-  constexpr int RPP = Cfg::RPP, OB = Cfg::OB;
+  constexpr int RPP = Cfg::RPP, OB = Cfg::OB, EC = Cfg::EC;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   u64* full = reinterpret_cast<u64*>(smem_raw);
   u64* empty = full + 16;
-  double* sOut = reinterpret_cast<double*>(smem_raw + align1024(smem_raw, 256));
+  double* sCe = reinterpret_cast<double*>(smem_raw + 256);  // [MK*4][EC] edge columns of C'
+  double* sOut = reinterpret_cast<double*>(smem_raw + align1024(smem_raw, 256 + Cfg::CE_DOUBLES * 8));
   double* ring = sOut + NW * Cfg::OUT_DOUBLES;  // multiple of 1024 bytes
 
   const int tid = threadIdx.x;
@@ -1555,6 +1564,26 @@ __global__ void __launch_bounds__(Cfg::NT) tsmm_cst_kernel(const __grid_constant
     }
     fence_mbar_init();
     fence_proxy_async_smem();
+  }
+  if constexpr (EC > 0) {  // edge columns of C' (rows >= M zero)
+    for (int i = tid; i < MK * 4 * EC; i += Cfg::NT) {
+      const int m = i / EC, n = (N - EC) + i % EC;
+      double re = 0.0, im = 0.0;
+      if (m < M) {
+        if constexpr (Cfg::ZR) {
+          const double* c2 = p.C + ((m >> 1) * (N >> 1) + (n >> 1)) * 2;
+          double cr = __ldg(c2), ci = __ldg(c2 + 1);
+          c_prime(p, cr, ci);
+          re = ((m & 1) == (n & 1)) ? cr : ((m & 1) ? -ci : ci);
+        } else {
+          re = __ldg(&p.C[(m * N + n) * S]);
+          if constexpr (Cfg::Z) im = __ldg(&p.C[(m * N + n) * S + 1]);
+          c_prime(p, re, im);
+        }
+      }
+      sCe[i * S] = re;
+      if constexpr (Cfg::Z) sCe[i * S + 1] = im;
+    }
   }
   __syncthreads();
 
@@ -1615,8 +1644,10 @@ __global__ void __launch_bounds__(Cfg::NT) tsmm_cst_kernel(const __grid_constant
     };
     // blocks of this warp's column group inside C (the last group may be
     // partial): compile-time, so no DMMA is issued for columns past N
-    auto consume = [&](auto nbv) {
-      constexpr int NBV = decltype(nbv)::value;
+    auto consume = [&](auto nbv, auto ecv) {
+      constexpr int NBV = decltype(nbv)::value;  // DMMA blocks of this group inside C
+      constexpr int ECV = decltype(ecv)::value;  // DFMA edge columns (last group only)
+      constexpr int ECA = ECV > 0 ? ECV : 1;
       Ring ring_it;
       for (long long c = blockIdx.x; c < p.nchunks; c += G, ring_it.next(stages)) {
         const int s = ring_it.s;
@@ -1635,6 +1666,13 @@ __global__ void __launch_bounds__(Cfg::NT) tsmm_cst_kernel(const __grid_constant
             for (int j = 0; j < NBW; j++)
   #pragma unroll
               for (int z = 0; z < S; z++) acc[i][j][z][0] = acc[i][j][z][1] = 0.0;
+          double eacc[WR][ECA][S];
+  #pragma unroll
+          for (int i = 0; i < WR; i++)
+  #pragma unroll
+            for (int e = 0; e < ECA; e++)
+  #pragma unroll
+              for (int z = 0; z < S; z++) eacc[i][e][z] = 0.0;
   #pragma unroll
           for (int ks = 0; ks < MK; ks++) {
             const int m = 4 * ks + q;
@@ -1646,6 +1684,10 @@ __global__ void __launch_bounds__(Cfg::NT) tsmm_cst_kernel(const __grid_constant
                 const double a = mv ? sA[aoff(r, m)] : 0.0;
   #pragma unroll
                 for (int j = 0; j < NBV; j++) dmma(acc[i][j][0][0], acc[i][j][0][1], a, cf[ks][j][0]);
+                if constexpr (ECV > 0) {
+  #pragma unroll
+                  for (int e = 0; e < ECV; e++) eacc[i][e][0] = fma(a, sCe[m * EC + e], eacc[i][e][0]);
+                }
               } else {
                 const double2 a = mv ? *reinterpret_cast<const double2*>(sA + aoff(r, m)) : make_double2(0.0, 0.0);
                 const double nai = -a.y;
@@ -1655,6 +1697,13 @@ __global__ void __launch_bounds__(Cfg::NT) tsmm_cst_kernel(const __grid_constant
                   dmma(acc[i][j][0][0], acc[i][j][0][1], nai, cf[ks][j][1]);  // re -= ai ci
                   dmma(acc[i][j][1][0], acc[i][j][1][1], a.x, cf[ks][j][1]);  // im += ar ci
                   dmma(acc[i][j][1][0], acc[i][j][1][1], a.y, cf[ks][j][0]);  // im += ai cr
+                }
+                if constexpr (ECV > 0) {
+  #pragma unroll
+                  for (int e = 0; e < ECV; e++) {
+                    const double2 ce = *reinterpret_cast<const double2*>(sCe + (m * EC + e) * 2);
+                    zfma(eacc[i][e][0], eacc[i][e][1], a.x, a.y, ce.x, ce.y);
+                  }
                 }
               }
             }
@@ -1680,10 +1729,34 @@ __global__ void __launch_bounds__(Cfg::NT) tsmm_cst_kernel(const __grid_constant
                 }
               }
             }
+          if constexpr (ECV > 0) {
+            // edge columns: sum the 4 q-lanes' partial m-sums (fixed butterfly order)
+  #pragma unroll
+            for (int i = 0; i < WR; i++)
+  #pragma unroll
+              for (int e = 0; e < ECV; e++) {
+                double v[S];
+  #pragma unroll
+                for (int z = 0; z < S; z++) {
+                  v[z] = eacc[i][e][z];
+                  v[z] += __shfl_xor_sync(0xffffffffu, v[z], 1);
+                  v[z] += __shfl_xor_sync(0xffffffffu, v[z], 2);
+                }
+                if (q == 0) {
+                  const int rr = 8 * i + rho, c0 = (8 * NBV + e) * S;
+                  double* dst = stg + (c0 >> 4) * (RW * 16) + swz128(rr, c0 & 15);
+                  if constexpr (S == 2)
+                    *reinterpret_cast<double2*>(dst) = make_double2(v[0], v[S - 1]);
+                  else
+                    dst[0] = v[0];
+                }
+              }
+          }
           fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0 && nb0 < NB) {
-            for (int b = 0; b < OB; b++)
+            constexpr int NBOX = ECV > 0 ? Cfg::OBL : OB;
+            for (int b = 0; b < NBOX; b++)
               b_out_tma(p, nb0 * 8 * S + b * 16, static_cast<int>(r0 + wr0), stg + b * RW * 16);
             bulk_commit();
           }
@@ -1694,9 +1767,9 @@ __global__ void __launch_bounds__(Cfg::NT) tsmm_cst_kernel(const __grid_constant
     };
     constexpr int NBL = NB - (NG - 1) * NBW;
     if (cg == NG - 1)
-      consume(IC<NBL>{});
+      consume(IC<NBL>{}, IC<EC>{});
     else
-      consume(IC<NBW>{});
+      consume(IC<NBW>{}, IC<0>{});
     if (lane == 0) bulk_wait_all();
   }
 }

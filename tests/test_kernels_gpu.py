@@ -206,3 +206,38 @@ def test_complex_as_real(tsm, op, M, N):
         torch.cuda.synchronize()
         assert np.array_equal(got.cpu().numpy(), ref), (key, c)
     assert ran
+
+
+@pytest.mark.parametrize("cplx,zr", [(False, False), (True, False), (True, True)], ids=["D", "Z", "ZR"])
+@pytest.mark.parametrize("M,N", [(50, 50), (42, 34), (16, 20), (17, 17), (9, 12), (64, 57)])
+def test_tsmm_edge_columns(tsm, M, N, cplx, zr):
+    """C-stationary TSMM with the last N mod 8 columns by DFMA (kernel 3 | 16):
+    ragged K, integer bit-exact; complex native and complex-as-real."""
+    if zr:
+        cands = [c for c in gi.zr_candidates("tsmm", M, N) if c.get("EDGE")]
+    else:
+        cands = gi.tsmm_cst_configs(M, N, cplx, edge=True)
+    if not cands:
+        pytest.skip("no edge-column configuration for this shape")
+    dt = "z" if cplx else "d"
+    for c in cands[:: max(1, len(cands) // 3)]:
+        try:
+            plan = tsm.Plan("tsmm", dt, M, N, 0, config=gi.to_tsm_config("tsmm", c, 3, 1))
+        except tsm.TsmError as e:
+            if e.status != 2:
+                raise
+            continue
+        assert plan.config()["kernel"] & 16 and "edge-columns" in plan.describe(1000)["kernel"]
+        for K in (1, 9, 4099, 65537):
+            A = ti.matrix(K, M, "A", complex_=cplx, seed=K + 41)
+            Cm = ti.matrix(M, N, "C", complex_=cplx, seed=K + 42)
+            got = tsm.tsmm(torch.from_numpy(A).cuda(), torch.from_numpy(Cm).cuda(), plan=plan)
+            torch.cuda.synchronize()
+            ref, bound = oracle.tsmm(A, Cm)
+            r, wi, _ = oracle.max_err_ratio(got.cpu().numpy(), ref, bound)
+            assert r <= 1e-13, (M, N, c, K, r, wi)
+        Ai = ti.matrix(40001, M, "A", complex_=cplx, mode="int")
+        Ci = ti.matrix(M, N, "C", complex_=cplx, mode="int")
+        got = tsm.tsmm(torch.from_numpy(Ai).cuda(), torch.from_numpy(Ci).cuda(), plan=plan)
+        torch.cuda.synchronize()
+        assert np.array_equal(got.cpu().numpy(), oracle.tsmm(Ai, Ci)[0]), c

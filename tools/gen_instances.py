@@ -320,7 +320,9 @@ def cfg_type(op, dt, M, N, c) -> str:
     if c.get("impl", 0) == 4:
         return f"tsm::TsmmCstbCfg<{M}, {N}, {z}, {c['NBW']}, {c['WR']}, {c['NT'] // 32 - 1}, {c['R']}>"
     if c.get("impl", 0) == 3:
-        return f"tsm::TsmmCstCfg<{M}, {N}, {z}, {c['NBW']}, {c['WR']}, {c['NT'] // 32 - 1}, {c['R']}, {zr}>"
+        ec = N % 8 if c.get("EDGE", 0) else 0
+        return (f"tsm::TsmmCstCfg<{M}, {N}, {z}, {c['NBW']}, {c['WR']}, {c['NT'] // 32 - 1}, {c['R']}, {zr}, "
+                f"{ec}>")
     if c.get("impl", 0) >= 1:
         tma = "true" if c["impl"] == 2 else "false"
         return (f"tsm::TsmmMmaCfg<{M}, {N}, {z}, {c['WR']}, {c['NT'] // 32 - 1}, {c['R']}, "
@@ -538,6 +540,7 @@ def candidates(op: str, M: int, N: int, z: bool) -> list:
                 MS *= 2
     if op == "tsmm":
         out.extend(tsmm_cst_configs(M, N, z))
+        out.extend(tsmm_cst_configs(M, N, z, edge=True))
         out.extend(tsmm_cstb_configs(M, N, z))
     if z:
         out.extend(zr_candidates(op, M, N))
@@ -578,7 +581,7 @@ def zr_candidates(op: str, M: int, N: int) -> list:
     else:
         if 2 * M < 16 or 2 * N < 16:
             return []
-        base = tsmm_cst_configs(2 * M, 2 * N, False)
+        base = tsmm_cst_configs(2 * M, 2 * N, False) + tsmm_cst_configs(2 * M, 2 * N, False, edge=True)
     return [dict(c, ZR=1) for c in base]
 
 
@@ -670,13 +673,18 @@ def tsmm_pick(M: int, N: int, z: bool) -> dict:
     return tsmm_default(M, N, z)
 
 
-def tsmm_cst_configs(M: int, N: int, z: bool) -> list:
+def tsmm_cst_configs(M: int, N: int, z: bool, edge: bool = False) -> list:
     """C-stationary DMMA TSMM candidates: NBW column blocks per warp such that
-    the warp's C slice (MK x NBW fragments) fits in <= 48 registers-doubles."""
+    the warp's C slice (MK x NBW fragments) fits in <= 48 registers-doubles.
+    edge=True: the last N mod 8 columns by DFMA (EDGE=1) instead of a padded
+    8-column DMMA block."""
     if not tma_ok(M, N, z):
         return []
+    if edge and (N < 8 or N % 8 == 0):
+        return []
     S = 2 if z else 1
-    MK, NB = cdiv(M, 4), cdiv(N, 8)
+    EC = N % 8 if edge else 0
+    MK, NB = cdiv(M, 4), cdiv(N - EC, 8)
     out = []
     for NBW in range(1, NB + 1):
         if (NBW * 8 * S) % 16 or MK * NBW * S > 48:
@@ -687,7 +695,7 @@ def tsmm_cst_configs(M: int, N: int, z: bool) -> list:
             if NW > 16 or NW < 2:
                 continue
             for WR in (1, 2, 4):
-                if WR * NBW * 2 * S > 32:
+                if WR * NBW * 2 * S > 32 or WR * EC * S > 16:
                     continue
                 rpp = 8 * WR * RG
                 if rpp > 256:
@@ -695,7 +703,10 @@ def tsmm_cst_configs(M: int, N: int, z: bool) -> list:
                 ab = cdiv(M * S, 16) * 128
                 for tgt in (16384, 32768):
                     R = rpp * max(1, min(256 // rpp, round(tgt / (rpp * ab))))
-                    out.append(dict(NBW=NBW, WR=WR, NT=(NW + 1) * 32, R=R, impl=3))
+                    c = dict(NBW=NBW, WR=WR, NT=(NW + 1) * 32, R=R, impl=3)
+                    if edge:
+                        c["EDGE"] = 1
+                    out.append(c)
     return out
 
 
