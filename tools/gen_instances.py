@@ -478,9 +478,10 @@ def candidates(op: str, M: int, N: int, z: bool) -> list:
                     continue
                 RB = NT // (MT * NTL)
                 step = RB if RB % 2 == 0 else 2 * RB
-                for tgt in (12288, 24576):
+                # big stages amortise the per-chunk block barrier at narrow widths
+                for tgt in ((12288, 24576, 65536) if M * N <= 16 else (12288, 24576)):
                     out.append(dict(MT=MT, NTL=NTL, NT=NT, R=_rows(step, row, tgt), impl=0))
-        if min(M, N) >= 4:
+        if min(M, N) >= 2:  # (narrow widths: fixed per-chunk cost beats the padded MMA work)
             MB, NB = cdiv(M, 8), cdiv(N, 8)
             wmax = 8 if z else 16
             wt = []
