@@ -155,6 +155,12 @@ tsm_status tsm_plan_get_config(tsm_plan p, tsm_config *cfg);
  *                  PAPER.md:108-112).  TSMM: B = A conj(C).  Same kernels: the
  *                  sign of Im(A) / Im(C) is flipped on load (exact). */
 #define TSM_FLAG_CONJ 1u
+/*   TSM_FLAG_STRIDED  (NEXT row N4) choose a kernel that takes strided row
+ *                  views (tsmttsm_ld_* / tsmm_ld_*): the TMA kernels, whose
+ *                  tensor maps carry the row stride.  TSM_ERR_UNSUPPORTED for
+ *                  shapes without one (rows must be >= 128 bytes and 16-byte
+ *                  multiples: D widths even and >= 16, Z widths >= 8). */
+#define TSM_FLAG_STRIDED 2u
 
 /* tsm_plan_create / tsm_plan_create_config with flags: cfg == NULL selects the
  * tuned default configuration.  TSM_ERR_INVALID_VALUE for unknown flags or
@@ -200,6 +206,23 @@ tsm_status tsmm_d(tsm_plan p, int64_t K, const double *A, const double *C, doubl
                   tsm_stream stream);
 tsm_status tsmm_z(tsm_plan p, int64_t K, const tsm_zcomplex *A, const tsm_zcomplex *C,
                   tsm_zcomplex *B, tsm_stream stream);
+
+/* ------------------------------------------------------------------------ */
+/* Strided row views (NEXT row N4; block vectors as column subsets of wider   */
+/* arrays): row k of A starts at A + k*lda, of B at B + k*ldb (elements, lda  */
+/* >= M, ldb >= N).  lda == M and ldb == N are the dense calls (any plan);    */
+/* otherwise the plan needs a TMA kernel (TSM_FLAG_STRIDED) and 16-byte row   */
+/* strides, else TSM_ERR_UNSUPPORTED.  C stays dense M x N.                   */
+/* ------------------------------------------------------------------------ */
+tsm_status tsmttsm_ld_d(tsm_plan p, int64_t K, const double *A, int64_t lda, const double *B, int64_t ldb,
+                        double *C, void *ws, size_t ws_bytes, tsm_stream stream);
+tsm_status tsmttsm_ld_z(tsm_plan p, int64_t K, const tsm_zcomplex *A, int64_t lda,
+                        const tsm_zcomplex *B, int64_t ldb, tsm_zcomplex *C, void *ws,
+                        size_t ws_bytes, tsm_stream stream);
+tsm_status tsmm_ld_d(tsm_plan p, int64_t K, const double *A, int64_t lda, const double *C, double *B,
+                     int64_t ldb, tsm_stream stream);
+tsm_status tsmm_ld_z(tsm_plan p, int64_t K, const tsm_zcomplex *A, int64_t lda, const tsm_zcomplex *C,
+                     tsm_zcomplex *B, int64_t ldb, tsm_stream stream);
 
 /* ------------------------------------------------------------------------ */
 /* TSMM update  B <- alpha * A C + beta * B   (SURVEY.md §8(f) NEXT row N1;  */

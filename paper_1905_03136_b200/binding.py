@@ -25,6 +25,7 @@ OP = {"tsmttsm": 0, "tsmm": 1}
 DTYPE = {"d": 0, "z": 1}
 TSM_COMM_DETERMINISTIC = 1
 TSM_FLAG_CONJ = 1
+TSM_FLAG_STRIDED = 2
 MAT_ID = {"A": 1, "B": 2, "C": 3}
 
 # exported symbols declared in include/libtsm.h (checked by tests/test_abi.py)
@@ -35,7 +36,7 @@ EXPORTS = [
     "tsm_comm_unique_id", "tsm_comm_init", "tsm_comm_destroy", "tsm_comm_workspace_extra_bytes",
     "tsmttsm_allreduce_d", "tsmttsm_allreduce_z", "tsmm_bcast_d", "tsmm_bcast_z",
     "tsm_build_info", "tsm_plan_create_ex", "tsm_plan_get_flags", "tsmm_update_d", "tsmm_update_z",
-    "tsm_cgs_step_d", "tsm_cgs_step_z",
+    "tsm_cgs_step_d", "tsm_cgs_step_z", "tsmttsm_ld_d", "tsmttsm_ld_z", "tsmm_ld_d", "tsmm_ld_z",
 ]
 
 
@@ -97,6 +98,10 @@ def _load():
         "tsmm_update_z": [P, I64, ZComplex, VP, VP, ZComplex, VP, VP],
         "tsm_cgs_step_d": [P, P, P, I64, VP, VP, VP, VP, SZ, VP],
         "tsm_cgs_step_z": [P, P, P, I64, VP, VP, VP, VP, SZ, VP],
+        "tsmttsm_ld_d": [P, I64, VP, I64, VP, I64, VP, VP, SZ, VP],
+        "tsmttsm_ld_z": [P, I64, VP, I64, VP, I64, VP, VP, SZ, VP],
+        "tsmm_ld_d": [P, I64, VP, I64, VP, VP, I64, VP],
+        "tsmm_ld_z": [P, I64, VP, I64, VP, VP, I64, VP],
     }
     for name, args in sig.items():
         f = getattr(lib, name)
@@ -232,13 +237,15 @@ class Plan:
     """Owning wrapper of a tsm_plan handle."""
 
     def __init__(self, op: str, dtype: str, M: int, N: int, device: int = 0,
-                 config: dict | None = None, conj: bool = False):
-        """conj=True (Z only, TSM_FLAG_CONJ): TSMTTSM C = A^H B, TSMM B = A conj(C)."""
+                 config: dict | None = None, conj: bool = False, strided: bool = False):
+        """conj=True (Z only, TSM_FLAG_CONJ): TSMTTSM C = A^H B, TSMM B = A conj(C).
+        strided=True (TSM_FLAG_STRIDED): a kernel that takes strided row views."""
         self.op, self.dtype, self.M, self.N, self.device = op, dtype, M, N, device
-        self.conj = conj
+        self.conj, self.strided = conj, strided
         self.handle = None
-        if conj:
-            self.handle = tsm_plan_create_ex(op, dtype, M, N, device, config, TSM_FLAG_CONJ)
+        if conj or strided:
+            flags = (TSM_FLAG_CONJ if conj else 0) | (TSM_FLAG_STRIDED if strided else 0)
+            self.handle = tsm_plan_create_ex(op, dtype, M, N, device, config, flags)
         elif config is None:
             self.handle = tsm_plan_create(op, dtype, M, N, device)
         else:
@@ -261,12 +268,13 @@ class Plan:
             self.handle = None
 
 
-def get_plan(op: str, dtype: str, M: int, N: int, device: int, conj: bool = False) -> Plan:
-    key = (op, dtype, M, N, device, conj)
+def get_plan(op: str, dtype: str, M: int, N: int, device: int, conj: bool = False,
+             strided: bool = False) -> Plan:
+    key = (op, dtype, M, N, device, conj, strided)
     with _mu:
         p = _plans.get(key)
         if p is None:
-            p = Plan(op, dtype, M, N, device, conj=conj)
+            p = Plan(op, dtype, M, N, device, conj=conj, strided=strided)
             _plans[key] = p
     return p
 
@@ -293,6 +301,19 @@ def _check_cuda(*ts):
             raise ValueError("libtsm needs contiguous row-major tensors")
 
 
+def _check_rows(*ts):
+    """CUDA 2-D tensors with unit column stride (row-strided views allowed, N4)."""
+    for t in ts:
+        if not t.is_cuda:
+            raise ValueError("libtsm needs CUDA tensors (there is no CPU path)")
+        if t.dim() != 2 or (t.shape[1] > 1 and t.stride(1) != 1) or t.stride(0) < t.shape[1]:
+            raise ValueError("libtsm needs row-major tensors with unit column stride")
+
+
+def _ld(t) -> int:
+    return t.stride(0) if t.shape[0] > 1 else t.shape[1]
+
+
 def workspace(plan: Plan, K: int, stream: int, min_bytes: int = 0):
     """Cached, counter-zeroed workspace for (device, stream); grows as needed."""
     torch = _torch()
@@ -308,41 +329,57 @@ def workspace(plan: Plan, K: int, stream: int, min_bytes: int = 0):
 
 def tsmttsm(A, B, out=None, plan: Plan | None = None, conj: bool = False):
     """C = A^T B (plain transpose; conj=True: A^H B, Z only) for torch CUDA
-    tensors A (K x M), B (K x N)."""
+    tensors A (K x M), B (K x N).  Row-strided views (e.g. column subsets of a
+    wider block vector) go through tsmttsm_ld_* with a TSM_FLAG_STRIDED plan."""
     torch = _torch()
-    _check_cuda(A, B)
+    _check_rows(A, B)
     dt = _dtype_code(A)
     if B.dtype != A.dtype or A.dim() != 2 or B.dim() != 2 or A.shape[0] != B.shape[0]:
         raise ValueError("A and B must be 2-D, same dtype, same row count")
     K, M = A.shape
     N = B.shape[1]
     dev = A.device.index
-    plan = plan or get_plan("tsmttsm", dt, M, N, dev, conj)
+    lda, ldb = _ld(A), _ld(B)
+    dense = lda == M and ldb == N
+    plan = plan or get_plan("tsmttsm", dt, M, N, dev, conj, strided=not dense)
     C = out if out is not None else torch.empty((M, N), dtype=A.dtype, device=A.device)
     _check_cuda(C)
     stream = torch.cuda.current_stream(A.device).cuda_stream
     ws = workspace(plan, K, stream)
-    f = tsmttsm_z if dt == "z" else tsmttsm_d
-    f(plan.handle, K, A.data_ptr(), B.data_ptr(), C.data_ptr(), ws.data_ptr(), ws.numel(), stream)
+    if dense:
+        f = tsmttsm_z if dt == "z" else tsmttsm_d
+        f(plan.handle, K, A.data_ptr(), B.data_ptr(), C.data_ptr(), ws.data_ptr(), ws.numel(), stream)
+    else:
+        f = lib.tsmttsm_ld_z if dt == "z" else lib.tsmttsm_ld_d
+        check(f(plan.handle, K, A.data_ptr(), lda, B.data_ptr(), ldb, C.data_ptr(), ws.data_ptr(), ws.numel(),
+                stream), "tsmttsm_ld")
     return C
 
 
 def tsmm(A, C, out=None, plan: Plan | None = None):
-    """B = A C for torch CUDA tensors A (K x M), C (M x N)."""
+    """B = A C for torch CUDA tensors A (K x M), C (M x N); A and `out` may be
+    row-strided views (TSM_FLAG_STRIDED plan, tsmm_ld_*)."""
     torch = _torch()
-    _check_cuda(A, C)
+    _check_rows(A)
+    _check_cuda(C)
     dt = _dtype_code(A)
     if C.dtype != A.dtype or A.dim() != 2 or C.dim() != 2 or A.shape[1] != C.shape[0]:
         raise ValueError("A (K x M) and C (M x N) must be 2-D with matching M and dtype")
     K, M = A.shape
     N = C.shape[1]
     dev = A.device.index
-    plan = plan or get_plan("tsmm", dt, M, N, dev)
     B = out if out is not None else torch.empty((K, N), dtype=A.dtype, device=A.device)
-    _check_cuda(B)
+    _check_rows(B)
+    lda, ldb = _ld(A), _ld(B)
+    dense = lda == M and ldb == N
+    plan = plan or get_plan("tsmm", dt, M, N, dev, strided=not dense)
     stream = torch.cuda.current_stream(A.device).cuda_stream
-    f = tsmm_z if dt == "z" else tsmm_d
-    f(plan.handle, K, A.data_ptr(), C.data_ptr(), B.data_ptr(), stream)
+    if dense:
+        f = tsmm_z if dt == "z" else tsmm_d
+        f(plan.handle, K, A.data_ptr(), C.data_ptr(), B.data_ptr(), stream)
+    else:
+        f = lib.tsmm_ld_z if dt == "z" else lib.tsmm_ld_d
+        check(f(plan.handle, K, A.data_ptr(), lda, C.data_ptr(), B.data_ptr(), ldb, stream), "tsmm_ld")
     return B
 
 

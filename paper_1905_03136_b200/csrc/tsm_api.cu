@@ -68,7 +68,8 @@ static std::once_flag g_encode_once;
 
 // 2-D map of a row-major rows x width (doubles) operand: 16-double (128-byte)
 // boxes of box_rows rows, 128-byte swizzle, zero fill past the last row.
-tsm_status make_tmap(TmaDesc* out, const void* base, long long rows, int width, int box_rows) {
+tsm_status make_tmap(TmaDesc* out, const void* base, long long rows, int width, int box_rows,
+                     long long stride = 0) {
   std::call_once(g_encode_once, [] {
     void* fn = nullptr;
     cudaDriverEntryPointQueryResult q;
@@ -79,7 +80,7 @@ tsm_status make_tmap(TmaDesc* out, const void* base, long long rows, int width, 
   if (!g_encode) return fail(TSM_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   static_assert(sizeof(TmaDesc) == sizeof(CUtensorMap), "TmaDesc must mirror CUtensorMap");
   cuuint64_t dims[2] = {static_cast<cuuint64_t>(width), static_cast<cuuint64_t>(rows)};
-  cuuint64_t strides[1] = {static_cast<cuuint64_t>(width) * 8};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(stride > 0 ? stride : width) * 8};
   cuuint32_t box[2] = {16, static_cast<cuuint32_t>(box_rows)};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = g_encode(reinterpret_cast<CUtensorMap*>(out), CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2,
@@ -471,11 +472,30 @@ tsm_status tsm_plan_create_ex(tsm_plan* out, tsm_op op, tsm_dtype dtype, int M, 
                               const tsm_config* cfg, unsigned flags) {
   if (!out) return fail(TSM_ERR_INVALID_VALUE, "out == NULL");
   *out = nullptr;
-  if (flags & ~TSM_FLAG_CONJ) return fail(TSM_ERR_INVALID_VALUE, "unknown plan flags");
+  if (flags & ~(TSM_FLAG_CONJ | TSM_FLAG_STRIDED)) return fail(TSM_ERR_INVALID_VALUE, "unknown plan flags");
   if ((flags & TSM_FLAG_CONJ) && dtype != TSM_Z)
     return fail(TSM_ERR_INVALID_VALUE, "TSM_FLAG_CONJ applies to Z plans");
-  tsm_status st = cfg ? tsm_plan_create_config(out, op, dtype, M, N, device, cfg)
-                      : tsm_plan_create(out, op, dtype, M, N, device);
+  tsm_status st;
+  if (cfg) {
+    st = tsm_plan_create_config(out, op, dtype, M, N, device, cfg);
+  } else if (flags & TSM_FLAG_STRIDED) {
+    if (op != TSM_OP_TSMTTSM && op != TSM_OP_TSMM) return fail(TSM_ERR_INVALID_VALUE, "bad op");
+    if (dtype != TSM_D && dtype != TSM_Z) return fail(TSM_ERR_INVALID_VALUE, "bad dtype");
+    if (M < 1 || M > 64 || N < 1 || N > 64)
+      return fail(TSM_ERR_INVALID_VALUE, "M and N must be in [1, 64] (PAPER.md:57-58)");
+    const KernelEntry* d = default_params_strided(op, dtype, M, N);
+    if (!d)
+      return fail(TSM_ERR_UNSUPPORTED, "no TMA kernel for this shape (strided views need rows of >= 128 "
+                                       "bytes that are 16-byte multiples)");
+    st = make_plan(out, *d, device, true);  // exactly this configuration (AOT if instantiated, else JIT)
+  } else {
+    st = tsm_plan_create(out, op, dtype, M, N, device);
+  }
+  if (st == TSM_SUCCESS && (flags & TSM_FLAG_STRIDED) && !strided_capable(*(*out)->k)) {
+    tsm_plan_destroy(*out);
+    *out = nullptr;
+    return fail(TSM_ERR_INVALID_VALUE, "TSM_FLAG_STRIDED needs a TMA kernel configuration (TSMTTSM 2, TSMM 2/3)");
+  }
   if (st == TSM_SUCCESS) (*out)->flags = flags;
   return st;
 }
@@ -557,8 +577,27 @@ static bool overlap(const void* a, size_t na, const void* b, size_t nb) {
   return na && nb && x < y + nb && y < x + na;
 }
 
+bool strided_capable(const KernelEntry& k) {
+  return k.op == KIND_TSMTTSM ? k.impl == 2 : (k.impl == 2 || k.impl == 3);
+}
+
+// Row strides (elements) of a call: 0 = dense.  Strided views need a TMA
+// kernel and 16-byte row strides (NEXT N4).
+static tsm_status check_ld(const tsm_plan_s* p, int dt, long long* lda, long long* ldb, int wa, int wb) {
+  if (*lda == 0) *lda = wa;
+  if (*ldb == 0) *ldb = wb;
+  if (*lda < wa || *ldb < wb) return fail(TSM_ERR_INVALID_VALUE, "leading dimension smaller than the width");
+  if (*lda == wa && *ldb == wb) return TSM_SUCCESS;
+  const int S = dt == TSM_Z ? 2 : 1;
+  if (!strided_capable(*p->k))
+    return fail(TSM_ERR_UNSUPPORTED, "strided views need a TMA kernel: create the plan with TSM_FLAG_STRIDED");
+  if ((*lda * S) % 2 || (*ldb * S) % 2) return fail(TSM_ERR_UNSUPPORTED, "strided rows must be 16-byte multiples");
+  return TSM_SUCCESS;
+}
+
 tsm_status launch_tsmttsm(const tsm_plan_s* p, int dt, long long K, const void* A, const void* B,
-                          void* C, void* ws, size_t ws_bytes, void* stream, bool allow_k0) {
+                          void* C, void* ws, size_t ws_bytes, void* stream, bool allow_k0,
+                          long long lda, long long ldb) {
   if (!p) return fail(TSM_ERR_INVALID_VALUE, "plan == NULL");
   if (p->op != TSM_OP_TSMTTSM || p->dt != dt)
     return fail(TSM_ERR_INVALID_VALUE, "plan op/dtype does not match the call");
@@ -566,8 +605,13 @@ tsm_status launch_tsmttsm(const tsm_plan_s* p, int dt, long long K, const void* 
   if (!C || !ws || (K > 0 && (!A || !B))) return fail(TSM_ERR_INVALID_VALUE, "null pointer");
   if (misaligned(A) || misaligned(B) || misaligned(C) || misaligned(ws))
     return fail(TSM_ERR_MISALIGNED, "A, B, C and ws must be 16-byte aligned");
+  {
+    tsm_status st = check_ld(p, dt, &lda, &ldb, p->M, p->N);
+    if (st != TSM_SUCCESS) return st;
+  }
   const size_t s = (dt == TSM_Z ? 16 : 8);
-  const size_t nA = static_cast<size_t>(K) * p->M * s, nB = static_cast<size_t>(K) * p->N * s;
+  const size_t nA = K > 0 ? (static_cast<size_t>(K - 1) * lda + p->M) * s : 0;
+  const size_t nB = K > 0 ? (static_cast<size_t>(K - 1) * ldb + p->N) * s : 0;
   const size_t nC = static_cast<size_t>(p->M) * p->N * s;
   const size_t need = workspace_bytes(p, K);
   if (ws_bytes < need)
@@ -591,8 +635,8 @@ tsm_status launch_tsmttsm(const tsm_plan_s* p, int dt, long long K, const void* 
   a.conj = (p->flags & TSM_FLAG_CONJ) ? (1ull << 63) : 0ull;
   if (p->k->impl == 2 && K > 0) {
     const int S = dt == TSM_Z ? 2 : 1;
-    tsm_status st = make_tmap(&a.tmA, A, K, p->M * S, p->k->R);
-    if (st == TSM_SUCCESS) st = make_tmap(&a.tmB, B, K, p->N * S, p->k->R);
+    tsm_status st = make_tmap(&a.tmA, A, K, p->M * S, p->k->R, lda * S);
+    if (st == TSM_SUCCESS) st = make_tmap(&a.tmB, B, K, p->N * S, p->k->R, ldb * S);
     if (st != TSM_SUCCESS) return st;
   }
   void* args[] = {&a};
@@ -603,7 +647,8 @@ tsm_status launch_tsmttsm(const tsm_plan_s* p, int dt, long long K, const void* 
 }
 
 tsm_status launch_tsmm(const tsm_plan_s* p, int dt, long long K, const void* A, const void* C,
-                       void* B, void* stream, bool allow_k0, const TsmmMode* mode) {
+                       void* B, void* stream, bool allow_k0, const TsmmMode* mode, long long lda,
+                       long long ldb) {
   if (!p) return fail(TSM_ERR_INVALID_VALUE, "plan == NULL");
   if (p->op != TSM_OP_TSMM || p->dt != dt)
     return fail(TSM_ERR_INVALID_VALUE, "plan op/dtype does not match the call");
@@ -611,8 +656,13 @@ tsm_status launch_tsmm(const tsm_plan_s* p, int dt, long long K, const void* A, 
   if (!C || (K > 0 && (!A || !B))) return fail(TSM_ERR_INVALID_VALUE, "null pointer");
   if (misaligned(A) || misaligned(B) || misaligned(C))
     return fail(TSM_ERR_MISALIGNED, "A, B and C must be 16-byte aligned");
+  {
+    tsm_status st = check_ld(p, dt, &lda, &ldb, p->M, p->N);
+    if (st != TSM_SUCCESS) return st;
+  }
   const size_t s = (dt == TSM_Z ? 16 : 8);
-  const size_t nA = static_cast<size_t>(K) * p->M * s, nB = static_cast<size_t>(K) * p->N * s;
+  const size_t nA = K > 0 ? (static_cast<size_t>(K - 1) * lda + p->M) * s : 0;
+  const size_t nB = K > 0 ? (static_cast<size_t>(K - 1) * ldb + p->N) * s : 0;
   const size_t nC = static_cast<size_t>(p->M) * p->N * s;
   if (overlap(B, nB, A, nA) || overlap(B, nB, C, nC))
     return fail(TSM_ERR_INVALID_VALUE, "B overlaps A or C");
@@ -636,8 +686,8 @@ tsm_status launch_tsmm(const tsm_plan_s* p, int dt, long long K, const void* A, 
   if (p->k->impl == 2 || p->k->impl == 3) {  // B store boxes: 8*WR rows (WR = p0 for kernel 2, p1 for kernel 3)
     const int S = dt == TSM_Z ? 2 : 1;
     const int wr = p->k->impl == 3 ? p->k->p1 : p->k->p0;
-    tsm_status st = make_tmap(&a.tmA, A, K, p->M * S, p->k->R);
-    if (st == TSM_SUCCESS) st = make_tmap(&a.tmB, B, K, p->N * S, 8 * wr);
+    tsm_status st = make_tmap(&a.tmA, A, K, p->M * S, p->k->R, lda * S);
+    if (st == TSM_SUCCESS) st = make_tmap(&a.tmB, B, K, p->N * S, 8 * wr, ldb * S);
     if (st != TSM_SUCCESS) return st;
   }
   void* args[] = {&a};
@@ -768,6 +818,27 @@ tsm_status tsmm_d(tsm_plan p, int64_t K, const double* A, const double* C, doubl
 tsm_status tsmm_z(tsm_plan p, int64_t K, const tsm_zcomplex* A, const tsm_zcomplex* C,
                   tsm_zcomplex* B, tsm_stream stream) {
   return launch_tsmm(p, TSM_Z, K, A, C, B, stream, false);
+}
+
+tsm_status tsmttsm_ld_d(tsm_plan p, int64_t K, const double* A, int64_t lda, const double* B, int64_t ldb,
+                        double* C, void* ws, size_t ws_bytes, tsm_stream stream) {
+  if (lda < 1 || ldb < 1) return fail(TSM_ERR_INVALID_VALUE, "lda, ldb must be >= 1");
+  return launch_tsmttsm(p, TSM_D, K, A, B, C, ws, ws_bytes, stream, false, lda, ldb);
+}
+tsm_status tsmttsm_ld_z(tsm_plan p, int64_t K, const tsm_zcomplex* A, int64_t lda, const tsm_zcomplex* B,
+                        int64_t ldb, tsm_zcomplex* C, void* ws, size_t ws_bytes, tsm_stream stream) {
+  if (lda < 1 || ldb < 1) return fail(TSM_ERR_INVALID_VALUE, "lda, ldb must be >= 1");
+  return launch_tsmttsm(p, TSM_Z, K, A, B, C, ws, ws_bytes, stream, false, lda, ldb);
+}
+tsm_status tsmm_ld_d(tsm_plan p, int64_t K, const double* A, int64_t lda, const double* C, double* B,
+                     int64_t ldb, tsm_stream stream) {
+  if (lda < 1 || ldb < 1) return fail(TSM_ERR_INVALID_VALUE, "lda, ldb must be >= 1");
+  return launch_tsmm(p, TSM_D, K, A, C, B, stream, false, nullptr, lda, ldb);
+}
+tsm_status tsmm_ld_z(tsm_plan p, int64_t K, const tsm_zcomplex* A, int64_t lda, const tsm_zcomplex* C,
+                     tsm_zcomplex* B, int64_t ldb, tsm_stream stream) {
+  if (lda < 1 || ldb < 1) return fail(TSM_ERR_INVALID_VALUE, "lda, ldb must be >= 1");
+  return launch_tsmm(p, TSM_Z, K, A, C, B, stream, false, nullptr, lda, ldb);
 }
 
 tsm_status tsmm_update_d(tsm_plan p, int64_t K, double alpha, const double* A, const double* C,

@@ -11,6 +11,9 @@ namespace tsm {
 const KernelEntry* find_aot(int op, int dt, int M, int N);
 const KernelEntry* find_aot_config(const KernelEntry& want);  // same shape AND config
 const KernelEntry* default_params(int op, int dt, int M, int N);
+// TSM_FLAG_STRIDED plans (NEXT N4): a TMA kernel configuration, nullptr if none
+const KernelEntry* default_params_strided(int op, int dt, int M, int N);
+bool strided_capable(const KernelEntry& k);
 const char* build_info_json();
 
 // NVRTC run-time instantiation (tsm_jit.cpp).
@@ -21,15 +24,18 @@ int jit_count();
 tsm_status fail(tsm_status s, const std::string& why);
 
 // Launch paths (tsm_api.cu).  allow_k0: the sharded layer may pass K = 0.
+// lda, ldb: row strides in elements (0 = dense: M, N); strided views need a TMA kernel.
 tsm_status launch_tsmttsm(const tsm_plan_s* p, int dt, long long K, const void* A, const void* B,
-                          void* C, void* ws, size_t ws_bytes, void* stream, bool allow_k0);
+                          void* C, void* ws, size_t ws_bytes, void* stream, bool allow_k0,
+                          long long lda = 0, long long ldb = 0);
 // TSMM output mode (NEXT N1): B = alpha A C (reduce = 0) or B += alpha A C (reduce = 1).
 struct TsmmMode {
   double alpha_re = 1.0, alpha_im = 0.0;
   int reduce = 0;
 };
 tsm_status launch_tsmm(const tsm_plan_s* p, int dt, long long K, const void* A, const void* C,
-                       void* B, void* stream, bool allow_k0, const TsmmMode* mode = nullptr);
+                       void* B, void* stream, bool allow_k0, const TsmmMode* mode = nullptr,
+                       long long lda = 0, long long ldb = 0);
 // B <- alpha A C + beta B (tsmm_update_*): beta in {0, 1} in one pass, else B *= beta first.
 tsm_status launch_tsmm_update(const tsm_plan_s* p, int dt, long long K, double ar, double ai,
                               const void* A, const void* C, double br, double bi, void* B,

@@ -156,3 +156,52 @@ def test_cgs_step_fp(tsm, cplx):
     # the update is checked against the oracle applied to the GPU's C
     Bref, bb = oracle.tsmm_update(A, C, B0, -1, 1)
     assert oracle.max_err_ratio(Bd.cpu().numpy(), Bref, bb)[0] <= 1e-13
+
+
+@pytest.mark.parametrize("cplx", [False, True], ids=["D", "Z"])
+@pytest.mark.parametrize("M,N", [(16, 16), (32, 48), (64, 20), (8, 8)])
+def test_strided_views(tsm, M, N, cplx):
+    """N4: column subsets of a wider block vector (row stride ld > width) through
+    tsmttsm_ld / tsmm_ld with a TSM_FLAG_STRIDED plan (TMA kernels)."""
+    if not cplx and min(M, N) < 16:
+        pytest.skip("D strided views need rows of >= 16 doubles")
+    K, W = 70001, 150
+    big = ti.matrix(K, W, "A", complex_=cplx, seed=5)
+    G = cu(big)
+    a0, b0 = 6, 80  # even offsets keep 16-byte alignment for D
+    A, B = G[:, a0:a0 + M], G[:, b0:b0 + N]
+    assert A.stride(0) == W and not A.is_contiguous()
+    C = tsm.tsmttsm(A, B)
+    torch.cuda.synchronize()
+    ref, bound = oracle.tsmttsm(big[:, a0:a0 + M], big[:, b0:b0 + N])
+    assert oracle.max_err_ratio(C.cpu().numpy(), ref, bound)[0] <= 1e-12
+    Cm = ti.matrix(M, N, "C", complex_=cplx, seed=6)
+    out = torch.zeros((K, W), dtype=G.dtype, device="cuda")
+    Bv = out[:, 40:40 + N]
+    tsm.tsmm(A, cu(Cm), out=Bv)
+    torch.cuda.synchronize()
+    refm, bm = oracle.tsmm(big[:, a0:a0 + M], Cm)
+    got = out.cpu().numpy()
+    assert oracle.max_err_ratio(got[:, 40:40 + N], refm, bm)[0] <= 1e-13
+    assert np.count_nonzero(got[:, :40]) == 0 and np.count_nonzero(got[:, 40 + N:]) == 0  # untouched
+
+
+def test_strided_rules(tsm):
+    # a dense-tuned plan that is not a TMA kernel refuses strided calls
+    p = tsm.Plan("tsmttsm", "d", 33, 33, 0)
+    if p.config()["kernel"] & 15 != 2:
+        A = torch.zeros((100, 40), dtype=torch.float64, device="cuda")
+        with pytest.raises(tsm.TsmError) as e:
+            tsm.tsmttsm(A[:, :33], A[:, 2:35], plan=p)
+        assert e.value.status == 2
+    # odd D widths have no TMA kernel
+    with pytest.raises(tsm.TsmError) as e:
+        tsm.Plan("tsmttsm", "d", 33, 33, 0, strided=True)
+    assert e.value.status == 2
+    # strided plans still serve dense calls
+    ps = tsm.Plan("tsmm", "d", 32, 32, 0, strided=True)
+    A = ti.matrix(5000, 32, "A")
+    Cm = ti.matrix(32, 32, "C")
+    got = tsm.tsmm(cu(A), cu(Cm), plan=ps).cpu().numpy()
+    ref, b = oracle.tsmm(A, Cm)
+    assert oracle.max_err_ratio(got, ref, b)[0] <= 1e-13

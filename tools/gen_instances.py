@@ -423,6 +423,25 @@ def main(per_file: int = 12) -> int:
                                  f"nullptr, {c['NT']}, {c['R']}, {p[0]}, {p[1]}, {p[2]}, {p[3]}, "
                                  f"{c['stages']}, {c['ctas']}, {c.get('impl', 0)}, "
                                  f"{flags(c)}}},")
+    lines += ["};", ""]
+    # strided-view defaults (TSM_FLAG_STRIDED, NEXT N4): a TMA kernel, whose
+    # tensor maps take any 16-byte row stride; impl -1 = no such kernel.
+    lines += ["extern const KernelEntry g_param_table_strided[] = {"]
+    for op in ("tsmttsm", "tsmm"):
+        for dt in ("d", "z"):
+            for M in range(1, 65):
+                for N in range(1, 65):
+                    c = strided_default(op, M, N, dt == "z",
+                                        tune.get(f"{op}_{dt}_{M}_{N}", {}).get("cfg"))
+                    if c is None:
+                        lines.append(f"  {{{0 if op == 'tsmttsm' else 1}, {1 if dt == 'z' else 0}, {M}, {N}, "
+                                     f"nullptr, 32, 2, 0, 0, 0, 0, 2, 1, -1, 0}},")
+                        continue
+                    p = params4(op, M, N, c)
+                    lines.append(f"  {{{0 if op == 'tsmttsm' else 1}, {1 if dt == 'z' else 0}, {M}, {N}, "
+                                 f"nullptr, {c['NT']}, {c['R']}, {p[0]}, {p[1]}, {p[2]}, {p[3]}, "
+                                 f"{c['stages']}, {c['ctas']}, {c.get('impl', 0)}, "
+                                 f"{flags(c)}}},")
     lines += ["};", "}  // namespace tsm", ""]
     _write(os.path.join(GEN, "params_gen.cpp"), "\n".join(lines))
 
@@ -569,6 +588,29 @@ def candidates(op: str, M: int, N: int, z: bool) -> list:
             seen.add(k)
             uniq.append(c)
     return uniq
+
+
+def strided_capable(op: str, c: dict) -> bool:
+    """Kernels whose A/B rows arrive by TMA tensor maps (any 16-byte stride)."""
+    return c.get("impl", 0) == 2 if op == "tsmttsm" else c.get("impl", 0) in (2, 3)
+
+
+def strided_default(op: str, M: int, N: int, z: bool, tuned: dict | None):
+    """Default configuration of a TSM_FLAG_STRIDED plan: the tuned one when it
+    is a TMA kernel, else a TMA heuristic; None when no TMA kernel applies."""
+    c = resolve(op, M, N, z, tuned)
+    if strided_capable(op, c):
+        return c
+    if not tma_ok(M, N, z):
+        return None
+    if op == "tsmttsm":
+        d = tsmttsm_mma_default(M, N, z)
+        return d if strided_capable(op, d) else None
+    cands = tsmm_cst_configs(M, N, z)
+    if not cands:
+        return None
+    pick = [x for x in cands if x["WR"] == 2] or cands
+    return dict(pick[0], stages=3, ctas=1)
 
 
 def zr_candidates(op: str, M: int, N: int) -> list:
