@@ -36,6 +36,7 @@ def main():
     ap.add_argument("--widths", default="1,2,4,8,16,24,32,40,48,56,64")
     ap.add_argument("--shapes", default="")
     ap.add_argument("--K", type=int, default=1 << 24)
+    ap.add_argument("--Ks", default="", help="comma list of K values (small-K study); overrides --K")
     ap.add_argument("--reps", type=int, default=10)
     ap.add_argument("--json", default="")
     a = ap.parse_args()
@@ -43,7 +44,8 @@ def main():
     shapes = [tuple(map(int, s.split("x"))) for s in a.shapes.split(",") if s] or \
         [(w, w) for w in map(int, a.widths.split(","))]
     maxw = max(max(s) for s in shapes)
-    K = a.K
+    Ks = [int(float(x)) for x in a.Ks.split(",") if x] or [a.K]
+    K = max(Ks)
     flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
     s = torch.cuda.current_stream().cuda_stream
     rows = []
@@ -55,6 +57,7 @@ def main():
         tsm.fill(Abuf, "A", 42)
         tsm.fill(Bbuf, "B", 42)
         for op in a.ops.split(","):
+          for K in Ks:
             for (M, N) in shapes:
                 A = Abuf[: K * M].view(K, M)
                 if op == "tsmttsm":
