@@ -169,6 +169,14 @@ tsm_status tsm_plan_create_ex(tsm_plan *out, tsm_op op, tsm_dtype dtype, int M, 
                               const tsm_config *cfg, unsigned flags);
 tsm_status tsm_plan_get_flags(tsm_plan p, unsigned *flags);
 
+/* Build tooling: compile the kernel a plan would use (default configuration,
+ * cfg, or the TSM_FLAG_STRIDED default) with NVRTC into the kernel cache
+ * (<directory of libtsm.so>/kcache, or TSM_JIT_CACHE_DIR) without touching a
+ * device.  Plans load cached kernels instead of compiling them.  Errors as
+ * tsm_plan_create_config; TSM_ERR_INTERNAL if NVRTC fails. */
+tsm_status tsm_jit_precompile(tsm_op op, tsm_dtype dtype, int M, int N, const tsm_config *cfg,
+                              unsigned flags);
+
 /* Bytes of device workspace a TSMTTSM call with K rows needs (partials of the
  * fixed-order grid reduction plus 2 counter words); 0 for TSMM plans.
  * The first 256 bytes hold counters that MUST be zero before the first use of

@@ -37,6 +37,7 @@ EXPORTS = [
     "tsmttsm_allreduce_d", "tsmttsm_allreduce_z", "tsmm_bcast_d", "tsmm_bcast_z",
     "tsm_build_info", "tsm_plan_create_ex", "tsm_plan_get_flags", "tsmm_update_d", "tsmm_update_z",
     "tsm_cgs_step_d", "tsm_cgs_step_z", "tsmttsm_ld_d", "tsmttsm_ld_z", "tsmm_ld_d", "tsmm_ld_z",
+    "tsm_jit_precompile",
 ]
 
 
@@ -102,6 +103,7 @@ def _load():
         "tsmttsm_ld_z": [P, I64, VP, I64, VP, I64, VP, VP, SZ, VP],
         "tsmm_ld_d": [P, I64, VP, I64, VP, VP, I64, VP],
         "tsmm_ld_z": [P, I64, VP, I64, VP, VP, I64, VP],
+        "tsm_jit_precompile": [I, I, I, I, ctypes.POINTER(TsmConfig), ctypes.c_uint],
     }
     for name, args in sig.items():
         f = getattr(lib, name)

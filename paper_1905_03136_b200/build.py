@@ -79,6 +79,7 @@ def build(jobs: int | None = None, verbose: bool = True) -> str:
     stamp = hashlib.sha1("".join(objs).encode()).hexdigest()[:16]
     stamp_file = os.path.join(OBJ, "libtsm.stamp")
     if os.path.exists(LIB) and os.path.exists(stamp_file) and open(stamp_file).read() == stamp:
+        precompile()
         return LIB
     tmp = LIB + f".tmp{os.getpid()}"
     cmd = [NVCC, *ARCH, "-shared", "-Xcompiler", "-fPIC", "-cudart", "static", "-o", tmp, *objs,
@@ -92,7 +93,17 @@ def build(jobs: int | None = None, verbose: bool = True) -> str:
         f.write(stamp)
     if verbose:
         print(f"built {LIB} from {len(srcs)} translation units")
+    precompile()
     return LIB
+
+
+def precompile() -> None:
+    """NVRTC-compile the tuned kernels into <package>/kcache (precompile.py,
+    in a fresh interpreter so torch's NVRTC is the one bound)."""
+    r = subprocess.run([sys.executable, os.path.join(PKG, "precompile.py")], capture_output=True, text=True)
+    sys.stdout.write(r.stdout)
+    if r.returncode != 0:
+        raise RuntimeError(f"kernel precompile failed:\n{r.stdout[-2000:]}{r.stderr[-2000:]}")
 
 
 if __name__ == "__main__":

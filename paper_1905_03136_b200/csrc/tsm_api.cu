@@ -387,8 +387,15 @@ static tsm_status make_plan(tsm_plan* out, const KernelEntry& want, int device, 
   if (st != TSM_SUCCESS) return st;
   DeviceGuard dg(device);
   if (dg.err != cudaSuccess) return cuda_fail(dg.err, "cudaSetDevice");
-  const KernelEntry* k = exact ? find_aot_config(want) : find_aot(want.op, want.dt, want.M, want.N);
+  // NVRTC first (the code the autotuner measured; cubins precompiled into
+  // <libdir>/kcache at build time), the nvcc AOT instantiation if NVRTC is
+  // unavailable or TSM_PREFER_AOT is set.
+  const KernelEntry* k = nullptr;
   bool jit = false;
+  const char* pa = getenv("TSM_PREFER_AOT");
+  const bool prefer_aot = pa && pa[0] && pa[0] != '0';
+  if (!prefer_aot && jit_kernel(want, &k) == TSM_SUCCESS) jit = true;
+  if (!k) k = exact ? find_aot_config(want) : find_aot(want.op, want.dt, want.M, want.N);
   if (!k) {
     st = jit_kernel(want, &k);
     if (st != TSM_SUCCESS) return st;
@@ -498,6 +505,37 @@ tsm_status tsm_plan_create_ex(tsm_plan* out, tsm_op op, tsm_dtype dtype, int M, 
   }
   if (st == TSM_SUCCESS) (*out)->flags = flags;
   return st;
+}
+
+tsm_status tsm_jit_precompile(tsm_op op, tsm_dtype dtype, int M, int N, const tsm_config* cfg, unsigned flags) {
+  if (op != TSM_OP_TSMTTSM && op != TSM_OP_TSMM) return fail(TSM_ERR_INVALID_VALUE, "bad op");
+  if (dtype != TSM_D && dtype != TSM_Z) return fail(TSM_ERR_INVALID_VALUE, "bad dtype");
+  if (M < 1 || M > 64 || N < 1 || N > 64) return fail(TSM_ERR_INVALID_VALUE, "M and N must be in [1, 64]");
+  KernelEntry e{};
+  if (cfg) {
+    e.op = op;
+    e.dt = dtype;
+    e.M = M;
+    e.N = N;
+    e.NT = cfg->threads;
+    e.R = cfg->rows_per_chunk;
+    e.p0 = cfg->p0;
+    e.p1 = cfg->p1;
+    e.impl = cfg->kernel & 15;
+    e.edge = (cfg->kernel >> 4) & 31;
+    e.p2 = (op == TSM_OP_TSMTTSM && e.impl == 0) ? 0 : cfg->p2;
+    e.p3 = (op == TSM_OP_TSMTTSM && e.impl >= 1) ? cfg->p3 : 0;
+    e.stages = cfg->stages;
+    e.ctas_per_sm = cfg->ctas_per_sm;
+    tsm_status st = validate_config(e);
+    if (st != TSM_SUCCESS) return st;
+  } else {
+    const KernelEntry* d = (flags & TSM_FLAG_STRIDED) ? default_params_strided(op, dtype, M, N)
+                                                       : default_params(op, dtype, M, N);
+    if (!d) return fail(TSM_ERR_UNSUPPORTED, "no configuration for this shape / flags");
+    e = *d;
+  }
+  return jit_precompile(e);
 }
 
 tsm_status tsm_plan_get_flags(tsm_plan p, unsigned* flags) {

@@ -18,6 +18,7 @@ const char* build_info_json();
 
 // NVRTC run-time instantiation (tsm_jit.cpp).
 tsm_status jit_kernel(const KernelEntry& want, const KernelEntry** out);
+tsm_status jit_precompile(const KernelEntry& want);  // NVRTC -> disk cache only (no device)
 int jit_count();
 
 // Error helpers (tsm_api.cu): record a thread-local detail string.

@@ -10,6 +10,8 @@
 #include <cuda_runtime.h>
 #include <nvrtc.h>
 
+#include <dlfcn.h>
+
 #include <cstdio>
 #include <cstdlib>
 #include <deque>
@@ -81,9 +83,19 @@ unsigned long long fnv1a(const std::string& s, unsigned long long h = 1469598103
   return h;
 }
 
+// Default cache: <directory of libtsm.so>/kcache (filled at build time by
+// tsm_jit_precompile, travels with the library), else $HOME/.cache/libtsm.
 std::string cache_dir() {
   const char* d = getenv("TSM_JIT_CACHE_DIR");
   if (d) return std::string(d);
+  Dl_info info;
+  if (dladdr(reinterpret_cast<void*>(&cache_dir), &info) && info.dli_fname) {
+    std::string lib(info.dli_fname);
+    const size_t slash = lib.rfind('/');
+    const std::string dir = (slash == std::string::npos ? std::string(".") : lib.substr(0, slash)) + "/kcache";
+    mkdir(dir.c_str(), 0755);
+    if (access(dir.c_str(), W_OK) == 0) return dir;
+  }
   const char* home = getenv("HOME");
   return home ? std::string(home) + "/.cache/libtsm" : std::string();
 }
@@ -144,6 +156,39 @@ tsm_status compile(const KernelEntry& e, std::vector<char>* cubin, std::string* 
 
 }  // namespace
 
+// cubin + lowered name of `want`: from the disk cache, else compiled by NVRTC
+// (and written to the cache).
+tsm_status cubin_for(const KernelEntry& want, std::vector<char>* cubin, std::string* lowered) {
+  const std::string key = kernel_name(want);
+  // one subdirectory per kernel-source version (stale ones can be pruned whole)
+  static const unsigned long long src_hash = fnv1a(kTsmKernelSource);
+  char sbuf[32];
+  snprintf(sbuf, sizeof sbuf, "/src_%016llx", src_hash);
+  std::string dir = cache_dir();
+  if (!dir.empty()) dir += sbuf;
+  char hbuf[32];
+  snprintf(hbuf, sizeof hbuf, "%016llx", fnv1a(key, src_hash));
+  const std::string cname = std::string("tsm_") + hbuf + ".cubin";
+  const std::string lname = std::string("tsm_") + hbuf + ".name";
+  std::vector<char> lowv;
+  if (!dir.empty() && read_file(dir + "/" + cname, cubin) && read_file(dir + "/" + lname, &lowv)) {
+    lowered->assign(lowv.begin(), lowv.end());
+    return TSM_SUCCESS;
+  }
+  tsm_status st = compile(want, cubin, lowered);
+  if (st != TSM_SUCCESS) return st;
+  write_file_atomic(dir, cname, *cubin);
+  write_file_atomic(dir, lname, std::vector<char>(lowered->begin(), lowered->end()));
+  return TSM_SUCCESS;
+}
+
+// Build-time: compile `want` into the disk cache (no CUDA device needed).
+tsm_status jit_precompile(const KernelEntry& want) {
+  std::vector<char> cubin;
+  std::string lowered;
+  return cubin_for(want, &cubin, &lowered);
+}
+
 // Returns a registry entry whose func is a JIT-compiled kernel for `want`.
 tsm_status jit_kernel(const KernelEntry& want, const KernelEntry** out) {
   const std::string key = kernel_name(want);
@@ -156,20 +201,11 @@ tsm_status jit_kernel(const KernelEntry& want, const KernelEntry** out) {
     }
   }
   // compile / load outside the lock: independent plans JIT in parallel
-  const std::string dir = cache_dir();
-  char hbuf[32];
-  snprintf(hbuf, sizeof hbuf, "%016llx", fnv1a(key, fnv1a(kTsmKernelSource)));
-  const std::string cname = std::string("tsm_") + hbuf + ".cubin";
-  const std::string lname = std::string("tsm_") + hbuf + ".name";
-  std::vector<char> cubin, lowv;
+  std::vector<char> cubin;
   std::string lowered;
-  if (!dir.empty() && read_file(dir + "/" + cname, &cubin) && read_file(dir + "/" + lname, &lowv)) {
-    lowered.assign(lowv.begin(), lowv.end());
-  } else {
-    tsm_status st = compile(want, &cubin, &lowered);
+  {
+    tsm_status st = cubin_for(want, &cubin, &lowered);
     if (st != TSM_SUCCESS) return st;
-    write_file_atomic(dir, cname, cubin);
-    write_file_atomic(dir, lname, std::vector<char>(lowered.begin(), lowered.end()));
   }
   cudaLibrary_t lib;
   cudaError_t e = cudaLibraryLoadData(&lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0);

@@ -308,3 +308,34 @@ def test_bad_config_rejected(tsm):
     with pytest.raises(TsmError, match="INVALID_VALUE"):
         tsm.Plan("tsmm", "d", 8, 8, 0, config=dict(threads=128, rows_per_chunk=63, p0=8, p1=4,
                                                   p2=1, stages=2, ctas_per_sm=1))
+
+
+def test_aot_path_parity():
+    """Plans load NVRTC kernels (precompiled into kcache); TSM_PREFER_AOT=1
+    selects the nvcc-compiled AOT instantiations instead -- same results."""
+    import subprocess
+    import sys
+    code = r'''
+import numpy as np, torch, oracle, tsminputs as ti
+from paper_1905_03136_b200 import binding as tsm
+for op, dt, M, N in [("tsmttsm", "d", 64, 64), ("tsmttsm", "z", 24, 24), ("tsmm", "d", 41, 41), ("tsmm", "z", 33, 17)]:
+    p = tsm.Plan(op, dt, M, N, 0)
+    assert p.describe(1000)["jit"] is False, p.describe(1000)
+    z = dt == "z"
+    A = ti.matrix(20001, M, "A", complex_=z, mode="int")
+    if op == "tsmttsm":
+        B = ti.matrix(20001, N, "B", complex_=z, mode="int")
+        got = tsm.tsmttsm(torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda(), plan=p).cpu().numpy()
+        ref = oracle.tsmttsm(A, B)[0]
+    else:
+        C = ti.matrix(M, N, "C", complex_=z, mode="int")
+        got = tsm.tsmm(torch.from_numpy(A).cuda(), torch.from_numpy(C).cuda(), plan=p).cpu().numpy()
+        ref = oracle.tsmm(A, C)[0]
+    assert np.array_equal(got, ref), (op, dt, M, N)
+print("ok")
+'''
+    import os
+    env = dict(os.environ, TSM_PREFER_AOT="1")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-3000:]
