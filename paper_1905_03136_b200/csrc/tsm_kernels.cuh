@@ -1785,6 +1785,35 @@ __global__ void __launch_bounds__(Cfg::NT) tsmm_cst_kernel(const __grid_constant
 // Before that barrier the issuing lane waits until its previous store has read
 // the other buffer, so a buffer is rewritten only after its store completed.
 // --------------------------------------------------------------------------
+// Row permutations rho(g) for the impl-4 A fragment (rows rho(g), columns q of
+// a dense stride-M stage) and the worst lanes-per-bank-unit they give.
+//   0: identity  1: [0,2,4,6,1,3,5,7]  2: [0,4,1,5,2,6,3,7]  3: bitrev [0,4,2,6,1,5,3,7]
+__host__ __device__ constexpr int cstb_rho(int sel, int g) {
+  return sel == 1 ? (((g & 3) << 1) | (g >> 2))
+       : sel == 2 ? (((g & 1) << 2) | (g >> 1))
+       : sel == 3 ? (((g & 1) << 2) | (g & 2) | (g >> 2))
+                  : g;
+}
+constexpr int cstb_conflict(int sel, int M, bool z) {
+  // D: two 16-lane phases of 8-byte units; Z: four 8-lane phases of 16-byte units
+  const int lanes = z ? 8 : 16, units = z ? 8 : 16;
+  int worst = 0;
+  for (int ph = 0; ph < 32 / lanes; ph++) {
+    int cnt[16] = {};
+    for (int l = ph * lanes; l < ph * lanes + lanes; l++) {
+      const int u = (cstb_rho(sel, l >> 2) * M + (l & 3)) % units;
+      if (++cnt[u] > worst) worst = cnt[u];
+    }
+  }
+  return worst;
+}
+constexpr int cstb_pick_rho(int M, bool z) {
+  int best = 0;
+  for (int sel = 1; sel < 4; sel++)
+    if (cstb_conflict(sel, M, z) < cstb_conflict(best, M, z)) best = sel;
+  return best;
+}
+
 template <int M_, int N_, bool Z_, int NBW_, int WR_, int NW_, int R_>
 struct TsmmCstbCfg {
   static constexpr int M = M_, N = N_, NBW = NBW_, WR = WR_, NW = NW_, R = R_;
@@ -1799,6 +1828,7 @@ struct TsmmCstbCfg {
   static constexpr int NT = (NW + 1) * 32;
   static constexpr int STAGE_DOUBLES = ((R * M * S + 15) / 16) * 16;
   static constexpr int OUT_DOUBLES = ((RW * N * S + 15) / 16) * 16;  // one staging buffer
+  static constexpr int RHO = cstb_pick_rho(M, Z);  // conflict-minimising row permutation
   static_assert(NW % NG == 0 && RG >= 1 && RG <= 15, "consumer warps: a multiple of the column groups, <= 15 row groups");
   static_assert(R % RPP == 0 && R % 2 == 0, "rows per chunk: whole passes");
 };
@@ -1853,6 +1883,7 @@ __global__ void __launch_bounds__(Cfg::NT) tsmm_cstb_kernel(const __grid_constan
     const int cg = warp % NG, rg = warp / NG;
     const int nb0 = cg * NBW;
     const bool issuer = (cg == 0 && lane == 0);
+    const int rho = cstb_rho(Cfg::RHO, g);  // MMA row g <-> stage row rho(g) (bank conflicts)
     // this warp's C' slice as MMA-B fragments: lane holds C'[4ks+q][8(nb0+j)+g]
     double cf[MK][NBW][S];
 #pragma unroll
@@ -1896,7 +1927,7 @@ __global__ void __launch_bounds__(Cfg::NT) tsmm_cstb_kernel(const __grid_constan
             const bool mv = (4 * ks + 4 <= M) || (m < M);
 #pragma unroll
             for (int i = 0; i < WR; i++) {
-              const int r = wr0 + 8 * i + g;  // rows past `rows`: stale, never stored
+              const int r = wr0 + 8 * i + rho;  // rows past `rows`: stale, never stored
               if constexpr (!Cfg::Z) {
                 const double a = mv ? sA[r * M + m] : 0.0;
 #pragma unroll
@@ -1923,7 +1954,7 @@ __global__ void __launch_bounds__(Cfg::NT) tsmm_cstb_kernel(const __grid_constan
             for (int j = 0; j < NBV; j++)
 #pragma unroll
               for (int e = 0; e < 2; e++) {
-                const int rr = 8 * i + g, n = 8 * (nb0 + j) + 2 * q + e;
+                const int rr = 8 * i + rho, n = 8 * (nb0 + j) + 2 * q + e;
                 if (n < N) {
 #pragma unroll
                   for (int z = 0; z < S; z++) stg[(rr * N + n) * S + z] = acc[i][j][z][e];

@@ -755,8 +755,10 @@ def tsmm_cst_configs(M: int, N: int, z: bool, edge: bool = False) -> list:
 
 def tsmm_cstb_configs(M: int, N: int, z: bool) -> list:
     """C-stationary DMMA TSMM with bulk copies (impl 4): the widths the TMA
-    kernel 3 cannot take (rows not 16-byte multiples or < 128 bytes)."""
-    if tma_ok(M, N, z) or N < 2:
+    kernel 3 cannot take (rows not 16-byte multiples or < 128 bytes), and
+    any width where one 8-column block per warp (NBW = 1, not possible with
+    kernel 3's whole 16-double output boxes) balances better."""
+    if N < 2:
         return []
     S = 2 if z else 1
     MK, NB = cdiv(M, 4), cdiv(N, 8)
