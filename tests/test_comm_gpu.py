@@ -58,3 +58,32 @@ def test_allreduce_and_bcast_one_rank(pg, deterministic, cplx):
         assert np.all(Z.cpu().numpy() == 0)
     finally:
         comm.close()
+
+
+@pytest.mark.parametrize("deterministic", [False, True])
+@pytest.mark.parametrize("cplx", [False, True])
+def test_cgs_step_through_comm(pg, deterministic, cplx):
+    """tsm_cgs_step with a communicator: C summed over ranks (NCCL), then the
+    local update B -= A C; exact with an orthonormal basis and integer B."""
+    from paper_1905_03136_b200 import binding as tsm
+    comm = tsm.Comm(0, 1, 0, deterministic=deterministic)
+    try:
+        j = 6
+        K, M, N = 4 ** j, 16, 7
+        A = ti.walsh(K, M, scale=2.0 ** -j)
+        if cplx:
+            A = 1j * A
+        B0 = ti.matrix(K, N, "B", complex_=cplx, mode="int")
+        dA, dB = torch.from_numpy(A).cuda(), torch.from_numpy(B0).cuda()
+        C = tsm.cgs_step(dA, dB, comm=comm)
+        torch.cuda.synchronize()
+        Cref, _ = oracle.tsmttsm(A, B0, conj=cplx)
+        assert np.array_equal(C.cpu().numpy(), Cref)
+        assert np.array_equal(dB.cpu().numpy(), oracle.tsmm_update(A, Cref, B0, -1, 1)[0])
+        # an empty local shard: C = sum of nothing = 0, B untouched
+        e = torch.zeros((0, N), dtype=dB.dtype, device="cuda")
+        C0 = tsm.cgs_step(dA[:0], e, comm=comm)
+        torch.cuda.synchronize()
+        assert np.all(C0.cpu().numpy() == 0)
+    finally:
+        comm.close()
