@@ -332,9 +332,8 @@ static tsm_status validate_config_real(const KernelEntry& e) {
       return bad("kernel 2 needs 16-byte rows of >= 128 bytes (M*S, N*S even and >= 16)");
     if (e.R % 8 || e.R > 256) return bad("kernel 2 needs rows_per_chunk a multiple of 8, <= 256");
     const int ed = edge_warps(e.edge);
-    const int pr = e.edge & 2;  // pair mode: 8x8 blocks in whole 16-wide pairs
-    const int MB = ed ? e.M / 8 : pr ? 2 * ((e.M + 15) / 16) : (e.M + 7) / 8;
-    const int NB = ed ? e.N / 8 : pr ? 2 * ((e.N + 15) / 16) : (e.N + 7) / 8;
+    const int MB = ed ? e.M / 8 : (e.M + 7) / 8;  // (pair mode: an odd last block loads single)
+    const int NB = ed ? e.N / 8 : (e.N + 7) / 8;
     if (e.p0 < 1 || e.p1 < 1 || e.p0 > MB || e.p1 > NB) return bad("WM, WN must be in [1, ceil(M/8)], [1, ceil(N/8)]");
     const int WT = ((MB + e.p0 - 1) / e.p0) * ((NB + e.p1 - 1) / e.p1);
     const int NW = e.NT / 32 - 1 - ed;
@@ -342,9 +341,8 @@ static tsm_status validate_config_real(const KernelEntry& e) {
     if (e.R % (4 * (NW / WT))) return bad("rows_per_chunk must be a multiple of 4 * row slots");
   } else if (e.op == KIND_TSMTTSM && e.impl == 1) {
     const int ed = edge_warps(e.edge);
-    const int pr = e.edge & 2;  // pair mode: 8x8 blocks in whole 16-wide pairs
-    const int MB = ed ? e.M / 8 : pr ? 2 * ((e.M + 15) / 16) : (e.M + 7) / 8;
-    const int NB = ed ? e.N / 8 : pr ? 2 * ((e.N + 15) / 16) : (e.N + 7) / 8;
+    const int MB = ed ? e.M / 8 : (e.M + 7) / 8;  // (pair mode: an odd last block loads single)
+    const int NB = ed ? e.N / 8 : (e.N + 7) / 8;
     if (e.p0 < 1 || e.p1 < 1 || e.p0 > MB || e.p1 > NB) return bad("WM, WN must be in [1, ceil(M/8)], [1, ceil(N/8)]");
     const int WT = ((MB + e.p0 - 1) / e.p0) * ((NB + e.p1 - 1) / e.p1);
     const int NW = e.NT / 32 - 1 - ed;

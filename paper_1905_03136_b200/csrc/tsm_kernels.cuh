@@ -594,8 +594,10 @@ struct TsmttsmMmaCfg {
   static_assert(!TMA || R % 8 == 0, "TMA swizzle atoms are 8 rows");
   static constexpr int MC = EDGE ? (M / 8) * 8 : M, NC = EDGE ? (N / 8) * 8 : N;  // DMMA core
   // 8x8 blocks of the core (pair mode: whole 16-wide pairs)
-  static constexpr int MB = PAIR ? 2 * ((MC + 15) / 16) : (MC + 7) / 8;
-  static constexpr int NB = PAIR ? 2 * ((NC + 15) / 16) : (NC + 7) / 8;
+  // 8x8 blocks of the core.  Pair mode pairs blocks (2p, 2p+1) over the
+  // 16-wide band [16p, 16p+16); an odd last block (MB odd) is loaded single.
+  static constexpr int MB = (MC + 7) / 8;
+  static constexpr int NB = (NC + 7) / 8;
   static constexpr int E = M * N - MC * NC;                    // edge cells (DFMA warp)
   static constexpr int TE = (E + 31) / 32;                     // edge cells per lane
   static constexpr int NE = EDGE_;                             // edge warps (split the rows)
@@ -714,6 +716,15 @@ __global__ void __launch_bounds__(Cfg::NT) tsmttsm_mma_kernel(const __grid_const
             v.x = sB[off(kr, n, bp)];
           b[2 * jp] = v.x;
           b[2 * jp + 1] = v.y;
+        }
+        // odd tile: its last block (the globally last, MB odd) is contiguous, loaded single
+        if constexpr (CM % 2) {
+          const int m = (wm * WM + CM - 1) * 8 + g;
+          a[CM - 1] = (rv && m < M) ? sA[off(kr, m, ap)] : 0.0;
+        }
+        if constexpr (CN % 2) {
+          const int n = (wn * WN + CN - 1) * 8 + g;
+          b[CN - 1] = (rv && n < N) ? sB[off(kr, n, bp)] : 0.0;
         }
       } else {
 #pragma unroll
@@ -907,14 +918,16 @@ __global__ void __launch_bounds__(Cfg::NT) tsmttsm_mma_kernel(const __grid_const
     if (warp < NW && slot == sl) {
 #pragma unroll
       for (int i = 0; i < WM; i++) {
-        // pair mode: blocks 2p / 2p+1 hold the even / odd rows of a 16-row band
-        const int m = Cfg::PAIR ? (wm * WM + (i & ~1)) * 8 + 2 * g + (i & 1) : (wm * WM + i) * 8 + g;
+        // pair mode: blocks 2p / 2p+1 hold the even / odd m of band 16p; the odd last block is contiguous
+        const bool msingle = !Cfg::PAIR || ((MB & 1) && wm * WM + i == MB - 1);
+        const int m = msingle ? (wm * WM + i) * 8 + g : (wm * WM + (i & ~1)) * 8 + 2 * g + (i & 1);
 #pragma unroll
         for (int j = 0; j < WN; j++) {
 #pragma unroll
           for (int e = 0; e < 2; e++) {
-            const int n = Cfg::PAIR ? (wn * WN + (j & ~1)) * 8 + 2 * (2 * q + e) + (j & 1)
-                                    : (wn * WN + j) * 8 + 2 * q + e;
+            const bool nsingle = !Cfg::PAIR || ((NB & 1) && wn * WN + j == NB - 1);
+            const int n = nsingle ? (wn * WN + j) * 8 + 2 * q + e
+                                  : (wn * WN + (j & ~1)) * 8 + 2 * (2 * q + e) + (j & 1);
             if (m < M && n < N && (wm * WM + i) < MB && (wn * WN + j) < NB) {
 #pragma unroll
               for (int z = 0; z < S; z++) {

@@ -121,7 +121,7 @@ def test_dmma_edge_warp(tsm, M, N, cplx):
         assert np.array_equal(got.cpu().numpy(), oracle.tsmttsm(Ai, Bi)[0])
 
 
-@pytest.mark.parametrize("M,N", [(64, 64), (48, 16), (40, 40), (34, 18), (16, 16), (62, 50), (20, 64)])
+@pytest.mark.parametrize("M,N", [(64, 64), (48, 16), (40, 40), (34, 18), (16, 16), (62, 50), (20, 64), (56, 56), (56, 24)])
 def test_dmma_pair_loads(tsm, M, N):
     """Real DMMA TSMTTSM with paired 16-byte fragment loads (kernel | 32):
     bulk-copy (padded conflict-free strides) and TMA (swizzle-aware k-row remap)

@@ -181,13 +181,13 @@ def pair_candidates(M: int, N: int, z: bool) -> list:
     fragment load instructions per DMMA.  Needs even WM, WN."""
     if z or M < 16 or N < 16:
         return []
-    MB, NB = 2 * cdiv(M, 16), 2 * cdiv(N, 16)
+    MB, NB = cdiv(M, 8), cdiv(N, 8)  # an odd last block is loaded single
     wt = []
     for WM in range(2, min(MB, 8) + 1, 2):
         for WN in range(2, min(NB, 8) + 1, 2):
             if WM * WN > 16 or cdiv(MB, WM) * cdiv(NB, WN) > 16:
                 continue
-            bal = cdiv(MB, WM) * WM * cdiv(NB, WN) * WN * 64 / (M * N)
+            bal = cdiv(MB, WM) * WM * cdiv(NB, WN) * WN / (MB * NB)
             wt.append((bal * (1 + 0.5 * (WM + WN) / (WM * WN)), WM, WN))
     wt.sort()
     out = []
