@@ -1,0 +1,5 @@
+# r24: validate pair-odd / impl-4 rho; full fresh retune on the current kernel source (no keep-better)
+timeout 1200 python -m pytest tests/test_kernels_gpu.py -m gpu -q -x -k "pair or edge_columns or family or complex_as_real" > gpurun_out/pytest_gpu24.log 2>&1; echo pytest rc=$?; tail -n 3 gpurun_out/pytest_gpu24.log
+timeout 4000 python tools/autotune.py --ops tsmttsm,tsmm --dtypes d,z --widths 1-64 --time-budget 3700 > gpurun_out/autotune24.log 2>&1; echo autotune rc=$?
+timeout 900 python tools/autotune.py --ops tsmttsm,tsmm --dtypes d,z --shapes 1x64,64x1,16x48,48x16,1x2,2x1,3x5,5x3,7x2,13x29,29x13,33x17,17x33,5x64,64x5,1x7,9x1,63x64,64x63 --time-budget 800 > gpurun_out/autotune24n.log 2>&1; echo autotune-n rc=$?
+cp tune/b200.json gpurun_out/b200_r24.json
