@@ -274,7 +274,6 @@ static tsm_status validate_config_real(const KernelEntry& e) {
     if (e.p0 % 2 || e.p1 % 2) return bad("the pair flag needs even WM and WN");
     if (e.impl == 1 && (e.p2 % 2 || e.p3 % 2 || e.M % 2 || e.N % 2))
       return bad("the pair flag needs even smem strides (and even M, N for kernel 1)");
-    if (e.edge & 1) return bad("the pair and edge flags are exclusive");
   }
   if ((e.edge & 1) && e.op == KIND_TSMM) {  // C-stationary TSMM: DFMA edge columns
     const int S = e.dt == TSM_Z ? 2 : 1;

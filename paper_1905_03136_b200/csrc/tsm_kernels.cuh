@@ -585,7 +585,7 @@ struct TsmttsmMmaCfg {
   static constexpr int M = M_, N = N_, WM = WM_, WN = WN_, NW = NW_, R = R_;
   static constexpr bool Z = Z_, TMA = TMA_, EDGE = EDGE_ > 0, PAIR = PAIR_, ZR = ZR_;
   static_assert(!ZR || (!Z_ && M_ % 2 == 0 && N_ % 2 == 0), "complex-as-real: real kernel on 2M x 2N");
-  static_assert(!PAIR || (!Z_ && !EDGE_ && WM_ % 2 == 0 && WN_ % 2 == 0), "pairs: real, even tiles, no edge");
+  static_assert(!PAIR || (!Z_ && WM_ % 2 == 0 && WN_ % 2 == 0), "pairs: real, even tiles");
   static constexpr int S = Z ? 2 : 1;
   static constexpr int NBA = (M * S + 15) / 16, NBB = (N * S + 15) / 16;  // 16-double boxes
   static constexpr int AP = TMA ? NBA * 16 / S : AP_, BP = TMA ? NBB * 16 / S : BP_;

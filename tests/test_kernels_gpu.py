@@ -93,7 +93,7 @@ def test_cstationary_int_bitwise(tsm, cplx):
 
 
 @pytest.mark.parametrize("cplx", [False, True], ids=["D", "Z"])
-@pytest.mark.parametrize("M,N", [(49, 49), (33, 17), (17, 33), (57, 58), (9, 10)])
+@pytest.mark.parametrize("M,N", [(49, 49), (33, 17), (17, 33), (57, 58), (9, 10), (50, 50), (42, 34)])
 def test_dmma_edge_warp(tsm, M, N, cplx):
     """DMMA core + DFMA edge warps (kernel | 16, warp count in bits 6-7): every edge candidate family."""
     dt = "z" if cplx else "d"
@@ -101,8 +101,8 @@ def test_dmma_edge_warp(tsm, M, N, cplx):
     assert cands
     picked = {}
     for c in cands:
-        picked.setdefault((c["impl"], c["EDGE"]), c)  # 1, 2, 4 edge warps
-    for (impl, _), c in picked.items():
+        picked.setdefault((c["impl"], c["EDGE"], c.get("PAIR", 0)), c)  # 1, 2, 4 edge warps; paired core
+    for (impl, _, _), c in picked.items():
         plan = tsm.Plan("tsmttsm", dt, M, N, 0, config=gi.to_tsm_config("tsmttsm", c, 3, 2))
         assert plan.config()["kernel"] == impl | (gi.flags(c) << 4)
         assert "edge" in plan.describe(1000)["kernel"]

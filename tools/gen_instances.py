@@ -162,6 +162,23 @@ def edge_candidates(M: int, N: int, z: bool) -> list:
                         Rt = min(256 // step * step, max(step, (tgt // tb) // step * step))
                         out.append(dict(MT=WM, NTL=WN, NT=(NW + ne + 1) * 32, R=Rt, impl=2, AP=M, BP=N,
                                         EDGE=ne))
+    # paired core fragments (TMA) + edge warps: the best even warp tiles
+    if not z and tma_ok(M, N, z):
+        tb = (cdiv(M, 16) + cdiv(N, 16)) * 128
+        for (_, WM, WN) in [t for t in wt if t[1] % 2 == 0 and t[2] % 2 == 0][:2]:
+            WT = cdiv(MB, WM) * cdiv(NB, WN)
+            for k in (1, 2, 4):
+                NW = WT * k
+                if NW > 16 or NW < 2:
+                    continue
+                for ne in (1, 2, 4):
+                    if NW + ne + 1 > 32:
+                        continue
+                    for tgt in (16384, 32768):
+                        step = 4 * k if (4 * k) % 8 == 0 else 8 * k
+                        Rt = min(256 // step * step, max(step, (tgt // tb) // step * step))
+                        out.append(dict(MT=WM, NTL=WN, NT=(NW + ne + 1) * 32, R=Rt, impl=2, AP=M, BP=N,
+                                        EDGE=ne, PAIR=1))
     return out
 
 
