@@ -1,6 +1,7 @@
 # r25: tune pair+edge / remaining candidates for the padding widths; full tests on the final source; bench; sweeps; ncu
 timeout 900 python -m pytest tests/test_kernels_gpu.py -m gpu -q -x -k "edge_warp or pair" > gpurun_out/pytest_gpu25a.log 2>&1; echo pytest-a rc=$?; tail -n 2 gpurun_out/pytest_gpu25a.log
 timeout 1500 python tools/autotune.py --ops tsmttsm --dtypes d --widths 33,34,35,41,42,43,49,50,51,57,58,59 --keep-better --time-budget 1300 > gpurun_out/autotune25.log 2>&1; echo autotune rc=$?
+timeout 1500 python tools/autotune.py --ops tsmttsm --dtypes z --widths 17-39 --filter "c.get('ZR') and c.get('EDGE')" --keep-better --time-budget 1300 > gpurun_out/autotune25z.log 2>&1; echo autotune-z rc=$?
 cp tune/b200.json gpurun_out/b200_r25.json
 python tools/gen_instances.py > /dev/null && python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build25.log 2>&1; echo build rc=$?
 timeout 2400 python -m pytest tests -m gpu -q -x > gpurun_out/pytest_gpu25.log 2>&1; echo pytest rc=$?; tail -n 3 gpurun_out/pytest_gpu25.log
