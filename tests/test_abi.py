@@ -10,6 +10,7 @@ import json
 import os
 import re
 import subprocess
+import sys
 
 import numpy as np
 import pytest
@@ -135,3 +136,28 @@ def test_generator_consistency_host():
     assert np.array_equal(ti.rows(np.array([0, 17, 49]), 7, "A"), A[[0, 17, 49]])
     Z = ti.matrix(20, 3, "B", complex_=True, mode="int")
     assert np.array_equal(ti.column(20, 3, 2, "B", complex_=True, mode="int"), Z[:, 2])
+
+
+def test_jit_precompile_without_device(tmp_path):
+    """tsm_jit_precompile (build tooling) compiles a kernel with NVRTC into the
+    cache without a GPU; bad shapes / configs are rejected (fresh process so
+    TSM_JIT_CACHE_DIR applies)."""
+    code = r'''
+import ctypes, os, sys
+from paper_1905_03136_b200 import binding as tsm
+f = tsm.lib.tsm_jit_precompile
+assert f(0, 0, 24, 24, None, 0) == 0, tsm.lib.tsm_last_error_detail()
+assert f(1, 1, 17, 17, None, 0) == 0
+assert f(0, 0, 65, 1, None, 0) == 1          # M out of range
+assert f(0, 0, 33, 33, None, 2) == 2         # no TMA kernel for odd D widths
+cfg = tsm.TsmConfig(threads=288, rows_per_chunk=30, p0=1, p1=1, p2=0, stages=3, ctas_per_sm=1, kernel=0, p3=0)
+assert f(0, 0, 8, 8, ctypes.byref(cfg), 0) == 0
+bad = tsm.TsmConfig(threads=100, rows_per_chunk=30, p0=1, p1=1, p2=0, stages=3, ctas_per_sm=1, kernel=0, p3=0)
+assert f(0, 0, 8, 8, ctypes.byref(bad), 0) == 1
+print("ok")
+'''
+    env = dict(os.environ, TSM_JIT_CACHE_DIR=str(tmp_path))
+    r = subprocess.run([sys.executable, "-c", code], env=env, cwd=ROOT, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
+    cubins = [p for p in tmp_path.rglob("*.cubin")]
+    assert len(cubins) >= 3
