@@ -134,6 +134,16 @@ __device__ __forceinline__ void zfma(double& re, double& im, double ar, double a
 // Position in the smem ring: stage index s, mbarrier phase parity ph of that
 // stage's current use, and how many times the ring wrapped (incremental, so
 // the hot loops carry no integer division by the run-time stage count).
+// Spread the warps of one tile (or column group) over the 4 SM sub-partitions.
+// Warp w runs on SMSP w % 4; with the plain order tile = w % T, T a multiple of
+// 4 puts every warp of a tile on one SMSP, so a partial tile leaves that SMSP's
+// tensor pipe half idle (ncu r23: D 56, tiles of 14/14/14/7 DMMAs, 82 % pipe).
+// Ordering the (slot, tile) pairs by L(w) = (w % 4) * (nw / 4) + w / 4 gives each
+// SMSP consecutive pairs, i.e. all tiles.  A bijection on [0, nw) for nw % 4 == 0.
+__device__ __forceinline__ int spread_warp(int w, int nw) {
+  return (nw % 4 == 0 && w < nw) ? (w % 4) * (nw / 4) + w / 4 : w;
+}
+
 // compile-time int as a value (dispatching generic lambdas on a constant)
 template <int V>
 struct IC {
@@ -660,8 +670,9 @@ __global__ void __launch_bounds__(Cfg::NT) tsmttsm_mma_kernel(const __grid_const
 #pragma unroll
       for (int z = 0; z < S; z++) acc[i][j][z][0] = acc[i][j][z][1] = 0.0;
 
-  const int slot = warp / WT;
-  const int wt = warp % WT;
+  const int wl = spread_warp(warp, NW);  // (slot, tile) of this consumer warp
+  const int slot = wl / WT;
+  const int wt = wl % WT;
   const int wm = wt % WTM, wn = wt / WTM;
 
   // offset (doubles) of element (row r, column x) of an operand of width W
@@ -1616,7 +1627,8 @@ __global__ void __launch_bounds__(Cfg::NT) tsmm_cst_kernel(const __grid_constant
     }
   } else {
     // ---------------- consumer warps ----------------
-    const int cg = warp % NG, rg = warp / NG;
+    const int wl = spread_warp(warp, NW);
+    const int cg = wl % NG, rg = wl / NG;
     const int nb0 = cg * NBW;  // first 8-column block of this warp
     // MMA row g of a block is A/B row rho(g) = bitrev3(g) ^ (g & 1) =
     // [0,5,2,7,1,4,3,6]: under the 128B swizzle the A fragment loads (D: 16
@@ -1893,7 +1905,8 @@ __global__ void __launch_bounds__(Cfg::NT) tsmm_cstb_kernel(const __grid_constan
     }
   } else {
     // ---------------- consumer warps ----------------
-    const int cg = warp % NG, rg = warp / NG;
+    const int wl = spread_warp(warp, NW);
+    const int cg = wl % NG, rg = wl / NG;
     const int nb0 = cg * NBW;
     const bool issuer = (cg == 0 && lane == 0);
     const int rho = cstb_rho(Cfg::RHO, g);  // MMA row g <-> stage row rho(g) (bank conflicts)
