@@ -287,8 +287,9 @@ static tsm_status validate_config_real(const KernelEntry& e) {
     if (e.M < 8 || e.N < 8 || (e.M % 8 == 0 && e.N % 8 == 0))
       return bad("edge mode needs M, N >= 8 and a width that is not a multiple of 8");
     const int S = e.dt == TSM_Z ? 2 : 1;
-    const int E = e.M * e.N - (e.M / 8) * 8 * (e.N / 8) * 8;
-    if ((E + 31) / 32 * S > 32) return bad("edge too large for one DFMA warp (<= 32 cells per lane)");
+    const int MC = (e.M / 8) * 8, NC = (e.N / 8) * 8;  // edge strips: accumulators per lane
+    const int eregs = ((e.M - MC) * ((e.N + 31) / 32) + ((MC + 31) / 32) * (e.N - NC)) * S;
+    if (eregs > 64) return bad("edge strips too large for the DFMA edge warps (> 64 accumulators per lane)");
   } else if (e.edge & 12) {
     return bad("edge warp count bits (kernel bits 6-7) need the edge flag (kernel | 16)");
   }

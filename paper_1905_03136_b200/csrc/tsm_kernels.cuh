@@ -608,8 +608,12 @@ struct TsmttsmMmaCfg {
   // 16-wide band [16p, 16p+16); an odd last block (MB odd) is loaded single.
   static constexpr int MB = (MC + 7) / 8;
   static constexpr int NB = (NC + 7) / 8;
-  static constexpr int E = M * N - MC * NC;                    // edge cells (DFMA warp)
-  static constexpr int TE = (E + 31) / 32;                     // edge cells per lane
+  static constexpr int E = M * N - MC * NC;                    // edge cells (DFMA warps)
+  // edge strips as outer products: rows m in [MC, M) x all n (lanes over n),
+  // columns n in [NC, N) x m < MC (lanes over m)
+  static constexpr int MR = M - MC, NR = N - NC;
+  static constexpr int UN = (N + 31) / 32, UM = (MC + 31) / 32;
+  static constexpr int EREGS = (MR * UN + UM * NR) * S;        // accumulator doubles per lane
   static constexpr int NE = EDGE_;                             // edge warps (split the rows)
   static_assert(NE >= 0 && NE <= 4, "0..4 edge warps");
   static_assert(!EDGE || (MB >= 1 && NB >= 1 && E > 0), "edge mode needs a core and an edge");
@@ -782,43 +786,79 @@ __global__ void __launch_bounds__(Cfg::NT) tsmttsm_mma_kernel(const __grid_const
     }
   };
 
-  // edge cells (EDGE mode): lane owns cells e = lane + 32 t of the strip
-  // {m >= MC} x [0, N)  followed by  [0, MC) x {n >= NC}
-  constexpr int TE = Cfg::EDGE ? Cfg::TE : 1;
-  double eacc[TE][S];
-  int em[TE], en[TE];
+  // edge cells (EDGE mode) as two outer-product strips: the row strip
+  // m in [MC, M) x n in [0, N) with lanes over n (B values loaded once per row,
+  // A[k][m] broadcast), and the column strip m in [0, MC) x n in [NC, N) with
+  // lanes over m (A loaded once, B[k][n] broadcast).  Per row and lane:
+  // ceil(N/32) + ceil(MC/32) loads + MR + NR broadcasts for the
+  // MR*ceil(N/32) + ceil(MC/32)*NR DFMA (or complex) updates.
+  constexpr int MR = Cfg::MR, NR = Cfg::NR, UN = Cfg::UN, UM = Cfg::UM;
+  constexpr int MRA = MR > 0 ? MR : 1, NRA = NR > 0 ? NR : 1;
+  double er[Cfg::EDGE ? MRA : 1][Cfg::EDGE ? UN : 1][S];  // row strip (MC + mi, lane + 32u)
+  double ec[Cfg::EDGE ? UM : 1][Cfg::EDGE ? NRA : 1][S];  // column strip (lane + 32u, NC + ni)
   if constexpr (Cfg::EDGE) {
-    constexpr int MR = M - Cfg::MC, NR = (N - Cfg::NC) > 0 ? (N - Cfg::NC) : 1;
 #pragma unroll
-    for (int t = 0; t < TE; t++) {
-      const int e = lane + 32 * t;
-      if (e < MR * N) {
-        em[t] = Cfg::MC + e / N;
-        en[t] = e % N;
-      } else {
-        const int e2 = e - MR * N;
-        em[t] = e2 / NR;
-        en[t] = Cfg::NC + e2 % NR;
-      }
-      if (e >= Cfg::E) em[t] = -1;  // no cell
+    for (int i = 0; i < MRA; i++)
 #pragma unroll
-      for (int z = 0; z < S; z++) eacc[t][z] = 0.0;
-    }
+      for (int u = 0; u < UN; u++)
+#pragma unroll
+        for (int z = 0; z < S; z++) er[i][u][z] = 0.0;
+#pragma unroll
+    for (int u = 0; u < UM; u++)
+#pragma unroll
+      for (int i = 0; i < NRA; i++)
+#pragma unroll
+        for (int z = 0; z < S; z++) ec[u][i][z] = 0.0;
   }
-  // DFMA over rows [0, rows) of a stage (or of global memory: the odd tail row)
+  // DFMA over rows [r_begin, rows) step NE of a stage (or of global memory: the odd tail row)
   auto edge_rows = [&](const double* __restrict__ sA, const double* __restrict__ sB, int r_begin, int rows,
                        int ap, int bp) {
 #pragma unroll 2
     for (int r = r_begin; r < rows; r += Cfg::NE) {
+      if constexpr (MR > 0) {
+        double bv[UN][S];
 #pragma unroll
-      for (int t = 0; t < TE; t++) {
-        if (em[t] < 0) continue;
-        if constexpr (!Cfg::Z) {
-          eacc[t][0] = fma(sA[off(r, em[t], ap)], sB[off(r, en[t], bp)], eacc[t][0]);
-        } else {
-          const double2 a = *reinterpret_cast<const double2*>(sA + off(r, em[t], ap));
-          const double2 b = *reinterpret_cast<const double2*>(sB + off(r, en[t], bp));
-          zfma(eacc[t][0], eacc[t][1], a.x, flip_sign(a.y, p.conj), b.x, b.y);
+        for (int u = 0; u < UN; u++) {
+          const int n = lane + 32 * u;
+#pragma unroll
+          for (int z = 0; z < S; z++) bv[u][z] = (n < N) ? sB[off(r, n, bp) + z] : 0.0;
+        }
+#pragma unroll
+        for (int i = 0; i < MR; i++) {
+          const int m = Cfg::MC + i;
+          if constexpr (!Cfg::Z) {
+            const double a = sA[off(r, m, ap)];
+#pragma unroll
+            for (int u = 0; u < UN; u++) er[i][u][0] = fma(a, bv[u][0], er[i][u][0]);
+          } else {
+            const double2 a = *reinterpret_cast<const double2*>(sA + off(r, m, ap));
+            const double ai = flip_sign(a.y, p.conj);
+#pragma unroll
+            for (int u = 0; u < UN; u++) zfma(er[i][u][0], er[i][u][1], a.x, ai, bv[u][0], bv[u][1]);
+          }
+        }
+      }
+      if constexpr (NR > 0) {
+        double av[UM][S];
+#pragma unroll
+        for (int u = 0; u < UM; u++) {
+          const int m = lane + 32 * u;
+#pragma unroll
+          for (int z = 0; z < S; z++) av[u][z] = (m < Cfg::MC) ? sA[off(r, m, ap) + z] : 0.0;
+        }
+#pragma unroll
+        for (int i = 0; i < NR; i++) {
+          const int n = Cfg::NC + i;
+          if constexpr (!Cfg::Z) {
+            const double b = sB[off(r, n, bp)];
+#pragma unroll
+            for (int u = 0; u < UM; u++) ec[u][i][0] = fma(av[u][0], b, ec[u][i][0]);
+          } else {
+            const double2 b = *reinterpret_cast<const double2*>(sB + off(r, n, bp));
+#pragma unroll
+            for (int u = 0; u < UM; u++)
+              zfma(ec[u][i][0], ec[u][i][1], av[u][0], flip_sign(av[u][1], p.conj), b.x, b.y);
+          }
         }
       }
     }
@@ -952,15 +992,27 @@ __global__ void __launch_bounds__(Cfg::NT) tsmttsm_mma_kernel(const __grid_const
     }
     if constexpr (Cfg::EDGE) {  // edge cells are disjoint from the core; edge warps in order
       if (warp == NW + sl && sl < Cfg::NE) {
+        auto put = [&](int m, int n, const double* v) {
 #pragma unroll
-        for (int t = 0; t < TE; t++)
-          if (em[t] >= 0) {
-#pragma unroll
-            for (int z = 0; z < S; z++) {
-              const int idx = (em[t] * N + en[t]) * S + z;
-              sP[idx] = (sl == 0) ? eacc[t][z] : sP[idx] + eacc[t][z];
-            }
+          for (int z = 0; z < S; z++) {
+            const int idx = (m * N + n) * S + z;
+            sP[idx] = (sl == 0) ? v[z] : sP[idx] + v[z];
           }
+        };
+        if constexpr (MR > 0) {
+#pragma unroll
+          for (int i = 0; i < MR; i++)
+#pragma unroll
+            for (int u = 0; u < UN; u++)
+              if (lane + 32 * u < N) put(Cfg::MC + i, lane + 32 * u, er[i][u]);
+        }
+        if constexpr (NR > 0) {
+#pragma unroll
+          for (int u = 0; u < UM; u++)
+#pragma unroll
+            for (int i = 0; i < NR; i++)
+              if (lane + 32 * u < Cfg::MC) put(lane + 32 * u, Cfg::NC + i, ec[u][i]);
+        }
       }
     }
     __syncthreads();

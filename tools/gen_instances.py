@@ -125,11 +125,11 @@ def tsmttsm_mma_default(M: int, N: int, z: bool) -> dict:
 def edge_candidates(M: int, N: int, z: bool) -> list:
     """DMMA on the 8-aligned core + one DFMA edge warp (EDGE=1), for widths
     just above a multiple of 8 (M % 8 or N % 8 in 1..3)."""
-    if M < 8 or N < 8 or (M % 8 not in (1, 2, 3) and N % 8 not in (1, 2, 3)):
+    if M < 8 or N < 8 or (M % 8 not in (1, 2, 3, 4) and N % 8 not in (1, 2, 3, 4)):
         return []
     S = 2 if z else 1
-    E = M * N - (M // 8) * 8 * (N // 8) * 8
-    if cdiv(E, 32) * S > 32:
+    MC, NC = (M // 8) * 8, (N // 8) * 8
+    if ((M - MC) * cdiv(N, 32) + cdiv(MC, 32) * (N - NC)) * S > 64:  # edge-strip accumulators per lane
         return []
     MB, NB = M // 8, N // 8
     wmax = 8 if z else 16
