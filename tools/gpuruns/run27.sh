@@ -2,6 +2,7 @@
 timeout 2400 python -m pytest tests -m gpu -q -x > gpurun_out/pytest_gpu27.log 2>&1; echo pytest rc=$?; tail -n 3 gpurun_out/pytest_gpu27.log
 timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke27.log 2>&1; echo smoke rc=$?; tail -n 3 gpurun_out/smoke27.log
 timeout 900 python bench.py --steps 5 --warmup 3 --report gpurun_out/bench_report27.json > gpurun_out/bench27.log 2>&1; echo bench rc=$?; tail -c 300 gpurun_out/bench27.log
+timeout 600 python bench.py --steps 2 --warmup 3 --force-comm --no-e2e --no-cpu > gpurun_out/bench27_comm.log 2>&1; echo bench-comm rc=$?; tail -c 200 gpurun_out/bench27_comm.log
 W=$(python -c "print(','.join(str(i) for i in range(1,65)))")
 timeout 900 python tools/quick_time.py --ops tsmttsm,tsmm --dtypes d,z --widths $W --reps 3 --json gpurun_out/sweep27_square.json > gpurun_out/sweep27_square.log 2>&1; echo sq rc=$?
 timeout 600 python tools/quick_time.py --ops tsmttsm,tsmm --dtypes d,z --shapes 1x64,64x1,16x48 --K 33554432 --reps 3 --json gpurun_out/sweep27_nonsq.json > gpurun_out/sweep27_nonsq.log 2>&1; echo nonsq rc=$?
