@@ -132,7 +132,13 @@ typedef struct tsm_config {
                    32  paired 16-byte fragment loads (D, even p0/p1);
                    256 complex-as-real (Z; TSMTTSM 1/2, TSMM 3): the real kernel runs
                        on the interleaved (re, im) view -- A, B as real K x 2M, K x 2N --
-                       and p0..p3, threads, rows refer to that 2M x 2N real problem.
+                       and p0..p3, threads, rows refer to that 2M x 2N real problem;
+                   512 3M / Gauss complex products (Z; TSMTTSM 1/2, not with 256):
+                       T1 = Ar^T Br, T2 = Ai^T Bi, T3 = (Ar+Ai)^T (Br+Bi) on the
+                       tensor pipe, C = (T1 - T2) + i (T3 - T1 - T2) -- 3 real
+                       DMMAs per 8x8 block instead of 4 (same bytes, 3/4 of the
+                       FP64 work; error within the |A|^T|B| tolerance, exact
+                       on integer-valued inputs).
                  Invalid combinations return TSM_ERR_INVALID_VALUE. */
   int p3;
 } tsm_config;

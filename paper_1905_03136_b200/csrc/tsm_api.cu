@@ -257,6 +257,17 @@ static tsm_status validate_config(const KernelEntry& ein) {
     if (!((ein.op == KIND_TSMTTSM && (ein.impl == 1 || ein.impl == 2)) || (ein.op == KIND_TSMM && ein.impl == 3)))
       return bad("complex-as-real applies to DMMA TSMTTSM kernels 1, 2 and TSMM kernel 3");
   }
+  if (g3_flag(ein.edge)) {  // 3M (Gauss) complex products
+    if (ein.dt != TSM_Z) return bad("the 3M flag (kernel | 512) needs dtype Z");
+    if (zr_flag(ein.edge)) return bad("the 3M flag (kernel | 512) excludes complex-as-real (kernel | 256)");
+    if (!((ein.op == KIND_TSMTTSM && (ein.impl == 1 || ein.impl == 2)) || (ein.op == KIND_TSMM && ein.impl == 3)))
+      return bad("the 3M flag (kernel | 512) applies to the DMMA TSMTTSM kernels 1, 2 and TSMM kernel 3");
+    if (ein.op == KIND_TSMM) {
+      const int NB = (ein.N - ((ein.edge & 1) ? ein.N % 8 : 0) + 7) / 8;
+      if (((ein.M + 3) / 4) * std::min(ein.p0, NB) * 3 > 64)
+        return bad("3M C slice too large for registers (MK * NBW * 3 > 64)");
+    }
+  }
   return validate_config_real(real_view(ein));
 }
 
@@ -463,7 +474,7 @@ tsm_status tsm_plan_create_config(tsm_plan* out, tsm_op op, tsm_dtype dtype, int
   e.p0 = cfg->p0;
   e.p1 = cfg->p1;
   e.impl = cfg->kernel & 15;
-  e.edge = (cfg->kernel >> 4) & 31;
+  e.edge = (cfg->kernel >> 4) & 63;
   e.p2 = (op == TSM_OP_TSMTTSM && e.impl == 0) ? 0 : cfg->p2;
   e.p3 = (op == TSM_OP_TSMTTSM && e.impl >= 1) ? cfg->p3 : 0;
   e.stages = cfg->stages;
@@ -520,7 +531,7 @@ tsm_status tsm_jit_precompile(tsm_op op, tsm_dtype dtype, int M, int N, const ts
     e.p0 = cfg->p0;
     e.p1 = cfg->p1;
     e.impl = cfg->kernel & 15;
-    e.edge = (cfg->kernel >> 4) & 31;
+    e.edge = (cfg->kernel >> 4) & 63;
     e.p2 = (op == TSM_OP_TSMTTSM && e.impl == 0) ? 0 : cfg->p2;
     e.p3 = (op == TSM_OP_TSMTTSM && e.impl >= 1) ? cfg->p3 : 0;
     e.stages = cfg->stages;
@@ -811,6 +822,7 @@ tsm_status tsm_plan_describe(tsm_plan p, int64_t K, char* buf, size_t len) {
   }
   if (p->op == TSM_OP_TSMM && (k->edge & 1)) kname += "+dfma-edge-columns";
   if (zr_flag(k->edge)) kname += "+complex-as-real(2Mx2N)";
+  if (g3_flag(k->edge)) kname += "+3m";
   if (p->op == TSM_OP_TSMTTSM && k->impl >= 1)
     snprintf(tmp, sizeof tmp,
              "{\"op\":\"tsmttsm\",\"dtype\":\"%c\",\"M\":%d,\"N\":%d,\"WM\":%d,\"WN\":%d,"

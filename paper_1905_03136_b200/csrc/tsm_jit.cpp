@@ -47,7 +47,7 @@ std::string cfg_type(const KernelEntry& ein) {
     os << "tsm::TsmttsmMmaCfg<" << e.M << ", " << e.N << ", " << z << ", " << e.p0 << ", " << e.p1
        << ", " << (e.NT / 32 - 1 - edge_warps(e.edge)) << ", " << e.R << ", " << e.p2 << ", " << e.p3 << ", "
        << (e.impl == 2 ? "true" : "false") << ", " << edge_warps(e.edge) << ", "
-       << ((e.edge & 2) ? "true" : "false") << ", " << zr << ">";
+       << ((e.edge & 2) ? "true" : "false") << ", " << zr << ", " << (g3_flag(e.edge) ? "true" : "false") << ">";
   else if (e.op == KIND_TSMTTSM)
     os << "tsm::TsmttsmCfg<" << e.M << ", " << e.N << ", " << z << ", " << e.p0 << ", " << e.p1
        << ", " << e.NT << ", " << e.R << ">";
@@ -56,7 +56,8 @@ std::string cfg_type(const KernelEntry& ein) {
        << ", " << (e.NT / 32 - 1) << ", " << e.R << ">";
   else if (e.impl == 3)
     os << "tsm::TsmmCstCfg<" << e.M << ", " << e.N << ", " << z << ", " << e.p0 << ", " << e.p1
-       << ", " << (e.NT / 32 - 1) << ", " << e.R << ", " << zr << ", " << ((e.edge & 1) ? e.N % 8 : 0) << ">";
+       << ", " << (e.NT / 32 - 1) << ", " << e.R << ", " << zr << ", " << ((e.edge & 1) ? e.N % 8 : 0) << ", "
+       << (g3_flag(e.edge) ? "true" : "false") << ">";
   else if (e.impl >= 1)
     os << "tsm::TsmmMmaCfg<" << e.M << ", " << e.N << ", " << z << ", " << e.p0 << ", "
        << (e.NT / 32 - 1) << ", " << e.R << ", " << e.p1 << ", " << e.p2 << ", "

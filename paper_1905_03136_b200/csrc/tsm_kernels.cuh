@@ -590,13 +590,15 @@ constexpr int pick_kdist(int ap, int bp, bool z, bool pair, int r) {
 // one 16-byte LDS.128 per lane feeds both fragments (half the load
 // instructions of one LDS.64 per fragment).
 template <int M_, int N_, bool Z_, int WM_, int WN_, int NW_, int R_, int AP_ = M_, int BP_ = N_,
-          bool TMA_ = false, int EDGE_ = 0, bool PAIR_ = false, bool ZR_ = false>
+          bool TMA_ = false, int EDGE_ = 0, bool PAIR_ = false, bool ZR_ = false, bool G3_ = false>
 struct TsmttsmMmaCfg {
   static constexpr int M = M_, N = N_, WM = WM_, WN = WN_, NW = NW_, R = R_;
-  static constexpr bool Z = Z_, TMA = TMA_, EDGE = EDGE_ > 0, PAIR = PAIR_, ZR = ZR_;
+  static constexpr bool Z = Z_, TMA = TMA_, EDGE = EDGE_ > 0, PAIR = PAIR_, ZR = ZR_, G3 = G3_;
+  static_assert(!G3 || Z_, "3M (Gauss) products: complex kernel");
   static_assert(!ZR || (!Z_ && M_ % 2 == 0 && N_ % 2 == 0), "complex-as-real: real kernel on 2M x 2N");
   static_assert(!PAIR || (!Z_ && WM_ % 2 == 0 && WN_ % 2 == 0), "pairs: real, even tiles");
   static constexpr int S = Z ? 2 : 1;
+  static constexpr int NA = G3 ? 3 : S;  // accumulator blocks per 8x8 block of C (3M: T1, T2, T3)
   static constexpr int NBA = (M * S + 15) / 16, NBB = (N * S + 15) / 16;  // 16-double boxes
   static constexpr int AP = TMA ? NBA * 16 / S : AP_, BP = TMA ? NBB * 16 / S : BP_;
   static_assert(!TMA || ((M * S) % 2 == 0 && (N * S) % 2 == 0 && M * S >= 16 && N * S >= 16),
@@ -665,14 +667,15 @@ __global__ void __launch_bounds__(Cfg::NT) tsmttsm_mma_kernel(const __grid_const
   }
   __syncthreads();
 
-  // accumulators: [WM][WN] blocks x 2 doubles (x re/im)
-  double acc[WM][WN][S][2];
+  // accumulators: [WM][WN] blocks x 2 doubles (x re/im; 3M: x T1, T2, T3)
+  constexpr int NA = Cfg::NA;
+  double acc[WM][WN][NA][2];
 #pragma unroll
   for (int i = 0; i < WM; i++)
 #pragma unroll
     for (int j = 0; j < WN; j++)
 #pragma unroll
-      for (int z = 0; z < S; z++) acc[i][j][z][0] = acc[i][j][z][1] = 0.0;
+      for (int z = 0; z < NA; z++) acc[i][j][z][0] = acc[i][j][z][1] = 0.0;
 
   const int wl = spread_warp(warp, NW);  // (slot, tile) of this consumer warp
   const int slot = wl / WT;
@@ -771,6 +774,28 @@ __global__ void __launch_bounds__(Cfg::NT) tsmttsm_mma_kernel(const __grid_const
         b[j] = (rv && n < N) ? *reinterpret_cast<const double2*>(sB + off(kr, n, bp))
                              : make_double2(0.0, 0.0);
       }
+      if constexpr (Cfg::G3) {
+        // 3M (Gauss) products: T1 += ar br, T2 += ai bi, T3 += (ar + ai)(br + bi);
+        // C = (T1 - T2) + i (T3 - T1 - T2) is formed once per block partial.
+        // 3 DMMAs per block instead of 4; the operand sums cost one DADD per
+        // fragment (exact for the integer-valued parity inputs).
+        double sa[WM], sb[WN];
+#pragma unroll
+        for (int i = 0; i < CM; i++) {
+          a[i].y = flip_sign(a[i].y, p.conj);  // A^H B (N2)
+          sa[i] = a[i].x + a[i].y;
+        }
+#pragma unroll
+        for (int j = 0; j < CN; j++) sb[j] = b[j].x + b[j].y;
+#pragma unroll
+        for (int i = 0; i < CM; i++)
+#pragma unroll
+          for (int j = 0; j < CN; j++) {
+            dmma(acc[i][j][0][0], acc[i][j][0][1], a[i].x, b[j].x);  // T1 += ar br
+            dmma(acc[i][j][1][0], acc[i][j][1][1], a[i].y, b[j].y);  // T2 += ai bi
+            dmma(acc[i][j][2][0], acc[i][j][2][1], sa[i], sb[j]);    // T3 += (ar+ai)(br+bi)
+          }
+      } else {
 #pragma unroll
       for (int i = 0; i < CM; i++) {
         a[i].y = flip_sign(a[i].y, p.conj);  // A^H B (N2)
@@ -782,6 +807,7 @@ __global__ void __launch_bounds__(Cfg::NT) tsmttsm_mma_kernel(const __grid_const
             dmma(acc[i][j][1][0], acc[i][j][1][1], a[i].x, b[j].y);  // im += ar bi
             dmma(acc[i][j][1][0], acc[i][j][1][1], a[i].y, b[j].x);  // im += ai br
           }
+      }
       }
     }
   };
@@ -980,10 +1006,18 @@ __global__ void __launch_bounds__(Cfg::NT) tsmttsm_mma_kernel(const __grid_const
             const int n = nsingle ? (wn * WN + j) * 8 + 2 * q + e
                                   : (wn * WN + (j & ~1)) * 8 + 2 * (2 * q + e) + (j & 1);
             if (m < M && n < N && (wm * WM + i) < MB && (wn * WN + j) < NB) {
+              double v[S];
+              if constexpr (Cfg::G3) {  // re = T1 - T2, im = T3 - T1 - T2
+                v[0] = acc[i][j][0][e] - acc[i][j][1][e];
+                v[1] = acc[i][j][2][e] - acc[i][j][0][e] - acc[i][j][1][e];
+              } else {
+#pragma unroll
+                for (int z = 0; z < S; z++) v[z] = acc[i][j][z][e];
+              }
 #pragma unroll
               for (int z = 0; z < S; z++) {
                 const int idx = (m * N + n) * S + z;
-                sP[idx] = (sl == 0) ? acc[i][j][z][e] : sP[idx] + acc[i][j][z][e];
+                sP[idx] = (sl == 0) ? v[z] : sP[idx] + v[z];
               }
             }
           }
@@ -1586,13 +1620,16 @@ __global__ void __launch_bounds__(Cfg::NT) tsmm_mma_kernel(const __grid_constant
 // computed with DFMA by the warps of the last column group (each lane adds its
 // m = 4ks+q terms, a 4-lane butterfly finishes the sum) instead of padding a
 // whole 8-column DMMA block; C' of those columns is staged in smem.
-template <int M_, int N_, bool Z_, int NBW_, int WR_, int NW_, int R_, bool ZR_ = false, int EC_ = 0>
+template <int M_, int N_, bool Z_, int NBW_, int WR_, int NW_, int R_, bool ZR_ = false, int EC_ = 0,
+          bool G3_ = false>
 struct TsmmCstCfg {
   static constexpr int M = M_, N = N_, NBW = NBW_, WR = WR_, NW = NW_, R = R_, EC = EC_;
-  static constexpr bool Z = Z_, ZR = ZR_;
+  static constexpr bool Z = Z_, ZR = ZR_, G3 = G3_;
+  static_assert(!G3 || Z_, "3M (Gauss) products: complex kernel");
   static_assert(!ZR || (!Z_ && M_ % 2 == 0 && N_ % 2 == 0), "complex-as-real: real kernel on 2M x 2N");
   static_assert(EC == 0 || (EC == N % 8 && N >= 8), "edge columns: EC = N mod 8, N >= 8");
   static constexpr int S = Z ? 2 : 1;
+  static constexpr int NA = G3 ? 3 : S;             // C fragments / accumulators per block (3M: 3)
   static constexpr int MK = (M + 3) / 4;            // k-steps over m
   static constexpr int NB = (N - EC + 7) / 8;       // 8-column DMMA blocks of B
   static constexpr int NG = (NB + NBW - 1) / NBW;   // column groups
@@ -1618,7 +1655,7 @@ template <class Cfg>
 __global__ void __launch_bounds__(Cfg::NT) tsmm_cst_kernel(const __grid_constant__ TsmmArgs p) {
   constexpr int M = Cfg::M, N = Cfg::N, S = Cfg::S, R = Cfg::R, NW = Cfg::NW, WR = Cfg::WR;
   constexpr int MK = Cfg::MK, NB = Cfg::NB, NBW = Cfg::NBW, NG = Cfg::NG, RW = Cfg::RW;
-  constexpr int RPP = Cfg::RPP, OB = Cfg::OB, EC = Cfg::EC;
+  constexpr int RPP = Cfg::RPP, OB = Cfg::OB, EC = Cfg::EC, NA = Cfg::NA;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   u64* full = reinterpret_cast<u64*>(smem_raw);
   u64* empty = full + 16;
@@ -1689,7 +1726,8 @@ __global__ void __launch_bounds__(Cfg::NT) tsmm_cst_kernel(const __grid_constant
     const int rho = ((((g & 1) << 2) | (g & 2) | (g >> 2)) ^ (g & 1));
     double* stg = sOut + warp * Cfg::OUT_DOUBLES;
     // this warp's C slice as MMA-B fragments: lane holds C[4ks+q][8(nb0+j)+g]
-    double cf[MK][NBW][S];
+    // (3M: Re c, Im c, Re c + Im c)
+    double cf[MK][NBW][NA];
 #pragma unroll
     for (int ks = 0; ks < MK; ks++)
 #pragma unroll
@@ -1711,6 +1749,7 @@ __global__ void __launch_bounds__(Cfg::NT) tsmm_cst_kernel(const __grid_constant
           for (int z = 0; z < S; z++) cf[ks][j][z] = (m < M && n < N) ? __ldg(&p.C[(m * N + n) * S + z]) : 0.0;
           if constexpr (Cfg::Z) {
             c_prime(p, cf[ks][j][0], cf[ks][j][1]);
+            if constexpr (Cfg::G3) cf[ks][j][NA - 1] = cf[ks][j][0] + cf[ks][j][1];
           } else {
             cf[ks][j][0] *= p.alpha_re;
           }
@@ -1736,13 +1775,13 @@ __global__ void __launch_bounds__(Cfg::NT) tsmm_cst_kernel(const __grid_constant
         for (int pr = 0; pr < rows; pr += RPP) {
           const int wr0 = pr + rg * RW;
           if (wr0 >= rows) break;
-          double acc[WR][NBW][S][2];
+          double acc[WR][NBW][NA][2];
   #pragma unroll
           for (int i = 0; i < WR; i++)
   #pragma unroll
             for (int j = 0; j < NBW; j++)
   #pragma unroll
-              for (int z = 0; z < S; z++) acc[i][j][z][0] = acc[i][j][z][1] = 0.0;
+              for (int z = 0; z < NA; z++) acc[i][j][z][0] = acc[i][j][z][1] = 0.0;
           double eacc[WR][ECA][S];
   #pragma unroll
           for (int i = 0; i < WR; i++)
@@ -1767,6 +1806,16 @@ __global__ void __launch_bounds__(Cfg::NT) tsmm_cst_kernel(const __grid_constant
                 }
               } else {
                 const double2 a = mv ? *reinterpret_cast<const double2*>(sA + aoff(r, m)) : make_double2(0.0, 0.0);
+                if constexpr (Cfg::G3) {
+                  // 3M: T1 += ar cr, T2 += ai ci, T3 += (ar + ai)(cr + ci)
+                  const double sa = a.x + a.y;
+  #pragma unroll
+                  for (int j = 0; j < NBV; j++) {
+                    dmma(acc[i][j][0][0], acc[i][j][0][1], a.x, cf[ks][j][0]);
+                    dmma(acc[i][j][1][0], acc[i][j][1][1], a.y, cf[ks][j][1]);
+                    dmma(acc[i][j][2][0], acc[i][j][2][1], sa, cf[ks][j][2]);
+                  }
+                } else {
                 const double nai = -a.y;
   #pragma unroll
                 for (int j = 0; j < NBV; j++) {
@@ -1774,6 +1823,7 @@ __global__ void __launch_bounds__(Cfg::NT) tsmm_cst_kernel(const __grid_constant
                   dmma(acc[i][j][0][0], acc[i][j][0][1], nai, cf[ks][j][1]);  // re -= ai ci
                   dmma(acc[i][j][1][0], acc[i][j][1][1], a.x, cf[ks][j][1]);  // im += ar ci
                   dmma(acc[i][j][1][0], acc[i][j][1][1], a.y, cf[ks][j][0]);  // im += ai cr
+                }
                 }
                 if constexpr (ECV > 0) {
   #pragma unroll
@@ -1801,8 +1851,13 @@ __global__ void __launch_bounds__(Cfg::NT) tsmm_cst_kernel(const __grid_constant
   #pragma unroll
                 for (int e = 0; e < 2; e++) {
                   const int c0 = 2 * (8 * j + 2 * q + e);
+                  double re = acc[i][j][0][e], im = acc[i][j][1][e];
+                  if constexpr (Cfg::G3) {  // re = T1 - T2, im = T3 - T1 - T2
+                    re = acc[i][j][0][e] - acc[i][j][1][e];
+                    im = acc[i][j][2][e] - acc[i][j][0][e] - acc[i][j][1][e];
+                  }
                   *reinterpret_cast<double2*>(stg + (c0 >> 4) * (RW * 16) + swz128(rr, c0 & 15)) =
-                      make_double2(acc[i][j][0][e], acc[i][j][1][e]);
+                      make_double2(re, im);
                 }
               }
             }

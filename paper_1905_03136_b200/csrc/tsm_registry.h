@@ -21,7 +21,8 @@ struct KernelEntry {
                      // 2 = DMMA + TMA tensor copies, 3 = C-stationary DMMA TSMM
   int edge;          // DMMA TSMTTSM flags: bit 0 = DFMA edge warps for the cells outside the
                      // 8-aligned core, bit 1 = paired 16-byte fragment loads, bits 2-3 =
-                     // edge warps - 1, bit 4 = complex-as-real (tsm_config.kernel bits 4..8)
+                     // edge warps - 1, bit 4 = complex-as-real, bit 5 = 3M (Gauss) complex
+                     // products (tsm_config.kernel bits 4..9)
 };
 
 // number of DFMA edge warps encoded in KernelEntry::edge
@@ -31,6 +32,10 @@ inline int edge_warps(int flags) { return (flags & 1) ? 1 + ((flags >> 2) & 3) :
 // as real K x 2M, K x 2N; TSMTTSM combines the 2M x 2N real product, TSMM uses
 // the real 2M x 2N image of C (tsm_kernels.cuh ZR)
 inline bool zr_flag(int flags) { return (flags & 16) != 0; }
+
+// bit 5: Z TSMTTSM by the 3M (Gauss) method -- 3 real DMMAs per 8x8 block
+// (T1 = Ar^T Br, T2 = Ai^T Bi, T3 = (Ar+Ai)^T (Br+Bi)) instead of 4
+inline bool g3_flag(int flags) { return (flags & 32) != 0; }
 
 // the real problem a complex-as-real entry runs (identity otherwise)
 inline KernelEntry real_view(const KernelEntry& k) {

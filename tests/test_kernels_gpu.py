@@ -208,6 +208,95 @@ def test_complex_as_real(tsm, op, M, N):
     assert ran
 
 
+@pytest.mark.parametrize("conj", [False, True], ids=["T", "H"])
+@pytest.mark.parametrize("M,N", [(32, 32), (17, 17), (25, 9), (40, 48), (64, 64), (8, 8), (3, 20)])
+def test_tsmttsm_3m(tsm, M, N, conj):
+    """Z TSMTTSM by 3M / Gauss products (kernel | 512): T1 = Ar^T Br,
+    T2 = Ai^T Bi, T3 = (Ar+Ai)^T (Br+Bi); every family the generator offers
+    (bulk / TMA, edge warps), plain and conjugate (A^H B), ragged K within the
+    1e-12 |A|^T|B| tolerance, integer-valued inputs bit-exact."""
+    base = [c for c in gi.candidates("tsmttsm", M, N, True) if c.get("G3")]
+    if not base:
+        pytest.skip("no DMMA candidate for this shape")
+    picked = {}
+    for c in base:
+        picked.setdefault((c.get("impl"), c.get("EDGE", 0)), c)
+    ran = 0
+    for key, c in sorted(picked.items()):
+        try:
+            plan = tsm.Plan("tsmttsm", "z", M, N, 0, config=gi.to_tsm_config("tsmttsm", c, 3, 1), conj=conj)
+        except tsm.TsmError as e:
+            if e.status != 2:
+                raise
+            continue
+        assert plan.config()["kernel"] & 512 and "+3m" in plan.describe(1000)["kernel"]
+        ran += 1
+        for K in (1, 6, 4099, 65537):
+            A = ti.matrix(K, M, "A", complex_=True, seed=K + 21)
+            B = ti.matrix(K, N, "B", complex_=True, seed=K + 22)
+            got = tsm.tsmttsm(torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda(), plan=plan, conj=conj)
+            torch.cuda.synchronize()
+            ref, bound = oracle.tsmttsm(A, B, conj=conj)
+            r, wi, _ = oracle.max_err_ratio(got.cpu().numpy(), ref, bound)
+            assert r <= 1e-12, (M, N, key, c, K, r, wi)
+        Ai = ti.matrix(30001, M, "A", complex_=True, mode="int")
+        Bi = ti.matrix(30001, N, "B", complex_=True, mode="int")
+        got = tsm.tsmttsm(torch.from_numpy(Ai).cuda(), torch.from_numpy(Bi).cuda(), plan=plan, conj=conj)
+        torch.cuda.synchronize()
+        assert np.array_equal(got.cpu().numpy(), oracle.tsmttsm(Ai, Bi, conj=conj)[0]), (key, c)
+    assert ran
+
+
+@pytest.mark.parametrize("conj", [False, True], ids=["C", "conjC"])
+@pytest.mark.parametrize("M,N", [(32, 32), (17, 17), (24, 40), (64, 64), (9, 8), (50, 13)])
+def test_tsmm_3m(tsm, M, N, conj):
+    """Z TSMM by 3M / Gauss products (C-stationary kernel 3 | 512, with and
+    without DFMA edge columns): B = A C and the update B <- alpha A C + beta B
+    (conj: A conj(C)) within the 1e-13 |A||C| tolerance on ragged K;
+    integer-valued inputs bit-exact."""
+    cands = [c for c in gi.candidates("tsmm", M, N, True) if c.get("G3")]
+    if not cands:
+        pytest.skip("no C-stationary candidate for this shape")
+    picked = {}
+    for c in cands:
+        picked.setdefault((c.get("EDGE", 0), c["NBW"]), c)
+    ran = 0
+    for key, c in sorted(picked.items()):
+        try:
+            plan = tsm.Plan("tsmm", "z", M, N, 0, config=gi.to_tsm_config("tsmm", c, 3, 1), conj=conj)
+        except tsm.TsmError as e:
+            if e.status != 2:
+                raise
+            continue
+        assert plan.config()["kernel"] & 512 and "+3m" in plan.describe(1000)["kernel"]
+        ran += 1
+        for K in (1, 9, 4099, 65537):
+            A = ti.matrix(K, M, "A", complex_=True, seed=K + 31)
+            Cm = ti.matrix(M, N, "C", complex_=True, seed=K + 32)
+            B0 = ti.matrix(K, N, "B", complex_=True, seed=K + 33)
+            Bg = torch.from_numpy(B0).cuda()
+            alpha, beta = (0.5 - 0.25j), (1.0 if K % 2 else 0.0)
+            tsm.tsmm_update(torch.from_numpy(A).cuda(), torch.from_numpy(Cm).cuda(), Bg, alpha, beta,
+                            plan=plan, conj=conj)
+            torch.cuda.synchronize()
+            ref, bound = oracle.tsmm_update(A, Cm, B0, alpha, beta, conj=conj)
+            r, wi, _ = oracle.max_err_ratio(Bg.cpu().numpy(), ref, bound)
+            assert r <= 1e-13, (M, N, key, c, K, r, wi)
+        Ai = ti.matrix(20001, M, "A", complex_=True, mode="int")
+        Ci = ti.matrix(M, N, "C", complex_=True, mode="int")
+        if conj:
+            got = torch.zeros(20001, N, dtype=torch.complex128, device="cuda")
+            tsm.tsmm_update(torch.from_numpy(Ai).cuda(), torch.from_numpy(Ci).cuda(), got, 1.0, 0.0,
+                            plan=plan, conj=True)
+            ref = oracle.tsmm(Ai, np.conj(Ci))[0]
+        else:
+            got = tsm.tsmm(torch.from_numpy(Ai).cuda(), torch.from_numpy(Ci).cuda(), plan=plan)
+            ref = oracle.tsmm(Ai, Ci)[0]
+        torch.cuda.synchronize()
+        assert np.array_equal(got.cpu().numpy(), ref), (key, c)
+    assert ran
+
+
 @pytest.mark.parametrize("cplx,zr", [(False, False), (True, False), (True, True)], ids=["D", "Z", "ZR"])
 @pytest.mark.parametrize("M,N", [(50, 50), (42, 34), (16, 20), (17, 17), (9, 12), (64, 57)])
 def test_tsmm_edge_columns(tsm, M, N, cplx, zr):

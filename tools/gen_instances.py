@@ -331,7 +331,8 @@ def cfg_type(op, dt, M, N, c) -> str:
         edge = c.get("EDGE", 0)
         pair = "true" if c.get("PAIR", 0) else "false"
         return (f"tsm::TsmttsmMmaCfg<{M}, {N}, {z}, {c['MT']}, {c['NTL']}, {c['NT'] // 32 - 1 - edge}, "
-                f"{c['R']}, {c.get('AP', M)}, {c.get('BP', N)}, {tma}, {edge}, {pair}, {zr}>")
+                f"{c['R']}, {c.get('AP', M)}, {c.get('BP', N)}, {tma}, {edge}, {pair}, {zr}, "
+                f"{'true' if c.get('G3', 0) else 'false'}>")
     if op == "tsmttsm":
         return f"tsm::TsmttsmCfg<{M}, {N}, {z}, {c['MT']}, {c['NTL']}, {c['NT']}, {c['R']}>"
     if c.get("impl", 0) == 4:
@@ -339,7 +340,7 @@ def cfg_type(op, dt, M, N, c) -> str:
     if c.get("impl", 0) == 3:
         ec = N % 8 if c.get("EDGE", 0) else 0
         return (f"tsm::TsmmCstCfg<{M}, {N}, {z}, {c['NBW']}, {c['WR']}, {c['NT'] // 32 - 1}, {c['R']}, {zr}, "
-                f"{ec}>")
+                f"{ec}, {'true' if c.get('G3', 0) else 'false'}>")
     if c.get("impl", 0) >= 1:
         tma = "true" if c["impl"] == 2 else "false"
         return (f"tsm::TsmmMmaCfg<{M}, {N}, {z}, {c['WR']}, {c['NT'] // 32 - 1}, {c['R']}, "
@@ -367,10 +368,10 @@ def entry_init(op, dt, M, N, c) -> str:
 def flags(c: dict) -> int:
     """KernelEntry.edge / tsm_config.kernel >> 4: bit 0 DFMA edge warps, bit 1
     paired 16-byte fragment loads, bits 2-3 edge warps - 1 (EDGE = edge warp count),
-    bit 4 complex-as-real (ZR)."""
+    bit 4 complex-as-real (ZR), bit 5 3M / Gauss complex products (G3)."""
     e = c.get("EDGE", 0)
     return ((1 if e else 0) | (c.get("PAIR", 0) << 1) | (((e - 1) & 3) << 2 if e else 0)
-            | (c.get("ZR", 0) << 4))
+            | (c.get("ZR", 0) << 4) | (c.get("G3", 0) << 5))
 
 
 def params4(op: str, M: int, N: int, c: dict) -> tuple:
@@ -581,6 +582,7 @@ def candidates(op: str, M: int, N: int, z: bool) -> list:
         out.extend(tsmm_cstb_configs(M, N, z))
     if z:
         out.extend(zr_candidates(op, M, N))
+        out.extend(g3_candidates(op, M, N, out))
     if op == "tsmm" and N >= 2:
         d = tsmm_mma_default(M, N, z)
         S_ = 2 if z else 1
@@ -643,6 +645,20 @@ def zr_candidates(op: str, M: int, N: int) -> list:
             return []
         base = tsmm_cst_configs(2 * M, 2 * N, False) + tsmm_cst_configs(2 * M, 2 * N, False, edge=True)
     return [dict(c, ZR=1) for c in base]
+
+
+def g3_candidates(op: str, M: int, N: int, base: list) -> list:
+    """3M / Gauss complex products (G3=1): the native complex DMMA candidates
+    -- TSMTTSM kernels 1/2 (with or without edge warps), TSMM C-stationary
+    kernel 3 (with or without edge columns) -- with 3 real DMMAs per 8x8
+    block instead of 4.  Warp tiles keep <= 6 blocks (3 x 2 accumulator
+    doubles per block and lane); TSMM C slices <= 48 doubles (MK x NBW x 3)."""
+    if op == "tsmttsm":
+        return [dict(c, G3=1) for c in base
+                if c.get("impl", 0) in (1, 2) and not c.get("ZR", 0) and c["MT"] * c["NTL"] <= 6]
+    return [dict(c, G3=1) for c in base
+            if c.get("impl", 0) == 3 and not c.get("ZR", 0) and c["WR"] * c["NBW"] <= 6
+            and cdiv(M, 4) * c["NBW"] * 3 <= 48]
 
 
 def to_tsm_config(op: str, c: dict, stages: int, ctas: int) -> dict:
