@@ -138,7 +138,11 @@ typedef struct tsm_config {
                        tensor pipe, C = (T1 - T2) + i (T3 - T1 - T2) -- 3 real
                        DMMAs per 8x8 block instead of 4 (same bytes, 3/4 of the
                        FP64 work; error within the |A|^T|B| tolerance, exact
-                       on integer-valued inputs).
+                       on integer-valued inputs);
+                   1024 plain consumer-warp order (DMMA kernels): by default the
+                       warps of one C tile / column group are spread over the 4 SM
+                       sub-partitions; this flag keeps warp w on tile w % tiles.
+                       A launch argument, not a separate kernel.
                  Invalid combinations return TSM_ERR_INVALID_VALUE. */
   int p3;
 } tsm_config;

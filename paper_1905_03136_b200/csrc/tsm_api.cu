@@ -220,6 +220,7 @@ struct tsm_plan_s {
   size_t smem;
   bool jit;  // kernel compiled at run time by NVRTC (shape/config outside the AOT set)
   unsigned flags = 0;  // TSM_FLAG_CONJ
+  int order = 0;       // consumer-warp order of the DMMA kernels: 0 spread over SMSPs, 1 plain (kernel | 1024)
 };
 
 extern "C" {
@@ -435,6 +436,7 @@ static tsm_status make_plan(tsm_plan* out, const KernelEntry& want, int device, 
   p->ctas_per_sm = std::min(occ, std::max(1, exact ? want.ctas_per_sm : k->ctas_per_sm));
   p->smem = smem;
   p->jit = jit;
+  p->order = (want.edge >> 6) & 1;  // run-time flag: not part of the (possibly shared) kernel entry
   *out = p;
   return TSM_SUCCESS;
 }
@@ -474,7 +476,7 @@ tsm_status tsm_plan_create_config(tsm_plan* out, tsm_op op, tsm_dtype dtype, int
   e.p0 = cfg->p0;
   e.p1 = cfg->p1;
   e.impl = cfg->kernel & 15;
-  e.edge = (cfg->kernel >> 4) & 63;
+  e.edge = (cfg->kernel >> 4) & 127;
   e.p2 = (op == TSM_OP_TSMTTSM && e.impl == 0) ? 0 : cfg->p2;
   e.p3 = (op == TSM_OP_TSMTTSM && e.impl >= 1) ? cfg->p3 : 0;
   e.stages = cfg->stages;
@@ -531,7 +533,7 @@ tsm_status tsm_jit_precompile(tsm_op op, tsm_dtype dtype, int M, int N, const ts
     e.p0 = cfg->p0;
     e.p1 = cfg->p1;
     e.impl = cfg->kernel & 15;
-    e.edge = (cfg->kernel >> 4) & 63;
+    e.edge = (cfg->kernel >> 4) & 127;
     e.p2 = (op == TSM_OP_TSMTTSM && e.impl == 0) ? 0 : cfg->p2;
     e.p3 = (op == TSM_OP_TSMTTSM && e.impl >= 1) ? cfg->p3 : 0;
     e.stages = cfg->stages;
@@ -561,7 +563,7 @@ tsm_status tsm_plan_get_config(tsm_plan p, tsm_config* cfg) {
   cfg->p1 = p->k->p1;
   cfg->p2 = p->k->p2;
   cfg->p3 = p->k->p3;
-  cfg->kernel = p->k->impl | (p->k->edge << 4);
+  cfg->kernel = p->k->impl | (((p->k->edge & 63) | (p->order << 6)) << 4);
   cfg->stages = p->stages;
   cfg->ctas_per_sm = p->ctas_per_sm;
   return TSM_SUCCESS;
@@ -679,6 +681,7 @@ tsm_status launch_tsmttsm(const tsm_plan_s* p, int dt, long long K, const void* 
   a.nchunks = g.nchunks;
   a.stages = p->stages;
   a.nfin = g.nfin;
+  a.order = p->order;
   a.conj = (p->flags & TSM_FLAG_CONJ) ? (1ull << 63) : 0ull;
   if (p->k->impl == 2 && K > 0) {
     const int S = dt == TSM_Z ? 2 : 1;
@@ -729,6 +732,7 @@ tsm_status launch_tsmm(const tsm_plan_s* p, int dt, long long K, const void* A, 
   a.reduce = mode->reduce;
   a.alpha_re = mode->alpha_re;
   a.alpha_im = dt == TSM_Z ? mode->alpha_im : 0.0;
+  a.order = p->order;
   a.conj = (p->flags & TSM_FLAG_CONJ) ? (1ull << 63) : 0ull;
   if (p->k->impl == 2 || p->k->impl == 3) {  // B store boxes: 8*WR rows (WR = p0 for kernel 2, p1 for kernel 3)
     const int S = dt == TSM_Z ? 2 : 1;
@@ -823,6 +827,7 @@ tsm_status tsm_plan_describe(tsm_plan p, int64_t K, char* buf, size_t len) {
   if (p->op == TSM_OP_TSMM && (k->edge & 1)) kname += "+dfma-edge-columns";
   if (zr_flag(k->edge)) kname += "+complex-as-real(2Mx2N)";
   if (g3_flag(k->edge)) kname += "+3m";
+  if (p->order) kname += "+plain-warp-order";
   if (p->op == TSM_OP_TSMTTSM && k->impl >= 1)
     snprintf(tmp, sizeof tmp,
              "{\"op\":\"tsmttsm\",\"dtype\":\"%c\",\"M\":%d,\"N\":%d,\"WM\":%d,\"WN\":%d,"

@@ -140,8 +140,10 @@ __device__ __forceinline__ void zfma(double& re, double& im, double ar, double a
 // tensor pipe half idle (ncu r23: D 56, tiles of 14/14/14/7 DMMAs, 82 % pipe).
 // Ordering the (slot, tile) pairs by L(w) = (w % 4) * (nw / 4) + w / 4 gives each
 // SMSP consecutive pairs, i.e. all tiles.  A bijection on [0, nw) for nw % 4 == 0.
-__device__ __forceinline__ int spread_warp(int w, int nw) {
-  return (nw % 4 == 0 && w < nw) ? (w % 4) * (nw / 4) + w / 4 : w;
+// order = 1 (plan flag kernel | 1024) keeps the plain order: which one balances
+// better depends on the tile shape, so the autotuner measures both.
+__device__ __forceinline__ int spread_warp(int w, int nw, int order) {
+  return (order == 0 && nw % 4 == 0 && w < nw) ? (w % 4) * (nw / 4) + w / 4 : w;
 }
 
 // compile-time int as a value (dispatching generic lambdas on a constant)
@@ -231,6 +233,7 @@ struct TsmttsmArgs {
   long long nchunks;   // ceil(K_even / R)  (TMA kernels: ceil(K / R))
   int stages;          // smem ring depth
   int nfin;            // finisher blocks of the grid reduction
+  int order;           // consumer-warp order (spread_warp)
   u64 conj;            // Z: sign mask XORed into Im(A) -- 1<<63 gives C = A^H B (NEXT N2)
 };
 
@@ -677,7 +680,7 @@ __global__ void __launch_bounds__(Cfg::NT) tsmttsm_mma_kernel(const __grid_const
 #pragma unroll
       for (int z = 0; z < NA; z++) acc[i][j][z][0] = acc[i][j][z][1] = 0.0;
 
-  const int wl = spread_warp(warp, NW);  // (slot, tile) of this consumer warp
+  const int wl = spread_warp(warp, NW, p.order);  // (slot, tile) of this consumer warp
   const int slot = wl / WT;
   const int wt = wl % WT;
   const int wm = wt % WTM, wn = wt / WTM;
@@ -1082,6 +1085,7 @@ struct TsmmArgs {
   int stages;
   int reduce;         // 0: B = A C' (store); 1: B += A C' (bulk / TMA reduce-add; NEXT N1)
   double alpha_re, alpha_im;  // C' = alpha * C (alpha = 1: C used as given, bit-exact)
+  int order;          // consumer-warp order (spread_warp)
   u64 conj;           // Z: sign mask XORed into Im(C) -- 1<<63 uses conj(C) (NEXT N2)
 };
 
@@ -1716,7 +1720,7 @@ __global__ void __launch_bounds__(Cfg::NT) tsmm_cst_kernel(const __grid_constant
     }
   } else {
     // ---------------- consumer warps ----------------
-    const int wl = spread_warp(warp, NW);
+    const int wl = spread_warp(warp, NW, p.order);
     const int cg = wl % NG, rg = wl / NG;
     const int nb0 = cg * NBW;  // first 8-column block of this warp
     // MMA row g of a block is A/B row rho(g) = bitrev3(g) ^ (g & 1) =
@@ -2012,7 +2016,7 @@ __global__ void __launch_bounds__(Cfg::NT) tsmm_cstb_kernel(const __grid_constan
     }
   } else {
     // ---------------- consumer warps ----------------
-    const int wl = spread_warp(warp, NW);
+    const int wl = spread_warp(warp, NW, p.order);
     const int cg = wl % NG, rg = wl / NG;
     const int nb0 = cg * NBW;
     const bool issuer = (cg == 0 && lane == 0);

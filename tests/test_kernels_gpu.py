@@ -330,3 +330,46 @@ def test_tsmm_edge_columns(tsm, M, N, cplx, zr):
         got = tsm.tsmm(torch.from_numpy(Ai).cuda(), torch.from_numpy(Ci).cuda(), plan=plan)
         torch.cuda.synchronize()
         assert np.array_equal(got.cpu().numpy(), oracle.tsmm(Ai, Ci)[0]), c
+
+
+@pytest.mark.parametrize("op", ["tsmttsm", "tsmm"])
+@pytest.mark.parametrize("dt,M,N", [("d", 48, 48), ("d", 56, 56), ("d", 41, 41), ("z", 32, 32), ("d", 63, 63)])
+def test_plain_warp_order(tsm, op, dt, M, N):
+    """The tuned DMMA plan with the consumer-warp order flipped (kernel ^ 1024,
+    a launch argument): same cells, other warp -> (slot, tile) assignment;
+    ragged K within tolerance, integer-valued inputs bit-exact."""
+    base = tsm.get_plan(op, dt, M, N, 0)
+    if not base.config()["kernel"] & 15:
+        pytest.skip("not a DMMA plan")
+    cfg = dict(base.config())
+    cfg["kernel"] ^= 1024
+    plan = tsm.Plan(op, dt, M, N, 0, config=cfg)
+    assert plan.config()["kernel"] == cfg["kernel"]
+    assert ("plain-warp-order" in plan.describe(1000)["kernel"]) == bool(cfg["kernel"] & 1024)
+    cplx = dt == "z"
+    for K in (3, 4099, 65537):
+        A = ti.matrix(K, M, "A", complex_=cplx, seed=K + 51)
+        if op == "tsmttsm":
+            B = ti.matrix(K, N, "B", complex_=cplx, seed=K + 52)
+            got = tsm.tsmttsm(torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda(), plan=plan)
+            ref, bound = oracle.tsmttsm(A, B)
+            tol = 1e-12
+        else:
+            Cm = ti.matrix(M, N, "C", complex_=cplx, seed=K + 53)
+            got = tsm.tsmm(torch.from_numpy(A).cuda(), torch.from_numpy(Cm).cuda(), plan=plan)
+            ref, bound = oracle.tsmm(A, Cm)
+            tol = 1e-13
+        torch.cuda.synchronize()
+        r, wi, _ = oracle.max_err_ratio(got.cpu().numpy(), ref, bound)
+        assert r <= tol, (op, dt, M, N, cfg, K, r, wi)
+    Ai = ti.matrix(30001, M, "A", complex_=cplx, mode="int")
+    if op == "tsmttsm":
+        Bi = ti.matrix(30001, N, "B", complex_=cplx, mode="int")
+        got = tsm.tsmttsm(torch.from_numpy(Ai).cuda(), torch.from_numpy(Bi).cuda(), plan=plan)
+        ref = oracle.tsmttsm(Ai, Bi)[0]
+    else:
+        Ci = ti.matrix(M, N, "C", complex_=cplx, mode="int")
+        got = tsm.tsmm(torch.from_numpy(Ai).cuda(), torch.from_numpy(Ci).cuda(), plan=plan)
+        ref = oracle.tsmm(Ai, Ci)[0]
+    torch.cuda.synchronize()
+    assert np.array_equal(got.cpu().numpy(), ref), cfg

@@ -151,18 +151,21 @@ def main():
                 res.sort(key=lambda r: r[0])
                 # phase 2: run-time parameters for the best 3
                 best = res[0]
-                for (_, c, _) in res[:3]:
-                    for stages in (2, 3, 4, 6):
-                        for ctas in (1, 2, 3, 4):
-                            p = make(c, stages, ctas)
-                            if isinstance(p, Exception):
-                                continue
-                            got = p.config()
-                            if got["stages"] != stages or got["ctas_per_sm"] != ctas:
-                                continue  # clipped: same as another point
-                            t = timeit(p)
-                            if t < best[0]:
-                                best = (t, c, got)
+                # (DMMA kernels: both consumer-warp orders, a launch argument)
+                dmma = lambda c: c.get("impl", 0) >= 1  # noqa: E731
+                for (_, c0, _) in res[:3]:
+                    for c in ([c0, dict(c0, PLAIN=1)] if dmma(c0) else [c0]):
+                        for stages in (2, 3, 4, 6):
+                            for ctas in (1, 2, 3, 4):
+                                p = make(c, stages, ctas)
+                                if isinstance(p, Exception):
+                                    continue
+                                got = p.config()
+                                if got["stages"] != stages or got["ctas_per_sm"] != ctas:
+                                    continue  # clipped: same as another point
+                                t = timeit(p)
+                                if t < best[0]:
+                                    best = (t, c, got)
                 t, c, got = best
                 cfg = dict(c)
                 cfg["stages"] = got["stages"]

@@ -368,10 +368,11 @@ def entry_init(op, dt, M, N, c) -> str:
 def flags(c: dict) -> int:
     """KernelEntry.edge / tsm_config.kernel >> 4: bit 0 DFMA edge warps, bit 1
     paired 16-byte fragment loads, bits 2-3 edge warps - 1 (EDGE = edge warp count),
-    bit 4 complex-as-real (ZR), bit 5 3M / Gauss complex products (G3)."""
+    bit 4 complex-as-real (ZR), bit 5 3M / Gauss complex products (G3), bit 6
+    plain consumer-warp order (PLAIN; a launch argument of the DMMA kernels)."""
     e = c.get("EDGE", 0)
     return ((1 if e else 0) | (c.get("PAIR", 0) << 1) | (((e - 1) & 3) << 2 if e else 0)
-            | (c.get("ZR", 0) << 4) | (c.get("G3", 0) << 5))
+            | (c.get("ZR", 0) << 4) | (c.get("G3", 0) << 5) | (c.get("PLAIN", 0) << 6))
 
 
 def params4(op: str, M: int, N: int, c: dict) -> tuple:

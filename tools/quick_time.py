@@ -39,7 +39,18 @@ def main():
     ap.add_argument("--Ks", default="", help="comma list of K values (small-K study); overrides --K")
     ap.add_argument("--reps", type=int, default=10)
     ap.add_argument("--json", default="")
+    ap.add_argument("--toggle-order", action="store_true",
+                    help="time the default plan's configuration with the consumer-warp order flipped "
+                         "(kernel ^ 1024, DMMA kernels)")
     a = ap.parse_args()
+
+    def get_plan(op, dt, M, N):
+        plan = tsm.get_plan(op, dt, M, N, 0)
+        if a.toggle_order and plan.config()["kernel"] & 15:
+            cfg = dict(plan.config())
+            cfg["kernel"] ^= 1024
+            plan = tsm.Plan(op, dt, M, N, 0, config=cfg)
+        return plan
     bw = hbm_peak()
     shapes = [tuple(map(int, s.split("x"))) for s in a.shapes.split(",") if s] or \
         [(w, w) for w in map(int, a.widths.split(","))]
@@ -63,14 +74,14 @@ def main():
                 if op == "tsmttsm":
                     B = Bbuf[: K * N].view(K, N)
                     C = torch.empty(M, N, dtype=tdt, device="cuda")
-                    plan = tsm.get_plan(op, dt, M, N, 0)
+                    plan = get_plan(op, dt, M, N)
                     fn = lambda: tsm.tsmttsm(A, B, out=C, plan=plan)  # noqa: E731
                     byts = sz * (K * M + K * N + M * N)
                 else:
                     Cm = torch.empty(M, N, dtype=tdt, device="cuda")
                     tsm.fill(Cm, "C", 42)
                     B = Bbuf[: K * N].view(K, N)
-                    plan = tsm.get_plan(op, dt, M, N, 0)
+                    plan = get_plan(op, dt, M, N)
                     fn = lambda: tsm.tsmm(A, Cm, out=B, plan=plan)  # noqa: E731
                     byts = sz * (K * M + K * N + M * N)
                 flops = (8 if dt == "z" else 2) * M * N * K
