@@ -1,6 +1,6 @@
 # r30: FP64-pipe concurrency probe; 3M defaults merged (r29) -- parity; Z sweep; D/Z warp-order A/B; D compute-width retune (both orders)
 ./tools/probes/fp64_mix > gpurun_out/fp64_mix30.log 2>&1; echo probe rc=$?; cat gpurun_out/fp64_mix30.log
-timeout 1500 python -m pytest tests/test_kernels_gpu.py tests/test_parity_gpu.py -m gpu -q -x -k "3m or plain_warp_order or parity or tuned or config" > gpurun_out/pytest_gpu30.log 2>&1; echo pytest rc=$?; tail -n 3 gpurun_out/pytest_gpu30.log
+timeout 1500 python -m pytest tests/test_kernels_gpu.py tests/test_parity_gpu.py -m gpu -q -x > gpurun_out/pytest_gpu30.log 2>&1; echo pytest rc=$?; tail -n 3 gpurun_out/pytest_gpu30.log
 W=$(python -c "print(','.join(str(i) for i in range(17,65)))")
 timeout 900 python tools/quick_time.py --ops tsmttsm,tsmm --dtypes z --widths $W --reps 3 --json gpurun_out/sweep30_z.json > gpurun_out/sweep30_z.log 2>&1; echo zsweep rc=$?
 timeout 900 python tools/quick_time.py --ops tsmttsm,tsmm --dtypes z --widths $W --reps 3 --toggle-order --json gpurun_out/sweep30_z_tog.json > gpurun_out/sweep30_z_tog.log 2>&1; echo ztog rc=$?
