@@ -27,7 +27,10 @@ def main():
     for (op, dt), v in sorted(by.items()):
         summ.append(f"| {op} | {dt.upper()} | {len(v)} | {min(v):.1f} | {sum(v) / len(v):.1f} | "
                     f"{sum(1 for x in v if x >= 90)} |")
-    open(out, "w").write("\n".join(summ[1:] + [""] + lines) + "\n")
+    note = ["", "% roofline counts the paper's flops (8 real flops per complex multiply-add, DESIGN.md R3); "
+            "kernels marked +3m execute 6 (3M / Gauss products, R12), so compute-bound Z shapes can exceed "
+            "100 %; for FP64-bound shapes their executed-flop fraction of the FP64 peak is 3/4 of the printed value."]
+    open(out, "w").write("\n".join(summ[1:] + note + [""] + lines) + "\n")
     print("\n".join(summ))
 
 
