@@ -161,3 +161,29 @@ print("ok")
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
     cubins = [p for p in tmp_path.rglob("*.cubin")]
     assert len(cubins) >= 3
+
+
+def test_flag_validation_without_device(tmp_path):
+    """The 3M flag (kernel | 512) and the warp-order flag (kernel | 1024) are
+    validated before any compilation: 3M needs dtype Z, a DMMA TSMTTSM kernel
+    1/2 or the C-stationary TSMM kernel 3, and excludes complex-as-real; valid
+    3M configurations compile with NVRTC on this CPU box (no device)."""
+    code = r'''
+import ctypes
+from paper_1905_03136_b200 import binding as tsm
+f = tsm.lib.tsm_jit_precompile
+def cfg(**k):
+    d = dict(threads=160, rows_per_chunk=32, p0=2, p1=2, p2=32, stages=3, ctas_per_sm=1, kernel=2, p3=32)
+    d.update(k)
+    return ctypes.byref(tsm.TsmConfig(**d))
+assert f(0, 1, 32, 32, cfg(kernel=2 | 512), 0) == 0, tsm.lib.tsm_last_error_detail()      # Z TSMTTSM 3M (TMA)
+assert f(0, 1, 32, 32, cfg(kernel=2 | 512 | 1024), 0) == 0                                # + plain warp order
+assert f(0, 0, 32, 32, cfg(kernel=2 | 512), 0) == 1                                       # 3M needs Z
+assert f(0, 1, 16, 16, cfg(kernel=2 | 512 | 256, p2=32, p3=32), 0) == 1                   # 3M excludes ZR
+assert f(1, 1, 32, 32, cfg(threads=160, rows_per_chunk=64, p0=2, p1=2, p2=0, p3=0, kernel=3 | 512), 0) == 0
+assert f(1, 1, 32, 32, cfg(threads=160, rows_per_chunk=64, p0=2, p1=2, p2=0, p3=0, kernel=4 | 512), 0) == 1
+print("ok")
+'''
+    env = dict(os.environ, TSM_JIT_CACHE_DIR=str(tmp_path))
+    r = subprocess.run([sys.executable, "-c", code], env=env, cwd=ROOT, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, (r.stdout[-2000:], r.stderr[-2000:])
