@@ -51,7 +51,8 @@ def bench_config(args, widths, world):
             "K_per_gpu": args.K, "widths": f"{widths[0]}..{widths[-1]}",
             "l2": "inputs > L2 (>=268 MB per kernel), no flush",
             "parallelism": f"K-sharded x{world}" if world > 1 else "single GPU",
-            "collectives": ("allgather+rank-order sum" if args.deterministic else "nccl allreduce")
+            "collectives": ("fused peer-memory reduction (tsmttsm_peer)" if getattr(args, "peer", False)
+                            else "allgather+rank-order sum" if args.deterministic else "nccl allreduce")
                            + " of C, nccl broadcast of C" if world > 1 else "none"}
 
 
@@ -199,6 +200,9 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--deterministic", action="store_true")
+    ap.add_argument("--peer", action="store_true",
+                    help="N>1: TSMTTSM with the grid reduction fused with the cross-GPU sum over "
+                         "peer memory (NEXT N3, tsmttsm_peer_*) instead of tsmttsm + NCCL allreduce")
     ap.add_argument("--force-comm", action="store_true",
                     help="use the NCCL process group + libtsm comm path even with one rank")
     ap.add_argument("--report", default="", help="write the per-kernel table (JSON) here")
@@ -229,6 +233,7 @@ def main():
         comm = tsm.Comm(rank, world, local, deterministic=args.deterministic)
     else:
         comm = None
+    peer = tsm.PeerComm(rank, world, local) if (dist_on and args.peer) else None
 
     if "-" in args.widths:
         lo, hi = map(int, args.widths.split("-"))
@@ -272,7 +277,11 @@ def main():
         if op == "tsmttsm":
             B = Bbuf[: K * M].view(K, M)
             C = Cs[M]
-            if comm is None:
+            if peer is not None:  # fused grid + cross-GPU reduction (NEXT N3)
+                f = tsm.lib.tsmttsm_peer_z if z else tsm.lib.tsmttsm_peer_d
+                tsm.check(f(p.handle, peer.handle, K, A.data_ptr(), B.data_ptr(), C.data_ptr(),
+                            ws.data_ptr(), ws.numel(), s_ptr), "tsmttsm_peer")
+            elif comm is None:
                 f = tsm.tsmttsm_z if z else tsm.tsmttsm_d
                 f(p.handle, K, A.data_ptr(), B.data_ptr(), C.data_ptr(), ws.data_ptr(), ws.numel(), s_ptr)
             else:

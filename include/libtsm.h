@@ -326,6 +326,47 @@ tsm_status tsmm_bcast_z(tsm_plan p, tsm_comm c, int root, int64_t K_local,
                         const tsm_zcomplex *A, tsm_zcomplex *C, tsm_zcomplex *B,
                         tsm_stream stream);
 
+/* ------------------------------------------------------------------------ */
+/* NEXT N3: TSMTTSM with the   */
+/* grid reduction FUSED with the cross-GPU sum over peer memory -- no NCCL    */
+/* call.  Each rank owns a symmetric "slot buffer" (device memory allocated   */
+/* by tsm_peer_create, 256 B + 2 x 8 x 64*64*2 doubles = 1 MiB); the buffers  */
+/* are mapped into every rank with CUDA IPC (NVLink / NVSwitch P2P).  The     */
+/* finisher blocks of the TSMTTSM kernel store this rank's C cells into the   */
+/* slot of every rank, signal with system-scope atomics, wait for all ranks   */
+/* and sum the slots in rank order: C ends replicated on every rank and is    */
+/* bitwise equal to the TSM_COMM_DETERMINISTIC (allgather + rank-order sum)   */
+/* result.  Setup: tsm_peer_create on every rank, tsm_peer_export -> 64-byte  */
+/* IPC handle, exchange all handles (e.g. torch.distributed all_gather), then */
+/* tsm_peer_open with the nranks handles in rank order (the own handle is     */
+/* ignored).  Ranks may share a device (separate processes).  Calls must be   */
+/* issued in the same order on every rank, one stream per tsm_peer.  A rank   */
+/* that never arrives makes the others give up after 2 s: C = NaN and         */
+/* tsm_peer_error reports 1 (after a stream sync) -- no GPU hang.             */
+/* ------------------------------------------------------------------------ */
+typedef struct tsm_peer_s *tsm_peer;
+/* nranks in [1, 8], rank in [0, nranks); allocates and zeroes the slot buffer
+ * on `device`.  TSM_ERR_CUDA on allocation failure. */
+tsm_status tsm_peer_create(tsm_peer *out, int nranks, int rank, int device);
+/* 64-byte cudaIpcMemHandle of this rank's slot buffer (host memory out). */
+tsm_status tsm_peer_export(tsm_peer p, void *handle64);
+/* handles: nranks x 64 bytes (host), rank order.  Opens every peer's buffer
+ * (cudaIpcOpenMemHandle, lazy peer access).  TSM_ERR_CUDA if a handle cannot
+ * be opened (e.g. no P2P path). */
+tsm_status tsm_peer_open(tsm_peer p, const void *handles);
+tsm_status tsm_peer_destroy(tsm_peer p);
+/* 1 if a fused reduction on this tsm_peer timed out waiting for a rank. */
+tsm_status tsm_peer_error(tsm_peer p, int *err);
+/* C = sum over ranks of A_r^T B_r (plain transpose; A^H B with a conj plan),
+ * replicated.  Arguments as tsmttsm_d / tsmttsm_z with K_local >= 0 (an
+ * empty shard contributes zeros); the plan's workspace rules apply. */
+tsm_status tsmttsm_peer_d(tsm_plan p, tsm_peer c, int64_t K_local, const double *A,
+                          const double *B, double *C, void *ws, size_t ws_bytes,
+                          tsm_stream stream);
+tsm_status tsmttsm_peer_z(tsm_plan p, tsm_peer c, int64_t K_local, const tsm_zcomplex *A,
+                          const tsm_zcomplex *B, tsm_zcomplex *C, void *ws, size_t ws_bytes,
+                          tsm_stream stream);
+
 /* Library / build information (JSON), e.g. the list of AOT instantiations. */
 const char *tsm_build_info(void);
 

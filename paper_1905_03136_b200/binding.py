@@ -37,7 +37,8 @@ EXPORTS = [
     "tsmttsm_allreduce_d", "tsmttsm_allreduce_z", "tsmm_bcast_d", "tsmm_bcast_z",
     "tsm_build_info", "tsm_plan_create_ex", "tsm_plan_get_flags", "tsmm_update_d", "tsmm_update_z",
     "tsm_cgs_step_d", "tsm_cgs_step_z", "tsmttsm_ld_d", "tsmttsm_ld_z", "tsmm_ld_d", "tsmm_ld_z",
-    "tsm_jit_precompile",
+    "tsm_jit_precompile", "tsm_peer_create", "tsm_peer_export", "tsm_peer_open", "tsm_peer_destroy",
+    "tsm_peer_error", "tsmttsm_peer_d", "tsmttsm_peer_z",
 ]
 
 
@@ -104,6 +105,13 @@ def _load():
         "tsmm_ld_d": [P, I64, VP, I64, VP, VP, I64, VP],
         "tsmm_ld_z": [P, I64, VP, I64, VP, VP, I64, VP],
         "tsm_jit_precompile": [I, I, I, I, ctypes.POINTER(TsmConfig), ctypes.c_uint],
+        "tsm_peer_create": [ctypes.POINTER(P), I, I, I],
+        "tsm_peer_export": [P, VP],
+        "tsm_peer_open": [P, VP],
+        "tsm_peer_destroy": [P],
+        "tsm_peer_error": [P, ctypes.POINTER(I)],
+        "tsmttsm_peer_d": [P, P, I64, VP, VP, VP, VP, SZ, VP],
+        "tsmttsm_peer_z": [P, P, I64, VP, VP, VP, VP, SZ, VP],
     }
     for name, args in sig.items():
         f = getattr(lib, name)
@@ -508,3 +516,57 @@ def tsmm_bcast(comm: Comm, A, C, root: int = 0, out=None):
     check(f(plan.handle, comm.handle, root, K, A.data_ptr(), C.data_ptr(), B.data_ptr(), stream),
           "tsmm_bcast")
     return B
+
+
+# ---------------------------------------------------------------------------
+# NEXT N3: TSMTTSM with the grid reduction fused with the cross-GPU sum over
+# peer memory (CUDA IPC + NVLink P2P; include/libtsm.h tsm_peer_*)
+# ---------------------------------------------------------------------------
+class PeerComm:
+    """One per rank.  The 64-byte IPC handles of the slot buffers are exchanged
+    with torch.distributed.all_gather_object (any backend, e.g. gloo)."""
+
+    def __init__(self, rank: int, world: int, device: int, group=None):
+        import torch.distributed as dist
+        h = ctypes.c_void_p()
+        check(lib.tsm_peer_create(ctypes.byref(h), world, rank, device), "tsm_peer_create")
+        self.handle = h.value
+        self.rank, self.world, self.device = rank, world, device
+        mine = ctypes.create_string_buffer(64)
+        check(lib.tsm_peer_export(self.handle, mine), "tsm_peer_export")
+        if world > 1:
+            got = [None] * world
+            dist.all_gather_object(got, bytes(mine.raw), group=group)
+        else:
+            got = [bytes(mine.raw)]
+        allh = ctypes.create_string_buffer(b"".join(got), 64 * world)
+        check(lib.tsm_peer_open(self.handle, allh), "tsm_peer_open")
+
+    def error(self) -> int:
+        v = ctypes.c_int()
+        check(lib.tsm_peer_error(self.handle, ctypes.byref(v)), "tsm_peer_error")
+        return v.value
+
+    def close(self):
+        if self.handle:
+            check(lib.tsm_peer_destroy(self.handle), "tsm_peer_destroy")
+            self.handle = None
+
+
+def tsmttsm_peer(peer: PeerComm, A, B, out=None, plan: Plan | None = None):
+    """C = sum over ranks of A_r^T B_r, replicated, with the grid reduction
+    fused with the cross-GPU rank-order sum (no NCCL call).  A, B: this rank's
+    K_local x M / K_local x N rows (K_local may be 0)."""
+    torch = _torch()
+    _check_cuda(A, B)
+    dt = _dtype_code(A)
+    K, M = A.shape
+    N = B.shape[1]
+    plan = plan or get_plan("tsmttsm", dt, M, N, A.device.index)
+    C = out if out is not None else torch.empty((M, N), dtype=A.dtype, device=A.device)
+    stream = torch.cuda.current_stream(A.device).cuda_stream
+    ws = workspace(plan, K, stream)
+    f = lib.tsmttsm_peer_z if dt == "z" else lib.tsmttsm_peer_d
+    check(f(plan.handle, peer.handle, K, A.data_ptr(), B.data_ptr(), C.data_ptr(), ws.data_ptr(),
+            ws.numel(), stream), "tsmttsm_peer")
+    return C

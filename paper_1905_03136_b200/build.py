@@ -27,7 +27,7 @@ HEADERS = ["tsm_kernels.cuh", "tsm_registry.h", "tsm_internal.h", "gen/kernel_so
 
 
 def _sources():
-    srcs = [os.path.join(CSRC, f) for f in ("tsm_api.cu", "tsm_comm.cu", "tsm_registry.cpp",
+    srcs = [os.path.join(CSRC, f) for f in ("tsm_api.cu", "tsm_comm.cu", "tsm_peer.cu", "tsm_registry.cpp",
                                             "tsm_jit.cpp")]
     gen = os.path.join(CSRC, "gen")
     srcs += sorted(os.path.join(gen, f) for f in os.listdir(gen)

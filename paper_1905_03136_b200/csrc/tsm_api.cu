@@ -646,7 +646,7 @@ static tsm_status check_ld(const tsm_plan_s* p, int dt, long long* lda, long lon
 
 tsm_status launch_tsmttsm(const tsm_plan_s* p, int dt, long long K, const void* A, const void* B,
                           void* C, void* ws, size_t ws_bytes, void* stream, bool allow_k0,
-                          long long lda, long long ldb) {
+                          long long lda, long long ldb, const PeerArgs* peer) {
   if (!p) return fail(TSM_ERR_INVALID_VALUE, "plan == NULL");
   if (p->op != TSM_OP_TSMTTSM || p->dt != dt)
     return fail(TSM_ERR_INVALID_VALUE, "plan op/dtype does not match the call");
@@ -683,6 +683,12 @@ tsm_status launch_tsmttsm(const tsm_plan_s* p, int dt, long long K, const void* 
   a.nfin = g.nfin;
   a.order = p->order;
   a.conj = (p->flags & TSM_FLAG_CONJ) ? (1ull << 63) : 0ull;
+  if (peer) {
+    a.peer = *peer;
+  } else {
+    a.peer = PeerArgs{};
+    a.peer.nranks = 0;
+  }
   if (p->k->impl == 2 && K > 0) {
     const int S = dt == TSM_Z ? 2 : 1;
     tsm_status st = make_tmap(&a.tmA, A, K, p->M * S, p->k->R, lda * S);

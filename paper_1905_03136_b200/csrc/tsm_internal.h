@@ -26,9 +26,10 @@ tsm_status fail(tsm_status s, const std::string& why);
 
 // Launch paths (tsm_api.cu).  allow_k0: the sharded layer may pass K = 0.
 // lda, ldb: row strides in elements (0 = dense: M, N); strided views need a TMA kernel.
+struct PeerArgs;  // tsm_kernels.cuh (NEXT N3: fused cross-GPU reduction)
 tsm_status launch_tsmttsm(const tsm_plan_s* p, int dt, long long K, const void* A, const void* B,
                           void* C, void* ws, size_t ws_bytes, void* stream, bool allow_k0,
-                          long long lda = 0, long long ldb = 0);
+                          long long lda = 0, long long ldb = 0, const PeerArgs* peer = nullptr);
 // TSMM output mode (NEXT N1): B = alpha A C (reduce = 0) or B += alpha A C (reduce = 1).
 struct TsmmMode {
   double alpha_re = 1.0, alpha_im = 0.0;

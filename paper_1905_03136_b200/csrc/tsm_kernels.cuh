@@ -121,6 +121,46 @@ __device__ __forceinline__ u32 ld_acquire_gpu(const u32* p) {
   return v;
 }
 
+__device__ __forceinline__ u64 ld_acquire_sys(const u64* p) {
+  u64 v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ u64 globaltimer_ns() {
+  u64 t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+// NEXT N3: the TSMTTSM grid
+// reduction fused with the cross-GPU sum over peer memory (CUDA IPC mappings
+// of every rank's slot buffer, NVLink P2P stores).  Slot buffer of a rank:
+//   [0, 256) bytes   header: u64 cnt[2] (arrivals per parity), u32 err
+//   [256, ...)       double slot[2 parities][kMaxPeers ranks][kPeerCells]
+// Each rank's finishers store their cells of the local C into slot[par][rank]
+// of EVERY rank; the last finisher then adds 1 to every rank's cnt[par]
+// (system-scope atomics after a system fence); every finisher waits for
+// cnt[par] >= target and sums the nranks slots in rank order into C -- C is
+// replicated and bitwise identical to the deterministic allgather + rank-order
+// sum.  Parities alternate per call: a rank can only reuse a parity after every
+// rank has finished the call before (it needed their arrivals), so a slot is
+// never overwritten while it is read.  A bounded wait (2 s) sets err and
+// leaves C = NaN instead of hanging the GPU.
+constexpr int kMaxPeers = 8;
+constexpr int kPeerCells = 64 * 64 * 2;
+constexpr int kPeerHeaderBytes = 256;
+struct PeerArgs {
+  double* base[kMaxPeers];  // slot buffers of every rank (this rank's own at [rank])
+  int nranks;               // 0: no peer reduction (C is the local result)
+  int rank;
+  int parity;
+  u64 target;               // cnt[parity] value that means "all ranks arrived"
+};
+__device__ __forceinline__ double* peer_slot(const PeerArgs& q, int owner, int src) {
+  return reinterpret_cast<double*>(reinterpret_cast<char*>(q.base[owner]) + kPeerHeaderBytes) +
+         (static_cast<long long>(q.parity) * kMaxPeers + src) * kPeerCells;
+}
+
 // Complex multiply-add on (re, im) accumulators, plain (non-conjugating):
 //   re += ar*br - ai*bi ; im += ar*bi + ai*br   (4 DFMA, 8 flops)
 __device__ __forceinline__ void zfma(double& re, double& im, double ar, double ai, double br,
@@ -235,6 +275,7 @@ struct TsmttsmArgs {
   int nfin;            // finisher blocks of the grid reduction
   int order;           // consumer-warp order (spread_warp)
   u64 conj;            // Z: sign mask XORed into Im(A) -- 1<<63 gives C = A^H B (NEXT N2)
+  PeerArgs peer;       // NEXT N3: fused cross-GPU reduction (peer.nranks == 0: off)
 };
 
 // M, N: widths.  Z: complex.  MT, NTL: tiles per row along m / n (powers of
@@ -343,6 +384,15 @@ __device__ __forceinline__ void grid_reduce(const TsmttsmArgs& p, const double* 
   __syncthreads();
   // finisher f owns cells [c0, c1); TPC threads per cell split the block
   // range into contiguous segments, combined afterwards in segment order.
+  const PeerArgs& pq = p.peer;
+  // local C cell -> C (single GPU), or -> slot[parity][rank] of every rank (N3)
+  auto put = [&](int idx, double v) {
+    if (pq.nranks == 0) {
+      p.C[idx] = v;
+    } else {
+      for (int r = 0; r < pq.nranks; r++) __stcg(peer_slot(pq, r, pq.rank) + idx, v);
+    }
+  };
   const int cpf = (CELLS + nfin - 1) / nfin;
   const int c0 = f * cpf;
   const int c1 = (c0 + cpf < CELLS) ? c0 + cpf : CELLS;
@@ -359,7 +409,7 @@ __device__ __forceinline__ void grid_reduce(const TsmttsmArgs& p, const double* 
         double s0 = 0.0;
 #pragma unroll 8
         for (int g = 0; g < G; g++) s0 += __ldcg(&p.partials[static_cast<long long>(g) * CELLS + idx]);
-        p.C[idx] = s0;
+        put(idx, s0);
       }
     } else {
       if (seg < tpc) {
@@ -375,18 +425,50 @@ __device__ __forceinline__ void grid_reduce(const TsmttsmArgs& p, const double* 
       if (tid < ncell) {
         double s0 = sSeg[tid];
         for (int q = 1; q < tpc; q++) s0 += sSeg[q * ncell + tid];
-        p.C[c0 + tid] = s0;
+        put(c0 + tid, s0);
       }
     }
   }
-  __threadfence();
+  if (pq.nranks == 0) __threadfence();
+  else __threadfence_system();  // peer stores visible before this rank's arrival is signalled
   __syncthreads();
   if (tid == 0) {
     const u32 d = atomicAdd(&p.counters[1], 1u);
     if (d == static_cast<u32>(nfin - 1)) {  // last finisher: reset for the next call
       p.counters[0] = 0;
       p.counters[1] = 0;
+      if (pq.nranks > 0) {  // every finisher of this rank has stored (and fenced): signal
+        __threadfence_system();
+        for (int r = 0; r < pq.nranks; r++)
+          atomicAdd_system(reinterpret_cast<unsigned long long*>(pq.base[r]) + pq.parity, 1ull);
+      }
     }
+  }
+  if (pq.nranks == 0) return;
+  // ---- N3: wait for every rank's cells, then the rank-order sum of this finisher's cells ----
+  __shared__ int s_ok;
+  if (tid == 0) {
+    const u64* cnt = reinterpret_cast<const u64*>(pq.base[pq.rank]) + pq.parity;
+    const u64 t0 = globaltimer_ns();
+    int ok = 1;
+    while (ld_acquire_sys(cnt) < pq.target) {
+      __nanosleep(128);
+      if (globaltimer_ns() - t0 > 2000000000ull) {  // a rank never arrived: report, do not hang
+        atomicExch(reinterpret_cast<u32*>(reinterpret_cast<char*>(pq.base[pq.rank]) + 16), 1u);
+        ok = 0;
+        break;
+      }
+    }
+    s_ok = ok;
+  }
+  __syncthreads();
+  for (int idx = c0 + tid; idx < c1; idx += NT) {
+    double v = __longlong_as_double(0x7ff8000000000000ll);  // NaN if the wait timed out
+    if (s_ok) {
+      v = __ldcv(peer_slot(pq, pq.rank, 0) + idx);
+      for (int r = 1; r < pq.nranks; r++) v += __ldcv(peer_slot(pq, pq.rank, r) + idx);
+    }
+    p.C[idx] = v;
   }
 }
 
