@@ -430,9 +430,11 @@ __device__ __forceinline__ void grid_reduce(const TsmttsmArgs& p, const double* 
     }
   }
   if (pq.nranks == 0) __threadfence();
-  else __threadfence_system();  // peer stores visible before this rank's arrival is signalled
   __syncthreads();
   if (tid == 0) {
+    // N3: one system-scope fence per block after the CTA barrier (cumulative over
+    // the block's peer stores) instead of one per thread
+    if (pq.nranks > 0) __threadfence_system();
     const u32 d = atomicAdd(&p.counters[1], 1u);
     if (d == static_cast<u32>(nfin - 1)) {  // last finisher: reset for the next call
       p.counters[0] = 0;
