@@ -142,7 +142,11 @@ typedef struct tsm_config {
                    1024 plain consumer-warp order (DMMA kernels): by default the
                        warps of one C tile / column group are spread over the 4 SM
                        sub-partitions; this flag keeps warp w on tile w % tiles.
-                       A launch argument, not a separate kernel.
+                       A launch argument, not a separate kernel;
+                   2048 inline edge (DMMA TSMTTSM 1/2, not with 16): DMMA on the
+                       8-aligned core, and the consumer warps themselves compute
+                       the cells outside it with DFMA between their DMMAs (each
+                       warp tile of a row slot owns some edge lane groups).
                  Invalid combinations return TSM_ERR_INVALID_VALUE. */
   int p3;
 } tsm_config;

@@ -305,6 +305,17 @@ static tsm_status validate_config_real(const KernelEntry& e) {
   } else if (e.edge & 12) {
     return bad("edge warp count bits (kernel bits 6-7) need the edge flag (kernel | 16)");
   }
+  if (ei_flag(e.edge)) {  // inline edge: consumer warps compute the edge strips
+    if (e.op != KIND_TSMTTSM || (e.impl != 1 && e.impl != 2))
+      return bad("inline edge (kernel | 2048) applies to the DMMA TSMTTSM kernels 1 and 2");
+    if (e.edge & 1) return bad("inline edge (kernel | 2048) excludes edge warps (kernel | 16)");
+    if (e.M < 8 || e.N < 8 || (e.M % 8 == 0 && e.N % 8 == 0))
+      return bad("inline edge needs M, N >= 8 and a width that is not a multiple of 8");
+    const int S = e.dt == TSM_Z ? 2 : 1;
+    const int MC = (e.M / 8) * 8, NC = (e.N / 8) * 8;
+    const int eregs = ((e.M - MC) * ((e.N + 31) / 32) + ((MC + 31) / 32) * (e.N - NC)) * S;
+    if (eregs > 16) return bad("inline edge strips too large for the consumer warps (> 16 accumulators per lane)");
+  }
   if (e.impl == 4) {
     if (e.op != KIND_TSMM) return bad("kernel 4 (C-stationary, bulk copies) is a TSMM kernel");
     const int S = e.dt == TSM_Z ? 2 : 1;
@@ -344,8 +355,8 @@ static tsm_status validate_config_real(const KernelEntry& e) {
       return bad("kernel 2 needs 16-byte rows of >= 128 bytes (M*S, N*S even and >= 16)");
     if (e.R % 8 || e.R > 256) return bad("kernel 2 needs rows_per_chunk a multiple of 8, <= 256");
     const int ed = edge_warps(e.edge);
-    const int MB = ed ? e.M / 8 : (e.M + 7) / 8;  // (pair mode: an odd last block loads single)
-    const int NB = ed ? e.N / 8 : (e.N + 7) / 8;
+    const int MB = (ed || ei_flag(e.edge)) ? e.M / 8 : (e.M + 7) / 8;  // (pair mode: an odd last block loads single)
+    const int NB = (ed || ei_flag(e.edge)) ? e.N / 8 : (e.N + 7) / 8;
     if (e.p0 < 1 || e.p1 < 1 || e.p0 > MB || e.p1 > NB) return bad("WM, WN must be in [1, ceil(M/8)], [1, ceil(N/8)]");
     const int WT = ((MB + e.p0 - 1) / e.p0) * ((NB + e.p1 - 1) / e.p1);
     const int NW = e.NT / 32 - 1 - ed;
@@ -353,8 +364,8 @@ static tsm_status validate_config_real(const KernelEntry& e) {
     if (e.R % (4 * (NW / WT))) return bad("rows_per_chunk must be a multiple of 4 * row slots");
   } else if (e.op == KIND_TSMTTSM && e.impl == 1) {
     const int ed = edge_warps(e.edge);
-    const int MB = ed ? e.M / 8 : (e.M + 7) / 8;  // (pair mode: an odd last block loads single)
-    const int NB = ed ? e.N / 8 : (e.N + 7) / 8;
+    const int MB = (ed || ei_flag(e.edge)) ? e.M / 8 : (e.M + 7) / 8;  // (pair mode: an odd last block loads single)
+    const int NB = (ed || ei_flag(e.edge)) ? e.N / 8 : (e.N + 7) / 8;
     if (e.p0 < 1 || e.p1 < 1 || e.p0 > MB || e.p1 > NB) return bad("WM, WN must be in [1, ceil(M/8)], [1, ceil(N/8)]");
     const int WT = ((MB + e.p0 - 1) / e.p0) * ((NB + e.p1 - 1) / e.p1);
     const int NW = e.NT / 32 - 1 - ed;
@@ -476,7 +487,7 @@ tsm_status tsm_plan_create_config(tsm_plan* out, tsm_op op, tsm_dtype dtype, int
   e.p0 = cfg->p0;
   e.p1 = cfg->p1;
   e.impl = cfg->kernel & 15;
-  e.edge = (cfg->kernel >> 4) & 127;
+  e.edge = (cfg->kernel >> 4) & 255;
   e.p2 = (op == TSM_OP_TSMTTSM && e.impl == 0) ? 0 : cfg->p2;
   e.p3 = (op == TSM_OP_TSMTTSM && e.impl >= 1) ? cfg->p3 : 0;
   e.stages = cfg->stages;
@@ -533,7 +544,7 @@ tsm_status tsm_jit_precompile(tsm_op op, tsm_dtype dtype, int M, int N, const ts
     e.p0 = cfg->p0;
     e.p1 = cfg->p1;
     e.impl = cfg->kernel & 15;
-    e.edge = (cfg->kernel >> 4) & 127;
+    e.edge = (cfg->kernel >> 4) & 255;
     e.p2 = (op == TSM_OP_TSMTTSM && e.impl == 0) ? 0 : cfg->p2;
     e.p3 = (op == TSM_OP_TSMTTSM && e.impl >= 1) ? cfg->p3 : 0;
     e.stages = cfg->stages;
@@ -563,7 +574,7 @@ tsm_status tsm_plan_get_config(tsm_plan p, tsm_config* cfg) {
   cfg->p1 = p->k->p1;
   cfg->p2 = p->k->p2;
   cfg->p3 = p->k->p3;
-  cfg->kernel = p->k->impl | (((p->k->edge & 63) | (p->order << 6)) << 4);
+  cfg->kernel = p->k->impl | (((p->k->edge & ~64) | (p->order << 6)) << 4);
   cfg->stages = p->stages;
   cfg->ctas_per_sm = p->ctas_per_sm;
   return TSM_SUCCESS;
@@ -833,6 +844,7 @@ tsm_status tsm_plan_describe(tsm_plan p, int64_t K, char* buf, size_t len) {
   if (p->op == TSM_OP_TSMM && (k->edge & 1)) kname += "+dfma-edge-columns";
   if (zr_flag(k->edge)) kname += "+complex-as-real(2Mx2N)";
   if (g3_flag(k->edge)) kname += "+3m";
+  if (ei_flag(k->edge)) kname += "+inline-edge";
   if (p->order) kname += "+plain-warp-order";
   if (p->op == TSM_OP_TSMTTSM && k->impl >= 1)
     snprintf(tmp, sizeof tmp,

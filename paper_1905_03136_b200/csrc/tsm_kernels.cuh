@@ -677,10 +677,15 @@ constexpr int pick_kdist(int ap, int bp, bool z, bool pair, int r) {
 // one 16-byte LDS.128 per lane feeds both fragments (half the load
 // instructions of one LDS.64 per fragment).
 template <int M_, int N_, bool Z_, int WM_, int WN_, int NW_, int R_, int AP_ = M_, int BP_ = N_,
-          bool TMA_ = false, int EDGE_ = 0, bool PAIR_ = false, bool ZR_ = false, bool G3_ = false>
+          bool TMA_ = false, int EDGE_ = 0, bool PAIR_ = false, bool ZR_ = false, bool G3_ = false,
+          bool EI_ = false>
 struct TsmttsmMmaCfg {
   static constexpr int M = M_, N = N_, WM = WM_, WN = WN_, NW = NW_, R = R_;
-  static constexpr bool Z = Z_, TMA = TMA_, EDGE = EDGE_ > 0, PAIR = PAIR_, ZR = ZR_, G3 = G3_;
+  // EI ("inline edge", kernel | 2048): the edge cells are computed by the
+  // consumer warps themselves, interleaved with their DMMAs (no edge warps)
+  static constexpr bool EI = EI_;
+  static constexpr bool Z = Z_, TMA = TMA_, EDGE = EDGE_ > 0 || EI_, PAIR = PAIR_, ZR = ZR_, G3 = G3_;
+  static_assert(!(EI_ && EDGE_ > 0), "inline edge excludes edge warps");
   static_assert(!G3 || Z_, "3M (Gauss) products: complex kernel");
   static_assert(!ZR || (!Z_ && M_ % 2 == 0 && N_ % 2 == 0), "complex-as-real: real kernel on 2M x 2N");
   static_assert(!PAIR || (!Z_ && WM_ % 2 == 0 && WN_ % 2 == 0), "pairs: real, even tiles");
@@ -977,6 +982,61 @@ __global__ void __launch_bounds__(Cfg::NT) tsmttsm_mma_kernel(const __grid_const
     }
   };
 
+  // EI: the consumer warps of a row slot share the edge work of the 4 rows of
+  // each k-step.  Groups: row-strip lane group u (cells (MC+i, lane+32u), i <
+  // MR, one B load + MR broadcasts of A) for u < UN, then column-strip lane
+  // group u (cells (lane+32u, NC+i), one A load + NR broadcasts of B); group g
+  // belongs to the warp tile g % WT of the slot.
+  constexpr int NGRP = UN + UM;
+  auto edge_inline = [&](const double* __restrict__ sA, const double* __restrict__ sB, int k0, int rows,
+                         int ap, int bp) {
+    constexpr int KD = Cfg::KD;
+    const int base = (k0 & ~(4 * KD - 1)) + ((k0 >> 2) & (KD - 1));
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+      const int r = base + KD * j;
+      if (r >= rows) break;  // (warp-uniform)
+#pragma unroll
+      for (int g = 0; g < NGRP; g++) {
+        if (g % Cfg::WT != wt) continue;  // (warp-uniform)
+        if (g < UN) {
+          if constexpr (MR > 0) {
+            const int u = g, n = lane + 32 * u;
+            double bv[S];
+#pragma unroll
+            for (int z = 0; z < S; z++) bv[z] = (n < N) ? sB[off(r, n, bp) + z] : 0.0;
+#pragma unroll
+            for (int i = 0; i < MR; i++) {
+              if constexpr (!Cfg::Z) {
+                er[i][u][0] = fma(sA[off(r, Cfg::MC + i, ap)], bv[0], er[i][u][0]);
+              } else {
+                const double2 a = *reinterpret_cast<const double2*>(sA + off(r, Cfg::MC + i, ap));
+                zfma(er[i][u][0], er[i][u][1], a.x, flip_sign(a.y, p.conj), bv[0], bv[S - 1]);
+              }
+            }
+          }
+        } else {
+          if constexpr (NR > 0) {
+            const int u = g - UN, m = lane + 32 * u;
+            double av[S];
+#pragma unroll
+            for (int z = 0; z < S; z++) av[z] = (m < Cfg::MC) ? sA[off(r, m, ap) + z] : 0.0;
+            if constexpr (Cfg::Z) av[S - 1] = flip_sign(av[S - 1], p.conj);
+#pragma unroll
+            for (int i = 0; i < NR; i++) {
+              if constexpr (!Cfg::Z) {
+                ec[u][i][0] = fma(av[0], sB[off(r, Cfg::NC + i, bp)], ec[u][i][0]);
+              } else {
+                const double2 b = *reinterpret_cast<const double2*>(sB + off(r, Cfg::NC + i, bp));
+                zfma(ec[u][i][0], ec[u][i][1], av[0], av[S - 1], b.x, b.y);
+              }
+            }
+          }
+        }
+      }
+    }
+  };
+
   if (warp == NW + Cfg::NE) {
     // ---------------- producer warp: bulk / tensor copies into the ring ----------------
     const u64 pol = policy_evict_first();
@@ -1047,18 +1107,26 @@ __global__ void __launch_bounds__(Cfg::NT) tsmttsm_mma_kernel(const __grid_const
         const int rows = Cfg::TMA ? R : static_cast<int>((K_even - r0 < R) ? (K_even - r0) : R);
         if (rows == R) {
 #pragma unroll 2
-          for (int k0 = slot * 4; k0 < R; k0 += RS * 4) kstep(cm, cn, sA, sB, k0, R, AP, BP);
+          for (int k0 = slot * 4; k0 < R; k0 += RS * 4) {
+            kstep(cm, cn, sA, sB, k0, R, AP, BP);
+            if constexpr (Cfg::EI) edge_inline(sA, sB, k0, R, AP, BP);
+          }
         } else {  // partial chunk: every k-step of the atoms that hold rows < rows
           const int kend = (rows + 4 * Cfg::KD - 1) & ~(4 * Cfg::KD - 1);
-          for (int k0 = slot * 4; k0 < kend; k0 += RS * 4) kstep(cm, cn, sA, sB, k0, rows, AP, BP);
+          for (int k0 = slot * 4; k0 < kend; k0 += RS * 4) {
+            kstep(cm, cn, sA, sB, k0, rows, AP, BP);
+            if constexpr (Cfg::EI) edge_inline(sA, sB, k0, rows, AP, BP);
+          }
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s]);
       }
       // odd last row: a k-step whose rows 1..3 are zero, from global memory
       if constexpr (!Cfg::TMA) {
-        if ((K & 1) && blockIdx.x == 0 && slot == 0)
+        if ((K & 1) && blockIdx.x == 0 && slot == 0) {
           kstep(cm, cn, p.A + (K - 1) * M * S, p.B + (K - 1) * N * S, 0, 1, M, N);
+          if constexpr (Cfg::EI) edge_inline(p.A + (K - 1) * M * S, p.B + (K - 1) * N * S, 0, 1, M, N);
+        }
       }
     };
     // warp-uniform dispatch on whether this warp's tile is the last (partial) one
@@ -1111,7 +1179,35 @@ __global__ void __launch_bounds__(Cfg::NT) tsmttsm_mma_kernel(const __grid_const
         }
       }
     }
-    if constexpr (Cfg::EDGE) {  // edge cells are disjoint from the core; edge warps in order
+    if constexpr (Cfg::EI) {  // inline edge: the owning warp tile of each group, slot by slot
+      if (warp < NW && slot == sl) {
+        auto put = [&](int m, int n, const double* v) {
+#pragma unroll
+          for (int z = 0; z < S; z++) {
+            const int idx = (m * N + n) * S + z;
+            sP[idx] = (sl == 0) ? v[z] : sP[idx] + v[z];
+          }
+        };
+#pragma unroll
+        for (int g = 0; g < NGRP; g++) {
+          if (g % Cfg::WT != wt) continue;
+          if (g < UN) {
+            if constexpr (MR > 0) {
+#pragma unroll
+              for (int i = 0; i < MR; i++)
+                if (lane + 32 * g < N) put(Cfg::MC + i, lane + 32 * g, er[i][g]);
+            }
+          } else {
+            if constexpr (NR > 0) {
+#pragma unroll
+              for (int i = 0; i < NR; i++)
+                if (lane + 32 * (g - UN) < Cfg::MC) put(lane + 32 * (g - UN), Cfg::NC + i, ec[g - UN][i]);
+            }
+          }
+        }
+      }
+    }
+    if constexpr (Cfg::EDGE && !Cfg::EI) {  // edge cells are disjoint from the core; edge warps in order
       if (warp == NW + sl && sl < Cfg::NE) {
         auto put = [&](int m, int n, const double* v) {
 #pragma unroll

@@ -23,7 +23,7 @@ const KernelEntry* find_aot_config(const KernelEntry& want) {
   const KernelEntry* e = find_aot(want.op, want.dt, want.M, want.N);
   if (e && e->NT == want.NT && e->R == want.R && e->p0 == want.p0 && e->p1 == want.p1 &&
       e->p2 == want.p2 && e->p3 == want.p3 && e->impl == want.impl &&
-      (e->edge & 63) == (want.edge & 63))  // bit 6 (warp order) is a launch argument
+      (e->edge & ~64) == (want.edge & ~64))  // bit 6 (warp order) is a launch argument
     return e;
   return nullptr;
 }

@@ -22,7 +22,8 @@ struct KernelEntry {
   int edge;          // DMMA TSMTTSM flags: bit 0 = DFMA edge warps for the cells outside the
                      // 8-aligned core, bit 1 = paired 16-byte fragment loads, bits 2-3 =
                      // edge warps - 1, bit 4 = complex-as-real, bit 5 = 3M (Gauss) complex
-                     // products (tsm_config.kernel bits 4..9)
+                     // products, bit 6 = plain warp order (launch argument), bit 7 = inline
+                     // edge (tsm_config.kernel bits 4..11)
 };
 
 // number of DFMA edge warps encoded in KernelEntry::edge
@@ -36,6 +37,10 @@ inline bool zr_flag(int flags) { return (flags & 16) != 0; }
 // bit 5: Z TSMTTSM by the 3M (Gauss) method -- 3 real DMMAs per 8x8 block
 // (T1 = Ar^T Br, T2 = Ai^T Bi, T3 = (Ar+Ai)^T (Br+Bi)) instead of 4
 inline bool g3_flag(int flags) { return (flags & 32) != 0; }
+
+// bit 7: inline edge -- the DMMA TSMTTSM consumer warps compute the cells outside
+// the 8-aligned core themselves (DFMA interleaved with their DMMAs), no edge warps
+inline bool ei_flag(int flags) { return (flags & 128) != 0; }
 
 // the real problem a complex-as-real entry runs (identity otherwise)
 inline KernelEntry real_view(const KernelEntry& k) {

@@ -247,6 +247,47 @@ def test_tsmttsm_3m(tsm, M, N, conj):
     assert ran
 
 
+@pytest.mark.parametrize("dt,M,N", [("d", 41, 41), ("d", 50, 50), ("d", 57, 57), ("d", 33, 20), ("d", 12, 9),
+                                    ("z", 17, 17), ("z", 33, 33), ("z", 9, 25), ("z", 20, 20)])
+def test_tsmttsm_inline_edge(tsm, dt, M, N):
+    """Inline edge (kernel | 2048): DMMA core + the edge strips computed by the
+    consumer warps between their DMMAs -- every family the generator offers
+    (bulk / TMA, pair, 3M, complex-as-real), plain and conjugate for Z, ragged
+    K within tolerance, integer inputs bit-exact."""
+    cplx = dt == "z"
+    base = [c for c in gi.candidates("tsmttsm", M, N, cplx) if c.get("EI")]
+    if not base:
+        pytest.skip("no inline-edge candidate for this shape")
+    picked = {}
+    for c in base:
+        picked.setdefault((c.get("impl"), c.get("PAIR", 0), c.get("G3", 0), c.get("ZR", 0)), c)
+    ran = 0
+    for key, c in sorted(picked.items()):
+        for conj in ([False, True] if cplx else [False]):
+            try:
+                plan = tsm.Plan("tsmttsm", dt, M, N, 0, config=gi.to_tsm_config("tsmttsm", c, 3, 1), conj=conj)
+            except tsm.TsmError as e:
+                if e.status != 2:
+                    raise
+                continue
+            assert plan.config()["kernel"] & 2048 and "inline-edge" in plan.describe(1000)["kernel"]
+            ran += 1
+            for K in (1, 7, 4099, 65537):
+                A = ti.matrix(K, M, "A", complex_=cplx, seed=K + 71)
+                B = ti.matrix(K, N, "B", complex_=cplx, seed=K + 72)
+                got = tsm.tsmttsm(torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda(), plan=plan, conj=conj)
+                torch.cuda.synchronize()
+                ref, bound = oracle.tsmttsm(A, B, conj=conj)
+                r, wi, _ = oracle.max_err_ratio(got.cpu().numpy(), ref, bound)
+                assert r <= 1e-12, (M, N, key, c, conj, K, r, wi)
+            Ai = ti.matrix(30001, M, "A", complex_=cplx, mode="int")
+            Bi = ti.matrix(30001, N, "B", complex_=cplx, mode="int")
+            got = tsm.tsmttsm(torch.from_numpy(Ai).cuda(), torch.from_numpy(Bi).cuda(), plan=plan, conj=conj)
+            torch.cuda.synchronize()
+            assert np.array_equal(got.cpu().numpy(), oracle.tsmttsm(Ai, Bi, conj=conj)[0]), (key, c, conj)
+    assert ran
+
+
 @pytest.mark.parametrize("conj", [False, True], ids=["C", "conjC"])
 @pytest.mark.parametrize("M,N", [(32, 32), (17, 17), (24, 40), (64, 64), (9, 8), (50, 13)])
 def test_tsmm_3m(tsm, M, N, conj):

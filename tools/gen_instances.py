@@ -182,6 +182,27 @@ def edge_candidates(M: int, N: int, z: bool) -> list:
     return out
 
 
+def inline_edge_candidates(M: int, N: int, z: bool) -> list:
+    """EI=1: the edge candidates without edge warps -- the consumer warps
+    compute the edge strips between their DMMAs (<= 16 strip accumulators
+    per lane)."""
+    S = 2 if z else 1
+    if M < 8 or N < 8 or (M % 8 == 0 and N % 8 == 0):
+        return []
+    MC, NC = (M // 8) * 8, (N // 8) * 8
+    if ((M - MC) * cdiv(N, 32) + cdiv(MC, 32) * (N - NC)) * S > 16:
+        return []
+    out, seen = [], set()
+    for c in edge_candidates(M, N, z):
+        ne = c.pop("EDGE")
+        c = dict(c, NT=c["NT"] - 32 * ne, EI=1)
+        k = tuple(sorted(c.items()))
+        if k not in seen:
+            seen.add(k)
+            out.append(c)
+    return out
+
+
 def pair_stride(w: int) -> int:
     """Smallest even smem stride >= w whose 4 fragment rows start 32 bytes
     apart modulo 128: the 8 lanes of each LDS.128 phase then read 8 distinct
@@ -332,7 +353,7 @@ def cfg_type(op, dt, M, N, c) -> str:
         pair = "true" if c.get("PAIR", 0) else "false"
         return (f"tsm::TsmttsmMmaCfg<{M}, {N}, {z}, {c['MT']}, {c['NTL']}, {c['NT'] // 32 - 1 - edge}, "
                 f"{c['R']}, {c.get('AP', M)}, {c.get('BP', N)}, {tma}, {edge}, {pair}, {zr}, "
-                f"{'true' if c.get('G3', 0) else 'false'}>")
+                f"{'true' if c.get('G3', 0) else 'false'}, {'true' if c.get('EI', 0) else 'false'}>")
     if op == "tsmttsm":
         return f"tsm::TsmttsmCfg<{M}, {N}, {z}, {c['MT']}, {c['NTL']}, {c['NT']}, {c['R']}>"
     if c.get("impl", 0) == 4:
@@ -369,10 +390,12 @@ def flags(c: dict) -> int:
     """KernelEntry.edge / tsm_config.kernel >> 4: bit 0 DFMA edge warps, bit 1
     paired 16-byte fragment loads, bits 2-3 edge warps - 1 (EDGE = edge warp count),
     bit 4 complex-as-real (ZR), bit 5 3M / Gauss complex products (G3), bit 6
-    plain consumer-warp order (PLAIN; a launch argument of the DMMA kernels)."""
+    plain consumer-warp order (PLAIN; a launch argument of the DMMA kernels),
+    bit 7 inline edge (EI: consumer warps compute the edge strips)."""
     e = c.get("EDGE", 0)
     return ((1 if e else 0) | (c.get("PAIR", 0) << 1) | (((e - 1) & 3) << 2 if e else 0)
-            | (c.get("ZR", 0) << 4) | (c.get("G3", 0) << 5) | (c.get("PLAIN", 0) << 6))
+            | (c.get("ZR", 0) << 4) | (c.get("G3", 0) << 5) | (c.get("PLAIN", 0) << 6)
+            | (c.get("EI", 0) << 7))
 
 
 def params4(op: str, M: int, N: int, c: dict) -> tuple:
@@ -554,6 +577,7 @@ def candidates(op: str, M: int, N: int, z: bool) -> list:
                             out.append(dict(MT=WM, NTL=WN, NT=(NW + 1) * 32, R=Rt, impl=2,
                                             AP=M, BP=N))
             out.extend(edge_candidates(M, N, z))
+            out.extend(inline_edge_candidates(M, N, z))
             out.extend(pair_candidates(M, N, z))
     else:
         acc_max = 16 if z else 32
