@@ -2123,10 +2123,33 @@ constexpr int cstb_conflict(int sel, int M, bool z) {
   }
   return worst;
 }
-constexpr int cstb_pick_rho(int M, bool z) {
-  int best = 0;
-  for (int sel = 1; sel < 4; sel++)
-    if (cstb_conflict(sel, M, z) < cstb_conflict(best, M, z)) best = sel;
+// D output staging stores: lane (g, q) writes element (rho(g), 2q + e) of the
+// dense [RW][N] block, one 8-byte store per e -> worst lanes per 8-byte unit
+// over the two 16-lane phases.
+constexpr int cstb_store_conflict(int sel, int N) {
+  int worst = 0;
+  for (int e = 0; e < 2; e++)
+    for (int ph = 0; ph < 2; ph++) {
+      int cnt[16] = {};
+      for (int l = ph * 16; l < ph * 16 + 16; l++) {
+        const int u = (cstb_rho(sel, l >> 2) * N + 2 * (l & 3) + e) % 16;
+        if (++cnt[u] > worst) worst = cnt[u];
+      }
+    }
+  return worst;
+}
+// Row permutation minimising the A fragment loads' conflicts (MK*WR loads per
+// pass, weight 3) plus the D staging stores' (2*NBW*WR per pass, weight 1):
+// ncu r32 showed the stores of D 63 4-way conflicted under the load-only choice.
+constexpr int cstb_pick_rho(int M, int N, bool z) {
+  int best = 0, bc = 1 << 20;
+  for (int sel = 0; sel < 4; sel++) {
+    const int c = 3 * cstb_conflict(sel, M, z) + (z ? 0 : cstb_store_conflict(sel, N));
+    if (c < bc) {
+      bc = c;
+      best = sel;
+    }
+  }
   return best;
 }
 
@@ -2144,7 +2167,7 @@ struct TsmmCstbCfg {
   static constexpr int NT = (NW + 1) * 32;
   static constexpr int STAGE_DOUBLES = ((R * M * S + 15) / 16) * 16;
   static constexpr int OUT_DOUBLES = ((RW * N * S + 15) / 16) * 16;  // one staging buffer
-  static constexpr int RHO = cstb_pick_rho(M, Z);  // conflict-minimising row permutation
+  static constexpr int RHO = cstb_pick_rho(M, N, Z);  // conflict-minimising row permutation
   static_assert(NW % NG == 0 && RG >= 1 && RG <= 15, "consumer warps: a multiple of the column groups, <= 15 row groups");
   static_assert(R % RPP == 0 && R % 2 == 0, "rows per chunk: whole passes");
 };
