@@ -198,3 +198,65 @@ def test_dense_kstep_row_spacing():
             assert lds64(st, 1) == 1, st
         else:
             assert best >= 2, st
+
+
+def test_cstb_row_permutation_loads_and_stores():
+    """Bulk C-stationary TSMM (kernel 4, dense stride-M stage, dense [RW][N]
+    output staging): the permutation chosen by tsm_kernels.cuh
+    cstb_pick_rho (3 x load conflicts + store conflicts) is never worse than
+    the load-only choice it replaced, and for odd widths (the D shapes that
+    need kernel 4) both accesses stay at the 2-way minimum an odd stride
+    allows -- the load-only choice left the D 63 stores 4-way (ncu r32)."""
+    def rho(sel, g):
+        return [g, ((g & 3) << 1) | (g >> 2), ((g & 1) << 2) | (g >> 1),
+                ((g & 1) << 2) | (g & 2) | (g >> 2)][sel]
+
+    def worst(unit):
+        w = 0
+        for ph in range(2):
+            cnt = {}
+            for lane in range(16 * ph, 16 * ph + 16):
+                u = unit(lane >> 2, lane & 3) % 16
+                cnt[u] = cnt.get(u, 0) + 1
+            w = max(w, max(cnt.values()))
+        return w
+
+    def load(sel, M):
+        return worst(lambda g, q: rho(sel, g) * M + q)
+
+    def store(sel, N):
+        return max(worst(lambda g, q: rho(sel, g) * N + 2 * q + e) for e in (0, 1))
+
+    def pick(M, N):  # mirror of cstb_pick_rho (D)
+        return min(range(4), key=lambda s: (3 * load(s, M) + store(s, N), s))
+
+    def pick_old(M):  # the load-only rule
+        best = 0
+        for s in range(1, 4):
+            if load(s, M) < load(best, M):
+                best = s
+        return best
+
+    for w in range(9, 65):
+        new, old = pick(w, w), pick_old(w)
+        assert 3 * load(new, w) + store(new, w) <= 3 * load(old, w) + store(old, w), w
+        if w % 2:
+            assert load(new, w) == 2 and store(new, w) == 2, (w, new)
+    assert store(pick_old(63), 63) == 4 and store(pick(63, 63), 63) == 2
+
+
+def test_flag_encoding_and_new_candidates():
+    """tsm_config.kernel flag bits written by the generator (include/libtsm.h):
+    3M 512, plain warp order 1024, inline edge 2048; inline-edge candidates
+    exist only for widths with an edge and carry no edge warps; 3M
+    candidates only for Z."""
+    base = dict(MT=2, NTL=2, NT=160, R=64, impl=2, AP=32, BP=32)
+    assert gi.to_tsm_config("tsmttsm", dict(base, G3=1), 3, 1)["kernel"] == 2 | 512
+    assert gi.to_tsm_config("tsmttsm", dict(base, PLAIN=1), 3, 1)["kernel"] == 2 | 1024
+    assert gi.to_tsm_config("tsmttsm", dict(base, EI=1), 3, 1)["kernel"] == 2 | 2048
+    assert not [c for c in gi.candidates("tsmttsm", 32, 32, False) if c.get("EI")]
+    ei = [c for c in gi.candidates("tsmttsm", 41, 41, False) if c.get("EI")]
+    assert ei and all("EDGE" not in c for c in ei)
+    assert not [c for c in gi.candidates("tsmttsm", 32, 32, False) if c.get("G3")]
+    assert [c for c in gi.candidates("tsmttsm", 32, 32, True) if c.get("G3")]
+    assert [c for c in gi.candidates("tsmm", 32, 32, True) if c.get("G3")]
