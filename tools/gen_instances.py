@@ -193,13 +193,42 @@ def inline_edge_candidates(M: int, N: int, z: bool) -> list:
     if ((M - MC) * cdiv(N, 32) + cdiv(MC, 32) * (N - NC)) * S > 16:
         return []
     out, seen = [], set()
-    for c in edge_candidates(M, N, z):
-        ne = c.pop("EDGE")
-        c = dict(c, NT=c["NT"] - 32 * ne, EI=1)
+
+    def add(c):
         k = tuple(sorted(c.items()))
         if k not in seen:
             seen.add(k)
             out.append(c)
+
+    for c in edge_candidates(M, N, z):
+        ne = c.pop("EDGE")
+        add(dict(c, NT=c["NT"] - 32 * ne, EI=1))
+    # a wider search of the core tiling: more warp tiles, more row slots (the
+    # consumer warps carry the edge work, so more of them share it)
+    MB, NB = M // 8, N // 8
+    wmax = 8 if z else 16
+    row = (M + N) * 8 * S
+    wt = []
+    for WM in range(1, min(MB, 8) + 1):
+        for WN in range(1, min(NB, 8) + 1):
+            if WM * WN > wmax or cdiv(MB, WM) * cdiv(NB, WN) > 16:
+                continue
+            bal = cdiv(MB, WM) * WM * cdiv(NB, WN) * WN / (MB * NB)
+            wt.append((bal * (1 + 0.5 * (WM + WN) / (WM * WN)), WM, WN))
+    wt.sort()
+    for (_, WM, WN) in wt[:6]:
+        WT = cdiv(MB, WM) * cdiv(NB, WN)
+        for k in (1, 2, 4, 8):
+            NW = WT * k
+            if NW > 16 or NW < 2:
+                continue
+            for tgt in (16384, 32768, 65536):
+                add(dict(MT=WM, NTL=WN, NT=(NW + 1) * 32, R=_rows(16 * k, row, tgt), impl=1, AP=M, BP=N, EI=1))
+                if tma_ok(M, N, z):
+                    tb = (cdiv(M * S, 16) + cdiv(N * S, 16)) * 128
+                    step = 4 * k if (4 * k) % 8 == 0 else 8 * k
+                    Rt = min(256 // step * step, max(step, (tgt // tb) // step * step))
+                    add(dict(MT=WM, NTL=WN, NT=(NW + 1) * 32, R=Rt, impl=2, AP=M, BP=N, EI=1))
     return out
 
 
