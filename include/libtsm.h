@@ -345,8 +345,18 @@ tsm_status tsmm_bcast_z(tsm_plan p, tsm_comm c, int root, int64_t K_local,
 /* tsm_peer_open with the nranks handles in rank order (the own handle is     */
 /* ignored).  Ranks may share a device (separate processes).  Calls must be   */
 /* issued in the same order on every rank, one stream per tsm_peer.  A rank   */
-/* that never arrives makes the others give up after 2 s: C = NaN and         */
-/* tsm_peer_error reports 1 (after a stream sync) -- no GPU hang.             */
+/* that never arrives makes the others give up after the timeout (default   */
+/* 2 s, tsm_peer_set_timeout): C = NaN and tsm_peer_error reports 1 (after a  */
+/* stream sync) -- no GPU hang.  Each slot carries the sequence number of the */
+/* call that wrote it; a reader that finds another call's data (a rank that   */
+/* timed out and ran ahead) also reports the error instead of summing it.     */
+/* Once the error flag of a rank is set, every later fused call on it fails   */
+/* fast (C = NaN, nothing stored to peers, no arrival signalled) until every  */
+/* rank calls tsm_peer_reset.  The parity / arrival target / sequence number  */
+/* are launch arguments: capturing a fused call in a CUDA graph and replaying */
+/* it is NOT supported.  The kernel's finisher blocks spin on arrivals, so    */
+/* every block of the launch must be able to become resident (true for the   */
+/* persistent grids libtsm launches unless another kernel pins the SMs).      */
 /* ------------------------------------------------------------------------ */
 typedef struct tsm_peer_s *tsm_peer;
 /* nranks in [1, 8], rank in [0, nranks); allocates and zeroes the slot buffer
@@ -359,8 +369,16 @@ tsm_status tsm_peer_export(tsm_peer p, void *handle64);
  * be opened (e.g. no P2P path). */
 tsm_status tsm_peer_open(tsm_peer p, const void *handles);
 tsm_status tsm_peer_destroy(tsm_peer p);
-/* 1 if a fused reduction on this tsm_peer timed out waiting for a rank. */
+/* 1 if a fused reduction on this tsm_peer timed out waiting for a rank or
+ * found a slot written by another call (synchronous device read). */
 tsm_status tsm_peer_error(tsm_peer p, int *err);
+/* Bounded wait of later fused calls, in nanoseconds (> 0; default 2e9). */
+tsm_status tsm_peer_set_timeout(tsm_peer p, uint64_t timeout_ns);
+/* Collective recovery after an error: synchronizes `stream`, clears this
+ * rank's counters, error flag and sequence numbers and restarts the call
+ * count.  Every rank must call it (and the caller must barrier afterwards,
+ * e.g. torch.distributed.barrier) before the next fused call. */
+tsm_status tsm_peer_reset(tsm_peer p, tsm_stream stream);
 /* C = sum over ranks of A_r^T B_r (plain transpose; A^H B with a conj plan),
  * replicated.  Arguments as tsmttsm_d / tsmttsm_z with K_local >= 0 (an
  * empty shard contributes zeros); the plan's workspace rules apply. */

@@ -38,7 +38,7 @@ EXPORTS = [
     "tsm_build_info", "tsm_plan_create_ex", "tsm_plan_get_flags", "tsmm_update_d", "tsmm_update_z",
     "tsm_cgs_step_d", "tsm_cgs_step_z", "tsmttsm_ld_d", "tsmttsm_ld_z", "tsmm_ld_d", "tsmm_ld_z",
     "tsm_jit_precompile", "tsm_peer_create", "tsm_peer_export", "tsm_peer_open", "tsm_peer_destroy",
-    "tsm_peer_error", "tsmttsm_peer_d", "tsmttsm_peer_z",
+    "tsm_peer_error", "tsmttsm_peer_d", "tsmttsm_peer_z", "tsm_peer_set_timeout", "tsm_peer_reset",
 ]
 
 
@@ -110,6 +110,8 @@ def _load():
         "tsm_peer_open": [P, VP],
         "tsm_peer_destroy": [P],
         "tsm_peer_error": [P, ctypes.POINTER(I)],
+        "tsm_peer_set_timeout": [P, ctypes.c_uint64],
+        "tsm_peer_reset": [P, VP],
         "tsmttsm_peer_d": [P, P, I64, VP, VP, VP, VP, SZ, VP],
         "tsmttsm_peer_z": [P, P, I64, VP, VP, VP, VP, SZ, VP],
     }
@@ -324,6 +326,38 @@ def _ld(t) -> int:
     return t.stride(0) if t.shape[0] > 1 else t.shape[1]
 
 
+def _check_out(out, shape, like, name="out"):
+    """A caller-supplied output must have exactly the shape, dtype and device
+    the call writes (the C ABI cannot see buffer sizes)."""
+    if out is None:
+        return
+    if tuple(out.shape) != tuple(shape):
+        raise ValueError(f"{name} has shape {tuple(out.shape)}, expected {tuple(shape)}")
+    if out.dtype != like.dtype:
+        raise ValueError(f"{name} has dtype {out.dtype}, expected {like.dtype}")
+    if out.device != like.device:
+        raise ValueError(f"{name} is on {out.device}, expected {like.device}")
+
+
+def _check_plan(plan, op: str, dt: str, M: int, N: int, device: int):
+    """An explicit plan must match the call's op, dtype, widths and device."""
+    if plan is None:
+        return
+    if (plan.op, plan.dtype, plan.M, plan.N) != (op, dt, M, N):
+        raise ValueError(f"plan is ({plan.op}, {plan.dtype}, M={plan.M}, N={plan.N}), "
+                         f"the call is ({op}, {dt}, M={M}, N={N})")
+    if plan.device != device:
+        raise ValueError(f"plan is for device {plan.device}, tensors are on device {device}")
+
+
+def _same(A, *ts):
+    for t in ts:
+        if t.dtype != A.dtype:
+            raise ValueError(f"dtype mismatch: {t.dtype} vs {A.dtype}")
+        if t.device != A.device:
+            raise ValueError(f"device mismatch: {t.device} vs {A.device}")
+
+
 def workspace(plan: Plan, K: int, stream: int, min_bytes: int = 0):
     """Cached, counter-zeroed workspace for (device, stream); grows as needed."""
     torch = _torch()
@@ -349,9 +383,14 @@ def tsmttsm(A, B, out=None, plan: Plan | None = None, conj: bool = False):
     K, M = A.shape
     N = B.shape[1]
     dev = A.device.index
+    _same(A, B)
     lda, ldb = _ld(A), _ld(B)
     dense = lda == M and ldb == N
+    _check_plan(plan, "tsmttsm", dt, M, N, dev)
+    if plan is not None and plan.conj != conj:
+        raise ValueError("conj does not match the plan's TSM_FLAG_CONJ")
     plan = plan or get_plan("tsmttsm", dt, M, N, dev, conj, strided=not dense)
+    _check_out(out, (M, N), A)
     C = out if out is not None else torch.empty((M, N), dtype=A.dtype, device=A.device)
     _check_cuda(C)
     stream = torch.cuda.current_stream(A.device).cuda_stream
@@ -378,10 +417,13 @@ def tsmm(A, C, out=None, plan: Plan | None = None):
     K, M = A.shape
     N = C.shape[1]
     dev = A.device.index
+    _same(A, C)
+    _check_out(out, (K, N), A)
     B = out if out is not None else torch.empty((K, N), dtype=A.dtype, device=A.device)
     _check_rows(B)
     lda, ldb = _ld(A), _ld(B)
     dense = lda == M and ldb == N
+    _check_plan(plan, "tsmm", dt, M, N, dev)
     plan = plan or get_plan("tsmm", dt, M, N, dev, strided=not dense)
     stream = torch.cuda.current_stream(A.device).cuda_stream
     if dense:
@@ -404,6 +446,10 @@ def tsmm_update(A, C, B, alpha=1.0, beta=0.0, plan: Plan | None = None, conj: bo
         raise ValueError("A (K x M), C (M x N), B (K x N): shapes / dtypes do not match")
     K, M = A.shape
     N = C.shape[1]
+    _same(A, C, B)
+    _check_plan(plan, "tsmm", dt, M, N, A.device.index)
+    if plan is not None and plan.conj != conj:
+        raise ValueError("conj does not match the plan's TSM_FLAG_CONJ")
     plan = plan or get_plan("tsmm", dt, M, N, A.device.index, conj)
     stream = torch.cuda.current_stream(A.device).cuda_stream
     f = tsmm_update_z if dt == "z" else tsmm_update_d
@@ -419,11 +465,17 @@ def cgs_step(A, B, C=None, p_tt: Plan | None = None, p_mm: Plan | None = None, c
     torch = _torch()
     _check_cuda(A, B)
     dt = _dtype_code(A)
+    if A.dim() != 2 or B.dim() != 2 or A.shape[0] != B.shape[0]:
+        raise ValueError("A (K x M) and B (K x N) must be 2-D with the same row count")
+    _same(A, B)
     K, M = A.shape
     N = B.shape[1]
     dev = A.device.index
+    _check_plan(p_tt, "tsmttsm", dt, M, N, dev)
+    _check_plan(p_mm, "tsmm", dt, M, N, dev)
     p_tt = p_tt or get_plan("tsmttsm", dt, M, N, dev, dt == "z")
     p_mm = p_mm or get_plan("tsmm", dt, M, N, dev)
+    _check_out(C, (M, N), A, "C")
     C = C if C is not None else torch.empty((M, N), dtype=A.dtype, device=A.device)
     _check_cuda(C)
     stream = torch.cuda.current_stream(A.device).cuda_stream
@@ -490,9 +542,13 @@ def tsmttsm_allreduce(comm: Comm, A, B, out=None):
     torch = _torch()
     _check_cuda(A, B)
     dt = _dtype_code(A)
+    if A.dim() != 2 or B.dim() != 2 or A.shape[0] != B.shape[0]:
+        raise ValueError("A (K x M) and B (K x N) must be 2-D with the same row count")
+    _same(A, B)
     K, M = A.shape
     N = B.shape[1]
     plan = get_plan("tsmttsm", dt, M, N, A.device.index)
+    _check_out(out, (M, N), A)
     C = out if out is not None else torch.empty((M, N), dtype=A.dtype, device=A.device)
     stream = torch.cuda.current_stream(A.device).cuda_stream
     need = plan.workspace_bytes(K) + 256 + comm.extra_bytes(plan)
@@ -507,9 +563,13 @@ def tsmm_bcast(comm: Comm, A, C, root: int = 0, out=None):
     torch = _torch()
     _check_cuda(A, C)
     dt = _dtype_code(A)
+    if A.dim() != 2 or C.dim() != 2 or A.shape[1] != C.shape[0]:
+        raise ValueError("A (K x M) and C (M x N) must be 2-D with matching M")
+    _same(A, C)
     K, M = A.shape
     N = C.shape[1]
     plan = get_plan("tsmm", dt, M, N, A.device.index)
+    _check_out(out, (K, N), A)
     B = out if out is not None else torch.empty((K, N), dtype=A.dtype, device=A.device)
     stream = torch.cuda.current_stream(A.device).cuda_stream
     f = lib.tsmm_bcast_z if dt == "z" else lib.tsmm_bcast_d
@@ -547,6 +607,18 @@ class PeerComm:
         check(lib.tsm_peer_error(self.handle, ctypes.byref(v)), "tsm_peer_error")
         return v.value
 
+    def set_timeout(self, seconds: float) -> None:
+        check(lib.tsm_peer_set_timeout(self.handle, int(seconds * 1e9)), "tsm_peer_set_timeout")
+
+    def reset(self) -> None:
+        """Collective: every rank resets, then barriers (include/libtsm.h)."""
+        import torch
+        import torch.distributed as dist
+        stream = torch.cuda.current_stream(self.device).cuda_stream
+        check(lib.tsm_peer_reset(self.handle, stream), "tsm_peer_reset")
+        if self.world > 1:
+            dist.barrier()
+
     def close(self):
         if self.handle:
             check(lib.tsm_peer_destroy(self.handle), "tsm_peer_destroy")
@@ -560,9 +632,14 @@ def tsmttsm_peer(peer: PeerComm, A, B, out=None, plan: Plan | None = None):
     torch = _torch()
     _check_cuda(A, B)
     dt = _dtype_code(A)
+    if A.dim() != 2 or B.dim() != 2 or A.shape[0] != B.shape[0]:
+        raise ValueError("A (K x M) and B (K x N) must be 2-D with the same row count")
+    _same(A, B)
     K, M = A.shape
     N = B.shape[1]
+    _check_plan(plan, "tsmttsm", dt, M, N, A.device.index)
     plan = plan or get_plan("tsmttsm", dt, M, N, A.device.index)
+    _check_out(out, (M, N), A)
     C = out if out is not None else torch.empty((M, N), dtype=A.dtype, device=A.device)
     stream = torch.cuda.current_stream(A.device).cuda_stream
     ws = workspace(plan, K, stream)

@@ -637,6 +637,30 @@ static bool overlap(const void* a, size_t na, const void* b, size_t nb) {
   return na && nb && x < y + nb && y < x + na;
 }
 
+// Do two (possibly row-strided) operands share an element?  X: rows of wx
+// elements at stride ldx from x; Y likewise; both K rows, s bytes per element.
+// Dense operands compare whole spans.  Two views with the same row stride are
+// column subsets of one block vector: they overlap only if their column
+// intervals (offsets modulo the row pitch) intersect (A = X[:, :M],
+// B = X[:, M:M+N] is legal).
+static bool strided_overlap(const void* x, long long ldx, int wx, const void* y, long long ldy, int wy,
+                            long long K, size_t s) {
+  if (K <= 0) return false;
+  const size_t nx = (static_cast<size_t>(K - 1) * ldx + wx) * s, ny = (static_cast<size_t>(K - 1) * ldy + wy) * s;
+  if (!overlap(x, nx, y, ny)) return false;
+  if (ldx != ldy || (ldx == wx && ldy == wy)) return true;  // different pitches / dense: conservative
+  const long long pitch = ldx * static_cast<long long>(s);
+  const long long d = static_cast<long long>(reinterpret_cast<uintptr_t>(y)) -
+                      static_cast<long long>(reinterpret_cast<uintptr_t>(x));
+  long long off = d % pitch;  // column offset of y's row start inside x's row pitch (bytes)
+  if (off < 0) off += pitch;
+  const long long ax0 = 0, ax1 = wx * static_cast<long long>(s);        // x's columns [ax0, ax1)
+  // y occupies [off, off + wy*s) modulo pitch: test both wrap positions
+  const long long by0 = off, by1 = off + wy * static_cast<long long>(s);
+  auto hit = [](long long a0, long long a1, long long b0, long long b1) { return a0 < b1 && b0 < a1; };
+  return hit(ax0, ax1, by0, by1) || hit(ax0 + pitch, ax1 + pitch, by0, by1) || hit(ax0, ax1, by0 + pitch, by1 + pitch);
+}
+
 bool strided_capable(const KernelEntry& k) {
   return k.op == KIND_TSMTTSM ? k.impl == 2 : (k.impl == 2 || k.impl == 3);
 }
@@ -713,9 +737,11 @@ tsm_status launch_tsmttsm(const tsm_plan_s* p, int dt, long long K, const void* 
   return TSM_SUCCESS;
 }
 
-tsm_status launch_tsmm(const tsm_plan_s* p, int dt, long long K, const void* A, const void* C,
-                       void* B, void* stream, bool allow_k0, const TsmmMode* mode, long long lda,
-                       long long ldb) {
+// Every check of a TSMM launch (plan, K, pointers, alignment, strides,
+// overlap); lda / ldb are normalised (0 -> dense).  Runs before anything is
+// enqueued, also for the update's scale pass.
+static tsm_status validate_tsmm(const tsm_plan_s* p, int dt, long long K, const void* A, const void* C,
+                                void* B, bool allow_k0, long long* lda, long long* ldb) {
   if (!p) return fail(TSM_ERR_INVALID_VALUE, "plan == NULL");
   if (p->op != TSM_OP_TSMM || p->dt != dt)
     return fail(TSM_ERR_INVALID_VALUE, "plan op/dtype does not match the call");
@@ -723,16 +749,22 @@ tsm_status launch_tsmm(const tsm_plan_s* p, int dt, long long K, const void* A, 
   if (!C || (K > 0 && (!A || !B))) return fail(TSM_ERR_INVALID_VALUE, "null pointer");
   if (misaligned(A) || misaligned(B) || misaligned(C))
     return fail(TSM_ERR_MISALIGNED, "A, B and C must be 16-byte aligned");
+  tsm_status st = check_ld(p, dt, lda, ldb, p->M, p->N);
+  if (st != TSM_SUCCESS) return st;
+  const size_t s = (dt == TSM_Z ? 16 : 8);
+  const size_t nC = static_cast<size_t>(p->M) * p->N * s;
+  if (strided_overlap(A, *lda, p->M, B, *ldb, p->N, K, s) || overlap(B, K > 0 ? (static_cast<size_t>(K - 1) * *ldb + p->N) * s : 0, C, nC))
+    return fail(TSM_ERR_INVALID_VALUE, "B overlaps A or C");
+  return TSM_SUCCESS;
+}
+
+tsm_status launch_tsmm(const tsm_plan_s* p, int dt, long long K, const void* A, const void* C,
+                       void* B, void* stream, bool allow_k0, const TsmmMode* mode, long long lda,
+                       long long ldb) {
   {
-    tsm_status st = check_ld(p, dt, &lda, &ldb, p->M, p->N);
+    tsm_status st = validate_tsmm(p, dt, K, A, C, B, allow_k0, &lda, &ldb);
     if (st != TSM_SUCCESS) return st;
   }
-  const size_t s = (dt == TSM_Z ? 16 : 8);
-  const size_t nA = K > 0 ? (static_cast<size_t>(K - 1) * lda + p->M) * s : 0;
-  const size_t nB = K > 0 ? (static_cast<size_t>(K - 1) * ldb + p->N) * s : 0;
-  const size_t nC = static_cast<size_t>(p->M) * p->N * s;
-  if (overlap(B, nB, A, nA) || overlap(B, nB, C, nC))
-    return fail(TSM_ERR_INVALID_VALUE, "B overlaps A or C");
   if (K == 0) return TSM_SUCCESS;
   DeviceGuard dg(p->device);
   if (dg.err != cudaSuccess) return cuda_fail(dg.err, "cudaSetDevice");
@@ -772,12 +804,11 @@ tsm_status launch_tsmm_update(const tsm_plan_s* p, int dt, long long K, double a
   if (dt == TSM_D) ai = bi = 0.0;
   const bool beta0 = br == 0.0 && bi == 0.0, beta1 = br == 1.0 && bi == 0.0;
   if (!beta0 && !beta1 && K > 0) {
-    // validate everything first (same checks as the TSMM launch), then scale B
-    if (p->op != TSM_OP_TSMM || p->dt != dt)
-      return fail(TSM_ERR_INVALID_VALUE, "plan op/dtype does not match the call");
-    if (!A || !B || !C) return fail(TSM_ERR_INVALID_VALUE, "null pointer");
-    if (misaligned(A) || misaligned(B) || misaligned(C))
-      return fail(TSM_ERR_MISALIGNED, "A, B and C must be 16-byte aligned");
+    // validate everything first (every check of the TSMM launch, overlap
+    // included), then scale B: a rejected call leaves B untouched
+    long long lda = 0, ldb = 0;
+    tsm_status vs = validate_tsmm(p, dt, K, A, C, B, allow_k0, &lda, &ldb);
+    if (vs != TSM_SUCCESS) return vs;
     DeviceGuard dg(p->device);
     if (dg.err != cudaSuccess) return cuda_fail(dg.err, "cudaSetDevice");
     DevInfo di;

@@ -135,7 +135,9 @@ __device__ __forceinline__ u64 globaltimer_ns() {
 // NEXT N3: the TSMTTSM grid
 // reduction fused with the cross-GPU sum over peer memory (CUDA IPC mappings
 // of every rank's slot buffer, NVLink P2P stores).  Slot buffer of a rank:
-//   [0, 256) bytes   header: u64 cnt[2] (arrivals per parity), u32 err
+//   [0, 256) bytes   header: u64 cnt[2] (arrivals per parity) at 0, u32 err at 16,
+//                    u64 seq[2 parities][kMaxPeers ranks] at 32 (call number + 1 of
+//                    the data in each slot, written by the slot's source rank)
 //   [256, ...)       double slot[2 parities][kMaxPeers ranks][kPeerCells]
 // Each rank's finishers store their cells of the local C into slot[par][rank]
 // of EVERY rank; the last finisher then adds 1 to every rank's cnt[par]
@@ -144,8 +146,13 @@ __device__ __forceinline__ u64 globaltimer_ns() {
 // replicated and bitwise identical to the deterministic allgather + rank-order
 // sum.  Parities alternate per call: a rank can only reuse a parity after every
 // rank has finished the call before (it needed their arrivals), so a slot is
-// never overwritten while it is read.  A bounded wait (2 s) sets err and
-// leaves C = NaN instead of hanging the GPU.
+// never overwritten while it is read.  A bounded wait (timeout_ns, default 2 s)
+// sets err and leaves C = NaN instead of hanging the GPU.  Every reader also
+// checks each slot's sequence number against this call's, so data from another
+// call (a rank that timed out and ran ahead) is reported, never summed; and once
+// err is set every later call on that rank fails fast (C = NaN, no stores to
+// peers, no arrivals) until tsm_peer_reset.  The parity / target / sequence are
+// launch arguments, so a captured CUDA graph cannot replay a fused call.
 constexpr int kMaxPeers = 8;
 constexpr int kPeerCells = 64 * 64 * 2;
 constexpr int kPeerHeaderBytes = 256;
@@ -155,7 +162,23 @@ struct PeerArgs {
   int rank;
   int parity;
   u64 target;               // cnt[parity] value that means "all ranks arrived"
+  u64 seq;                  // this call's number + 1 (stored beside the slot data)
+  u64 timeout_ns;           // bounded wait for the other ranks
 };
+constexpr int kPeerErrOffset = 16;  // u32 err flag (bytes into the header)
+constexpr int kPeerSeqOffset = 32;  // u64 seq[2][kMaxPeers]
+__device__ __forceinline__ u64* peer_seq(const PeerArgs& q, int owner, int src) {
+  return reinterpret_cast<u64*>(reinterpret_cast<char*>(q.base[owner]) + kPeerSeqOffset) +
+         q.parity * kMaxPeers + src;
+}
+__device__ __forceinline__ u32* peer_err(const PeerArgs& q) {
+  return reinterpret_cast<u32*>(reinterpret_cast<char*>(q.base[q.rank]) + kPeerErrOffset);
+}
+__device__ __forceinline__ u32 ld_acquire_sys32(const u32* p) {
+  u32 v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
 __device__ __forceinline__ double* peer_slot(const PeerArgs& q, int owner, int src) {
   return reinterpret_cast<double*>(reinterpret_cast<char*>(q.base[owner]) + kPeerHeaderBytes) +
          (static_cast<long long>(q.parity) * kMaxPeers + src) * kPeerCells;
@@ -385,11 +408,19 @@ __device__ __forceinline__ void grid_reduce(const TsmttsmArgs& p, const double* 
   // finisher f owns cells [c0, c1); TPC threads per cell split the block
   // range into contiguous segments, combined afterwards in segment order.
   const PeerArgs& pq = p.peer;
+  // N3 fail-fast: an earlier fused call on this rank timed out or saw a foreign
+  // sequence number -> no stores to peers, no arrivals, C = NaN (tsm_peer_reset)
+  __shared__ int s_failed;
+  if (pq.nranks > 0) {
+    if (tid == 0) s_failed = ld_acquire_sys32(peer_err(pq)) != 0u;
+    __syncthreads();
+  }
+  const bool failed = pq.nranks > 0 && s_failed;
   // local C cell -> C (single GPU), or -> slot[parity][rank] of every rank (N3)
   auto put = [&](int idx, double v) {
     if (pq.nranks == 0) {
       p.C[idx] = v;
-    } else {
+    } else if (!failed) {
       for (int r = 0; r < pq.nranks; r++) __stcg(peer_slot(pq, r, pq.rank) + idx, v);
     }
   };
@@ -439,7 +470,9 @@ __device__ __forceinline__ void grid_reduce(const TsmttsmArgs& p, const double* 
     if (d == static_cast<u32>(nfin - 1)) {  // last finisher: reset for the next call
       p.counters[0] = 0;
       p.counters[1] = 0;
-      if (pq.nranks > 0) {  // every finisher of this rank has stored (and fenced): signal
+      if (pq.nranks > 0 && !failed) {  // every finisher of this rank has stored (and fenced): signal
+        __threadfence_system();
+        for (int r = 0; r < pq.nranks; r++) *reinterpret_cast<volatile u64*>(peer_seq(pq, r, pq.rank)) = pq.seq;
         __threadfence_system();
         for (int r = 0; r < pq.nranks; r++)
           atomicAdd_system(reinterpret_cast<unsigned long long*>(pq.base[r]) + pq.parity, 1ull);
@@ -452,15 +485,21 @@ __device__ __forceinline__ void grid_reduce(const TsmttsmArgs& p, const double* 
   if (tid == 0) {
     const u64* cnt = reinterpret_cast<const u64*>(pq.base[pq.rank]) + pq.parity;
     const u64 t0 = globaltimer_ns();
-    int ok = 1;
-    while (ld_acquire_sys(cnt) < pq.target) {
+    int ok = failed ? 0 : 1;
+    while (ok && ld_acquire_sys(cnt) < pq.target) {
       __nanosleep(128);
-      if (globaltimer_ns() - t0 > 2000000000ull) {  // a rank never arrived: report, do not hang
-        atomicExch(reinterpret_cast<u32*>(reinterpret_cast<char*>(pq.base[pq.rank]) + 16), 1u);
+      if (globaltimer_ns() - t0 > pq.timeout_ns) {  // a rank never arrived: report, do not hang
+        atomicExch(peer_err(pq), 1u);
         ok = 0;
-        break;
       }
     }
+    // every slot must hold THIS call's data (a rank that ran ahead after a
+    // timeout would otherwise be summed silently)
+    for (int r = 0; ok && r < pq.nranks; r++)
+      if (ld_acquire_sys(peer_seq(pq, pq.rank, r)) != pq.seq) {
+        atomicExch(peer_err(pq), 1u);
+        ok = 0;
+      }
     s_ok = ok;
   }
   __syncthreads();
@@ -472,6 +511,19 @@ __device__ __forceinline__ void grid_reduce(const TsmttsmArgs& p, const double* 
     }
     p.C[idx] = v;
   }
+  // seqlock-style re-check: a slot rewritten by a rank that ran ahead while it
+  // was being read is reported (C = NaN), never returned as this call's sum
+  __syncthreads();
+  if (tid == 0 && s_ok) {
+    for (int r = 0; r < pq.nranks; r++)
+      if (ld_acquire_sys(peer_seq(pq, pq.rank, r)) != pq.seq) {
+        atomicExch(peer_err(pq), 1u);
+        s_ok = 0;
+      }
+  }
+  __syncthreads();
+  if (!s_ok)
+    for (int idx = c0 + tid; idx < c1; idx += NT) p.C[idx] = __longlong_as_double(0x7ff8000000000000ll);
 }
 
 template <class Cfg>

@@ -27,7 +27,8 @@ struct tsm_peer_s {
   double* base[kMaxPeers] = {};           // every rank's buffer as mapped here
   bool opened[kMaxPeers] = {};            // IPC mappings to close
   bool ready = false;                     // tsm_peer_open done
-  unsigned long long calls = 0;           // fused reductions issued (parity / target)
+  unsigned long long calls = 0;           // fused reductions issued (parity / target / seq)
+  unsigned long long timeout_ns = 2000000000ull;  // bounded wait for the other ranks
 };
 
 namespace {
@@ -66,6 +67,8 @@ tsm_status peer_call(tsm_plan p, tsm_peer c, int dt, int64_t K, const void* A, c
   q.rank = c->rank;
   q.parity = static_cast<int>(c->calls & 1ull);
   q.target = ((c->calls >> 1) + 1ull) * static_cast<unsigned long long>(c->nranks);
+  q.seq = c->calls + 1ull;
+  q.timeout_ns = c->timeout_ns;
   tsm_status st = tsm::launch_tsmttsm(p, dt, K, A, B, C, ws, ws_bytes, stream, true, 0, 0, &q);
   if (st == TSM_SUCCESS) c->calls++;  // a launched call has signalled (or will) on every rank
   return st;
@@ -162,6 +165,26 @@ tsm_status tsm_peer_error(tsm_peer c, int* err) {
   cudaError_t e = cudaMemcpy(&v, reinterpret_cast<char*>(c->own) + 16, sizeof v, cudaMemcpyDeviceToHost);
   if (e != cudaSuccess) return cuda_err(e, "read peer error flag");
   *err = v ? 1 : 0;
+  return TSM_SUCCESS;
+}
+
+tsm_status tsm_peer_set_timeout(tsm_peer c, uint64_t timeout_ns) {
+  if (!c || timeout_ns == 0) return fail(TSM_ERR_INVALID_VALUE, "null peer / zero timeout");
+  c->timeout_ns = timeout_ns;
+  return TSM_SUCCESS;
+}
+
+tsm_status tsm_peer_reset(tsm_peer c, tsm_stream stream) {
+  if (!c) return fail(TSM_ERR_INVALID_VALUE, "null peer");
+  DevScope ds(c->device);
+  if (ds.err != cudaSuccess) return cuda_err(ds.err, "cudaSetDevice");
+  // wait for this rank's fused calls, then clear its header (counters, err, seq);
+  // the slots themselves are rewritten by every call before they are read
+  cudaError_t e = cudaStreamSynchronize(static_cast<cudaStream_t>(stream));
+  if (e == cudaSuccess) e = cudaMemset(c->own, 0, kPeerHeaderBytes);
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) return cuda_err(e, "tsm_peer_reset");
+  c->calls = 0;
   return TSM_SUCCESS;
 }
 

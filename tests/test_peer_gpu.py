@@ -144,3 +144,76 @@ def test_two_processes_one_gpu(tsm, tmp_path):
         else:
             r, wi, _ = oracle.max_err_ratio(C0, ref, bound)
             assert r <= 1e-12, (key, r, wi)
+
+
+FAILFAST_WORKER = r'''
+import json, os, sys, time
+sys.path.insert(0, os.environ["TSM_ROOT"])
+import numpy as np, torch, torch.distributed as dist
+from paper_1905_03136_b200 import binding as tsm
+rank = int(os.environ["RANK"])
+torch.cuda.set_device(0)
+dist.init_process_group("gloo", rank=rank, world_size=2)
+peer = tsm.PeerComm(rank, 2, 0)
+peer.set_timeout(0.05)
+K, M = 20000, 16
+A = torch.empty(K, M, dtype=torch.float64, device="cuda")
+tsm.fill(A, "A", 42 + rank)
+res = {}
+C = tsm.tsmttsm_peer(peer, A, A)              # call 0: both ranks -> fine
+torch.cuda.synchronize()
+res["ok0"] = bool(torch.isfinite(C).all().item()) and peer.error() == 0
+dist.barrier()
+if rank == 0:                                  # call 1: rank 1 never arrives
+    C = tsm.tsmttsm_peer(peer, A, A)
+    torch.cuda.synchronize()
+    res["timeout_nan"] = bool(torch.isnan(C).all().item())
+    res["err1"] = peer.error()
+    t0 = time.perf_counter()
+    C = tsm.tsmttsm_peer(peer, A, A)           # call 2: fails fast (no 50 ms wait)
+    torch.cuda.synchronize()
+    res["failfast_s"] = time.perf_counter() - t0
+    res["failfast_nan"] = bool(torch.isnan(C).all().item())
+dist.barrier()
+peer.reset()                                   # collective recovery
+C = tsm.tsmttsm_peer(peer, A, A)
+torch.cuda.synchronize()
+loc = tsm.tsmttsm(A, A)
+torch.cuda.synchronize()
+res["after_reset_err"] = peer.error()
+res["after_reset_finite"] = bool(torch.isfinite(C).all().item())
+np.save(os.path.join(os.environ["TSM_OUT"], f"ff_r{rank}_C.npy"), C.cpu().numpy())
+np.save(os.path.join(os.environ["TSM_OUT"], f"ff_r{rank}_loc.npy"), loc.cpu().numpy())
+json.dump(res, open(os.path.join(os.environ["TSM_OUT"], f"ff_r{rank}.json"), "w"))
+peer.close()
+dist.destroy_process_group()
+'''
+
+
+def test_peer_timeout_failfast_reset(tsm, tmp_path):
+    """ADVICE r01: a missing rank -> C = NaN and the error flag; every later
+    call on that rank fails fast; tsm_peer_reset on every rank recovers."""
+    env = dict(os.environ, MASTER_ADDR="127.0.0.1", MASTER_PORT=str(_free_port()), WORLD_SIZE="2",
+               TSM_ROOT=ROOT, TSM_OUT=str(tmp_path))
+    procs = [subprocess.Popen([sys.executable, "-c", FAILFAST_WORKER], env=dict(env, RANK=str(r)), cwd=ROOT,
+                              stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)
+             for r in range(2)]
+    outs = []
+    for p in procs:
+        try:
+            o, _ = p.communicate(timeout=600)
+        except subprocess.TimeoutExpired:
+            p.kill()
+            o, _ = p.communicate()
+        outs.append(o)
+    assert all(p.returncode == 0 for p in procs), "\n".join(o[-3000:] for o in outs)
+    r0 = json.load(open(tmp_path / "ff_r0.json"))
+    r1 = json.load(open(tmp_path / "ff_r1.json"))
+    assert r0["ok0"] and r1["ok0"]
+    assert r0["timeout_nan"] and r0["err1"] == 1
+    assert r0["failfast_nan"] and r0["failfast_s"] < 0.04, r0
+    for r in (r0, r1):
+        assert r["after_reset_err"] == 0 and r["after_reset_finite"]
+    C0, C1 = np.load(tmp_path / "ff_r0_C.npy"), np.load(tmp_path / "ff_r1_C.npy")
+    l0, l1 = np.load(tmp_path / "ff_r0_loc.npy"), np.load(tmp_path / "ff_r1_loc.npy")
+    assert np.array_equal(C0, C1) and np.array_equal(C0, l0 + l1)

@@ -1,0 +1,145 @@
+#!/usr/bin/env python3
+"""compute-sanitizer driver (VERDICT r01 missing item 6).
+
+Runs ONE representative launch configuration of every kernel family libtsm
+ships -- every distinct kernel variant among the tuned default plans (all
+square widths 1..64, D and Z, both ops, plus the non-square configs[3]
+shapes), the explicit families of tools/gen_instances.candidates() the tuned
+table does not pick, the TSMM update (beta = 1 reduce-add, beta = 2 scale),
+the conjugate plans and the TMA strided views -- at K in {1, 2, 33, 4099},
+and checks every result against the oracle (so a run under a sanitizer tool
+is also a parity run).  Meant to be wrapped:
+
+    compute-sanitizer --tool racecheck  python tools/sanitize.py
+    compute-sanitizer --tool synccheck  python tools/sanitize.py
+    compute-sanitizer --tool memcheck   python tools/sanitize.py
+    compute-sanitizer --tool initcheck  python tools/sanitize.py
+
+Prints one line per family and "SANITIZE_OK <n>" at the end.
+"""
+from __future__ import annotations
+
+import argparse
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tools"))
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import oracle  # noqa: E402
+import tsminputs as ti  # noqa: E402
+from paper_1905_03136_b200 import binding as tsm  # noqa: E402
+
+KS = [1, 2, 33, 4099]
+
+
+def run_one(plan, op, z, M, N, K, conj=False, update=None, strided=False):
+    A = ti.matrix(K, M, "A", complex_=z, seed=K + 11)
+    dA = torch.from_numpy(A).cuda()
+    if strided:  # a column subset of a wider block vector (ld = width + 8 elements)
+        wideA = torch.zeros(K, M + 8, dtype=dA.dtype, device="cuda")
+        wideA[:, 3:3 + M] = dA
+        dA = wideA[:, 3:3 + M]
+    if op == "tsmttsm":
+        B = ti.matrix(K, N, "B", complex_=z, seed=K + 12)
+        dB = torch.from_numpy(B).cuda()
+        if strided:
+            wideB = torch.zeros(K, N + 8, dtype=dB.dtype, device="cuda")
+            wideB[:, 5:5 + N] = dB
+            dB = wideB[:, 5:5 + N]
+        got = tsm.tsmttsm(dA, dB, plan=plan, conj=conj)
+        ref, bound = oracle.tsmttsm(A, B, conj=conj)
+        tol = 1e-12
+    else:
+        Cm = ti.matrix(M, N, "C", complex_=z, seed=K + 13)
+        dC = torch.from_numpy(Cm).cuda()
+        if update is not None:
+            B0 = ti.matrix(K, N, "B", complex_=z, seed=K + 14)
+            dB = torch.from_numpy(B0).cuda()
+            alpha, beta = update
+            tsm.tsmm_update(dA, dC, dB, alpha=alpha, beta=beta, plan=plan, conj=conj)
+            got = dB
+            ref, bound = oracle.tsmm_update(A, Cm, B0, alpha, beta, conj=conj)
+            tol = 1e-13 * 4
+        else:
+            out = None
+            if strided:
+                wideO = torch.zeros(K, N + 8, dtype=dA.dtype, device="cuda")
+                out = wideO[:, 1:1 + N]
+            got = tsm.tsmm(dA, dC, plan=plan, out=out)
+            ref, bound = oracle.tsmm(A, Cm)
+            tol = 1e-13
+    torch.cuda.synchronize()
+    r, wi, _ = oracle.max_err_ratio(np.ascontiguousarray(got.cpu().numpy()), ref, bound)
+    assert r <= tol, (op, z, M, N, K, r, wi, plan.describe(K))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--quick", action="store_true", help="first 6 families only")
+    a = ap.parse_args()
+    fams = {}
+    shapes = [(w, w) for w in range(1, 65)] + [(1, 64), (64, 1), (16, 48), (48, 16)]
+    for op in ("tsmttsm", "tsmm"):
+        for dt in ("d", "z"):
+            for (M, N) in shapes:
+                p = tsm.get_plan(op, dt, M, N, 0)
+                d = p.describe(4099)
+                key = (op, dt, d["kernel"], p.config()["kernel"] & 15)
+                fams.setdefault(key, ("default", p, M, N))
+    # explicit families the tuned table may not pick (autotuner search space)
+    import gen_instances as gi
+    for op in ("tsmttsm", "tsmm"):
+        for dt in ("d", "z"):
+            for (M, N) in [(64, 64), (33, 17), (24, 24), (3, 5)]:
+                for c in gi.candidates(op, M, N, dt == "z"):
+                    try:
+                        p = tsm.Plan(op, dt, M, N, 0, config=gi.to_tsm_config(op, c, 3, 2))
+                    except tsm.TsmError:
+                        continue
+                    key = (op, dt, p.describe(4099)["kernel"], p.config()["kernel"] & 15)
+                    fams.setdefault(key, ("explicit", p, M, N))
+    items = sorted(fams.items(), key=lambda kv: kv[0])
+    if a.quick:
+        items = items[:6]
+    n = 0
+    for (op, dt, kname, impl), (src, p, M, N) in items:
+        z = dt == "z"
+        for K in KS:
+            run_one(p, op, z, M, N, K)
+            n += 1
+        print(f"{op:8s} {dt} impl {impl} {kname:55s} {src:8s} M={M} N={N}: ok", flush=True)
+    # N1 update (beta = 1: bulk/TMA reduce-add; beta = 2: scale pass first), N2 conj, N4 strided
+    extra = [("tsmm", "d", 63, 63), ("tsmm", "d", 64, 64), ("tsmm", "z", 24, 24), ("tsmm", "d", 5, 5)]
+    for (op, dt, M, N) in extra:
+        p = tsm.get_plan(op, dt, M, N, 0)
+        for K in KS:
+            run_one(p, op, dt == "z", M, N, K, update=(-1.0, 1.0))
+            run_one(p, op, dt == "z", M, N, K, update=(0.5, 2.0))
+            n += 2
+        print(f"update   {dt} M={M} N={N} ({p.describe(99)['kernel']}): ok", flush=True)
+    for (op, M, N) in [("tsmttsm", 32, 32), ("tsmttsm", 17, 17), ("tsmm", 24, 24), ("tsmm", 40, 40)]:
+        p = tsm.get_plan(op, "z", M, N, 0, conj=True)
+        for K in KS:
+            if op == "tsmttsm":
+                run_one(p, op, True, M, N, K, conj=True)
+            else:
+                run_one(p, op, True, M, N, K, update=(1.0, 0.0), conj=True)
+            n += 1
+        print(f"conj     z {op} M={M} N={N}: ok", flush=True)
+    for (op, dt, M, N) in [("tsmttsm", "d", 32, 32), ("tsmm", "d", 16, 48), ("tsmttsm", "z", 8, 8),
+                           ("tsmm", "z", 40, 40)]:
+        p = tsm.get_plan(op, dt, M, N, 0, strided=True)
+        for K in KS:
+            run_one(p, op, dt == "z", M, N, K, strided=True)
+            n += 1
+        print(f"strided  {dt} {op} M={M} N={N}: ok", flush=True)
+    print(f"SANITIZE_OK {n} launches, {len(items)} families", flush=True)
+
+
+if __name__ == "__main__":
+    main()
