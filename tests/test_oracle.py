@@ -515,3 +515,22 @@ def test_comparator_rules():
     # complex: |(3+4i) - 0| = 5 (modulus, not max(|re|, |im|) = 4 or |re| + |im| = 7)
     r, _, ma = oracle.max_err_ratio(np.array([3 + 4j]), np.array([0j]), np.array([10.0]))
     assert ma == 5.0 and r == 0.5
+
+
+def test_generator_c_matches_numpy():
+    """tsminputs/gen.c (used for full-size host regeneration) equals the numpy
+    definition element for element, real and complex, fp and int modes."""
+    import tsminputs as ti
+    for mode, seed in (("fp", 42), ("int", 7)):
+        for mat in ("A", "B", "C"):
+            ref = ti.raw_values_numpy(5000, seed, mat, mode, start=123456789)
+            got = ti.raw_values(5000, seed, mat, mode, start=123456789)
+            assert np.array_equal(ref, got)
+    K, w = 3001, 13
+    for cplx in (False, True):
+        full = np.stack([ti.values_at(np.arange(K * w * (2 if cplx else 1), dtype=np.uint64), 42, "A", "fp")])[0]
+        full = full.view(np.complex128).reshape(K, w) if cplx else full.reshape(K, w)
+        cols = [0, 5, 12]
+        assert np.array_equal(ti.columns(K, w, cols, "A", complex_=cplx), full[:, cols])
+        assert np.array_equal(ti.column(K, w, 12, "A", complex_=cplx), full[:, 12])
+        assert np.array_equal(ti.matrix(K, w, "A", complex_=cplx), full)

@@ -187,61 +187,7 @@ def test_device_generator_matches_host(tsm):
             assert np.array_equal(host(t), ref)
 
 
-# ---------------------------------------------------------------------------
-# Full BASELINE sizes (K = 2^24), same plans / launch configuration bench.py
-# times; sampled outputs the oracle computes one by one.
-# ---------------------------------------------------------------------------
-def _full_inputs(tsm, K, M, N, cplx, mats):
-    dt = torch.complex128 if cplx else torch.float64
-    out = {}
-    for name, (r, c) in mats.items():
-        t = torch.empty(r, c, dtype=dt, device="cuda")
-        tsm.fill(t, name, ti.SEED_FP, "fp")
-        out[name] = t
-    return out
-
-
-@pytest.mark.parametrize("cplx", [False, True], ids=["D", "Z"])
-@pytest.mark.parametrize("w", [1, 8, 32, 64])
-def test_full_size_tsmttsm_sampled(tsm, w, cplx):
-    K = 1 << 24
-    if cplx and w == 64:
-        K = 1 << 23  # memory: 2 x 17 GB is fine, keep the oracle columns cheap
-    d = _full_inputs(tsm, K, w, w, cplx, {"A": (K, w), "B": (K, w)})
-    C = host(tsm.tsmttsm(d["A"], d["B"]))
-    rng = np.random.default_rng(w)
-    cells = {(0, 0), (w - 1, w - 1), (0, w - 1), (w - 1, 0)}
-    cells |= {tuple(x) for x in rng.integers(0, w, size=(3, 2))}
-    for (m, n) in sorted(cells):
-        a = ti.column(K, w, m, "A", complex_=cplx)[:, None]
-        b = ti.column(K, w, n, "B", complex_=cplx)[:, None]
-        # the device-generated inputs equal the host generator on these columns
-        assert np.array_equal(host(d["A"][:, m]), a[:, 0])
-        ref, bound = oracle.tsmttsm(a, b)
-        r, _, _ = oracle.max_err_ratio(C[m:m + 1, n:n + 1], ref, bound)
-        assert r <= TOL_TSMTTSM, (m, n, r)
-    del d
-    torch.cuda.empty_cache()
-
-
-@pytest.mark.parametrize("cplx", [False, True], ids=["D", "Z"])
-@pytest.mark.parametrize("w", [1, 8, 32, 64])
-def test_full_size_tsmm_sampled(tsm, w, cplx):
-    K = 1 << 24
-    d = _full_inputs(tsm, K, w, w, cplx, {"A": (K, w), "C": (w, w)})
-    Bo = tsm.tsmm(d["A"], d["C"])
-    torch.cuda.synchronize()
-    rng = np.random.default_rng(100 + w)
-    rows = np.unique(np.concatenate([[0, 1, K - 2, K - 1], rng.integers(0, K, 2048)]))
-    a = ti.rows(rows, w, "A", complex_=cplx)
-    Cm = ti.matrix(w, w, "C", complex_=cplx)
-    assert np.array_equal(host(d["C"]), Cm)
-    ref, bound = oracle.tsmm(a, Cm)
-    got = host(Bo[torch.from_numpy(rows).cuda()])
-    r, wi, _ = oracle.max_err_ratio(got, ref, bound)
-    assert r <= TOL_TSMM, (r, rows[wi // w])
-    del d, Bo
-    torch.cuda.empty_cache()
+# Full BASELINE sizes (K = 2^24 / 2^25) for every tuned plan: tests/test_fullsize_gpu.py
 
 
 def test_workspace_reuse_across_shapes(tsm):

@@ -31,6 +31,10 @@ performance (no data-dependent control flow in any kernel).
 """
 from __future__ import annotations
 
+import ctypes
+import os
+import subprocess
+
 import numpy as np
 
 MAT_ID = {"A": 1, "B": 2, "C": 3}
@@ -58,8 +62,68 @@ def key(seed: int, mat: str) -> np.uint64:
     return np.uint64((int(seed) * 0xD1B54A32D192ED03 + (MAT_ID[mat] << 48)) % (1 << 64))
 
 
+# ---------------------------------------------------------------------------
+# gen.c: the same generator in C (OpenMP), for full-size host regeneration.
+# ---------------------------------------------------------------------------
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_GEN_SRC = os.path.join(_HERE, "gen.c")
+_GEN_LIB = os.path.join(_HERE, "libtsmgen.so")
+_gen = None
+_MODE = {"fp": 0, "int": 1}
+
+
+def build(force: bool = False) -> str:
+    if force or not os.path.exists(_GEN_LIB) or os.path.getmtime(_GEN_LIB) < os.path.getmtime(_GEN_SRC):
+        tmp = _GEN_LIB + f".tmp{os.getpid()}"
+        subprocess.check_call(["gcc", "-O2", "-fopenmp", "-shared", "-fPIC", "-std=c99", "-o", tmp, _GEN_SRC])
+        os.replace(tmp, _GEN_LIB)
+    return _GEN_LIB
+
+
+def _lib():
+    global _gen
+    if _gen is None:
+        lib = ctypes.CDLL(build())
+        dp = ctypes.POINTER(ctypes.c_double)
+        u64, i64 = ctypes.c_uint64, ctypes.c_int64
+        lib.tsmgen_strided.argtypes = [dp, i64, u64, u64, u64, ctypes.c_int]
+        lib.tsmgen_strided.restype = None
+        lib.tsmgen_columns.argtypes = [dp, i64, i64, ctypes.POINTER(i64), ctypes.c_int, u64, ctypes.c_int,
+                                       ctypes.c_int]
+        lib.tsmgen_columns.restype = None
+        _gen = lib
+    return _gen
+
+
+def _dptr(a):
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+
+
 def raw_values(n: int, seed: int, mat: str, mode: str, start: int = 0) -> np.ndarray:
-    """Flat stream of n real values for indices start .. start+n-1."""
+    """Flat stream of n real values for indices start .. start+n-1 (gen.c)."""
+    if mode not in _MODE:
+        raise ValueError(f"unknown mode {mode!r}")
+    out = np.empty(n, dtype=np.float64)
+    _lib().tsmgen_strided(_dptr(out), n, start, 1, int(key(seed, mat)), _MODE[mode])
+    return out
+
+
+def columns(K: int, width: int, cols, mat: str, *, complex_: bool = False, mode: str = "fp",
+            seed: int | None = None) -> np.ndarray:
+    """Columns `cols` of matrix(K, width, mat, ...) as a K x len(cols) array (gen.c)."""
+    if seed is None:
+        seed = SEED_FP if mode == "fp" else SEED_INT
+    c = np.ascontiguousarray(cols, dtype=np.int64)
+    if c.size and (c.min() < 0 or c.max() >= width):
+        raise ValueError("column out of range")
+    out = np.empty((K, c.size), dtype=np.complex128 if complex_ else np.float64)
+    _lib().tsmgen_columns(_dptr(out), K, width, c.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), c.size,
+                          int(key(seed, mat)), _MODE[mode], int(complex_))
+    return out
+
+
+def raw_values_numpy(n: int, seed: int, mat: str, mode: str, start: int = 0) -> np.ndarray:
+    """numpy version of raw_values (the readable definition; tests compare the two)."""
     base = key(seed, mat)
     out = np.empty(n, dtype=np.float64)
     step = 1 << 22
@@ -94,14 +158,7 @@ def values_at(idx: np.ndarray, seed: int, mat: str, mode: str) -> np.ndarray:
 def column(K: int, width: int, col: int, mat: str, *, complex_: bool = False, mode: str = "fp",
            seed: int | None = None) -> np.ndarray:
     """Column `col` (length K) of the K x width matrix(K, width, mat, ...)."""
-    if seed is None:
-        seed = SEED_FP if mode == "fp" else SEED_INT
-    elem = np.arange(K, dtype=np.uint64) * np.uint64(width) + np.uint64(col)
-    if complex_:
-        re = values_at(2 * elem, seed, mat, mode)
-        im = values_at(2 * elem + np.uint64(1), seed, mat, mode)
-        return re + 1j * im
-    return values_at(elem, seed, mat, mode)
+    return columns(K, width, [col], mat, complex_=complex_, mode=mode, seed=seed)[:, 0].copy()
 
 
 def rows(row_idx: np.ndarray, width: int, mat: str, *, complex_: bool = False, mode: str = "fp",
