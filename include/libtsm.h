@@ -296,6 +296,25 @@ tsm_status tsm_fill(double *dst, int64_t n, uint64_t seed, int mat_id, int mode,
 tsm_status tsm_l2_flush(void *scratch, size_t bytes, tsm_stream stream);
 
 /* ------------------------------------------------------------------------ */
+/* Roofline-denominator probes (measurement only, not part of the path).    */
+/* "b_s is measured in the same run, following the paper's */
+/* convention: read-only streaming for TSMTTSM, read +   */
+/* write copy for TSMM"; "measure P_fp64 sustained; do not assume boost"    */
+/* (PAPER.md:280-289 measures its peaks the same way).  One launch on       */
+/* `stream`; the caller times it with events.  *work receives the launch's  */
+/* work: bytes moved (READ: `bytes` read; COPY: bytes/2 read + bytes/2      */
+/* written) or FP64 flops (DMMA: mma.sync.m8n8k4.f64 chains, `iters` loop   */
+/* trips, 8 blocks x 4 warps per SM).  buf: caller-owned device memory,     */
+/* 16-byte aligned; READ reads it, COPY overwrites its second half, DMMA    */
+/* writes at most buf[0].  Errors: TSM_ERR_INVALID_VALUE (bad kind, buffer, */
+/* iters), TSM_ERR_CUDA (launch).                                           */
+/* ------------------------------------------------------------------------ */
+#define TSM_PROBE_READ 0
+#define TSM_PROBE_COPY 1
+#define TSM_PROBE_DMMA 2
+tsm_status tsm_probe(int kind, void *buf, size_t bytes, int64_t iters, tsm_stream stream, double *work);
+
+/* ------------------------------------------------------------------------ */
 /* Multi-GPU: one process per GPU, K sharded by rows.      */
 /* The 128-byte NCCL unique id is created on rank 0 with tsm_comm_unique_id  */
 /* and exchanged by the caller (torch.distributed).  NCCL is loaded          */

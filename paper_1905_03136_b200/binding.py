@@ -39,6 +39,7 @@ EXPORTS = [
     "tsm_cgs_step_d", "tsm_cgs_step_z", "tsmttsm_ld_d", "tsmttsm_ld_z", "tsmm_ld_d", "tsmm_ld_z",
     "tsm_jit_precompile", "tsm_peer_create", "tsm_peer_export", "tsm_peer_open", "tsm_peer_destroy",
     "tsm_peer_error", "tsmttsm_peer_d", "tsmttsm_peer_z", "tsm_peer_set_timeout", "tsm_peer_reset",
+    "tsm_probe",
 ]
 
 
@@ -114,6 +115,7 @@ def _load():
         "tsm_peer_reset": [P, VP],
         "tsmttsm_peer_d": [P, P, I64, VP, VP, VP, VP, SZ, VP],
         "tsmttsm_peer_z": [P, P, I64, VP, VP, VP, VP, SZ, VP],
+        "tsm_probe": [I, VP, SZ, I64, VP, ctypes.POINTER(ctypes.c_double)],
     }
     for name, args in sig.items():
         f = getattr(lib, name)
@@ -231,6 +233,17 @@ def tsm_fill(dst, n, seed, mat_id, mode, start, stream):
 
 def tsm_l2_flush(scratch, nbytes, stream):
     check(lib.tsm_l2_flush(scratch, nbytes, stream), "tsm_l2_flush")
+
+
+PROBE = {"read": 0, "copy": 1, "dmma": 2}
+
+
+def probe(kind: str, buf, nbytes: int, iters: int, stream) -> float:
+    """Launch one roofline-denominator probe (measurement only); returns the
+    launch's work (bytes or FP64 flops) -- the caller times it with events."""
+    w = ctypes.c_double()
+    check(lib.tsm_probe(PROBE[kind], buf, nbytes, iters, stream, ctypes.byref(w)), "tsm_probe")
+    return w.value
 
 
 def tsm_build_info() -> str:

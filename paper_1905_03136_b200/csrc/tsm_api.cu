@@ -128,10 +128,12 @@ size_t smem_bytes(const KernelEntry& kin, int stages) {
     return static_cast<size_t>(128 + need * 8);
   }
   if (k.impl == 4) {  // C-stationary DMMA TSMM, bulk copies: p0 = NBW, p1 = WR (TsmmCstbCfg)
-    const long long NW = k.NT / 32 - 1, NB = (k.N + 7) / 8, NG = (NB + k.p0 - 1) / k.p0, RG = NW / NG;
+    const long long EC = (k.edge & 1) ? k.N % 8 : 0;
+    const long long NW = k.NT / 32 - 1, NB = (k.N - EC + 7) / 8, NG = (NB + k.p0 - 1) / k.p0, RG = NW / NG;
     const long long outd = ((8LL * k.p1 * k.N * S + 15) / 16) * 16;
     const long long stg = ((static_cast<long long>(k.R) * k.M * S + 15) / 16) * 16;
-    return static_cast<size_t>(256 + (RG * 2 * outd + stages * stg) * 8);
+    const long long ce = ((((k.M + 3) / 4) * 4 * EC * S + 15) / 16) * 16;
+    return static_cast<size_t>(256 + (ce + RG * 2 * outd + stages * stg) * 8);
   }
   if (k.impl == 3) {  // C-stationary DMMA TSMM: p0 = NBW, p1 = WR (must match TsmmCstCfg)
     const long long NW = k.NT / 32 - 1, EC = (k.edge & 1) ? k.N % 8 : 0;
@@ -205,6 +207,55 @@ __global__ void l2_flush_kernel(double4* __restrict__ dst, long long n4) {
   long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
   const long long st = static_cast<long long>(gridDim.x) * blockDim.x;
   for (; i < n4; i += st) dst[i] = make_double4(0.0, 0.0, 0.0, static_cast<double>(i));
+}
+
+// --------------------------------------------------------------------------
+// Roofline-denominator probes (b_s measured in the same run,
+// read-only for TSMTTSM, read+write for TSMM; FP64 peak measured, not assumed).
+// --------------------------------------------------------------------------
+__global__ void probe_read_kernel(const double2* __restrict__ p, long long n2, double* sink) {
+  double s0 = 0, s1 = 0, s2 = 0, s3 = 0;
+  long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  const long long st = static_cast<long long>(gridDim.x) * blockDim.x;
+  for (; i + 3 * st < n2; i += 4 * st) {
+    const double2 a = __ldg(p + i), b = __ldg(p + i + st), c = __ldg(p + i + 2 * st), d = __ldg(p + i + 3 * st);
+    s0 += a.x + a.y;
+    s1 += b.x + b.y;
+    s2 += c.x + c.y;
+    s3 += d.x + d.y;
+  }
+  for (; i < n2; i += st) s0 += p[i].x + p[i].y;
+  const double s = s0 + s1 + s2 + s3;
+  if (s == 1.2345678e300) sink[0] = s;  // never true for generator data; keeps the loads live
+}
+
+__global__ void probe_copy_kernel(const double2* __restrict__ p, double2* __restrict__ q, long long n2) {
+  long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  const long long st = static_cast<long long>(gridDim.x) * blockDim.x;
+  for (; i + st < n2; i += 2 * st) {
+    const double2 a = p[i], b = p[i + st];
+    q[i] = a;
+    q[i + st] = b;
+  }
+  for (; i < n2; i += st) q[i] = p[i];
+}
+
+__global__ void probe_dmma_kernel(double* sink, long long iters) {
+  double acc[8][2];
+#pragma unroll
+  for (int j = 0; j < 8; j++) acc[j][0] = acc[j][1] = 0.0;
+  const double a = 1e-3 * threadIdx.x, b = 2e-3 * threadIdx.x;
+  for (long long it = 0; it < iters; it++) {
+#pragma unroll
+    for (int j = 0; j < 8; j++)
+      asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                   : "+d"(acc[j][0]), "+d"(acc[j][1])
+                   : "d"(a), "d"(b));
+  }
+  double s = 0;
+#pragma unroll
+  for (int j = 0; j < 8; j++) s += acc[j][0] + acc[j][1];
+  if (s == 1.2345678e300) sink[0] = s;
 }
 
 }  // namespace tsm
@@ -289,7 +340,7 @@ static tsm_status validate_config_real(const KernelEntry& e) {
   }
   if ((e.edge & 1) && e.op == KIND_TSMM) {  // C-stationary TSMM: DFMA edge columns
     const int S = e.dt == TSM_Z ? 2 : 1;
-    if (e.impl != 3) return bad("edge columns (kernel | 16) apply to TSMM kernel 3");
+    if (e.impl != 3 && e.impl != 4) return bad("edge columns (kernel | 16) apply to TSMM kernels 3 and 4");
     if (e.edge & 14) return bad("TSMM edge columns take no other flag bits");
     if (e.N < 8 || e.N % 8 == 0) return bad("edge columns need N >= 8 and N not a multiple of 8");
     if (e.p1 * (e.N % 8) * S > 16) return bad("edge columns: WR * (N mod 8) * S must be <= 16");
@@ -319,7 +370,8 @@ static tsm_status validate_config_real(const KernelEntry& e) {
   if (e.impl == 4) {
     if (e.op != KIND_TSMM) return bad("kernel 4 (C-stationary, bulk copies) is a TSMM kernel");
     const int S = e.dt == TSM_Z ? 2 : 1;
-    const int NB = (e.N + 7) / 8, NW = e.NT / 32 - 1;
+    const int EC = (e.edge & 1) ? e.N % 8 : 0;  // DFMA edge columns
+    const int NB = (e.N - EC + 7) / 8, NW = e.NT / 32 - 1;
     if (e.p0 < 1 || e.p0 > NB) return bad("NBW must be in [1, ceil(N/8)]");
     const int NG = (NB + e.p0 - 1) / e.p0;
     if (NW < NG || NW % NG || NW / NG > 15) return bad("consumer warps must be 1..15 row groups of the column groups");
@@ -986,6 +1038,42 @@ tsm_status tsm_l2_flush(void* scratch, size_t bytes, tsm_stream stream) {
       static_cast<double4*>(scratch), n4);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "l2_flush_kernel launch");
+  return TSM_SUCCESS;
+}
+
+tsm_status tsm_probe(int kind, void* buf, size_t bytes, int64_t iters, tsm_stream stream, double* work) {
+  if (!work) return fail(TSM_ERR_INVALID_VALUE, "work == NULL");
+  if (!buf || misaligned(buf)) return fail(TSM_ERR_INVALID_VALUE, "bad probe buffer");
+  int dev = 0;
+  cudaGetDevice(&dev);
+  DevInfo di;
+  tsm_status st = dev_info(dev, &di);
+  if (st != TSM_SUCCESS) return st;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const long long n2 = static_cast<long long>(bytes / 16);
+  switch (kind) {
+    case TSM_PROBE_READ:
+      if (n2 < 1) return fail(TSM_ERR_INVALID_VALUE, "probe buffer too small");
+      probe_read_kernel<<<di.sms * 16, 256, 0, s>>>(static_cast<const double2*>(buf), n2, static_cast<double*>(buf));
+      *work = static_cast<double>(n2) * 16.0;
+      break;
+    case TSM_PROBE_COPY:
+      if (n2 < 2) return fail(TSM_ERR_INVALID_VALUE, "probe buffer too small");
+      probe_copy_kernel<<<di.sms * 4, 256, 0, s>>>(static_cast<const double2*>(buf),
+                                                   static_cast<double2*>(buf) + n2 / 2, n2 / 2);
+      *work = static_cast<double>(n2 / 2) * 32.0;
+      break;
+    case TSM_PROBE_DMMA:
+      if (iters < 1) return fail(TSM_ERR_INVALID_VALUE, "iters must be >= 1");
+      probe_dmma_kernel<<<di.sms * 8, 128, 0, s>>>(static_cast<double*>(buf), iters);
+      // 8 mma per iteration per warp, 8x8x4 FMAs = 256 FMA = 512 flops each
+      *work = static_cast<double>(di.sms) * 8 * 4 * static_cast<double>(iters) * 8 * 512.0;
+      break;
+    default:
+      return fail(TSM_ERR_INVALID_VALUE, "unknown probe kind");
+  }
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "probe launch");
   return TSM_SUCCESS;
 }
 

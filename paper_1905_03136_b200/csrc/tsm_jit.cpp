@@ -54,7 +54,7 @@ std::string cfg_type(const KernelEntry& ein) {
        << ", " << e.NT << ", " << e.R << ">";
   else if (e.impl == 4)
     os << "tsm::TsmmCstbCfg<" << e.M << ", " << e.N << ", " << z << ", " << e.p0 << ", " << e.p1
-       << ", " << (e.NT / 32 - 1) << ", " << e.R << ">";
+       << ", " << (e.NT / 32 - 1) << ", " << e.R << ", " << ((e.edge & 1) ? e.N % 8 : 0) << ">";
   else if (e.impl == 3)
     os << "tsm::TsmmCstCfg<" << e.M << ", " << e.N << ", " << z << ", " << e.p0 << ", " << e.p1
        << ", " << (e.NT / 32 - 1) << ", " << e.R << ", " << zr << ", " << ((e.edge & 1) ? e.N % 8 : 0) << ", "

@@ -2205,13 +2205,18 @@ constexpr int cstb_pick_rho(int M, int N, bool z) {
   return best;
 }
 
-template <int M_, int N_, bool Z_, int NBW_, int WR_, int NW_, int R_>
+// EC > 0 (kernel | 16): the last EC = N mod 8 columns of B by DFMA in the
+// warps of the last column group (as kernel 3's edge columns) instead of a
+// padded 8-column DMMA block: D 57 costs 57 x 60 lane-FMAs per row instead of
+// 64 x 60 on the shared FP64 pipe.
+template <int M_, int N_, bool Z_, int NBW_, int WR_, int NW_, int R_, int EC_ = 0>
 struct TsmmCstbCfg {
-  static constexpr int M = M_, N = N_, NBW = NBW_, WR = WR_, NW = NW_, R = R_;
+  static constexpr int M = M_, N = N_, NBW = NBW_, WR = WR_, NW = NW_, R = R_, EC = EC_;
   static constexpr bool Z = Z_;
+  static_assert(EC == 0 || (EC == N % 8 && N >= 8), "edge columns: EC = N mod 8, N >= 8");
   static constexpr int S = Z ? 2 : 1;
   static constexpr int MK = (M + 3) / 4;            // k-steps over m
-  static constexpr int NB = (N + 7) / 8;            // 8-column blocks of B
+  static constexpr int NB = (N - EC + 7) / 8;       // 8-column DMMA blocks of B
   static constexpr int NG = (NB + NBW - 1) / NBW;   // column groups
   static constexpr int RG = NW / NG;                // row groups (warps per column group)
   static constexpr int RW = 8 * WR;                 // rows per row group per pass
@@ -2219,6 +2224,7 @@ struct TsmmCstbCfg {
   static constexpr int NT = (NW + 1) * 32;
   static constexpr int STAGE_DOUBLES = ((R * M * S + 15) / 16) * 16;
   static constexpr int OUT_DOUBLES = ((RW * N * S + 15) / 16) * 16;  // one staging buffer
+  static constexpr int CE_DOUBLES = ((MK * 4 * EC * S + 15) / 16) * 16;  // edge columns of C' in smem
   static constexpr int RHO = cstb_pick_rho(M, N, Z);  // conflict-minimising row permutation
   static_assert(NW % NG == 0 && RG >= 1 && RG <= 15, "consumer warps: a multiple of the column groups, <= 15 row groups");
   static_assert(R % RPP == 0 && R % 2 == 0, "rows per chunk: whole passes");
@@ -2228,11 +2234,12 @@ template <class Cfg>
 __global__ void __launch_bounds__(Cfg::NT) tsmm_cstb_kernel(const __grid_constant__ TsmmArgs p) {
   constexpr int M = Cfg::M, N = Cfg::N, S = Cfg::S, R = Cfg::R, NW = Cfg::NW, WR = Cfg::WR;
   constexpr int MK = Cfg::MK, NB = Cfg::NB, NBW = Cfg::NBW, NG = Cfg::NG, RW = Cfg::RW;
-  constexpr int RPP = Cfg::RPP;
+  constexpr int RPP = Cfg::RPP, EC = Cfg::EC;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   u64* full = reinterpret_cast<u64*>(smem_raw);
   u64* empty = full + 16;
-  double* stage_out = reinterpret_cast<double*>(smem_raw + 256);
+  double* sCe = reinterpret_cast<double*>(smem_raw + 256);  // [MK*4][EC] edge columns of C'
+  double* stage_out = sCe + Cfg::CE_DOUBLES;
   double* ring = stage_out + Cfg::RG * 2 * Cfg::OUT_DOUBLES;
 
   const int tid = threadIdx.x;
@@ -2250,6 +2257,19 @@ __global__ void __launch_bounds__(Cfg::NT) tsmm_cstb_kernel(const __grid_constan
     }
     fence_mbar_init();
     fence_proxy_async_smem();
+  }
+  if constexpr (EC > 0) {  // edge columns of C' (rows >= M zero)
+    for (int i = tid; i < MK * 4 * EC; i += Cfg::NT) {
+      const int m = i / EC, n = (N - EC) + i % EC;
+      double re = 0.0, im = 0.0;
+      if (m < M) {
+        re = __ldg(&p.C[(m * N + n) * S]);
+        if constexpr (Cfg::Z) im = __ldg(&p.C[(m * N + n) * S + 1]);
+        c_prime(p, re, im);
+      }
+      sCe[i * S] = re;
+      if constexpr (Cfg::Z) sCe[i * S + 1] = im;
+    }
   }
   __syncthreads();
 
@@ -2292,8 +2312,10 @@ __global__ void __launch_bounds__(Cfg::NT) tsmm_cstb_kernel(const __grid_constan
         cf[ks][j][0] = re;
         if constexpr (Cfg::Z) cf[ks][j][S - 1] = im;
       }
-    auto consume = [&](auto nbv) {
+    auto consume = [&](auto nbv, auto ecv) {
       constexpr int NBV = decltype(nbv)::value;  // blocks of this column group inside C
+      constexpr int ECV = decltype(ecv)::value;  // DFMA edge columns (last group only)
+      constexpr int ECA = ECV > 0 ? ECV : 1;
       int pass = 0;
       Ring ring_it;
       for (long long c = blockIdx.x; c < p.nchunks; c += G, ring_it.next(stages)) {
@@ -2313,6 +2335,13 @@ __global__ void __launch_bounds__(Cfg::NT) tsmm_cstb_kernel(const __grid_constan
             for (int j = 0; j < NBW; j++)
 #pragma unroll
               for (int z = 0; z < S; z++) acc[i][j][z][0] = acc[i][j][z][1] = 0.0;
+          double eacc[WR][ECA][S];
+#pragma unroll
+          for (int i = 0; i < WR; i++)
+#pragma unroll
+            for (int e = 0; e < ECA; e++)
+#pragma unroll
+              for (int z = 0; z < S; z++) eacc[i][e][z] = 0.0;
 #pragma unroll
           for (int ks = 0; ks < MK; ks++) {
             const int m = 4 * ks + q;
@@ -2324,6 +2353,10 @@ __global__ void __launch_bounds__(Cfg::NT) tsmm_cstb_kernel(const __grid_constan
                 const double a = mv ? sA[r * M + m] : 0.0;
 #pragma unroll
                 for (int j = 0; j < NBV; j++) dmma(acc[i][j][0][0], acc[i][j][0][1], a, cf[ks][j][0]);
+                if constexpr (ECV > 0) {  // this lane's m-term of the edge columns (m >= M: C' row 0)
+#pragma unroll
+                  for (int e = 0; e < ECV; e++) eacc[i][e][0] = fma(a, sCe[m * EC + e], eacc[i][e][0]);
+                }
               } else {
                 const double2 a = mv ? *reinterpret_cast<const double2*>(sA + (r * M + m) * 2)
                                      : make_double2(0.0, 0.0);
@@ -2334,6 +2367,13 @@ __global__ void __launch_bounds__(Cfg::NT) tsmm_cstb_kernel(const __grid_constan
                   dmma(acc[i][j][0][0], acc[i][j][0][1], nai, cf[ks][j][1]);  // re -= ai ci
                   dmma(acc[i][j][1][0], acc[i][j][1][1], a.x, cf[ks][j][1]);  // im += ar ci
                   dmma(acc[i][j][1][0], acc[i][j][1][1], a.y, cf[ks][j][0]);  // im += ai cr
+                }
+                if constexpr (ECV > 0) {
+#pragma unroll
+                  for (int e = 0; e < ECV; e++) {
+                    const double2 ce = *reinterpret_cast<const double2*>(sCe + (m * EC + e) * 2);
+                    zfma(eacc[i][e][0], eacc[i][e][1], a.x, a.y, ce.x, ce.y);
+                  }
                 }
               }
             }
@@ -2352,6 +2392,26 @@ __global__ void __launch_bounds__(Cfg::NT) tsmm_cstb_kernel(const __grid_constan
                   for (int z = 0; z < S; z++) stg[(rr * N + n) * S + z] = acc[i][j][z][e];
                 }
               }
+          if constexpr (ECV > 0) {
+            // edge columns: sum the 4 q-lanes' partial m-sums (fixed butterfly order)
+#pragma unroll
+            for (int i = 0; i < WR; i++)
+#pragma unroll
+              for (int e = 0; e < ECV; e++) {
+                double v[S];
+#pragma unroll
+                for (int z = 0; z < S; z++) {
+                  v[z] = eacc[i][e][z];
+                  v[z] += __shfl_xor_sync(0xffffffffu, v[z], 1);
+                  v[z] += __shfl_xor_sync(0xffffffffu, v[z], 2);
+                }
+                if (q == 0) {
+                  const int rr = 8 * i + rho, n = N - EC + e;
+#pragma unroll
+                  for (int z = 0; z < S; z++) stg[(rr * N + n) * S + z] = v[z];
+                }
+              }
+          }
           fence_proxy_async_smem();
           if (issuer) bulk_wait_read<0>();  // the previous pass's store has read the other buffer
           asm volatile("bar.sync %0, %1;" ::"r"(1 + rg), "r"(NG * 32) : "memory");
@@ -2368,9 +2428,9 @@ __global__ void __launch_bounds__(Cfg::NT) tsmm_cstb_kernel(const __grid_constan
     };
     constexpr int NBL = NB - (NG - 1) * NBW;
     if (cg == NG - 1)
-      consume(IC<NBL>{});
+      consume(IC<NBL>{}, IC<EC>{});
     else
-      consume(IC<NBW>{});
+      consume(IC<NBW>{}, IC<0>{});
     if (issuer) bulk_wait_all();
     // Odd last row (K odd): warp 0 of block 0 from global A and C' (plain fma).
     if ((K & 1) && blockIdx.x == 0 && warp == 0) {

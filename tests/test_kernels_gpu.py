@@ -414,3 +414,46 @@ def test_plain_warp_order(tsm, op, dt, M, N):
         ref = oracle.tsmm(Ai, Ci)[0]
     torch.cuda.synchronize()
     assert np.array_equal(got.cpu().numpy(), ref), cfg
+
+
+@pytest.mark.parametrize("dt,M,N", [("d", 57, 57), ("d", 49, 49), ("d", 41, 41), ("d", 63, 63), ("d", 13, 29),
+                                    ("d", 9, 9), ("z", 17, 17), ("z", 25, 11), ("z", 9, 31)])
+def test_tsmm_cstb_edge_columns(tsm, dt, M, N):
+    """C-stationary bulk-copy TSMM (kernel 4) with the last N mod 8 columns by
+    DFMA (kernel | 16): every NBW / WR class the generator offers, B = A C and
+    the update B <- alpha A C + beta B (beta 0, 1, 2: store, bulk reduce-add,
+    scale pass) on ragged K (odd K: the global last-row path) within the 1e-13
+    |A||C| tolerance; integer-valued inputs bit-exact."""
+    cplx = dt == "z"
+    cands = [c for c in gi.candidates("tsmm", M, N, cplx) if c.get("impl") == 4 and c.get("EDGE")]
+    assert cands, "no kernel-4 edge-column candidate"
+    picked = {}
+    for c in cands:
+        picked.setdefault((c["NBW"], c["WR"]), c)
+    ran = 0
+    for key, c in sorted(picked.items())[:4]:
+        try:
+            plan = tsm.Plan("tsmm", dt, M, N, 0, config=gi.to_tsm_config("tsmm", c, 3, 1))
+        except tsm.TsmError as e:
+            if e.status != 2:
+                raise
+            continue
+        assert plan.config()["kernel"] & 16 and "dfma-edge-columns" in plan.describe(1000)["kernel"]
+        ran += 1
+        for K, beta in ((1, 0.0), (9, 1.0), (4099, 2.0), (65537, 0.0), (65536, 1.0)):
+            A = ti.matrix(K, M, "A", complex_=cplx, seed=K + 41)
+            Cm = ti.matrix(M, N, "C", complex_=cplx, seed=K + 42)
+            B0 = ti.matrix(K, N, "B", complex_=cplx, seed=K + 43)
+            Bg = torch.from_numpy(B0).cuda()
+            alpha = (0.5 - 0.25j) if cplx else 0.75
+            tsm.tsmm_update(torch.from_numpy(A).cuda(), torch.from_numpy(Cm).cuda(), Bg, alpha, beta, plan=plan)
+            torch.cuda.synchronize()
+            ref, bound = oracle.tsmm_update(A, Cm, B0, alpha, beta)
+            r, wi, _ = oracle.max_err_ratio(Bg.cpu().numpy(), ref, bound)
+            assert r <= 1e-13, (M, N, key, c, K, beta, r, wi)
+        Ai = ti.matrix(20001, M, "A", complex_=cplx, mode="int")
+        Ci = ti.matrix(M, N, "C", complex_=cplx, mode="int")
+        got = tsm.tsmm(torch.from_numpy(Ai).cuda(), torch.from_numpy(Ci).cuda(), plan=plan)
+        torch.cuda.synchronize()
+        assert np.array_equal(got.cpu().numpy(), oracle.tsmm(Ai, Ci)[0]), (key, c)
+    assert ran

@@ -386,7 +386,8 @@ def cfg_type(op, dt, M, N, c) -> str:
     if op == "tsmttsm":
         return f"tsm::TsmttsmCfg<{M}, {N}, {z}, {c['MT']}, {c['NTL']}, {c['NT']}, {c['R']}>"
     if c.get("impl", 0) == 4:
-        return f"tsm::TsmmCstbCfg<{M}, {N}, {z}, {c['NBW']}, {c['WR']}, {c['NT'] // 32 - 1}, {c['R']}>"
+        ec = N % 8 if c.get("EDGE", 0) else 0
+        return f"tsm::TsmmCstbCfg<{M}, {N}, {z}, {c['NBW']}, {c['WR']}, {c['NT'] // 32 - 1}, {c['R']}, {ec}>"
     if c.get("impl", 0) == 3:
         ec = N % 8 if c.get("EDGE", 0) else 0
         return (f"tsm::TsmmCstCfg<{M}, {N}, {z}, {c['NBW']}, {c['WR']}, {c['NT'] // 32 - 1}, {c['R']}, {zr}, "
@@ -634,6 +635,7 @@ def candidates(op: str, M: int, N: int, z: bool) -> list:
         out.extend(tsmm_cst_configs(M, N, z))
         out.extend(tsmm_cst_configs(M, N, z, edge=True))
         out.extend(tsmm_cstb_configs(M, N, z))
+        out.extend(tsmm_cstb_configs(M, N, z, edge=True))
     if z:
         out.extend(zr_candidates(op, M, N))
         out.extend(g3_candidates(op, M, N, out))
@@ -840,15 +842,19 @@ def tsmm_cst_configs(M: int, N: int, z: bool, edge: bool = False) -> list:
     return out
 
 
-def tsmm_cstb_configs(M: int, N: int, z: bool) -> list:
+def tsmm_cstb_configs(M: int, N: int, z: bool, edge: bool = False) -> list:
     """C-stationary DMMA TSMM with bulk copies (impl 4): the widths the TMA
     kernel 3 cannot take (rows not 16-byte multiples or < 128 bytes), and
     any width where one 8-column block per warp (NBW = 1, not possible with
-    kernel 3's whole 16-double output boxes) balances better."""
+    kernel 3's whole 16-double output boxes) balances better.  edge=True: the
+    last N mod 8 columns by DFMA (EDGE=1) instead of a padded DMMA block."""
     if N < 2:
         return []
+    if edge and (N < 8 or N % 8 == 0):
+        return []
     S = 2 if z else 1
-    MK, NB = cdiv(M, 4), cdiv(N, 8)
+    EC = N % 8 if edge else 0
+    MK, NB = cdiv(M, 4), cdiv(N - EC, 8)
     out = []
     for NBW in range(1, NB + 1):
         if MK * NBW * S > 48:
@@ -859,12 +865,15 @@ def tsmm_cstb_configs(M: int, N: int, z: bool) -> list:
             if NW > 16 or NW < 2 or RG > 15:
                 continue
             for WR in (1, 2, 4):
-                if WR * NBW * 2 * S > 32:
+                if WR * NBW * 2 * S > 32 or WR * EC * S > 16:
                     continue
                 rpp = 8 * WR * RG
                 for tgt in (16384, 32768):
                     R = rpp * max(1, round(tgt / (rpp * M * S * 8)))
-                    out.append(dict(NBW=NBW, WR=WR, NT=(NW + 1) * 32, R=R, impl=4))
+                    c = dict(NBW=NBW, WR=WR, NT=(NW + 1) * 32, R=R, impl=4)
+                    if edge:
+                        c["EDGE"] = 1
+                    out.append(c)
     return out
 
 
