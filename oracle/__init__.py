@@ -63,6 +63,14 @@ def _load():
         lib.oracle_tsmm_update_d.restype = None
         lib.oracle_tsmm_update_z.argtypes = [ctypes.c_int64, i, i, d, d, dp, dp, d, d, dp, dp, i]
         lib.oracle_tsmm_update_z.restype = None
+        i64 = ctypes.c_int64
+        lib.oracle_tsmttsm_d_blocks.argtypes = [i64, i, i, dp, dp, dp]
+        lib.oracle_tsmttsm_d_blocks.restype = None
+        lib.oracle_tsmttsm_z_blocks.argtypes = [i64, i, i, dp, dp, dp, i]
+        lib.oracle_tsmttsm_z_blocks.restype = None
+        for name in ("oracle_tsmttsm_d_combine", "oracle_tsmttsm_z_combine"):
+            getattr(lib, name).argtypes = [i64, i, i, dp, dp, dp]
+            getattr(lib, name).restype = None
         lib.oracle_max_err_ratio.argtypes = [ctypes.c_int64, ctypes.c_int, dp, dp, dp,
                                              ctypes.POINTER(ctypes.c_int64), dp]
         lib.oracle_max_err_ratio.restype = ctypes.c_double
@@ -107,6 +115,42 @@ def tsmttsm(A: np.ndarray, B: np.ndarray, conj: bool = False):
     bound = np.zeros((M, N), dtype=np.float64)
     f = (_load().oracle_tsmttsm_zc if conj else _load().oracle_tsmttsm_z) if is_c else _load().oracle_tsmttsm_d
     f(K, M, N, _ptr(A), _ptr(B), _ptr(C), _ptr(bound))
+    return C, bound
+
+
+ORACLE_BLOCK = 1 << 16  # rows per block of the TSMTTSM summation structure (oracle.c)
+
+
+def tsmttsm_stream(K: int, M: int, N: int, rows, is_complex: bool, conj: bool = False,
+                   seg_rows: int = 1 << 22):
+    """Streaming TSMTTSM: C = A^T B over K rows without a
+    host copy of A or B.  ``rows(k0, k1)`` returns (A[k0:k1], B[k0:k1]) as
+    arrays (e.g. regenerated by tsminputs).  Segments are whole 2^16-row
+    blocks, so the result equals ``tsmttsm`` on the full arrays bit for bit.
+    -> (C M x N, bound M x N)."""
+    if seg_rows % ORACLE_BLOCK:
+        raise ValueError("segments must be whole oracle blocks")
+    lib = _load()
+    MN = M * N
+    nblk = (K + ORACLE_BLOCK - 1) // ORACLE_BLOCK
+    per = 5 if is_complex else 3
+    bs = np.zeros(nblk * MN * per + 1, dtype=np.float64)
+    for k0 in range(0, K, seg_rows):
+        k1 = min(K, k0 + seg_rows)
+        A, B = rows(k0, k1)
+        A, B = _prep(A, is_complex), _prep(B, is_complex)
+        if A.shape != (k1 - k0, M) or B.shape != (k1 - k0, N):
+            raise ValueError("rows() returned the wrong shape")
+        b0 = k0 // ORACLE_BLOCK
+        view = bs[b0 * MN * per:]
+        if is_complex:
+            lib.oracle_tsmttsm_z_blocks(k1 - k0, M, N, _ptr(A), _ptr(B), _ptr(view), int(conj))
+        else:
+            lib.oracle_tsmttsm_d_blocks(k1 - k0, M, N, _ptr(A), _ptr(B), _ptr(view))
+    C = np.zeros((M, N), dtype=np.complex128 if is_complex else np.float64)
+    bound = np.zeros((M, N), dtype=np.float64)
+    (lib.oracle_tsmttsm_z_combine if is_complex else lib.oracle_tsmttsm_d_combine)(nblk, M, N, _ptr(bs),
+                                                                                   _ptr(C), _ptr(bound))
     return C, bound
 
 

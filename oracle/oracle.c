@@ -30,7 +30,13 @@
  *        inside a block of ORACLE_BLOCK = 2^16 rows,
  *     3. Neumaier-compensated accumulation of the block sums in block order.
  *   The structure is fixed by K alone, so results are bitwise independent of
- *   the OpenMP thread count.  Complex cells use the 4 fmas
+ *   the OpenMP thread count.  Steps 1-2 (oracle_tsmttsm_{d,z}_blocks) and
+ *   step 3 (oracle_tsmttsm_{d,z}_combine) are also exported on their own:
+ *   the streaming mode of SURVEY.md §8(c) feeds the rows segment by segment
+ *   (segments of whole 2^16-row blocks, regenerated from the input generator)
+ *   and combines all blocks at the end -- the same operations in the same
+ *   order as the one-shot call, so the same result bit for bit, with no host
+ *   copy of a K = 2^28 matrix.  Complex cells use the 4 fmas
  *     re += ar*br; re -= ai*bi; im += ar*bi; im += ai*br
  *   in that order (8 real flops per complex multiply-add).
  *   TSMM sums only M <= 64 terms: a serial fma chain over m increasing.
@@ -90,12 +96,13 @@ void oracle_set_num_threads(int n) {
 /* TSMTTSM, real double.  C = A^T B (Listing 1).           */
 /* C and bound are M*N row-major outputs; bound may be NULL.                 */
 /* ------------------------------------------------------------------------ */
-void oracle_tsmttsm_d(int64_t K, int M, int N, const double *A, const double *B,
-                      double *C, double *bound) {
+/* Steps 1-2 for every 2^16-row block of rows [0, K): per block and cell the
+ * compensated sum of its chunk sums (S, Cc) and the bound term (Bd), written
+ * to bs[b][3][MN] (zeroed by the caller). */
+void oracle_tsmttsm_d_blocks(int64_t K, int M, int N, const double *A, const double *B,
+                             double *bs) {
   const int64_t MN = (int64_t)M * N;
   const int64_t nblk = (K + ORACLE_BLOCK - 1) / ORACLE_BLOCK;
-  /* per block: sum, compensation, bound */
-  double *bs = (double *)calloc((size_t)(nblk * MN * 3 + 1), sizeof(double));
 #pragma omp parallel
   {
     double *acc = (double *)malloc(sizeof(double) * (size_t)MN);
@@ -126,6 +133,11 @@ void oracle_tsmttsm_d(int64_t K, int M, int N, const double *A, const double *B,
     free(acc);
     free(accb);
   }
+}
+
+/* Step 3: the block results combined in block order (compensated). */
+void oracle_tsmttsm_d_combine(int64_t nblk, int M, int N, const double *bs, double *C, double *bound) {
+  const int64_t MN = (int64_t)M * N;
   for (int64_t i = 0; i < MN; i++) {
     double s = 0, c = 0, bd = 0;
     for (int64_t b = 0; b < nblk; b++) {
@@ -137,6 +149,16 @@ void oracle_tsmttsm_d(int64_t K, int M, int N, const double *A, const double *B,
     C[i] = s + c;
     if (bound) bound[i] = bd;
   }
+}
+
+void oracle_tsmttsm_d(int64_t K, int M, int N, const double *A, const double *B,
+                      double *C, double *bound) {
+  const int64_t MN = (int64_t)M * N;
+  const int64_t nblk = (K + ORACLE_BLOCK - 1) / ORACLE_BLOCK;
+  /* per block: sum, compensation, bound */
+  double *bs = (double *)calloc((size_t)(nblk * MN * 3 + 1), sizeof(double));
+  oracle_tsmttsm_d_blocks(K, M, N, A, B, bs);
+  oracle_tsmttsm_d_combine(nblk, M, N, bs, C, bound);
   free(bs);
 }
 
@@ -146,12 +168,12 @@ void oracle_tsmttsm_d(int64_t K, int M, int N, const double *A, const double *B,
 /* Gram-Schmidt use of PAPER.md:108-112 needs A^H): conj(a) = ar - i ai is   */
 /* substituted for a, i.e. ai -> -ai in the same 4 fmas.                     */
 /* ------------------------------------------------------------------------ */
-static void tsmttsm_z_impl(int64_t K, int M, int N, const double *A, const double *B,
-                           double *C, double *bound, int conj) {
+/* Steps 1-2 per block (complex): bs[b][5][MN] = re sum, re comp, im sum,
+ * im comp, bound (zeroed by the caller). */
+void oracle_tsmttsm_z_blocks(int64_t K, int M, int N, const double *A, const double *B,
+                             double *bs, int conj) {
   const int64_t MN = (int64_t)M * N;
   const int64_t nblk = (K + ORACLE_BLOCK - 1) / ORACLE_BLOCK;
-  /* per block: re sum, re comp, im sum, im comp, bound */
-  double *bs = (double *)calloc((size_t)(nblk * MN * 5 + 1), sizeof(double));
 #pragma omp parallel
   {
     double *acc = (double *)malloc(sizeof(double) * (size_t)MN * 2);
@@ -194,6 +216,11 @@ static void tsmttsm_z_impl(int64_t K, int M, int N, const double *A, const doubl
     free(acc);
     free(accb);
   }
+}
+
+/* Step 3 (complex): block results in block order. */
+void oracle_tsmttsm_z_combine(int64_t nblk, int M, int N, const double *bs, double *C, double *bound) {
+  const int64_t MN = (int64_t)M * N;
   for (int64_t i = 0; i < MN; i++) {
     double sr = 0, cr = 0, si = 0, ci = 0, bd = 0;
     for (int64_t b = 0; b < nblk; b++) {
@@ -208,8 +235,19 @@ static void tsmttsm_z_impl(int64_t K, int M, int N, const double *A, const doubl
     C[2 * i + 1] = si + ci;
     if (bound) bound[i] = bd;
   }
+}
+
+static void tsmttsm_z_impl(int64_t K, int M, int N, const double *A, const double *B,
+                           double *C, double *bound, int conj) {
+  const int64_t MN = (int64_t)M * N;
+  const int64_t nblk = (K + ORACLE_BLOCK - 1) / ORACLE_BLOCK;
+  /* per block: re sum, re comp, im sum, im comp, bound */
+  double *bs = (double *)calloc((size_t)(nblk * MN * 5 + 1), sizeof(double));
+  oracle_tsmttsm_z_blocks(K, M, N, A, B, bs, conj);
+  oracle_tsmttsm_z_combine(nblk, M, N, bs, C, bound);
   free(bs);
 }
+
 
 void oracle_tsmttsm_z(int64_t K, int M, int N, const double *A, const double *B,
                       double *C, double *bound) {

@@ -534,3 +534,25 @@ def test_generator_c_matches_numpy():
         assert np.array_equal(ti.columns(K, w, cols, "A", complex_=cplx), full[:, cols])
         assert np.array_equal(ti.column(K, w, 12, "A", complex_=cplx), full[:, 12])
         assert np.array_equal(ti.matrix(K, w, "A", complex_=cplx), full)
+
+
+def test_streaming_mode_equals_one_shot():
+    """oracle.tsmttsm_stream (rows regenerated segment by segment, SURVEY.md
+    §8(c) streaming mode) equals the one-shot oracle bit for bit, D / Z / conj,
+    with a ragged last block and segments of several blocks."""
+    import tsminputs as ti
+    K = 5 * (1 << 16) + 777
+    for cplx, conj in ((False, False), (True, False), (True, True)):
+        M, N = 3, 4
+        A = ti.columns(K, 7, [0, 2, 6], "A", complex_=cplx)
+        B = ti.columns(K, 9, [1, 2, 3, 8], "B", complex_=cplx)
+
+        def rows(k0, k1):
+            return (ti.columns(k1 - k0, 7, [0, 2, 6], "A", complex_=cplx, row0=k0),
+                    ti.columns(k1 - k0, 9, [1, 2, 3, 8], "B", complex_=cplx, row0=k0))
+        ref, rb = oracle.tsmttsm(A, B, conj=conj)
+        got, gb = oracle.tsmttsm_stream(K, M, N, rows, cplx, conj=conj, seg_rows=2 << 16)
+        assert np.array_equal(got, ref) and np.array_equal(gb, rb)
+        # the columns of the full matrices are the same values
+        full = ti.matrix(K, 7, "A", complex_=cplx)
+        assert np.array_equal(full[:, [0, 2, 6]], A)

@@ -88,7 +88,7 @@ def _lib():
         u64, i64 = ctypes.c_uint64, ctypes.c_int64
         lib.tsmgen_strided.argtypes = [dp, i64, u64, u64, u64, ctypes.c_int]
         lib.tsmgen_strided.restype = None
-        lib.tsmgen_columns.argtypes = [dp, i64, i64, ctypes.POINTER(i64), ctypes.c_int, u64, ctypes.c_int,
+        lib.tsmgen_columns.argtypes = [dp, i64, i64, i64, ctypes.POINTER(i64), ctypes.c_int, u64, ctypes.c_int,
                                        ctypes.c_int]
         lib.tsmgen_columns.restype = None
         _gen = lib
@@ -109,15 +109,16 @@ def raw_values(n: int, seed: int, mat: str, mode: str, start: int = 0) -> np.nda
 
 
 def columns(K: int, width: int, cols, mat: str, *, complex_: bool = False, mode: str = "fp",
-            seed: int | None = None) -> np.ndarray:
-    """Columns `cols` of matrix(K, width, mat, ...) as a K x len(cols) array (gen.c)."""
+            seed: int | None = None, row0: int = 0) -> np.ndarray:
+    """Rows [row0, row0 + K) of columns `cols` of a `width`-column generator
+    matrix as a K x len(cols) array (gen.c)."""
     if seed is None:
         seed = SEED_FP if mode == "fp" else SEED_INT
     c = np.ascontiguousarray(cols, dtype=np.int64)
     if c.size and (c.min() < 0 or c.max() >= width):
         raise ValueError("column out of range")
     out = np.empty((K, c.size), dtype=np.complex128 if complex_ else np.float64)
-    _lib().tsmgen_columns(_dptr(out), K, width, c.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), c.size,
+    _lib().tsmgen_columns(_dptr(out), row0, K, width, c.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), c.size,
                           int(key(seed, mat)), _MODE[mode], int(complex_))
     return out
 

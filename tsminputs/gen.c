@@ -36,14 +36,15 @@ void tsmgen_strided(double *out, int64_t n, uint64_t start, uint64_t stride, uin
   for (int64_t j = 0; j < n; j++) out[j] = value(key, start + (uint64_t)j * stride, mode);
 }
 
-/* Columns cols[0..ncol) of the K x width matrix, written row-major into out
- * (K x ncol; complex: interleaved re, im, element e -> indices 2e, 2e+1). */
-void tsmgen_columns(double *out, int64_t K, int64_t width, const int64_t *cols, int ncol,
+/* Rows [row0, row0 + K) x columns cols[0..ncol) of a matrix of `width`
+ * columns, written row-major into out (K x ncol; complex: interleaved re, im,
+ * element e -> indices 2e, 2e+1). */
+void tsmgen_columns(double *out, int64_t row0, int64_t K, int64_t width, const int64_t *cols, int ncol,
                     uint64_t key, int mode, int cplx) {
 #pragma omp parallel for schedule(static)
   for (int64_t k = 0; k < K; k++) {
     for (int c = 0; c < ncol; c++) {
-      uint64_t e = (uint64_t)k * (uint64_t)width + (uint64_t)cols[c];
+      uint64_t e = (uint64_t)(row0 + k) * (uint64_t)width + (uint64_t)cols[c];
       if (cplx) {
         out[2 * (k * ncol + c)] = value(key, 2 * e, mode);
         out[2 * (k * ncol + c) + 1] = value(key, 2 * e + 1, mode);
