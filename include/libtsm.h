@@ -128,7 +128,10 @@ typedef struct tsm_config {
                      per-row-group output staging (any width; p0 = NBW, p1 = WR).
                  Flags (OR-ed in, DMMA TSMTTSM kernels 1/2 unless noted):
                    16  DFMA edge warps for the cells outside the 8-aligned core;
-                       bits 6-7 = edge warps - 1 (1..4 warps splitting the rows);
+                       bits 6-7 = edge warps - 1 (1..4 warps splitting the rows).
+                       TSMM kernels 3 and 4: the last N mod 8 columns of B by DFMA
+                       in the warps of the last column group instead of a padded
+                       8-column DMMA block (N >= 8, N not a multiple of 8);
                    32  paired 16-byte fragment loads (D, even p0/p1);
                    256 complex-as-real (Z; TSMTTSM 1/2, TSMM 3): the real kernel runs
                        on the interleaved (re, im) view -- A, B as real K x 2M, K x 2N --
@@ -175,6 +178,12 @@ tsm_status tsm_plan_get_config(tsm_plan p, tsm_config *cfg);
  *                  shapes without one (rows must be >= 128 bytes and 16-byte
  *                  multiples: D widths even and >= 16, Z widths >= 8). */
 #define TSM_FLAG_STRIDED 2u
+/*   TSM_FLAG_NO_GRID_REDUCE  MEASUREMENT ONLY (TSMTTSM): the reduction-     */
+/*                  overhead baseline of PAPER.md:1000-1016 ("a kernel      */
+/*                  without a global reduction"): every block computes and  */
+/*                  writes its partial to the workspace, the grid reduction */
+/*                  (T4) is skipped and C is NOT written.  Not for results. */
+#define TSM_FLAG_NO_GRID_REDUCE 4u
 
 /* tsm_plan_create / tsm_plan_create_config with flags: cfg == NULL selects the
  * tuned default configuration.  TSM_ERR_INVALID_VALUE for unknown flags or
@@ -214,6 +223,17 @@ const char *tsm_last_error_detail(void);
 /* TSMTTSM  C = A^T B                         */
 /*   A: K x M device, B: K x N device, C: M x N device (overwritten).        */
 /*   ws: workspace of >= tsm_plan_workspace_bytes(p, K) bytes.               */
+/*   Grid-reduction progress rule (T4): each block writes its partial, takes */
+/*   a ticket, and the last `nfin` blocks to arrive wait (spin) until every  */
+/*   block of the launch has arrived, then sum the partials in fixed block   */
+/*   order.  The grid is at most SMs x CTAs/SM, so on an otherwise idle GPU  */
+/*   every block is resident and the wait ends.  The call relies on the      */
+/*   remaining blocks becoming resident eventually: a kernel running         */
+/*   concurrently on another stream (or another MPS client) that holds SMs   */
+/*   indefinitely -- e.g. a persistent kernel, or an NCCL kernel waiting for */
+/*   a peer that itself waits on this call -- can stall it.  Concurrent      */
+/*   kernels that finish on their own (any libtsm call, NCCL collectives     */
+/*   whose peers progress independently) only delay it.                      */
 /* ------------------------------------------------------------------------ */
 tsm_status tsmttsm_d(tsm_plan p, int64_t K, const double *A, const double *B, double *C,
                      void *ws, size_t ws_bytes, tsm_stream stream);

@@ -26,6 +26,7 @@ DTYPE = {"d": 0, "z": 1}
 TSM_COMM_DETERMINISTIC = 1
 TSM_FLAG_CONJ = 1
 TSM_FLAG_STRIDED = 2
+TSM_FLAG_NO_GRID_REDUCE = 4  # measurement only: TSMTTSM without T4, C not written
 MAT_ID = {"A": 1, "B": 2, "C": 3}
 
 # exported symbols declared in include/libtsm.h (checked by tests/test_abi.py)
@@ -262,14 +263,18 @@ class Plan:
     """Owning wrapper of a tsm_plan handle."""
 
     def __init__(self, op: str, dtype: str, M: int, N: int, device: int = 0,
-                 config: dict | None = None, conj: bool = False, strided: bool = False):
+                 config: dict | None = None, conj: bool = False, strided: bool = False,
+                 no_grid_reduce: bool = False):
         """conj=True (Z only, TSM_FLAG_CONJ): TSMTTSM C = A^H B, TSMM B = A conj(C).
-        strided=True (TSM_FLAG_STRIDED): a kernel that takes strided row views."""
+        strided=True (TSM_FLAG_STRIDED): a kernel that takes strided row views.
+        no_grid_reduce=True (TSM_FLAG_NO_GRID_REDUCE): MEASUREMENT ONLY, the
+        reduction-overhead baseline; C is not written."""
         self.op, self.dtype, self.M, self.N, self.device = op, dtype, M, N, device
         self.conj, self.strided = conj, strided
         self.handle = None
-        if conj or strided:
-            flags = (TSM_FLAG_CONJ if conj else 0) | (TSM_FLAG_STRIDED if strided else 0)
+        if conj or strided or no_grid_reduce:
+            flags = (TSM_FLAG_CONJ if conj else 0) | (TSM_FLAG_STRIDED if strided else 0) | \
+                (TSM_FLAG_NO_GRID_REDUCE if no_grid_reduce else 0)
             self.handle = tsm_plan_create_ex(op, dtype, M, N, device, config, flags)
         elif config is None:
             self.handle = tsm_plan_create(op, dtype, M, N, device)

@@ -553,7 +553,10 @@ tsm_status tsm_plan_create_ex(tsm_plan* out, tsm_op op, tsm_dtype dtype, int M, 
                               const tsm_config* cfg, unsigned flags) {
   if (!out) return fail(TSM_ERR_INVALID_VALUE, "out == NULL");
   *out = nullptr;
-  if (flags & ~(TSM_FLAG_CONJ | TSM_FLAG_STRIDED)) return fail(TSM_ERR_INVALID_VALUE, "unknown plan flags");
+  if (flags & ~(TSM_FLAG_CONJ | TSM_FLAG_STRIDED | TSM_FLAG_NO_GRID_REDUCE))
+    return fail(TSM_ERR_INVALID_VALUE, "unknown plan flags");
+  if ((flags & TSM_FLAG_NO_GRID_REDUCE) && op != TSM_OP_TSMTTSM)
+    return fail(TSM_ERR_INVALID_VALUE, "TSM_FLAG_NO_GRID_REDUCE applies to TSMTTSM plans");
   if ((flags & TSM_FLAG_CONJ) && dtype != TSM_Z)
     return fail(TSM_ERR_INVALID_VALUE, "TSM_FLAG_CONJ applies to Z plans");
   tsm_status st;
@@ -767,7 +770,7 @@ tsm_status launch_tsmttsm(const tsm_plan_s* p, int dt, long long K, const void* 
   a.K = K;
   a.nchunks = g.nchunks;
   a.stages = p->stages;
-  a.nfin = g.nfin;
+  a.nfin = (p->flags & TSM_FLAG_NO_GRID_REDUCE) ? 0 : g.nfin;
   a.order = p->order;
   a.conj = (p->flags & TSM_FLAG_CONJ) ? (1ull << 63) : 0ull;
   if (peer) {

@@ -391,6 +391,9 @@ __device__ __forceinline__ void grid_reduce(const TsmttsmArgs& p, const double* 
   const int G = gridDim.x;
   double* myP = p.partials + static_cast<long long>(blockIdx.x) * CELLS;
   for (int idx = tid; idx < CELLS; idx += NT) __stcg(&myP[idx], sP[idx]);
+  // nfin == 0: the reduction-overhead baseline (TSM_FLAG_NO_GRID_REDUCE,
+  // PAPER.md:1000-1016 "a kernel without a global reduction"): partials only
+  if (p.nfin == 0) return;
 
   // ---- T4: deterministic grid reduction by the last NFIN blocks ----
   __threadfence();

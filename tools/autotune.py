@@ -137,6 +137,11 @@ def main():
                     ts.sort()
                     return ts[len(ts) // 2]
 
+                # the current default plan (tuned table entry), timed in this run
+                try:
+                    default_ms = timeit(tsm.Plan(op, dt, M, N, 0))
+                except Exception:  # noqa: BLE001
+                    default_ms = None
                 t0 = time.time()
                 plans = list(pool.map(make, cands))
                 t_comp = time.time() - t0
@@ -171,11 +176,15 @@ def main():
                 cfg["stages"] = got["stages"]
                 cfg["ctas"] = got["ctas_per_sm"]
                 prev = db["entries"].get(key)
-                if a.keep_better and prev and prev["ms"] <= t:
-                    print(f"{key}: kept stored {prev['ms']:.4f} ms (this run {t:.4f} ms {cfg})", flush=True)
+                # keep-better: compare with the default plan timed in THIS run (same
+                # clocks), else with the stored time
+                ref_ms = default_ms if default_ms is not None else (prev["ms"] if prev else None)
+                if a.keep_better and prev and ref_ms is not None and ref_ms <= t:
+                    print(f"{key}: kept stored (default {ref_ms:.4f} ms this run; best candidate {t:.4f} ms "
+                          f"{cfg})", flush=True)
                     continue
                 db["entries"][key] = {"cfg": cfg, "ms": t, "frac": roof / (t * 1e-3),
-                                      "candidates": len(res), "default_ms": None}
+                                      "candidates": len(res), "default_ms": default_ms}
                 print(f"{key}: best {t:.4f} ms ({100 * roof / (t * 1e-3):.1f}% roof) "
                       f"{cfg} [{len(res)} cands, compile {t_comp:.1f}s]"
                       + (f" prev {prev['ms']:.4f}" if prev else ""), flush=True)
