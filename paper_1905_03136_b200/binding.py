@@ -389,10 +389,12 @@ def workspace(plan: Plan, K: int, stream: int, min_bytes: int = 0):
     return buf
 
 
-def tsmttsm(A, B, out=None, plan: Plan | None = None, conj: bool = False):
+def tsmttsm(A, B, out=None, plan: Plan | None = None, conj: bool | None = None):
     """C = A^T B (plain transpose; conj=True: A^H B, Z only) for torch CUDA
     tensors A (K x M), B (K x N).  Row-strided views (e.g. column subsets of a
-    wider block vector) go through tsmttsm_ld_* with a TSM_FLAG_STRIDED plan."""
+    wider block vector) go through tsmttsm_ld_* with a TSM_FLAG_STRIDED plan.
+    conj=None takes the plan's TSM_FLAG_CONJ (False without a plan); an
+    explicit value must match the plan's."""
     torch = _torch()
     _check_rows(A, B)
     dt = _dtype_code(A)
@@ -405,6 +407,8 @@ def tsmttsm(A, B, out=None, plan: Plan | None = None, conj: bool = False):
     lda, ldb = _ld(A), _ld(B)
     dense = lda == M and ldb == N
     _check_plan(plan, "tsmttsm", dt, M, N, dev)
+    if conj is None:
+        conj = plan.conj if plan is not None else False
     if plan is not None and plan.conj != conj:
         raise ValueError("conj does not match the plan's TSM_FLAG_CONJ")
     plan = plan or get_plan("tsmttsm", dt, M, N, dev, conj, strided=not dense)
@@ -453,9 +457,9 @@ def tsmm(A, C, out=None, plan: Plan | None = None):
     return B
 
 
-def tsmm_update(A, C, B, alpha=1.0, beta=0.0, plan: Plan | None = None, conj: bool = False):
-    """In place B <- alpha * A C + beta * B (NEXT N1; conj: A conj(C), Z only).
-    Returns B."""
+def tsmm_update(A, C, B, alpha=1.0, beta=0.0, plan: Plan | None = None, conj: bool | None = None):
+    """In place B <- alpha * A C + beta * B (NEXT N1; conj: A conj(C), Z only;
+    conj=None takes the plan's TSM_FLAG_CONJ).  Returns B."""
     torch = _torch()
     _check_cuda(A, C, B)
     dt = _dtype_code(A)
@@ -466,6 +470,8 @@ def tsmm_update(A, C, B, alpha=1.0, beta=0.0, plan: Plan | None = None, conj: bo
     N = C.shape[1]
     _same(A, C, B)
     _check_plan(plan, "tsmm", dt, M, N, A.device.index)
+    if conj is None:
+        conj = plan.conj if plan is not None else False
     if plan is not None and plan.conj != conj:
         raise ValueError("conj does not match the plan's TSM_FLAG_CONJ")
     plan = plan or get_plan("tsmm", dt, M, N, A.device.index, conj)

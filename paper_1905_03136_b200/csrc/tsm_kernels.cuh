@@ -2417,6 +2417,10 @@ __global__ void __launch_bounds__(Cfg::NT) tsmm_cstb_kernel(const __grid_constan
           }
           fence_proxy_async_smem();
           if (issuer) bulk_wait_read<0>();  // the previous pass's store has read the other buffer
+          // reconverge after the issuer-only wait: bar.sync is .aligned (every lane of
+          // the warp at the same instruction; compute-sanitizer synccheck flagged the
+          // divergent arrival)
+          __syncwarp();
           asm volatile("bar.sync %0, %1;" ::"r"(1 + rg), "r"(NG * 32) : "memory");
           if (issuer) {
             const int nr = (rows - wr0 < RW) ? rows - wr0 : RW;

@@ -42,15 +42,17 @@ def run_one(plan, op, z, M, N, K, conj=False, update=None, strided=False):
     dA = torch.from_numpy(A).cuda()
     if strided:  # a column subset of a wider block vector (ld = width + 8 elements)
         wideA = torch.zeros(K, M + 8, dtype=dA.dtype, device="cuda")
-        wideA[:, 3:3 + M] = dA
-        dA = wideA[:, 3:3 + M]
+        oa = 3 if z else 2  # column offset: 16-byte aligned base (TMA / bulk copies)
+        wideA[:, oa:oa + M] = dA
+        dA = wideA[:, oa:oa + M]
     if op == "tsmttsm":
         B = ti.matrix(K, N, "B", complex_=z, seed=K + 12)
         dB = torch.from_numpy(B).cuda()
         if strided:
             wideB = torch.zeros(K, N + 8, dtype=dB.dtype, device="cuda")
-            wideB[:, 5:5 + N] = dB
-            dB = wideB[:, 5:5 + N]
+            ob = 5 if z else 4
+            wideB[:, ob:ob + N] = dB
+            dB = wideB[:, ob:ob + N]
         got = tsm.tsmttsm(dA, dB, plan=plan, conj=conj)
         ref, bound = oracle.tsmttsm(A, B, conj=conj)
         tol = 1e-12
@@ -69,7 +71,8 @@ def run_one(plan, op, z, M, N, K, conj=False, update=None, strided=False):
             out = None
             if strided:
                 wideO = torch.zeros(K, N + 8, dtype=dA.dtype, device="cuda")
-                out = wideO[:, 1:1 + N]
+                oo = 1 if z else 2
+                out = wideO[:, oo:oo + N]
             got = tsm.tsmm(dA, dC, plan=plan, out=out)
             ref, bound = oracle.tsmm(A, Cm)
             tol = 1e-13
