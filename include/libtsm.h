@@ -173,10 +173,11 @@ tsm_status tsm_plan_get_config(tsm_plan p, tsm_config *cfg);
  *                  sign of Im(A) / Im(C) is flipped on load (exact). */
 #define TSM_FLAG_CONJ 1u
 /*   TSM_FLAG_STRIDED  (NEXT row N4) choose a kernel that takes strided row
- *                  views (tsmttsm_ld_* / tsmm_ld_*): the TMA kernels, whose
- *                  tensor maps carry the row stride.  TSM_ERR_UNSUPPORTED for
- *                  shapes without one (rows must be >= 128 bytes and 16-byte
- *                  multiples: D widths even and >= 16, Z widths >= 8). */
+ *                  views (tsmttsm_ld_* / tsmm_ld_*): a TMA kernel, whose tensor
+ *                  maps carry the row stride, for shapes with 16-byte rows of
+ *                  >= 128 bytes (D widths even and >= 16, Z widths >= 8) --
+ *                  calls then need 16-byte row strides and bases; other shapes
+ *                  get the gather-capable kernel of TSM_FLAG_GATHER. */
 #define TSM_FLAG_STRIDED 2u
 /*   TSM_FLAG_NO_GRID_REDUCE  MEASUREMENT ONLY (TSMTTSM): the reduction-     */
 /*                  overhead baseline of PAPER.md:1000-1016 ("a kernel      */
@@ -184,6 +185,15 @@ tsm_status tsm_plan_get_config(tsm_plan p, tsm_config *cfg);
 /*                  writes its partial to the workspace, the grid reduction */
 /*                  (T4) is skipped and C is NOT written.  Not for results. */
 #define TSM_FLAG_NO_GRID_REDUCE 4u
+/*   TSM_FLAG_GATHER  (NEXT row N4) a gather-capable kernel (TSMTTSM kernel 1,*/
+/*                  TSMM kernel 4) for strided views of ANY row stride and,  */
+/*                  for D, 8-byte aligned A / B bases (column subsets at odd  */
+/*                  offsets): the producer warp copies row elements with     */
+/*                  cp.async (8 / 16 bytes) completing on the stage mbarrier,*/
+/*                  TSMM stores B rows element-wise.  Every shape has one.   */
+/*                  TSM_FLAG_STRIDED picks a TMA kernel when the shape has   */
+/*                  one (16-byte row strides and bases) and this otherwise.  */
+#define TSM_FLAG_GATHER 8u
 
 /* tsm_plan_create / tsm_plan_create_config with flags: cfg == NULL selects the
  * tuned default configuration.  TSM_ERR_INVALID_VALUE for unknown flags or
@@ -253,8 +263,10 @@ tsm_status tsmm_z(tsm_plan p, int64_t K, const tsm_zcomplex *A, const tsm_zcompl
 /* Strided row views (NEXT row N4; block vectors as column subsets of wider   */
 /* arrays): row k of A starts at A + k*lda, of B at B + k*ldb (elements, lda  */
 /* >= M, ldb >= N).  lda == M and ldb == N are the dense calls (any plan);    */
-/* otherwise the plan needs a TMA kernel (TSM_FLAG_STRIDED) and 16-byte row   */
-/* strides, else TSM_ERR_UNSUPPORTED.  C stays dense M x N.                   */
+/* otherwise the plan needs a TSM_FLAG_STRIDED plan with a TMA kernel and     */
+/* 16-byte row strides / bases, or a gather-capable plan (TSM_FLAG_GATHER,    */
+/* or TSM_FLAG_STRIDED on a shape without a TMA kernel): any row stride, D    */
+/* bases 8-byte aligned.  Other plans: TSM_ERR_UNSUPPORTED.  C stays dense.   */
 /* ------------------------------------------------------------------------ */
 tsm_status tsmttsm_ld_d(tsm_plan p, int64_t K, const double *A, int64_t lda, const double *B, int64_t ldb,
                         double *C, void *ws, size_t ws_bytes, tsm_stream stream);

@@ -27,6 +27,7 @@ TSM_COMM_DETERMINISTIC = 1
 TSM_FLAG_CONJ = 1
 TSM_FLAG_STRIDED = 2
 TSM_FLAG_NO_GRID_REDUCE = 4  # measurement only: TSMTTSM without T4, C not written
+TSM_FLAG_GATHER = 8  # gather-capable kernel: any row stride, 8-byte D bases (N4)
 MAT_ID = {"A": 1, "B": 2, "C": 3}
 
 # exported symbols declared in include/libtsm.h (checked by tests/test_abi.py)
@@ -264,17 +265,19 @@ class Plan:
 
     def __init__(self, op: str, dtype: str, M: int, N: int, device: int = 0,
                  config: dict | None = None, conj: bool = False, strided: bool = False,
-                 no_grid_reduce: bool = False):
+                 no_grid_reduce: bool = False, gather: bool = False):
         """conj=True (Z only, TSM_FLAG_CONJ): TSMTTSM C = A^H B, TSMM B = A conj(C).
         strided=True (TSM_FLAG_STRIDED): a kernel that takes strided row views.
         no_grid_reduce=True (TSM_FLAG_NO_GRID_REDUCE): MEASUREMENT ONLY, the
-        reduction-overhead baseline; C is not written."""
+        reduction-overhead baseline; C is not written.
+        gather=True (TSM_FLAG_GATHER): a kernel for strided views of any row
+        stride and 8-byte aligned D bases."""
         self.op, self.dtype, self.M, self.N, self.device = op, dtype, M, N, device
-        self.conj, self.strided = conj, strided
+        self.conj, self.strided, self.gather = conj, strided, gather
         self.handle = None
-        if conj or strided or no_grid_reduce:
+        if conj or strided or no_grid_reduce or gather:
             flags = (TSM_FLAG_CONJ if conj else 0) | (TSM_FLAG_STRIDED if strided else 0) | \
-                (TSM_FLAG_NO_GRID_REDUCE if no_grid_reduce else 0)
+                (TSM_FLAG_NO_GRID_REDUCE if no_grid_reduce else 0) | (TSM_FLAG_GATHER if gather else 0)
             self.handle = tsm_plan_create_ex(op, dtype, M, N, device, config, flags)
         elif config is None:
             self.handle = tsm_plan_create(op, dtype, M, N, device)
@@ -299,12 +302,12 @@ class Plan:
 
 
 def get_plan(op: str, dtype: str, M: int, N: int, device: int, conj: bool = False,
-             strided: bool = False) -> Plan:
-    key = (op, dtype, M, N, device, conj, strided)
+             strided: bool = False, gather: bool = False) -> Plan:
+    key = (op, dtype, M, N, device, conj, strided, gather)
     with _mu:
         p = _plans.get(key)
         if p is None:
-            p = Plan(op, dtype, M, N, device, conj=conj, strided=strided)
+            p = Plan(op, dtype, M, N, device, conj=conj, strided=strided, gather=gather)
             _plans[key] = p
     return p
 
@@ -342,6 +345,19 @@ def _check_rows(*ts):
 
 def _ld(t) -> int:
     return t.stride(0) if t.shape[0] > 1 else t.shape[1]
+
+
+def _view_mode(dt: str, views) -> str:
+    """Plan kind for a call on (tensor, ld, width) views: "dense" (contiguous,
+    16-byte aligned), "strided" (16-byte row strides and bases: TMA kernel when
+    the shape has one), else "gather" (any stride, 8-byte D bases)."""
+    S = 2 if dt == "z" else 1
+    aligned = all(t.data_ptr() % 16 == 0 for t, _, _ in views)
+    if aligned and all(ld == w for _, ld, w in views):
+        return "dense"
+    if aligned and all((ld * S) % 2 == 0 for _, ld, _ in views):
+        return "strided"
+    return "gather"
 
 
 def _check_out(out, shape, like, name="out"):
@@ -405,13 +421,14 @@ def tsmttsm(A, B, out=None, plan: Plan | None = None, conj: bool | None = None):
     dev = A.device.index
     _same(A, B)
     lda, ldb = _ld(A), _ld(B)
-    dense = lda == M and ldb == N
+    mode = _view_mode(dt, [(A, lda, M), (B, ldb, N)])
+    dense = mode == "dense"
     _check_plan(plan, "tsmttsm", dt, M, N, dev)
     if conj is None:
         conj = plan.conj if plan is not None else False
     if plan is not None and plan.conj != conj:
         raise ValueError("conj does not match the plan's TSM_FLAG_CONJ")
-    plan = plan or get_plan("tsmttsm", dt, M, N, dev, conj, strided=not dense)
+    plan = plan or get_plan("tsmttsm", dt, M, N, dev, conj, strided=mode == "strided", gather=mode == "gather")
     _check_out(out, (M, N), A)
     C = out if out is not None else torch.empty((M, N), dtype=A.dtype, device=A.device)
     _check_cuda(C)
@@ -444,9 +461,10 @@ def tsmm(A, C, out=None, plan: Plan | None = None):
     B = out if out is not None else torch.empty((K, N), dtype=A.dtype, device=A.device)
     _check_rows(B)
     lda, ldb = _ld(A), _ld(B)
-    dense = lda == M and ldb == N
+    mode = _view_mode(dt, [(A, lda, M), (B, ldb, N)])
+    dense = mode == "dense"
     _check_plan(plan, "tsmm", dt, M, N, dev)
-    plan = plan or get_plan("tsmm", dt, M, N, dev, strided=not dense)
+    plan = plan or get_plan("tsmm", dt, M, N, dev, strided=mode == "strided", gather=mode == "gather")
     stream = torch.cuda.current_stream(A.device).cuda_stream
     if dense:
         f = tsmm_z if dt == "z" else tsmm_d

@@ -553,7 +553,7 @@ tsm_status tsm_plan_create_ex(tsm_plan* out, tsm_op op, tsm_dtype dtype, int M, 
                               const tsm_config* cfg, unsigned flags) {
   if (!out) return fail(TSM_ERR_INVALID_VALUE, "out == NULL");
   *out = nullptr;
-  if (flags & ~(TSM_FLAG_CONJ | TSM_FLAG_STRIDED | TSM_FLAG_NO_GRID_REDUCE))
+  if (flags & ~(TSM_FLAG_CONJ | TSM_FLAG_STRIDED | TSM_FLAG_NO_GRID_REDUCE | TSM_FLAG_GATHER))
     return fail(TSM_ERR_INVALID_VALUE, "unknown plan flags");
   if ((flags & TSM_FLAG_NO_GRID_REDUCE) && op != TSM_OP_TSMTTSM)
     return fail(TSM_ERR_INVALID_VALUE, "TSM_FLAG_NO_GRID_REDUCE applies to TSMTTSM plans");
@@ -562,15 +562,14 @@ tsm_status tsm_plan_create_ex(tsm_plan* out, tsm_op op, tsm_dtype dtype, int M, 
   tsm_status st;
   if (cfg) {
     st = tsm_plan_create_config(out, op, dtype, M, N, device, cfg);
-  } else if (flags & TSM_FLAG_STRIDED) {
+  } else if (flags & (TSM_FLAG_STRIDED | TSM_FLAG_GATHER)) {
     if (op != TSM_OP_TSMTTSM && op != TSM_OP_TSMM) return fail(TSM_ERR_INVALID_VALUE, "bad op");
     if (dtype != TSM_D && dtype != TSM_Z) return fail(TSM_ERR_INVALID_VALUE, "bad dtype");
     if (M < 1 || M > 64 || N < 1 || N > 64)
       return fail(TSM_ERR_INVALID_VALUE, "M and N must be in [1, 64] (PAPER.md:57-58)");
-    const KernelEntry* d = default_params_strided(op, dtype, M, N);
-    if (!d)
-      return fail(TSM_ERR_UNSUPPORTED, "no TMA kernel for this shape (strided views need rows of >= 128 "
-                                       "bytes that are 16-byte multiples)");
+    const KernelEntry* d = (flags & TSM_FLAG_GATHER) ? default_params_gather(op, dtype, M, N)
+                                                     : default_params_strided(op, dtype, M, N);
+    if (!d) return fail(TSM_ERR_UNSUPPORTED, "no strided-view kernel for this shape");
     st = make_plan(out, *d, device, true);  // exactly this configuration (AOT if instantiated, else JIT)
   } else {
     st = tsm_plan_create(out, op, dtype, M, N, device);
@@ -578,7 +577,13 @@ tsm_status tsm_plan_create_ex(tsm_plan* out, tsm_op op, tsm_dtype dtype, int M, 
   if (st == TSM_SUCCESS && (flags & TSM_FLAG_STRIDED) && !strided_capable(*(*out)->k)) {
     tsm_plan_destroy(*out);
     *out = nullptr;
-    return fail(TSM_ERR_INVALID_VALUE, "TSM_FLAG_STRIDED needs a TMA kernel configuration (TSMTTSM 2, TSMM 2/3)");
+    return fail(TSM_ERR_INVALID_VALUE,
+                "TSM_FLAG_STRIDED needs a TMA (TSMTTSM 2, TSMM 2/3) or gather-capable (TSMTTSM 1, TSMM 4) kernel");
+  }
+  if (st == TSM_SUCCESS && (flags & TSM_FLAG_GATHER) && !gather_capable(*(*out)->k)) {
+    tsm_plan_destroy(*out);
+    *out = nullptr;
+    return fail(TSM_ERR_INVALID_VALUE, "TSM_FLAG_GATHER needs kernel 1 (TSMTTSM) or 4 (TSMM)");
   }
   if (st == TSM_SUCCESS) (*out)->flags = flags;
   return st;
@@ -607,7 +612,8 @@ tsm_status tsm_jit_precompile(tsm_op op, tsm_dtype dtype, int M, int N, const ts
     tsm_status st = validate_config(e);
     if (st != TSM_SUCCESS) return st;
   } else {
-    const KernelEntry* d = (flags & TSM_FLAG_STRIDED) ? default_params_strided(op, dtype, M, N)
+    const KernelEntry* d = (flags & TSM_FLAG_GATHER)    ? default_params_gather(op, dtype, M, N)
+                           : (flags & TSM_FLAG_STRIDED) ? default_params_strided(op, dtype, M, N)
                                                        : default_params(op, dtype, M, N);
     if (!d) return fail(TSM_ERR_UNSUPPORTED, "no configuration for this shape / flags");
     e = *d;
@@ -716,22 +722,39 @@ static bool strided_overlap(const void* x, long long ldx, int wx, const void* y,
   return hit(ax0, ax1, by0, by1) || hit(ax0 + pitch, ax1 + pitch, by0, by1) || hit(ax0, ax1, by0 + pitch, by1 + pitch);
 }
 
-bool strided_capable(const KernelEntry& k) {
+static bool tma_kernel(const KernelEntry& k) {
   return k.op == KIND_TSMTTSM ? k.impl == 2 : (k.impl == 2 || k.impl == 3);
 }
+bool gather_capable(const KernelEntry& k) { return k.op == KIND_TSMTTSM ? k.impl == 1 : k.impl == 4; }
+bool strided_capable(const KernelEntry& k) { return tma_kernel(k) || gather_capable(k); }
 
-// Row strides (elements) of a call: 0 = dense.  Strided views need a TMA
-// kernel and 16-byte row strides (NEXT N4).
+// Row strides (elements) of a call: 0 = dense.  Strided views (NEXT N4) need a
+// TMA kernel (16-byte row strides) or a gather-capable kernel (any stride).
 static tsm_status check_ld(const tsm_plan_s* p, int dt, long long* lda, long long* ldb, int wa, int wb) {
   if (*lda == 0) *lda = wa;
   if (*ldb == 0) *ldb = wb;
   if (*lda < wa || *ldb < wb) return fail(TSM_ERR_INVALID_VALUE, "leading dimension smaller than the width");
   if (*lda == wa && *ldb == wb) return TSM_SUCCESS;
+  if (gather_capable(*p->k)) return TSM_SUCCESS;
   const int S = dt == TSM_Z ? 2 : 1;
-  if (!strided_capable(*p->k))
-    return fail(TSM_ERR_UNSUPPORTED, "strided views need a TMA kernel: create the plan with TSM_FLAG_STRIDED");
-  if ((*lda * S) % 2 || (*ldb * S) % 2) return fail(TSM_ERR_UNSUPPORTED, "strided rows must be 16-byte multiples");
+  if (!tma_kernel(*p->k))
+    return fail(TSM_ERR_UNSUPPORTED,
+                "strided views need a TSM_FLAG_STRIDED or TSM_FLAG_GATHER plan (TMA or gather-capable kernel)");
+  if ((*lda * S) % 2 || (*ldb * S) % 2)
+    return fail(TSM_ERR_UNSUPPORTED, "TMA plans need 16-byte row strides: use a TSM_FLAG_GATHER plan");
   return TSM_SUCCESS;
+}
+
+// Base alignment of A / B: 16 bytes, except 8 bytes for D views on a
+// gather-capable plan (element-wise copies; *gather is set).
+static bool ab_misaligned(const tsm_plan_s* p, int dt, const void* A, const void* B, bool* gather) {
+  if (!misaligned(A) && !misaligned(B)) return false;
+  auto a8 = [](const void* x) { return (reinterpret_cast<uintptr_t>(x) & 7u) == 0; };
+  if (dt == TSM_D && gather_capable(*p->k) && a8(A) && a8(B)) {
+    *gather = true;
+    return false;
+  }
+  return true;
 }
 
 tsm_status launch_tsmttsm(const tsm_plan_s* p, int dt, long long K, const void* A, const void* B,
@@ -742,12 +765,15 @@ tsm_status launch_tsmttsm(const tsm_plan_s* p, int dt, long long K, const void* 
     return fail(TSM_ERR_INVALID_VALUE, "plan op/dtype does not match the call");
   if (K < (allow_k0 ? 0 : 1)) return fail(TSM_ERR_INVALID_VALUE, "K must be >= 1");
   if (!C || !ws || (K > 0 && (!A || !B))) return fail(TSM_ERR_INVALID_VALUE, "null pointer");
-  if (misaligned(A) || misaligned(B) || misaligned(C) || misaligned(ws))
-    return fail(TSM_ERR_MISALIGNED, "A, B, C and ws must be 16-byte aligned");
+  bool gather = false;
+  if (ab_misaligned(p, dt, A, B, &gather) || misaligned(C) || misaligned(ws))
+    return fail(TSM_ERR_MISALIGNED, "A, B, C and ws must be 16-byte aligned (8 bytes for D A, B on a "
+                                    "gather-capable plan)");
   {
     tsm_status st = check_ld(p, dt, &lda, &ldb, p->M, p->N);
     if (st != TSM_SUCCESS) return st;
   }
+  gather = gather_capable(*p->k) && (gather || lda != p->M || ldb != p->N);
   const size_t s = (dt == TSM_Z ? 16 : 8);
   const size_t nA = K > 0 ? (static_cast<size_t>(K - 1) * lda + p->M) * s : 0;
   const size_t nB = K > 0 ? (static_cast<size_t>(K - 1) * ldb + p->N) * s : 0;
@@ -773,6 +799,10 @@ tsm_status launch_tsmttsm(const tsm_plan_s* p, int dt, long long K, const void* 
   a.nfin = (p->flags & TSM_FLAG_NO_GRID_REDUCE) ? 0 : g.nfin;
   a.order = p->order;
   a.conj = (p->flags & TSM_FLAG_CONJ) ? (1ull << 63) : 0ull;
+  // (complex-as-real kernels see the interleaved rows as 2M / 2N real elements)
+  a.lda = lda * (zr_flag(p->k->edge) ? 2 : 1);
+  a.ldb = ldb * (zr_flag(p->k->edge) ? 2 : 1);
+  a.gather = gather ? 1 : 0;
   if (peer) {
     a.peer = *peer;
   } else {
@@ -796,16 +826,19 @@ tsm_status launch_tsmttsm(const tsm_plan_s* p, int dt, long long K, const void* 
 // overlap); lda / ldb are normalised (0 -> dense).  Runs before anything is
 // enqueued, also for the update's scale pass.
 static tsm_status validate_tsmm(const tsm_plan_s* p, int dt, long long K, const void* A, const void* C,
-                                void* B, bool allow_k0, long long* lda, long long* ldb) {
+                                void* B, bool allow_k0, long long* lda, long long* ldb, bool* gather) {
   if (!p) return fail(TSM_ERR_INVALID_VALUE, "plan == NULL");
   if (p->op != TSM_OP_TSMM || p->dt != dt)
     return fail(TSM_ERR_INVALID_VALUE, "plan op/dtype does not match the call");
   if (K < (allow_k0 ? 0 : 1)) return fail(TSM_ERR_INVALID_VALUE, "K must be >= 1");
   if (!C || (K > 0 && (!A || !B))) return fail(TSM_ERR_INVALID_VALUE, "null pointer");
-  if (misaligned(A) || misaligned(B) || misaligned(C))
-    return fail(TSM_ERR_MISALIGNED, "A, B and C must be 16-byte aligned");
+  bool g = false;
+  if (ab_misaligned(p, dt, A, B, &g) || misaligned(C))
+    return fail(TSM_ERR_MISALIGNED, "A, B and C must be 16-byte aligned (8 bytes for D A, B on a "
+                                    "gather-capable plan)");
   tsm_status st = check_ld(p, dt, lda, ldb, p->M, p->N);
   if (st != TSM_SUCCESS) return st;
+  *gather = gather_capable(*p->k) && (g || *lda != p->M || *ldb != p->N);
   const size_t s = (dt == TSM_Z ? 16 : 8);
   const size_t nC = static_cast<size_t>(p->M) * p->N * s;
   if (strided_overlap(A, *lda, p->M, B, *ldb, p->N, K, s) || overlap(B, K > 0 ? (static_cast<size_t>(K - 1) * *ldb + p->N) * s : 0, C, nC))
@@ -816,8 +849,9 @@ static tsm_status validate_tsmm(const tsm_plan_s* p, int dt, long long K, const 
 tsm_status launch_tsmm(const tsm_plan_s* p, int dt, long long K, const void* A, const void* C,
                        void* B, void* stream, bool allow_k0, const TsmmMode* mode, long long lda,
                        long long ldb) {
+  bool gather = false;
   {
-    tsm_status st = validate_tsmm(p, dt, K, A, C, B, allow_k0, &lda, &ldb);
+    tsm_status st = validate_tsmm(p, dt, K, A, C, B, allow_k0, &lda, &ldb, &gather);
     if (st != TSM_SUCCESS) return st;
   }
   if (K == 0) return TSM_SUCCESS;
@@ -838,6 +872,9 @@ tsm_status launch_tsmm(const tsm_plan_s* p, int dt, long long K, const void* A, 
   a.alpha_im = dt == TSM_Z ? mode->alpha_im : 0.0;
   a.order = p->order;
   a.conj = (p->flags & TSM_FLAG_CONJ) ? (1ull << 63) : 0ull;
+  a.lda = lda;
+  a.ldb = ldb;
+  a.gather = gather ? 1 : 0;
   if (p->k->impl == 2 || p->k->impl == 3) {  // B store boxes: 8*WR rows (WR = p0 for kernel 2, p1 for kernel 3)
     const int S = dt == TSM_Z ? 2 : 1;
     const int wr = p->k->impl == 3 ? p->k->p1 : p->k->p0;
@@ -862,7 +899,8 @@ tsm_status launch_tsmm_update(const tsm_plan_s* p, int dt, long long K, double a
     // validate everything first (every check of the TSMM launch, overlap
     // included), then scale B: a rejected call leaves B untouched
     long long lda = 0, ldb = 0;
-    tsm_status vs = validate_tsmm(p, dt, K, A, C, B, allow_k0, &lda, &ldb);
+    bool gather = false;
+    tsm_status vs = validate_tsmm(p, dt, K, A, C, B, allow_k0, &lda, &ldb, &gather);
     if (vs != TSM_SUCCESS) return vs;
     DeviceGuard dg(p->device);
     if (dg.err != cudaSuccess) return cuda_fail(dg.err, "cudaSetDevice");

@@ -11,9 +11,12 @@ namespace tsm {
 const KernelEntry* find_aot(int op, int dt, int M, int N);
 const KernelEntry* find_aot_config(const KernelEntry& want);  // same shape AND config
 const KernelEntry* default_params(int op, int dt, int M, int N);
-// TSM_FLAG_STRIDED plans (NEXT N4): a TMA kernel configuration, nullptr if none
+// TSM_FLAG_STRIDED plans (NEXT N4): a TMA kernel configuration when the shape
+// has one, else a gather-capable one; TSM_FLAG_GATHER: always gather-capable
 const KernelEntry* default_params_strided(int op, int dt, int M, int N);
-bool strided_capable(const KernelEntry& k);
+const KernelEntry* default_params_gather(int op, int dt, int M, int N);
+bool strided_capable(const KernelEntry& k);  // TMA or gather-capable
+bool gather_capable(const KernelEntry& k);   // TSMTTSM 1 / TSMM 4: any row stride, 8-byte D bases
 const char* build_info_json();
 
 // NVRTC run-time instantiation (tsm_jit.cpp).

@@ -105,6 +105,31 @@ __device__ __forceinline__ void bulk_red_add(void* dst, const void* src, u32 byt
                "r"(smem_u32(src)), "r"(bytes)
                : "memory");
 }
+// Strided row views without TMA (NEXT N4, "gather" mode): one element per lane
+// per instruction, asynchronous (Ampere-style cp.async, 8 bytes D / 16 bytes Z);
+// completion is tracked by the stage's mbarrier through
+// cp.async.mbarrier.arrive.noinc (one arrival per producer lane).
+template <int BYTES>
+__device__ __forceinline__ void cp_async_el(void* dst, const void* src) {
+  if constexpr (BYTES == 16)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_mbar_arrive_noinc(u64* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+// rows x W elements (S doubles each) of a row-strided global matrix (row stride
+// ld elements, first row r0) -> shared rows of stride sp elements; lanes of one
+// warp split the elements.
+template <int W, int S>
+__device__ __forceinline__ void gather_rows(double* dst, int sp, const double* src, long long r0, long long ld,
+                                            int rows, int lane) {
+  for (int i = lane; i < rows * W; i += 32) {
+    const int r = i / W, c = i - r * W;
+    cp_async_el<8 * S>(dst + (r * sp + c) * S, src + ((r0 + r) * ld + c) * S);
+  }
+}
 __device__ __forceinline__ void bulk_commit() {
   asm volatile("cp.async.bulk.commit_group;" ::: "memory");
 }
@@ -299,6 +324,8 @@ struct TsmttsmArgs {
   int order;           // consumer-warp order (spread_warp)
   u64 conj;            // Z: sign mask XORed into Im(A) -- 1<<63 gives C = A^H B (NEXT N2)
   PeerArgs peer;       // NEXT N3: fused cross-GPU reduction (peer.nranks == 0: off)
+  long long lda, ldb;  // row strides (elements) of A and B (= M, N when dense)
+  int gather;          // DMMA bulk kernel: strided rows copied element-wise (NEXT N4)
 };
 
 // M, N: widths.  Z: complex.  MT, NTL: tiles per row along m / n (powers of
@@ -806,7 +833,7 @@ __global__ void __launch_bounds__(Cfg::NT) tsmttsm_mma_kernel(const __grid_const
 
   if (tid == 0) {
     for (int s = 0; s < stages; s++) {
-      mbar_init(&full[s], 1);
+      mbar_init(&full[s], p.gather ? 32 : 1);  // gather: one noinc arrival per producer lane
       mbar_init(&empty[s], NW + Cfg::NE);  // consumer + edge warps release a stage
     }
     fence_mbar_init();
@@ -1112,6 +1139,11 @@ __global__ void __launch_bounds__(Cfg::NT) tsmttsm_mma_kernel(const __grid_const
           for (int b = 0; b < Cfg::NBB; b++)
             tma_load_2d(dB + b * R * 16, &p.tmB, b * 16, static_cast<int>(r0), &full[s], pol);
         }
+      } else if (p.gather) {  // strided rows (N4): element copies, any row stride
+        const int rows = static_cast<int>((K_even - r0 < R) ? (K_even - r0) : R);
+        gather_rows<M, S>(dA, AP, p.A, r0, p.lda, rows, lane);
+        gather_rows<N, S>(dB, BP, p.B, r0, p.ldb, rows, lane);
+        cp_async_mbar_arrive_noinc(&full[s]);
       } else {
         const int rows = static_cast<int>((K_even - r0 < R) ? (K_even - r0) : R);
         if (lane == 0) mbar_arrive_expect_tx(&full[s], static_cast<u32>(rows * (M + N) * S * 8));
@@ -1147,7 +1179,7 @@ __global__ void __launch_bounds__(Cfg::NT) tsmttsm_mma_kernel(const __grid_const
     }
     if constexpr (!Cfg::TMA) {
       if ((K & 1) && blockIdx.x == 0 && ew == 0)
-        edge_rows(p.A + (K - 1) * M * S, p.B + (K - 1) * N * S, 0, 1, M, N);
+        edge_rows(p.A + (K - 1) * p.lda * S, p.B + (K - 1) * p.ldb * S, 0, 1, M, N);
     }
   } else {
     // ---------------- consumer warps ----------------
@@ -1179,8 +1211,8 @@ __global__ void __launch_bounds__(Cfg::NT) tsmttsm_mma_kernel(const __grid_const
       // odd last row: a k-step whose rows 1..3 are zero, from global memory
       if constexpr (!Cfg::TMA) {
         if ((K & 1) && blockIdx.x == 0 && slot == 0) {
-          kstep(cm, cn, p.A + (K - 1) * M * S, p.B + (K - 1) * N * S, 0, 1, M, N);
-          if constexpr (Cfg::EI) edge_inline(p.A + (K - 1) * M * S, p.B + (K - 1) * N * S, 0, 1, M, N);
+          kstep(cm, cn, p.A + (K - 1) * p.lda * S, p.B + (K - 1) * p.ldb * S, 0, 1, M, N);
+          if constexpr (Cfg::EI) edge_inline(p.A + (K - 1) * p.lda * S, p.B + (K - 1) * p.ldb * S, 0, 1, M, N);
         }
       }
     };
@@ -1322,6 +1354,8 @@ struct TsmmArgs {
   double alpha_re, alpha_im;  // C' = alpha * C (alpha = 1: C used as given, bit-exact)
   int order;          // consumer-warp order (spread_warp)
   u64 conj;           // Z: sign mask XORed into Im(C) -- 1<<63 uses conj(C) (NEXT N2)
+  long long lda, ldb; // row strides (elements) of A and B (= M, N when dense)
+  int gather;         // kernel 4: strided rows of A copied element-wise, B stored element-wise (N4)
 };
 
 // TSMM: the C the kernels multiply by, C' = alpha * (conj ? conj(c) : c).
@@ -2255,7 +2289,7 @@ __global__ void __launch_bounds__(Cfg::NT) tsmm_cstb_kernel(const __grid_constan
 
   if (tid == 0) {
     for (int s = 0; s < stages; s++) {
-      mbar_init(&full[s], 1);
+      mbar_init(&full[s], p.gather ? 32 : 1);  // gather: one noinc arrival per producer lane
       mbar_init(&empty[s], NW);
     }
     fence_mbar_init();
@@ -2278,7 +2312,17 @@ __global__ void __launch_bounds__(Cfg::NT) tsmm_cstb_kernel(const __grid_constan
 
   if (warp == NW) {
     // ---------------- producer warp: one bulk copy per chunk of A ----------------
-    if (lane == 0) {
+    if (p.gather) {  // strided rows of A (N4): element copies by the 32 lanes, any row stride
+      Ring ring_it;
+      for (long long c = blockIdx.x; c < p.nchunks; c += G, ring_it.next(stages)) {
+        const int s = ring_it.s;
+        if (ring_it.round > 0) mbar_wait(&empty[s], ring_it.ph ^ 1u);
+        const long long r0 = c * R;
+        const int rows = static_cast<int>((K_even - r0 < R) ? (K_even - r0) : R);
+        gather_rows<M, S>(ring + static_cast<long long>(s) * Cfg::STAGE_DOUBLES, M, p.A, r0, p.lda, rows, lane);
+        cp_async_mbar_arrive_noinc(&full[s]);
+      }
+    } else if (lane == 0) {
       const u64 pol = policy_evict_first();
       Ring ring_it;
       for (long long c = blockIdx.x; c < p.nchunks; c += G, ring_it.next(stages)) {
@@ -2422,7 +2466,19 @@ __global__ void __launch_bounds__(Cfg::NT) tsmm_cstb_kernel(const __grid_constan
           // divergent arrival)
           __syncwarp();
           asm volatile("bar.sync %0, %1;" ::"r"(1 + rg), "r"(NG * 32) : "memory");
-          if (issuer) {
+          if (p.gather) {
+            // strided B (N4): the NG warps of the row group store the staged rows
+            // element-wise (each element by one thread; update mode: B += value).
+            // A buffer is rewritten two passes later, after the next pass's
+            // barrier, which every thread reaches only after this loop.
+            const int nr = (rows - wr0 < RW) ? rows - wr0 : RW;
+            for (int i = cg * 32 + lane; i < nr * N; i += NG * 32) {
+              const int r = i / N, n = i - r * N;
+              double* o = p.B + ((r0 + wr0 + r) * p.ldb + n) * S;
+#pragma unroll
+              for (int z = 0; z < S; z++) o[z] = p.reduce ? o[z] + stg[i * S + z] : stg[i * S + z];
+            }
+          } else if (issuer) {
             const int nr = (rows - wr0 < RW) ? rows - wr0 : RW;
             b_out_bulk(p, p.B + (r0 + wr0) * N * S, stg, static_cast<u32>(nr * N * S * 8));
             bulk_commit();
@@ -2441,7 +2497,7 @@ __global__ void __launch_bounds__(Cfg::NT) tsmm_cstb_kernel(const __grid_constan
     if (issuer) bulk_wait_all();
     // Odd last row (K odd): warp 0 of block 0 from global A and C' (plain fma).
     if ((K & 1) && blockIdx.x == 0 && warp == 0) {
-      const double* a = p.A + (K - 1) * M * S;
+      const double* a = p.A + (K - 1) * p.lda * S;
       for (int n = lane; n < N; n += 32) {
         double re = 0.0, im = 0.0;
         for (int m = 0; m < M; m++) {
@@ -2454,7 +2510,7 @@ __global__ void __launch_bounds__(Cfg::NT) tsmm_cstb_kernel(const __grid_constan
             re = fma(a[m], cr, re);
           }
         }
-        double* o = p.B + ((K - 1) * N + n) * S;
+        double* o = p.B + ((K - 1) * p.ldb + n) * S;
         o[0] = p.reduce ? o[0] + re : re;
         if constexpr (Cfg::Z) o[1] = p.reduce ? o[1] + im : im;
       }

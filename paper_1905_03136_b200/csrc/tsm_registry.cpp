@@ -9,6 +9,7 @@ extern const int g_gen_ntables;
 extern const char* g_gen_info;
 extern const KernelEntry g_param_table[];
 extern const KernelEntry g_param_table_strided[];
+extern const KernelEntry g_param_table_gather[];
 
 const KernelEntry* find_aot(int op, int dt, int M, int N) {
   for (int t = 0; t < g_gen_ntables; t++)
@@ -36,6 +37,12 @@ const KernelEntry* default_params(int op, int dt, int M, int N) {
 const KernelEntry* default_params_strided(int op, int dt, int M, int N) {
   if (op < 0 || op > 1 || dt < 0 || dt > 1 || M < 1 || M > 64 || N < 1 || N > 64) return nullptr;
   const KernelEntry* e = &g_param_table_strided[((op * 2 + dt) * 64 + (M - 1)) * 64 + (N - 1)];
+  return e->impl < 0 ? nullptr : e;
+}
+
+const KernelEntry* default_params_gather(int op, int dt, int M, int N) {
+  if (op < 0 || op > 1 || dt < 0 || dt > 1 || M < 1 || M > 64 || N < 1 || N > 64) return nullptr;
+  const KernelEntry* e = &g_param_table_gather[((op * 2 + dt) * 64 + (M - 1)) * 64 + (N - 1)];
   return e->impl < 0 ? nullptr : e;
 }
 

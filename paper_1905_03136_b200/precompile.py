@@ -35,6 +35,7 @@ def main() -> int:
             for (M, N) in gi.SHAPES:
                 jobs.append((op, dt, M, N, 0))
                 jobs.append((op, dt, M, N, 2))  # TSM_FLAG_STRIDED default (skipped if none)
+                jobs.append((op, dt, M, N, 8))  # TSM_FLAG_GATHER default
     t0 = time.time()
 
     def one(j):

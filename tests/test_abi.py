@@ -149,7 +149,9 @@ f = tsm.lib.tsm_jit_precompile
 assert f(0, 0, 24, 24, None, 0) == 0, tsm.lib.tsm_last_error_detail()
 assert f(1, 1, 17, 17, None, 0) == 0
 assert f(0, 0, 65, 1, None, 0) == 1          # M out of range
-assert f(0, 0, 33, 33, None, 2) == 2         # no TMA kernel for odd D widths
+assert f(0, 0, 33, 33, None, 2) == 0         # odd D widths: the strided default is the gather kernel
+assert f(1, 0, 7, 1, None, 8) == 0           # TSM_FLAG_GATHER default exists for every shape
+assert f(0, 1, 64, 64, None, 8) == 0
 cfg = tsm.TsmConfig(threads=288, rows_per_chunk=30, p0=1, p1=1, p2=0, stages=3, ctas_per_sm=1, kernel=0, p3=0)
 assert f(0, 0, 8, 8, ctypes.byref(cfg), 0) == 0
 bad = tsm.TsmConfig(threads=100, rows_per_chunk=30, p0=1, p1=1, p2=0, stages=3, ctas_per_sm=1, kernel=0, p3=0)

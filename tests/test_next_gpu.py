@@ -158,50 +158,67 @@ def test_cgs_step_fp(tsm, cplx):
     assert oracle.max_err_ratio(Bd.cpu().numpy(), Bref, bb)[0] <= 1e-13
 
 
+STRIDED_SHAPES = [(16, 16), (32, 48), (64, 20), (8, 8), (1, 1), (3, 5), (7, 1), (1, 64), (33, 33), (57, 57),
+                  (63, 64), (12, 9), (2, 2), (64, 1)]
+
+
 @pytest.mark.parametrize("cplx", [False, True], ids=["D", "Z"])
-@pytest.mark.parametrize("M,N", [(16, 16), (32, 48), (64, 20), (8, 8)])
-def test_strided_views(tsm, M, N, cplx):
+@pytest.mark.parametrize("offs", [(6, 80, 40), (3, 71, 17)], ids=["even", "odd"])
+@pytest.mark.parametrize("M,N", STRIDED_SHAPES)
+def test_strided_views(tsm, M, N, cplx, offs):
     """N4: column subsets of a wider block vector (row stride ld > width) through
-    tsmttsm_ld / tsmm_ld with a TSM_FLAG_STRIDED plan (TMA kernels)."""
-    if not cplx and min(M, N) < 16:
-        pytest.skip("D strided views need rows of >= 16 doubles")
-    K, W = 70001, 150
-    big = ti.matrix(K, W, "A", complex_=cplx, seed=5)
-    G = cu(big)
-    a0, b0 = 6, 80  # even offsets keep 16-byte alignment for D
-    A, B = G[:, a0:a0 + M], G[:, b0:b0 + N]
-    assert A.stride(0) == W and not A.is_contiguous()
-    C = tsm.tsmttsm(A, B)
-    torch.cuda.synchronize()
-    ref, bound = oracle.tsmttsm(big[:, a0:a0 + M], big[:, b0:b0 + N])
-    assert oracle.max_err_ratio(C.cpu().numpy(), ref, bound)[0] <= 1e-12
-    Cm = ti.matrix(M, N, "C", complex_=cplx, seed=6)
-    out = torch.zeros((K, W), dtype=G.dtype, device="cuda")
-    Bv = out[:, 40:40 + N]
-    tsm.tsmm(A, cu(Cm), out=Bv)
-    torch.cuda.synchronize()
-    refm, bm = oracle.tsmm(big[:, a0:a0 + M], Cm)
-    got = out.cpu().numpy()
-    assert oracle.max_err_ratio(got[:, 40:40 + N], refm, bm)[0] <= 1e-13
-    assert np.count_nonzero(got[:, :40]) == 0 and np.count_nonzero(got[:, 40 + N:]) == 0  # untouched
+    tsmttsm_ld / tsmm_ld for every width class: TMA kernels (16-byte row
+    strides and bases), else the gather-capable kernels (any width; odd column
+    offsets give 8-byte aligned D bases).  Ragged K (odd: the last-row path);
+    the columns around the TSMM output view stay untouched."""
+    for K in (1, 4099, 70001):
+        W = 151  # odd row stride: no 16-byte rows for D
+        big = ti.matrix(K, W, "A", complex_=cplx, seed=5 + K)
+        G = cu(big)
+        a0, b0, o0 = offs
+        A, B = G[:, a0:a0 + M], G[:, b0:b0 + N]
+        C = tsm.tsmttsm(A, B)
+        torch.cuda.synchronize()
+        ref, bound = oracle.tsmttsm(big[:, a0:a0 + M], big[:, b0:b0 + N])
+        r = oracle.max_err_ratio(C.cpu().numpy(), ref, bound)[0]
+        assert r <= 1e-12, (M, N, K, offs, r)
+        Cm = ti.matrix(M, N, "C", complex_=cplx, seed=6)
+        out = torch.zeros((K, W), dtype=G.dtype, device="cuda")
+        Bv = out[:, o0:o0 + N]
+        tsm.tsmm(A, cu(Cm), out=Bv)
+        torch.cuda.synchronize()
+        refm, bm = oracle.tsmm(big[:, a0:a0 + M], Cm)
+        got = out.cpu().numpy()
+        r2 = oracle.max_err_ratio(np.ascontiguousarray(got[:, o0:o0 + N]), refm, bm)[0]
+        assert r2 <= 1e-13, (M, N, K, offs, r2)
+        assert np.count_nonzero(got[:, :o0]) == 0 and np.count_nonzero(got[:, o0 + N:]) == 0  # untouched
 
 
 def test_strided_rules(tsm):
-    # a dense-tuned plan that is not a TMA kernel refuses strided calls
-    p = tsm.Plan("tsmttsm", "d", 33, 33, 0)
-    if p.config()["kernel"] & 15 != 2:
-        A = torch.zeros((100, 40), dtype=torch.float64, device="cuda")
+    # a dense-tuned plan that is neither a TMA nor a gather-capable kernel refuses strided calls
+    p = tsm.Plan("tsmttsm", "d", 8, 8, 0)
+    A = torch.zeros((100, 40), dtype=torch.float64, device="cuda")
+    if p.config()["kernel"] & 15 == 0:
         with pytest.raises(tsm.TsmError) as e:
-            tsm.tsmttsm(A[:, :33], A[:, 2:35], plan=p)
+            tsm.tsmttsm(A[:, :8], A[:, 10:18], plan=p)
         assert e.value.status == 2
-    # odd D widths have no TMA kernel
-    with pytest.raises(tsm.TsmError) as e:
-        tsm.Plan("tsmttsm", "d", 33, 33, 0, strided=True)
-    assert e.value.status == 2
+    # every shape has a strided plan: odd D widths get the gather kernel
+    ps = tsm.Plan("tsmttsm", "d", 33, 33, 0, strided=True)
+    assert ps.config()["kernel"] & 15 == 1
+    pg = tsm.Plan("tsmm", "d", 32, 32, 0, gather=True)
+    assert pg.config()["kernel"] & 15 == 4
+    # a TMA strided plan refuses row strides that are not 16-byte multiples
+    pt = tsm.Plan("tsmm", "d", 32, 32, 0, strided=True)
+    if pt.config()["kernel"] & 15 in (2, 3):
+        X = torch.zeros((100, 41), dtype=torch.float64, device="cuda")
+        with pytest.raises(tsm.TsmError) as e:
+            tsm.tsmm(X[:, :32], torch.zeros(32, 32, dtype=torch.float64, device="cuda"),
+                     out=torch.zeros((100, 41), dtype=torch.float64, device="cuda")[:, :32], plan=pt)
+        assert e.value.status == 2
     # strided plans still serve dense calls
-    ps = tsm.Plan("tsmm", "d", 32, 32, 0, strided=True)
-    A = ti.matrix(5000, 32, "A")
-    Cm = ti.matrix(32, 32, "C")
-    got = tsm.tsmm(cu(A), cu(Cm), plan=ps).cpu().numpy()
-    ref, b = oracle.tsmm(A, Cm)
-    assert oracle.max_err_ratio(got, ref, b)[0] <= 1e-13
+    for plan in (pt, pg):
+        A = ti.matrix(5000, 32, "A")
+        Cm = ti.matrix(32, 32, "C")
+        got = tsm.tsmm(cu(A), cu(Cm), plan=plan).cpu().numpy()
+        ref, b = oracle.tsmm(A, Cm)
+        assert oracle.max_err_ratio(got, ref, b)[0] <= 1e-13

@@ -514,6 +514,20 @@ def main(per_file: int = 12) -> int:
                                  f"nullptr, {c['NT']}, {c['R']}, {p[0]}, {p[1]}, {p[2]}, {p[3]}, "
                                  f"{c['stages']}, {c['ctas']}, {c.get('impl', 0)}, "
                                  f"{flags(c)}}},")
+    lines += ["};", ""]
+    # gather-capable defaults (TSM_FLAG_GATHER, NEXT N4): TSMTTSM kernel 1 /
+    # TSMM kernel 4, any row stride
+    lines += ["extern const KernelEntry g_param_table_gather[] = {"]
+    for op in ("tsmttsm", "tsmm"):
+        for dt in ("d", "z"):
+            for M in range(1, 65):
+                for N in range(1, 65):
+                    c = gather_default(op, M, N, dt == "z", tune.get(f"{op}_{dt}_{M}_{N}", {}).get("cfg"))
+                    p = params4(op, M, N, c)
+                    lines.append(f"  {{{0 if op == 'tsmttsm' else 1}, {1 if dt == 'z' else 0}, {M}, {N}, "
+                                 f"nullptr, {c['NT']}, {c['R']}, {p[0]}, {p[1]}, {p[2]}, {p[3]}, "
+                                 f"{c['stages']}, {c['ctas']}, {c.get('impl', 0)}, "
+                                 f"{flags(c)}}},")
     lines += ["};", "}  // namespace tsm", ""]
     _write(os.path.join(GEN, "params_gen.cpp"), "\n".join(lines))
 
@@ -670,14 +684,47 @@ def strided_capable(op: str, c: dict) -> bool:
     return c.get("impl", 0) == 2 if op == "tsmttsm" else c.get("impl", 0) in (2, 3)
 
 
+def gather_capable(op: str, c: dict) -> bool:
+    """Kernels with the element-wise (cp.async) gather producer: any row stride."""
+    return c.get("impl", 0) == 1 if op == "tsmttsm" else c.get("impl", 0) == 4
+
+
+def gather_default(op: str, M: int, N: int, z: bool, tuned: dict | None) -> dict:
+    """Default configuration of a TSM_FLAG_GATHER plan (every shape has one):
+    the tuned configuration when it is gather-capable, else TSMTTSM kernel 1
+    with the DMMA default tiles / TSMM kernel 4 (C-stationary, bulk)."""
+    c = resolve(op, M, N, z, tuned)
+    if gather_capable(op, c):
+        return c
+    if op == "tsmttsm":
+        d = dict(tsmttsm_mma_default(M, N, z))
+        if d["impl"] != 1:  # the TMA branch: same tiles, dense-stride stages
+            S = 2 if z else 1
+            WT = cdiv(cdiv(M, 8), d["MT"]) * cdiv(cdiv(N, 8), d["NTL"])
+            RS = (d["NT"] // 32 - 1) // WT
+            step = 4 * RS
+            R = max(step, (24576 // ((M + N) * 8 * S)) // step * step)
+            d.update(impl=1, R=R, AP=pick_stride(M, z, "t"), BP=pick_stride(N, z, "t"))
+        return d
+    cands = tsmm_cstb_configs(M, N, z)
+    if cands:
+        pick = [x for x in cands if x["WR"] == 2] or cands
+        return dict(pick[0], stages=3, ctas=1)
+    # N = 1: one 8-column block (7 padded columns), two row groups of one warp
+    S = 2 if z else 1
+    R = 32 * max(1, round(16384 / (32 * M * S * 8)))
+    return dict(NBW=1, WR=2, NT=3 * 32, R=R, impl=4, stages=3, ctas=1)
+
+
 def strided_default(op: str, M: int, N: int, z: bool, tuned: dict | None):
     """Default configuration of a TSM_FLAG_STRIDED plan: the tuned one when it
-    is a TMA kernel, else a TMA heuristic; None when no TMA kernel applies."""
+    is a TMA kernel, else a TMA heuristic; the gather-capable default for
+    shapes without a TMA kernel."""
     c = resolve(op, M, N, z, tuned)
     if strided_capable(op, c):
         return c
     if not tma_ok(M, N, z):
-        return None
+        return gather_default(op, M, N, z, tuned)
     if op == "tsmttsm":
         d = tsmttsm_mma_default(M, N, z)
         return d if strided_capable(op, d) else None
