@@ -78,7 +78,7 @@ def test_conj_flag_rules(tsm):
         tsm.Plan("tsmttsm", "d", 8, 8, 0, conj=True)
     assert e.value.status == 1
     h = tsm.ctypes.c_void_p()
-    assert tsm.lib.tsm_plan_create_ex(tsm.ctypes.byref(h), 0, 1, 8, 8, 0, None, 4) == 1  # unknown flag
+    assert tsm.lib.tsm_plan_create_ex(tsm.ctypes.byref(h), 0, 1, 8, 8, 0, None, 64) == 1  # unknown flag
     # conj plan differs from the plain plan exactly by the sign of Im(A)
     A = ti.matrix(1000, 9, "A", complex_=True, mode="int")
     B = ti.matrix(1000, 4, "B", complex_=True, mode="int")

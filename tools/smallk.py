@@ -29,6 +29,9 @@ def main():
     ap.add_argument("--dtype", default="d")
     ap.add_argument("--reps", type=int, default=21)
     ap.add_argument("--json", default="")
+    ap.add_argument("--flush", default="write", choices=["write", "read", "none"],
+                    help="L2 flush before every rep: write 512 MB (leaves dirty lines that the timed "
+                         "call must write back), read 512 MB (clean), or none")
     a = ap.parse_args()
     widths = [int(w) for w in a.widths.split(",")]
     Ks = [int(float(k)) for k in a.Ks.split(",")]
@@ -49,7 +52,10 @@ def main():
             fn()
         ts = []
         for _ in range(a.reps):
-            tsm.tsm_l2_flush(flush.data_ptr(), flush.numel(), s_ptr)
+            if a.flush == "write":
+                tsm.tsm_l2_flush(flush.data_ptr(), flush.numel(), s_ptr)
+            elif a.flush == "read":
+                tsm.probe("read", flush.data_ptr(), flush.numel(), 1, s_ptr)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
             fn()
@@ -91,7 +97,7 @@ def main():
                   f"overhead {100*row['reduction_overhead']:6.1f}%  roof {row['pct_roof']:5.1f}%  "
                   f"grid {row['plan']['grid']} nfin {row['plan']['nfin']}", flush=True)
     if a.json:
-        json.dump({"read_gbs": bw / 1e9, "rows": rows}, open(a.json, "w"), indent=1)
+        json.dump({"read_gbs": bw / 1e9, "flush": a.flush, "rows": rows}, open(a.json, "w"), indent=1)
 
 
 if __name__ == "__main__":
