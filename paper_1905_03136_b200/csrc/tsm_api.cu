@@ -145,7 +145,7 @@ size_t smem_bytes(const KernelEntry& kin, int stages) {
   }
   if (k.impl >= 1) {  // DMMA TSMM: p0 = WR, p1 = AP, p2 = NOP (must match TsmmMmaCfg)
     const long long MK = (k.M + 3) / 4, NB = (k.N + 7) / 8;
-    const long long NCP = S == 2 ? 8 * NB + 4 : ((8 * NB) % 16 == 8 ? 8 * NB : 8 * NB + 8);
+    const long long NCP = 8 * NB + 4;  // = TsmmMmaCfg::NCP
     const long long NW = k.NT / 32 - 1;
     const long long cd = ((MK * 4 * NCP * S + 15) / 16) * 16;
     if (k.impl == 2) {  // TMA: swizzled boxes, staging and ring 1024-byte aligned

@@ -258,6 +258,20 @@ struct WsLayout {
   static constexpr int kCounterBytes = 256;  // u32 ticket, u32 done, padding
 };
 
+// 16-row windows (D, odd dense A stride M, WR even): MMA block i of a warp's
+// pass and lane row g -> pass row.  Blocks 2t, 2t+1 share rows [16t, 16t+16);
+// half-warp h = g >> 2 of block b takes the 4 rows w = 4p + x(b, h), p = g & 3,
+// with x(0,0) = 0, x(0,1) = M mod 4, x(1,0) = 2, x(1,1) = 4 - M mod 4.  The
+// rows of one half-warp are then a coset M w = c (mod 4), so its 16 LDS.64 of
+// the A fragment (columns q = 0..3) hit 16 distinct 8-byte units -- an 8-row
+// block cannot do better than 2-way for an odd stride (ncu r4: TSMM D 57 / 63
+// A loads at 2x the ideal wavefronts).
+__device__ __forceinline__ constexpr int win16_row(int M, int i, int g) {
+  const int b = i & 1, h = g >> 2;
+  const int x = b == 0 ? (h == 0 ? 0 : (M & 3)) : (h == 0 ? 2 : 4 - (M & 3));
+  return 16 * (i >> 1) + 4 * (g & 3) + x;
+}
+
 // --------------------------------------------------------------------------
 // TMA tensor copies (cp.async.bulk.tensor.2d, SASS UTMALDG / UTMASTG).
 // A row-major K x W (doubles) operand is described by a 2-D tensor map
@@ -1652,8 +1666,10 @@ struct TsmmMmaCfg {
   static constexpr int NBA = (M * S + 15) / 16, NBO = (N * S + 15) / 16;  // TMA boxes per row
   static constexpr int AP = TMA ? NBA * 16 / S : AP_;
   static constexpr int NOP = TMA ? NBO * 16 / S : NOP_;
-  // C row stride (elements): D = 8 mod 16 words, Z = 4 mod 8 16-byte units
-  static constexpr int NCP = Z ? (8 * NB + 4) : ((8 * NB) % 16 == 8 ? 8 * NB : 8 * NB + 8);
+  // C row stride (elements), = 4 mod 8 units: the MMA-B fragment (rows q,
+  // columns g) of each 16-lane half-warp (D LDS.64) / 8-lane quarter (Z
+  // LDS.128) then hits distinct banks (ncu r4: 8 mod 16 left the D loads 2-way)
+  static constexpr int NCP = 8 * NB + 4;
   static constexpr int RW = 8 * WR;        // rows per warp per pass
   static constexpr int RPP = RW * NW;      // rows per pass
   static constexpr int NT = (NW + 1) * 32;
@@ -1691,8 +1707,16 @@ __global__ void __launch_bounds__(Cfg::NT) tsmm_mma_kernel(const __grid_constant
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, q = lane & 3;
-  // swizzled (TMA) boxes: MMA row g <-> A/B row rho(g), conflict-free (see tsmm_cst_kernel)
+  // swizzled (TMA) boxes: MMA row g <-> A/B row rho(g), conflict-free (see tsmm_cst_kernel);
+  // dense odd D strides with WR even: 16-row windows (win16_row)
   const int rho = Cfg::TMA ? ((((g & 1) << 2) | (g & 2) | (g >> 2)) ^ (g & 1)) : g;
+  constexpr bool WIN16 = !Cfg::TMA && !Cfg::Z && Cfg::WR % 2 == 0 && Cfg::AP % 2 == 1;
+  auto prow = [&](int i) -> int {  // pass row of MMA row g of block i
+    if constexpr (WIN16)
+      return win16_row(Cfg::AP, i, g);
+    else
+      return 8 * i + rho;
+  };
   const long long K = p.K;
   const long long K_even = K & ~1LL;
   const long long Kc = Cfg::TMA ? K : K_even;
@@ -1800,7 +1824,7 @@ __global__ void __launch_bounds__(Cfg::NT) tsmm_mma_kernel(const __grid_constant
           double a[WR][S];
 #pragma unroll
           for (int i = 0; i < WR; i++) {
-            const int r = wr0 + 8 * i + rho;
+            const int r = wr0 + prow(i);
 #pragma unroll
             for (int z = 0; z < S; z++) a[i][z] = mv ? sA[aoff(r, m) + z] : 0.0;
           }
@@ -1839,7 +1863,7 @@ __global__ void __launch_bounds__(Cfg::NT) tsmm_mma_kernel(const __grid_constant
 #pragma unroll
           for (int j = 0; j < NB; j++) {
             const int n = 8 * j + 2 * q;
-            const int rr = 8 * i + rho;
+            const int rr = prow(i);
             if constexpr (!Cfg::Z && (Cfg::TMA || NOP % 2 == 0)) {
               // 16-byte store (conflict-free: NOP = 2 mod 4, or swizzled boxes)
               double* dst = stg + ooff(rr, n);
@@ -2384,6 +2408,14 @@ __global__ void __launch_bounds__(Cfg::NT) tsmm_cstb_kernel(const __grid_constan
     const int nb0 = cg * NBW;
     const bool issuer = (cg == 0 && lane == 0);
     const int rho = cstb_rho(Cfg::RHO, g);  // MMA row g <-> stage row rho(g) (bank conflicts)
+    // D, odd M, WR even: 16-row windows instead (conflict-free A fragment loads)
+    constexpr bool WIN16 = !Cfg::Z && WR % 2 == 0 && M % 2 == 1;
+    auto prow = [&](int i) -> int {
+      if constexpr (WIN16)
+        return win16_row(M, i, g);
+      else
+        return 8 * i + rho;
+    };
     // this warp's C' slice as MMA-B fragments: lane holds C'[4ks+q][8(nb0+j)+g]
     double cf[MK][NBW][S];
 #pragma unroll
@@ -2443,7 +2475,7 @@ __global__ void __launch_bounds__(Cfg::NT) tsmm_cstb_kernel(const __grid_constan
             const bool mv = (4 * ks + 4 <= M) || (m < M);
 #pragma unroll
             for (int i = 0; i < WR; i++) {
-              const int r = wr0 + 8 * i + rho;  // rows past `rows`: stale, never stored
+              const int r = wr0 + prow(i);  // rows past `rows`: stale, never stored
               if constexpr (!Cfg::Z) {
                 const double a = mv ? sA[r * M + m] : 0.0;
 #pragma unroll
@@ -2481,7 +2513,7 @@ __global__ void __launch_bounds__(Cfg::NT) tsmm_cstb_kernel(const __grid_constan
             for (int j = 0; j < NBV; j++)
 #pragma unroll
               for (int e = 0; e < 2; e++) {
-                const int rr = 8 * i + rho, n = 8 * (nb0 + j) + 2 * q + e;
+                const int rr = prow(i), n = 8 * (nb0 + j) + 2 * q + e;
                 if (n < N) {
 #pragma unroll
                   for (int z = 0; z < S; z++) stg[(rr * N + n) * S + z] = acc[i][j][z][e];
@@ -2503,7 +2535,7 @@ __global__ void __launch_bounds__(Cfg::NT) tsmm_cstb_kernel(const __grid_constan
                   v[z] += __shfl_xor_sync(0xffffffffu, v[z], 2);
                 }
                 if (q == 0) {
-                  const int rr = 8 * i + rho, n = N - EC + e;
+                  const int rr = prow(i), n = N - EC + e;
 #pragma unroll
                   for (int z = 0; z < S; z++) stg[(rr * N + n) * S + z] = v[z];
                 }
@@ -2511,11 +2543,14 @@ __global__ void __launch_bounds__(Cfg::NT) tsmm_cstb_kernel(const __grid_constan
           }
           fence_proxy_async_smem();
           if (issuer) bulk_wait_read<0>();  // the previous pass's store has read the other buffer
-          // reconverge after the issuer-only wait: bar.sync is .aligned (every lane of
-          // the warp at the same instruction; compute-sanitizer synccheck flagged the
-          // divergent arrival)
+          // Named barrier of the row group.  Its warps reach it from different
+          // instantiations of this lambda (the last column group's has other
+          // block / edge counts), i.e. from different instructions, which the
+          // .aligned form (bar.sync) forbids -- compute-sanitizer synccheck
+          // flagged it -- so the non-aligned barrier.sync, after reconverging
+          // the warp from the issuer-only wait.
           __syncwarp();
-          asm volatile("bar.sync %0, %1;" ::"r"(1 + rg), "r"(NG * 32) : "memory");
+          asm volatile("barrier.sync %0, %1;" ::"r"(1 + rg), "r"(NG * 32) : "memory");
           if (p.gather) {
             // strided B (N4): the NG warps of the row group store the staged rows
             // element-wise (each element by one thread; update mode: B += value).

@@ -79,18 +79,53 @@ def test_invalid_config_rejected_before_cuda(tsm):
 
 
 def test_conflict_model_pins():
-    # TSMTTSM fragment (4 rows x 8 consecutive doubles): stride 64 words -> 4-way
-    assert gi._degree(64, False, "t") == 2.0  # 4 wavefronts vs the 2-wavefront minimum
-    assert gi._degree(72, False, "t") == 1.0  # stride 8 mod 16: minimum
+    # the bank model: 8-byte accesses per 16-lane half-warp over 16 units, 16-byte
+    # ones per 8-lane quarter over 8 units (ncu r4, profiles/r02_ncu_run4.md: the
+    # TSMM D 57 C fragment at stride 72 took 2x the ideal wavefronts although its
+    # 32 lanes cover every unit exactly twice)
+    assert gi._degree(72, False, "t") == 2.0  # the measured case
+    assert gi._degree(68, False, "t") == 1.0  # stride 4 mod 16: conflict-free
+    assert gi._degree(64, False, "t") == 4.0  # 4 rows on the same 4 units per half-warp
     assert gi.pick_stride(64, False, "t") == 64  # dense by default (one bulk copy per chunk)
     assert gi._degree(gi.pick_stride(64, False, "t", pad=True), False, "t") == 1.0
-    # complex: 4 rows x 8 consecutive 16-byte elements always use every bank 4x
-    assert gi._degree(64, True, "t") == 1.0
-    # TSMM A fragment (8 rows x 4 consecutive): stride 0 mod 16 words -> 8 rows on 4 words
+    # complex (16-byte elements): stride 0 mod 8 units -> the 4 rows of a quarter on 2 units
+    assert gi._degree(64, True, "t") == 4.0
+    assert gi._degree(66, True, "t") == 1.0
+    # TSMM A fragment (8 rows x 4 consecutive): stride 0 mod 16 -> 4 rows per unit per half-warp
     assert gi._degree(64, False, "a") == 4.0
     assert gi._degree(gi.pick_stride(64, False, "a", pad=True), False, "a") == 1.0
     # odd widths stay dense (rows are not 16-byte multiples)
     assert gi.pick_stride(63, False, "a", pad=True) == 63 and gi.pick_stride(33, False, "t", pad=True) == 33
+
+
+def _win16_row(M, i, g):  # mirror of tsm_kernels.cuh win16_row
+    b, h = i & 1, g >> 2
+    x = (0 if h == 0 else (M & 3)) if b == 0 else (2 if h == 0 else 4 - (M & 3))
+    return 16 * (i >> 1) + 4 * (g & 3) + x
+
+
+def test_win16_rows_conflict_free_for_odd_strides():
+    """TSMM kernels 1 / 4 with a dense odd-width D stage and WR even: the
+    16-row window map is a bijection onto the pass rows, and every half-warp
+    of an A fragment load (rows of one MMA block, columns q = 0..3) hits 16
+    distinct 8-byte units -- the best 8-row permutation leaves 2-way
+    conflicts for every odd stride (ncu r4: TSMM D 57 / 63 loads at 2x)."""
+    for M in range(9, 65, 2):
+        for WR in (2, 4, 8):
+            rows = sorted(_win16_row(M, i, g) for i in range(WR) for g in range(8))
+            assert rows == list(range(8 * WR)), (M, WR)
+            for i in range(WR):
+                for ph in range(2):
+                    units = {(_win16_row(M, i, g) * M + q) % 16 for g in range(4 * ph, 4 * ph + 4)
+                             for q in range(4)}
+                    assert len(units) == 16, (M, WR, i, ph)
+        # any 8-row permutation: some half-warp stays 2-way conflicted
+        import itertools
+        best = min(max(len([1 for g in range(4 * ph, 4 * ph + 4) for q in range(4)]) -
+                       len({(perm[g] * M + q) % 16 for g in range(4 * ph, 4 * ph + 4) for q in range(4)})
+                       for ph in range(2))
+                   for perm in itertools.islice(itertools.permutations(range(8)), 0, 40320, 97))
+        assert best > 0, M
 
 
 def _lds128_worst(addr):

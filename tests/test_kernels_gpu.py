@@ -457,3 +457,42 @@ def test_tsmm_cstb_edge_columns(tsm, dt, M, N):
         torch.cuda.synchronize()
         assert np.array_equal(got.cpu().numpy(), oracle.tsmm(Ai, Ci)[0]), (key, c)
     assert ran
+
+
+@pytest.mark.parametrize("M,N", [(57, 57), (63, 63), (33, 20), (9, 41), (41, 9), (49, 49)])
+def test_tsmm_win16_row_windows(tsm, M, N):
+    """TSMM kernels 1 (dense) and 4 with an odd-width D stage and WR even use
+    16-row windows (win16_row) for the MMA rows: every such candidate (and the
+    edge-column variants) on ragged K, store and reduce-add (beta = 1),
+    within tolerance; integer-valued inputs bit-exact."""
+    cands = [c for c in gi.candidates("tsmm", M, N, False)
+             if c.get("impl") in (1, 4) and c.get("WR", 1) % 2 == 0 and c.get("AP", M) % 2 == 1]
+    picked = {}
+    for c in cands:
+        picked.setdefault((c["impl"], c["WR"], c.get("EDGE", 0), c.get("NBW", 0)), c)
+    assert picked, "no window candidate"
+    ran = 0
+    for key, c in sorted(picked.items())[:6]:
+        try:
+            plan = tsm.Plan("tsmm", "d", M, N, 0, config=gi.to_tsm_config("tsmm", c, 3, 1))
+        except tsm.TsmError as e:
+            if e.status != 2:
+                raise
+            continue
+        ran += 1
+        for K, beta in ((1, 0.0), (17, 1.0), (4099, 0.0), (65537, 1.0), (65536, 0.0)):
+            A = ti.matrix(K, M, "A", seed=K + 51)
+            Cm = ti.matrix(M, N, "C", seed=K + 52)
+            B0 = ti.matrix(K, N, "B", seed=K + 53)
+            Bg = torch.from_numpy(B0).cuda()
+            tsm.tsmm_update(torch.from_numpy(A).cuda(), torch.from_numpy(Cm).cuda(), Bg, 1.0, beta, plan=plan)
+            torch.cuda.synchronize()
+            ref, bound = oracle.tsmm_update(A, Cm, B0, 1.0, beta)
+            r, wi, _ = oracle.max_err_ratio(Bg.cpu().numpy(), ref, bound)
+            assert r <= 1e-13, (M, N, key, c, K, beta, r, wi)
+        Ai = ti.matrix(20001, M, "A", mode="int")
+        Ci = ti.matrix(M, N, "C", mode="int")
+        got = tsm.tsmm(torch.from_numpy(Ai).cuda(), torch.from_numpy(Ci).cuda(), plan=plan)
+        torch.cuda.synchronize()
+        assert np.array_equal(got.cpu().numpy(), oracle.tsmm(Ai, Ci)[0]), (key, c)
+    assert ran

@@ -781,25 +781,34 @@ def to_tsm_config(op: str, c: dict, stages: int, ctas: int) -> dict:
 # fragment loads / accumulator stores use the minimum number of wavefronts.
 # ---------------------------------------------------------------------------
 def _degree(stride: int, z: bool, kind: str) -> float:
-    """Smem wavefronts per warp access / minimum, lanes (g = l/4, q = l%4)."""
-    counts = {}
-    for lane in range(32):
-        g, q = lane >> 2, lane & 3
-        if kind == "a":          # TSMM A fragment: element (row g, col q)
-            idx = g * stride + q
-        elif kind == "t":        # TSMTTSM A/B fragment: element (row q, col g)
-            idx = q * stride + g
-        elif z:                  # Z output: element (g, 2q) (e = 0 store)
-            idx = g * stride + 2 * q
-        elif stride % 2 == 0:    # D output, 16-byte store of (2q, 2q+1)
-            idx = (g * stride + 2 * q) // 2
-        else:                    # D output, 8-byte store
-            idx = g * stride + 2 * q
-        wide = z or (kind == "o" and stride % 2 == 0)
-        unit = idx % (8 if wide else 16)
-        counts[unit] = counts.get(unit, 0) + 1
-    minimum = 4 if (z or (kind == "o" and stride % 2 == 0)) else 2
-    return max(counts.values()) / minimum
+    """Smem wavefronts per warp access / minimum, lanes (g = l/4, q = l%4).
+    8-byte accesses are served per 16-lane half-warp over 16 8-byte units,
+    16-byte ones per 8-lane quarter over 8 16-byte units (measured, ncu r4:
+    a pattern whose 32 lanes cover every unit exactly twice -- the former
+    model's minimum -- still took 2x the ideal wavefronts when both lanes of
+    a unit fell in the same half-warp)."""
+    wide_o = kind == "o" and stride % 2 == 0 and not z
+    wide = z or wide_o
+    lanes = 8 if wide else 16
+    worst = 0
+    for ph in range(32 // lanes):
+        counts = {}
+        for lane in range(ph * lanes, ph * lanes + lanes):
+            g, q = lane >> 2, lane & 3
+            if kind == "a":          # TSMM A fragment: element (row g, col q)
+                idx = g * stride + q
+            elif kind == "t":        # TSMTTSM A/B fragment: element (row q, col g)
+                idx = q * stride + g
+            elif z:                  # Z output: element (g, 2q) (e = 0 store)
+                idx = g * stride + 2 * q
+            elif wide_o:             # D output, 16-byte store of (2q, 2q+1)
+                idx = (g * stride + 2 * q) // 2
+            else:                    # D output, 8-byte store
+                idx = g * stride + 2 * q
+            unit = idx % (8 if wide else 16)
+            counts[unit] = counts.get(unit, 0) + 1
+        worst = max(worst, max(counts.values()))
+    return float(worst)
 
 
 def pick_stride(w: int, z: bool, kind: str, pad: bool = False) -> int:
@@ -824,7 +833,7 @@ def tsmm_mma_default(M: int, N: int, z: bool) -> dict:
     S = 2 if z else 1
     MK, NB = cdiv(M, 4), cdiv(N, 8)
     AP, NOP = pick_stride(M, z, "a"), pick_stride(N, z, "o")
-    NCP = 8 * NB + 4 if z else (8 * NB if (8 * NB) % 16 == 8 else 8 * NB + 8)
+    NCP = 8 * NB + 4  # = tsm_kernels.cuh TsmmMmaCfg::NCP
     wr0 = max(1, min(4, 16 // (NB * S)))
     tma = tma_ok(M, N, z)
     for NW in (8, 4):
