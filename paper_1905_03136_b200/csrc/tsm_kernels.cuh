@@ -1024,75 +1024,54 @@ __global__ void __launch_bounds__(Cfg::NT) tsmttsm_mma_kernel(const __grid_const
 #pragma unroll
         for (int z = 0; z < S; z++) ec[u][i][z] = 0.0;
   }
-  // sum of the 4 rows' products x[j] * y[j] (complex: with Im(x) sign-flipped by conj)
-  auto tree4 = [&](const double (&x)[4][S], const double (&y)[4][S], double (&acc)[S]) {
-    if constexpr (!Cfg::Z) {
-      const double s01 = fma(x[1][0], y[1][0], x[0][0] * y[0][0]);
-      const double s23 = fma(x[3][0], y[3][0], x[2][0] * y[2][0]);
-      acc[0] += s01 + s23;
-    } else {
-      double pr = 0.0, pi = 0.0, qr = 0.0, qi = 0.0;
-#pragma unroll
-      for (int j = 0; j < 2; j++) {
-        zfma(pr, pi, x[j][0], flip_sign(x[j][1], p.conj), y[j][0], y[j][1]);
-        zfma(qr, qi, x[2 + j][0], flip_sign(x[2 + j][1], p.conj), y[2 + j][0], y[2 + j][1]);
-      }
-      acc[0] += pr + qr;
-      acc[1] += pi + qi;
-    }
-  };
-  // DFMA over rows [r_begin, rows) step NE of a stage (or of global memory: the
-  // odd tail row), 4 rows per iteration summed as a tree (tree4) and added to
-  // the accumulators once: one dependent DFMA per row waited on the FP64 pipe
-  // the consumer warps' DMMAs keep busy, and slow edge warps hold the stages
+  // DFMA over rows [r_begin, rows) step NE of a stage (or of global memory: the odd tail row)
   auto edge_rows = [&](const double* __restrict__ sA, const double* __restrict__ sB, int r_begin, int rows,
                        int ap, int bp) {
-    for (int r = r_begin; r < rows; r += 4 * Cfg::NE) {
+#pragma unroll 2
+    for (int r = r_begin; r < rows; r += Cfg::NE) {
       if constexpr (MR > 0) {
+        double bv[UN][S];
 #pragma unroll
         for (int u = 0; u < UN; u++) {
           const int n = lane + 32 * u;
-          double bv[4][S];
 #pragma unroll
-          for (int j = 0; j < 4; j++) {
-            const int rj = r + j * Cfg::NE;
+          for (int z = 0; z < S; z++) bv[u][z] = (n < N) ? sB[off(r, n, bp) + z] : 0.0;
+        }
 #pragma unroll
-            for (int z = 0; z < S; z++) bv[j][z] = (rj < rows && n < N) ? sB[off(rj, n, bp) + z] : 0.0;
-          }
+        for (int i = 0; i < MR; i++) {
+          const int m = Cfg::MC + i;
+          if constexpr (!Cfg::Z) {
+            const double a = sA[off(r, m, ap)];
 #pragma unroll
-          for (int i = 0; i < MR; i++) {
-            double av[4][S];
+            for (int u = 0; u < UN; u++) er[i][u][0] = fma(a, bv[u][0], er[i][u][0]);
+          } else {
+            const double2 a = *reinterpret_cast<const double2*>(sA + off(r, m, ap));
+            const double ai = flip_sign(a.y, p.conj);
 #pragma unroll
-            for (int j = 0; j < 4; j++) {
-              const int rj = r + j * Cfg::NE;
-#pragma unroll
-              for (int z = 0; z < S; z++) av[j][z] = (rj < rows) ? sA[off(rj, Cfg::MC + i, ap) + z] : 0.0;
-            }
-            tree4(av, bv, er[i][u]);
+            for (int u = 0; u < UN; u++) zfma(er[i][u][0], er[i][u][1], a.x, ai, bv[u][0], bv[u][1]);
           }
         }
       }
       if constexpr (NR > 0) {
+        double av[UM][S];
 #pragma unroll
         for (int u = 0; u < UM; u++) {
           const int m = lane + 32 * u;
-          double av[4][S];
 #pragma unroll
-          for (int j = 0; j < 4; j++) {
-            const int rj = r + j * Cfg::NE;
+          for (int z = 0; z < S; z++) av[u][z] = (m < Cfg::MC) ? sA[off(r, m, ap) + z] : 0.0;
+        }
 #pragma unroll
-            for (int z = 0; z < S; z++) av[j][z] = (rj < rows && m < Cfg::MC) ? sA[off(rj, m, ap) + z] : 0.0;
-          }
+        for (int i = 0; i < NR; i++) {
+          const int n = Cfg::NC + i;
+          if constexpr (!Cfg::Z) {
+            const double b = sB[off(r, n, bp)];
 #pragma unroll
-          for (int i = 0; i < NR; i++) {
-            double bv[4][S];
+            for (int u = 0; u < UM; u++) ec[u][i][0] = fma(av[u][0], b, ec[u][i][0]);
+          } else {
+            const double2 b = *reinterpret_cast<const double2*>(sB + off(r, n, bp));
 #pragma unroll
-            for (int j = 0; j < 4; j++) {
-              const int rj = r + j * Cfg::NE;
-#pragma unroll
-              for (int z = 0; z < S; z++) bv[j][z] = (rj < rows) ? sB[off(rj, Cfg::NC + i, bp) + z] : 0.0;
-            }
-            tree4(av, bv, ec[u][i]);
+            for (int u = 0; u < UM; u++)
+              zfma(ec[u][i][0], ec[u][i][1], av[u][0], flip_sign(av[u][1], p.conj), b.x, b.y);
           }
         }
       }
@@ -1103,61 +1082,51 @@ __global__ void __launch_bounds__(Cfg::NT) tsmttsm_mma_kernel(const __grid_const
   // each k-step.  Groups: row-strip lane group u (cells (MC+i, lane+32u), i <
   // MR, one B load + MR broadcasts of A) for u < UN, then column-strip lane
   // group u (cells (lane+32u, NC+i), one A load + NR broadcasts of B); group g
-  // belongs to the warp tile g % WT of the slot.  The 4 rows' products are
-  // summed as a tree, (p0 + p1) + (p2 + p3) with p0 + p1 = fma(a1, b1, a0 b0),
-  // and added to the accumulator once per k-step: a single dependent chain of
-  // 4 DFMAs per k-step stalled the warp's next DMMAs behind each DFMA's wait
-  // in the FP64 pipe the DMMAs of every warp of the SMSP share (SASS r2).
+  // belongs to the warp tile g % WT of the slot.
   constexpr int NGRP = UN + UM;
   auto edge_inline = [&](const double* __restrict__ sA, const double* __restrict__ sB, int k0, int rows,
                          int ap, int bp) {
     constexpr int KD = Cfg::KD;
     const int base = (k0 & ~(4 * KD - 1)) + ((k0 >> 2) & (KD - 1));
 #pragma unroll
-    for (int g = 0; g < NGRP; g++) {
-      if (g % Cfg::WT != wt) continue;  // (warp-uniform)
-      if (g < UN) {
-        if constexpr (MR > 0) {
-          const int u = g, n = lane + 32 * u;
-          double bv[4][S];
+    for (int j = 0; j < 4; j++) {
+      const int r = base + KD * j;
+      if (r >= rows) break;  // (warp-uniform)
 #pragma unroll
-          for (int j = 0; j < 4; j++) {
-            const int r = base + KD * j;
+      for (int g = 0; g < NGRP; g++) {
+        if (g % Cfg::WT != wt) continue;  // (warp-uniform)
+        if (g < UN) {
+          if constexpr (MR > 0) {
+            const int u = g, n = lane + 32 * u;
+            double bv[S];
 #pragma unroll
-            for (int z = 0; z < S; z++) bv[j][z] = (r < rows && n < N) ? sB[off(r, n, bp) + z] : 0.0;
-          }
+            for (int z = 0; z < S; z++) bv[z] = (n < N) ? sB[off(r, n, bp) + z] : 0.0;
 #pragma unroll
-          for (int i = 0; i < MR; i++) {
-            double av[4][S];
-#pragma unroll
-            for (int j = 0; j < 4; j++) {
-              const int r = base + KD * j;
-#pragma unroll
-              for (int z = 0; z < S; z++) av[j][z] = (r < rows) ? sA[off(r, Cfg::MC + i, ap) + z] : 0.0;
+            for (int i = 0; i < MR; i++) {
+              if constexpr (!Cfg::Z) {
+                er[i][u][0] = fma(sA[off(r, Cfg::MC + i, ap)], bv[0], er[i][u][0]);
+              } else {
+                const double2 a = *reinterpret_cast<const double2*>(sA + off(r, Cfg::MC + i, ap));
+                zfma(er[i][u][0], er[i][u][1], a.x, flip_sign(a.y, p.conj), bv[0], bv[S - 1]);
+              }
             }
-            tree4(av, bv, er[i][u]);
           }
-        }
-      } else {
-        if constexpr (NR > 0) {
-          const int u = g - UN, m = lane + 32 * u;
-          double av[4][S];
+        } else {
+          if constexpr (NR > 0) {
+            const int u = g - UN, m = lane + 32 * u;
+            double av[S];
 #pragma unroll
-          for (int j = 0; j < 4; j++) {
-            const int r = base + KD * j;
+            for (int z = 0; z < S; z++) av[z] = (m < Cfg::MC) ? sA[off(r, m, ap) + z] : 0.0;
+            if constexpr (Cfg::Z) av[S - 1] = flip_sign(av[S - 1], p.conj);
 #pragma unroll
-            for (int z = 0; z < S; z++) av[j][z] = (r < rows && m < Cfg::MC) ? sA[off(r, m, ap) + z] : 0.0;
-          }
-#pragma unroll
-          for (int i = 0; i < NR; i++) {
-            double bv[4][S];
-#pragma unroll
-            for (int j = 0; j < 4; j++) {
-              const int r = base + KD * j;
-#pragma unroll
-              for (int z = 0; z < S; z++) bv[j][z] = (r < rows) ? sB[off(r, Cfg::NC + i, bp) + z] : 0.0;
+            for (int i = 0; i < NR; i++) {
+              if constexpr (!Cfg::Z) {
+                ec[u][i][0] = fma(av[0], sB[off(r, Cfg::NC + i, bp)], ec[u][i][0]);
+              } else {
+                const double2 b = *reinterpret_cast<const double2*>(sB + off(r, Cfg::NC + i, bp));
+                zfma(ec[u][i][0], ec[u][i][1], av[0], av[S - 1], b.x, b.y);
+              }
             }
-            tree4(av, bv, ec[u][i]);
           }
         }
       }
@@ -1313,8 +1282,7 @@ __global__ void __launch_bounds__(Cfg::NT) tsmttsm_mma_kernel(const __grid_const
     }
     if constexpr (Cfg::EI) {  // inline edge: the owning warp tile of each group, slot by slot
       if (warp < NW && slot == sl) {
-        // (by value: taking the address of er / ec would move them to local memory)
-        auto put = [&](int m, int n, const double (&v)[S]) {
+        auto put = [&](int m, int n, const double* v) {
 #pragma unroll
           for (int z = 0; z < S; z++) {
             const int idx = (m * N + n) * S + z;
@@ -1342,7 +1310,7 @@ __global__ void __launch_bounds__(Cfg::NT) tsmttsm_mma_kernel(const __grid_const
     }
     if constexpr (Cfg::EDGE && !Cfg::EI) {  // edge cells are disjoint from the core; edge warps in order
       if (warp == NW + sl && sl < Cfg::NE) {
-        auto put = [&](int m, int n, const double (&v)[S]) {
+        auto put = [&](int m, int n, const double* v) {
 #pragma unroll
           for (int z = 0; z < S; z++) {
             const int idx = (m * N + n) * S + z;
@@ -2111,20 +2079,13 @@ __global__ void __launch_bounds__(Cfg::NT) tsmm_cst_kernel(const __grid_constant
             for (int j = 0; j < NBW; j++)
   #pragma unroll
               for (int z = 0; z < NA; z++) acc[i][j][z][0] = acc[i][j][z][1] = 0.0;
-          // NACC independent accumulators, k-step ks -> ks % NACC: the edge DFMAs
-          // share the FP64 pipe with the queued DMMAs of every warp of the SMSP,
-          // so one dependent chain per (row block, column) would stall this warp's
-          // next DMMAs behind each DFMA's queueing latency
-          constexpr int NACC = (WR * ECA * S * 4 <= 16) ? 4 : (WR * ECA * S * 2 <= 24) ? 2 : 1;
-          double eacc[NACC][WR][ECA][S];
-#pragma unroll
-          for (int w = 0; w < NACC; w++)
-#pragma unroll
-            for (int i = 0; i < WR; i++)
-#pragma unroll
-              for (int e = 0; e < ECA; e++)
-#pragma unroll
-                for (int z = 0; z < S; z++) eacc[w][i][e][z] = 0.0;
+          double eacc[WR][ECA][S];
+  #pragma unroll
+          for (int i = 0; i < WR; i++)
+  #pragma unroll
+            for (int e = 0; e < ECA; e++)
+  #pragma unroll
+              for (int z = 0; z < S; z++) eacc[i][e][z] = 0.0;
   #pragma unroll
           for (int ks = 0; ks < MK; ks++) {
             const int m = 4 * ks + q;
@@ -2138,7 +2099,7 @@ __global__ void __launch_bounds__(Cfg::NT) tsmm_cst_kernel(const __grid_constant
                 for (int j = 0; j < NBV; j++) dmma(acc[i][j][0][0], acc[i][j][0][1], a, cf[ks][j][0]);
                 if constexpr (ECV > 0) {
   #pragma unroll
-                  for (int e = 0; e < ECV; e++) eacc[ks % NACC][i][e][0] = fma(a, sCe[m * EC + e], eacc[ks % NACC][i][e][0]);
+                  for (int e = 0; e < ECV; e++) eacc[i][e][0] = fma(a, sCe[m * EC + e], eacc[i][e][0]);
                 }
               } else {
                 const double2 a = mv ? *reinterpret_cast<const double2*>(sA + aoff(r, m)) : make_double2(0.0, 0.0);
@@ -2165,7 +2126,7 @@ __global__ void __launch_bounds__(Cfg::NT) tsmm_cst_kernel(const __grid_constant
   #pragma unroll
                   for (int e = 0; e < ECV; e++) {
                     const double2 ce = *reinterpret_cast<const double2*>(sCe + (m * EC + e) * 2);
-                    zfma(eacc[ks % NACC][i][e][0], eacc[ks % NACC][i][e][1], a.x, a.y, ce.x, ce.y);
+                    zfma(eacc[i][e][0], eacc[i][e][1], a.x, a.y, ce.x, ce.y);
                   }
                 }
               }
@@ -2206,9 +2167,7 @@ __global__ void __launch_bounds__(Cfg::NT) tsmm_cst_kernel(const __grid_constant
                 double v[S];
   #pragma unroll
                 for (int z = 0; z < S; z++) {
-                  v[z] = eacc[0][i][e][z];
-#pragma unroll
-                  for (int w = 1; w < NACC; w++) v[z] += eacc[w][i][e][z];  // fixed order
+                  v[z] = eacc[i][e][z];
                   v[z] += __shfl_xor_sync(0xffffffffu, v[z], 1);
                   v[z] += __shfl_xor_sync(0xffffffffu, v[z], 2);
                 }
@@ -2455,20 +2414,13 @@ __global__ void __launch_bounds__(Cfg::NT) tsmm_cstb_kernel(const __grid_constan
             for (int j = 0; j < NBW; j++)
 #pragma unroll
               for (int z = 0; z < S; z++) acc[i][j][z][0] = acc[i][j][z][1] = 0.0;
-          // NACC independent accumulators, k-step ks -> ks % NACC: the edge DFMAs
-          // share the FP64 pipe with the queued DMMAs of every warp of the SMSP,
-          // so one dependent chain per (row block, column) would stall this warp's
-          // next DMMAs behind each DFMA's queueing latency
-          constexpr int NACC = (WR * ECA * S * 4 <= 16) ? 4 : (WR * ECA * S * 2 <= 24) ? 2 : 1;
-          double eacc[NACC][WR][ECA][S];
+          double eacc[WR][ECA][S];
 #pragma unroll
-          for (int w = 0; w < NACC; w++)
+          for (int i = 0; i < WR; i++)
 #pragma unroll
-            for (int i = 0; i < WR; i++)
+            for (int e = 0; e < ECA; e++)
 #pragma unroll
-              for (int e = 0; e < ECA; e++)
-#pragma unroll
-                for (int z = 0; z < S; z++) eacc[w][i][e][z] = 0.0;
+              for (int z = 0; z < S; z++) eacc[i][e][z] = 0.0;
 #pragma unroll
           for (int ks = 0; ks < MK; ks++) {
             const int m = 4 * ks + q;
@@ -2482,7 +2434,7 @@ __global__ void __launch_bounds__(Cfg::NT) tsmm_cstb_kernel(const __grid_constan
                 for (int j = 0; j < NBV; j++) dmma(acc[i][j][0][0], acc[i][j][0][1], a, cf[ks][j][0]);
                 if constexpr (ECV > 0) {  // this lane's m-term of the edge columns (m >= M: C' row 0)
 #pragma unroll
-                  for (int e = 0; e < ECV; e++) eacc[ks % NACC][i][e][0] = fma(a, sCe[m * EC + e], eacc[ks % NACC][i][e][0]);
+                  for (int e = 0; e < ECV; e++) eacc[i][e][0] = fma(a, sCe[m * EC + e], eacc[i][e][0]);
                 }
               } else {
                 const double2 a = mv ? *reinterpret_cast<const double2*>(sA + (r * M + m) * 2)
@@ -2499,7 +2451,7 @@ __global__ void __launch_bounds__(Cfg::NT) tsmm_cstb_kernel(const __grid_constan
 #pragma unroll
                   for (int e = 0; e < ECV; e++) {
                     const double2 ce = *reinterpret_cast<const double2*>(sCe + (m * EC + e) * 2);
-                    zfma(eacc[ks % NACC][i][e][0], eacc[ks % NACC][i][e][1], a.x, a.y, ce.x, ce.y);
+                    zfma(eacc[i][e][0], eacc[i][e][1], a.x, a.y, ce.x, ce.y);
                   }
                 }
               }
@@ -2528,9 +2480,7 @@ __global__ void __launch_bounds__(Cfg::NT) tsmm_cstb_kernel(const __grid_constan
                 double v[S];
 #pragma unroll
                 for (int z = 0; z < S; z++) {
-                  v[z] = eacc[0][i][e][z];
-#pragma unroll
-                  for (int w = 1; w < NACC; w++) v[z] += eacc[w][i][e][z];  // fixed order
+                  v[z] = eacc[i][e][z];
                   v[z] += __shfl_xor_sync(0xffffffffu, v[z], 1);
                   v[z] += __shfl_xor_sync(0xffffffffu, v[z], 2);
                 }
