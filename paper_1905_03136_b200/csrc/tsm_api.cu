@@ -356,6 +356,14 @@ static tsm_status validate_config_real(const KernelEntry& e) {
   } else if (e.edge & 12) {
     return bad("edge warp count bits (kernel bits 6-7) need the edge flag (kernel | 16)");
   }
+  if (lb_flag(e.edge)) {  // L-blocks (tsm_kernels.cuh LB)
+    if (e.op != KIND_TSMTTSM || (e.impl != 1 && e.impl != 2) || e.dt != TSM_D)
+      return bad("L-blocks (kernel | 4096) apply to the real DMMA TSMTTSM kernels 1 and 2");
+    if (e.edge & (1 | 12 | 16 | 32 | 128)) return bad("L-blocks exclude edge warps, complex-as-real, 3M and inline edge");
+    const int MR = e.M % 8, NR = e.N % 8;
+    if (e.M < 8 || e.N < 8 || MR < 1 || MR > 6 || NR < 1 || NR > 6)
+      return bad("L-blocks need M, N >= 8 with 1..6 edge rows and columns (M, N mod 8)");
+  }
   if (ei_flag(e.edge)) {  // inline edge: consumer warps compute the edge strips
     if (e.op != KIND_TSMTTSM || (e.impl != 1 && e.impl != 2))
       return bad("inline edge (kernel | 2048) applies to the DMMA TSMTTSM kernels 1 and 2");
@@ -407,8 +415,9 @@ static tsm_status validate_config_real(const KernelEntry& e) {
       return bad("kernel 2 needs 16-byte rows of >= 128 bytes (M*S, N*S even and >= 16)");
     if (e.R % 8 || e.R > 256) return bad("kernel 2 needs rows_per_chunk a multiple of 8, <= 256");
     const int ed = edge_warps(e.edge);
-    const int MB = (ed || ei_flag(e.edge)) ? e.M / 8 : (e.M + 7) / 8;  // (pair mode: an odd last block loads single)
-    const int NB = (ed || ei_flag(e.edge)) ? e.N / 8 : (e.N + 7) / 8;
+    const bool core = ed || ei_flag(e.edge) || lb_flag(e.edge);  // blocks of the 8-aligned core only
+    const int MB = core ? e.M / 8 : (e.M + 7) / 8;  // (pair mode: an odd last block loads single)
+    const int NB = core ? e.N / 8 : (e.N + 7) / 8;
     if (e.p0 < 1 || e.p1 < 1 || e.p0 > MB || e.p1 > NB) return bad("WM, WN must be in [1, ceil(M/8)], [1, ceil(N/8)]");
     const int WT = ((MB + e.p0 - 1) / e.p0) * ((NB + e.p1 - 1) / e.p1);
     const int NW = e.NT / 32 - 1 - ed;
@@ -416,8 +425,9 @@ static tsm_status validate_config_real(const KernelEntry& e) {
     if (e.R % (4 * (NW / WT))) return bad("rows_per_chunk must be a multiple of 4 * row slots");
   } else if (e.op == KIND_TSMTTSM && e.impl == 1) {
     const int ed = edge_warps(e.edge);
-    const int MB = (ed || ei_flag(e.edge)) ? e.M / 8 : (e.M + 7) / 8;  // (pair mode: an odd last block loads single)
-    const int NB = (ed || ei_flag(e.edge)) ? e.N / 8 : (e.N + 7) / 8;
+    const bool core = ed || ei_flag(e.edge) || lb_flag(e.edge);  // blocks of the 8-aligned core only
+    const int MB = core ? e.M / 8 : (e.M + 7) / 8;  // (pair mode: an odd last block loads single)
+    const int NB = core ? e.N / 8 : (e.N + 7) / 8;
     if (e.p0 < 1 || e.p1 < 1 || e.p0 > MB || e.p1 > NB) return bad("WM, WN must be in [1, ceil(M/8)], [1, ceil(N/8)]");
     const int WT = ((MB + e.p0 - 1) / e.p0) * ((NB + e.p1 - 1) / e.p1);
     const int NW = e.NT / 32 - 1 - ed;
@@ -539,7 +549,7 @@ tsm_status tsm_plan_create_config(tsm_plan* out, tsm_op op, tsm_dtype dtype, int
   e.p0 = cfg->p0;
   e.p1 = cfg->p1;
   e.impl = cfg->kernel & 15;
-  e.edge = (cfg->kernel >> 4) & 255;
+  e.edge = (cfg->kernel >> 4) & 511;
   e.p2 = (op == TSM_OP_TSMTTSM && e.impl == 0) ? 0 : cfg->p2;
   e.p3 = (op == TSM_OP_TSMTTSM && e.impl >= 1) ? cfg->p3 : 0;
   e.stages = cfg->stages;
@@ -604,7 +614,7 @@ tsm_status tsm_jit_precompile(tsm_op op, tsm_dtype dtype, int M, int N, const ts
     e.p0 = cfg->p0;
     e.p1 = cfg->p1;
     e.impl = cfg->kernel & 15;
-    e.edge = (cfg->kernel >> 4) & 255;
+    e.edge = (cfg->kernel >> 4) & 511;
     e.p2 = (op == TSM_OP_TSMTTSM && e.impl == 0) ? 0 : cfg->p2;
     e.p3 = (op == TSM_OP_TSMTTSM && e.impl >= 1) ? cfg->p3 : 0;
     e.stages = cfg->stages;
@@ -969,6 +979,7 @@ tsm_status tsm_plan_describe(tsm_plan p, int64_t K, char* buf, size_t len) {
   if (zr_flag(k->edge)) kname += "+complex-as-real(2Mx2N)";
   if (g3_flag(k->edge)) kname += "+3m";
   if (ei_flag(k->edge)) kname += "+inline-edge";
+  if (lb_flag(k->edge)) kname += "+l-blocks";
   if (p->order) kname += "+plain-warp-order";
   if (p->op == TSM_OP_TSMTTSM && k->impl >= 1)
     snprintf(tmp, sizeof tmp,

@@ -48,7 +48,7 @@ std::string cfg_type(const KernelEntry& ein) {
        << ", " << (e.NT / 32 - 1 - edge_warps(e.edge)) << ", " << e.R << ", " << e.p2 << ", " << e.p3 << ", "
        << (e.impl == 2 ? "true" : "false") << ", " << edge_warps(e.edge) << ", "
        << ((e.edge & 2) ? "true" : "false") << ", " << zr << ", " << (g3_flag(e.edge) ? "true" : "false") << ", "
-       << (ei_flag(e.edge) ? "true" : "false") << ">";
+       << (ei_flag(e.edge) ? "true" : "false") << ", " << (lb_flag(e.edge) ? "true" : "false") << ">";
   else if (e.op == KIND_TSMTTSM)
     os << "tsm::TsmttsmCfg<" << e.M << ", " << e.N << ", " << z << ", " << e.p0 << ", " << e.p1
        << ", " << e.NT << ", " << e.R << ">";

@@ -768,20 +768,36 @@ constexpr int pick_kdist(int ap, int bp, bool z, bool pair, int r) {
 // (MC = 8*floor(M/8)); one extra consumer warp computes the E = M*N - MC*NC
 // edge cells with DFMA (worth it when M or N is just above a multiple of 8,
 // where 8x8 blocks would waste up to (ceil8(M)/M)^2 of the DMMA work).
+// LB = true (D, kernel | 4096): "L-blocks" instead of padding for the cells
+// outside the 8-aligned core MC x NC, all on the tensor pipe.  With ER = M - MC
+// edge rows and EC = N - NC edge columns (both 1..6), L-block l is the 8 x 8
+// MMA block with rows {MC .. M-1} plus the core rows [l (8-ER), (l+1)(8-ER)) and
+// columns {NC .. N-1} plus the core columns [l (8-EC), (l+1)(8-EC)).  Its
+// edge-row x core-column and core-row x edge-column cells are the edge strips
+// (each cell in exactly one block; the corner from block 0); its core x core
+// interior repeats core cells and is dropped.  NL = max(ceil(MC / (8-ER)),
+// ceil(NC / (8-EC))) blocks replace the ceil(M/8) ceil(N/8) - MB NB padded
+// ones: D 57 57 blocks instead of 64, D 49 43 instead of 49, D 41 31 / 36.
+// An MMA output block is an 8 x 8 outer-product structure, so a strip one cell
+// wide is at best 1/8 useful per block; pairing a row strip with a column
+// strip in one block doubles that.
 // PAIR = true (D only): blocks are used in pairs covering 16 consecutive m (n);
 // block 2p holds the even, block 2p+1 the odd rows (columns) of the pair, so
 // one 16-byte LDS.128 per lane feeds both fragments (half the load
 // instructions of one LDS.64 per fragment).
 template <int M_, int N_, bool Z_, int WM_, int WN_, int NW_, int R_, int AP_ = M_, int BP_ = N_,
           bool TMA_ = false, int EDGE_ = 0, bool PAIR_ = false, bool ZR_ = false, bool G3_ = false,
-          bool EI_ = false>
+          bool EI_ = false, bool LB_ = false>
 struct TsmttsmMmaCfg {
   static constexpr int M = M_, N = N_, WM = WM_, WN = WN_, NW = NW_, R = R_;
   // EI ("inline edge", kernel | 2048): the edge cells are computed by the
   // consumer warps themselves, interleaved with their DMMAs (no edge warps)
   static constexpr bool EI = EI_;
-  static constexpr bool Z = Z_, TMA = TMA_, EDGE = EDGE_ > 0 || EI_, PAIR = PAIR_, ZR = ZR_, G3 = G3_;
+  static constexpr bool LB = LB_;
+  static constexpr bool Z = Z_, TMA = TMA_, EDGE = EDGE_ > 0 || EI_ || LB_, PAIR = PAIR_, ZR = ZR_, G3 = G3_;
+  static constexpr bool DEDGE = EDGE_ > 0 || EI_;  // DFMA edge strips (edge warps or inline)
   static_assert(!(EI_ && EDGE_ > 0), "inline edge excludes edge warps");
+  static_assert(!LB_ || (!Z_ && !ZR_ && !G3_ && !EI_ && EDGE_ == 0), "L-blocks: real kernel, no DFMA edges");
   static_assert(!G3 || Z_, "3M (Gauss) products: complex kernel");
   static_assert(!ZR || (!Z_ && M_ % 2 == 0 && N_ % 2 == 0), "complex-as-real: real kernel on 2M x 2N");
   static_assert(!PAIR || (!Z_ && WM_ % 2 == 0 && WN_ % 2 == 0), "pairs: real, even tiles");
@@ -805,6 +821,10 @@ struct TsmttsmMmaCfg {
   static constexpr int UN = (N + 31) / 32, UM = (MC + 31) / 32;
   static constexpr int EREGS = (MR * UN + UM * NR) * S;        // accumulator doubles per lane
   static constexpr int NE = EDGE_;                             // edge warps (split the rows)
+  static_assert(!LB_ || (MR >= 1 && MR <= 6 && NR >= 1 && NR <= 6), "L-blocks: 1..6 edge rows and columns");
+  static constexpr int NL = !LB_ ? 0
+                            : ((MC + 7 - MR) / (8 - MR) > (NC + 7 - NR) / (8 - NR) ? (MC + 7 - MR) / (8 - MR)
+                                                                                    : (NC + 7 - NR) / (8 - NR));
   static_assert(NE >= 0 && NE <= 4, "0..4 edge warps");
   static_assert(!EDGE || (MB >= 1 && NB >= 1 && E > 0), "edge mode needs a core and an edge");
   static constexpr int WTM = (MB + WM - 1) / WM, WTN = (NB + WN - 1) / WN;
@@ -1008,9 +1028,9 @@ __global__ void __launch_bounds__(Cfg::NT) tsmttsm_mma_kernel(const __grid_const
   // MR*ceil(N/32) + ceil(MC/32)*NR DFMA (or complex) updates.
   constexpr int MR = Cfg::MR, NR = Cfg::NR, UN = Cfg::UN, UM = Cfg::UM;
   constexpr int MRA = MR > 0 ? MR : 1, NRA = NR > 0 ? NR : 1;
-  double er[Cfg::EDGE ? MRA : 1][Cfg::EDGE ? UN : 1][S];  // row strip (MC + mi, lane + 32u)
-  double ec[Cfg::EDGE ? UM : 1][Cfg::EDGE ? NRA : 1][S];  // column strip (lane + 32u, NC + ni)
-  if constexpr (Cfg::EDGE) {
+  double er[Cfg::DEDGE ? MRA : 1][Cfg::DEDGE ? UN : 1][S];  // row strip (MC + mi, lane + 32u)
+  double ec[Cfg::DEDGE ? UM : 1][Cfg::DEDGE ? NRA : 1][S];  // column strip (lane + 32u, NC + ni)
+  if constexpr (Cfg::DEDGE) {
 #pragma unroll
     for (int i = 0; i < MRA; i++)
 #pragma unroll
@@ -1133,6 +1153,29 @@ __global__ void __launch_bounds__(Cfg::NT) tsmttsm_mma_kernel(const __grid_const
     }
   };
 
+  // LB: the L-blocks l = wt, wt + WT, ... of this warp's tile (one DMMA each per
+  // k-step, A and B fragments gathered from the block's row / column lists)
+  constexpr int NLW = Cfg::LB ? (Cfg::NL + Cfg::WT - 1) / Cfg::WT : 1;
+  double lacc[NLW][2];
+#pragma unroll
+  for (int t = 0; t < NLW; t++) lacc[t][0] = lacc[t][1] = 0.0;
+  auto lstep = [&](const double* __restrict__ sA, const double* __restrict__ sB, int k0, int rows, int ap,
+                   int bp) {
+    constexpr int KD = Cfg::KD;
+    const int kr = (k0 & ~(4 * KD - 1)) + ((k0 >> 2) & (KD - 1)) + KD * q;
+    const bool rv = kr < rows;
+#pragma unroll
+    for (int t = 0; t < NLW; t++) {
+      const int l = wt + t * Cfg::WT;
+      if (l >= Cfg::NL) break;  // (warp-uniform)
+      const int mr = g < MR ? Cfg::MC + g : l * (8 - MR) + (g - MR);  // MMA row g -> m
+      const int nc = g < NR ? Cfg::NC + g : l * (8 - NR) + (g - NR);  // MMA column g -> n
+      const double a = (rv && (g < MR || mr < Cfg::MC)) ? sA[off(kr, mr, ap)] : 0.0;
+      const double b = (rv && (g < NR || nc < Cfg::NC)) ? sB[off(kr, nc, bp)] : 0.0;
+      dmma(lacc[t][0], lacc[t][1], a, b);
+    }
+  };
+
   if (warp == NW + Cfg::NE) {
     // ---------------- producer warp: bulk / tensor copies into the ring ----------------
     const u64 pol = policy_evict_first();
@@ -1176,7 +1219,7 @@ __global__ void __launch_bounds__(Cfg::NT) tsmttsm_mma_kernel(const __grid_const
         }
       }
     }
-  } else if (Cfg::EDGE && warp >= NW) {  // (warp < NW + NE: the producer is NW + NE)
+  } else if (Cfg::DEDGE && warp >= NW) {  // (warp < NW + NE: the producer is NW + NE)
     // ---------------- edge warps: DFMA on the cells outside the DMMA core ----------------
     // (edge warp ew takes rows ew, ew + NE, ... of every chunk)
     const int ew = warp - NW;
@@ -1211,12 +1254,14 @@ __global__ void __launch_bounds__(Cfg::NT) tsmttsm_mma_kernel(const __grid_const
           for (int k0 = slot * 4; k0 < R; k0 += RS * 4) {
             kstep(cm, cn, sA, sB, k0, R, AP, BP);
             if constexpr (Cfg::EI) edge_inline(sA, sB, k0, R, AP, BP);
+            if constexpr (Cfg::LB) lstep(sA, sB, k0, R, AP, BP);
           }
         } else {  // partial chunk: every k-step of the atoms that hold rows < rows
           const int kend = (rows + 4 * Cfg::KD - 1) & ~(4 * Cfg::KD - 1);
           for (int k0 = slot * 4; k0 < kend; k0 += RS * 4) {
             kstep(cm, cn, sA, sB, k0, rows, AP, BP);
             if constexpr (Cfg::EI) edge_inline(sA, sB, k0, rows, AP, BP);
+            if constexpr (Cfg::LB) lstep(sA, sB, k0, rows, AP, BP);
           }
         }
         __syncwarp();
@@ -1227,6 +1272,7 @@ __global__ void __launch_bounds__(Cfg::NT) tsmttsm_mma_kernel(const __grid_const
         if ((K & 1) && blockIdx.x == 0 && slot == 0) {
           kstep(cm, cn, p.A + (K - 1) * p.lda * S, p.B + (K - 1) * p.ldb * S, 0, 1, M, N);
           if constexpr (Cfg::EI) edge_inline(p.A + (K - 1) * p.lda * S, p.B + (K - 1) * p.ldb * S, 0, 1, M, N);
+          if constexpr (Cfg::LB) lstep(p.A + (K - 1) * p.lda * S, p.B + (K - 1) * p.ldb * S, 0, 1, M, N);
         }
       }
     };
@@ -1308,7 +1354,33 @@ __global__ void __launch_bounds__(Cfg::NT) tsmttsm_mma_kernel(const __grid_const
         }
       }
     }
-    if constexpr (Cfg::EDGE && !Cfg::EI) {  // edge cells are disjoint from the core; edge warps in order
+    if constexpr (Cfg::LB) {  // L-blocks: the edge cells of each block, slot by slot
+      if (warp < NW && slot == sl) {
+#pragma unroll
+        for (int t = 0; t < NLW; t++) {
+          const int l = wt + t * Cfg::WT;
+          if (l >= Cfg::NL) break;
+#pragma unroll
+          for (int e = 0; e < 2; e++) {
+            const int j = 2 * q + e;  // MMA column; g is the MMA row
+            int m = -1, n = -1;
+            if (g < MR) {  // edge row x (edge columns: block 0 only | core columns)
+              m = Cfg::MC + g;
+              n = j < NR ? (l == 0 ? Cfg::NC + j : -1) : l * (8 - NR) + (j - NR);
+              if (n >= Cfg::NC && j >= NR) n = -1;
+            } else if (j < NR) {  // core row x edge column
+              m = l * (8 - MR) + (g - MR);
+              n = m < Cfg::MC ? Cfg::NC + j : -1;
+            }
+            if (n >= 0) {
+              const int idx = m * N + n;
+              sP[idx] = (sl == 0) ? lacc[t][e] : sP[idx] + lacc[t][e];
+            }
+          }
+        }
+      }
+    }
+    if constexpr (Cfg::DEDGE && !Cfg::EI) {  // edge cells are disjoint from the core; edge warps in order
       if (warp == NW + sl && sl < Cfg::NE) {
         auto put = [&](int m, int n, const double* v) {
 #pragma unroll

@@ -23,7 +23,7 @@ struct KernelEntry {
                      // 8-aligned core, bit 1 = paired 16-byte fragment loads, bits 2-3 =
                      // edge warps - 1, bit 4 = complex-as-real, bit 5 = 3M (Gauss) complex
                      // products, bit 6 = plain warp order (launch argument), bit 7 = inline
-                     // edge (tsm_config.kernel bits 4..11)
+                     // edge, bit 8 = L-blocks (tsm_config.kernel bits 4..12)
 };
 
 // number of DFMA edge warps encoded in KernelEntry::edge
@@ -41,6 +41,11 @@ inline bool g3_flag(int flags) { return (flags & 32) != 0; }
 // bit 7: inline edge -- the DMMA TSMTTSM consumer warps compute the cells outside
 // the 8-aligned core themselves (DFMA interleaved with their DMMAs), no edge warps
 inline bool ei_flag(int flags) { return (flags & 128) != 0; }
+
+// bit 8: L-blocks (D DMMA TSMTTSM) -- the cells outside the 8-aligned core by
+// MMA blocks pairing edge rows with core columns and core rows with edge
+// columns (tsm_kernels.cuh LB), instead of padded blocks
+inline bool lb_flag(int flags) { return (flags & 256) != 0; }
 
 // the real problem a complex-as-real entry runs (identity otherwise)
 inline KernelEntry real_view(const KernelEntry& k) {

@@ -496,3 +496,43 @@ def test_tsmm_win16_row_windows(tsm, M, N):
         torch.cuda.synchronize()
         assert np.array_equal(got.cpu().numpy(), oracle.tsmm(Ai, Ci)[0]), (key, c)
     assert ran
+
+
+@pytest.mark.parametrize("M,N", [(57, 57), (49, 49), (41, 41), (33, 33), (9, 9), (58, 58), (60, 60), (17, 42),
+                                 (50, 11), (35, 59)])
+def test_tsmttsm_lblocks(tsm, M, N):
+    """L-blocks (kernel | 4096, D): the cells outside the 8-aligned core on MMA
+    blocks pairing edge rows with core columns and core rows with edge columns
+    -- every family the generator offers (bulk / TMA, pair loads) on ragged K
+    (odd K: the global last-row path) within the 1e-12 |A|^T|B| tolerance,
+    integer-valued inputs bit-exact (every edge cell written exactly once)."""
+    base = [c for c in gi.candidates("tsmttsm", M, N, False) if c.get("LB")]
+    if not base:
+        pytest.skip("L-blocks do not pay for this shape")
+    picked = {}
+    for c in base:
+        picked.setdefault((c.get("impl"), c.get("PAIR", 0), c["MT"], c["NTL"]), c)
+    ran = 0
+    for key, c in sorted(picked.items())[:6]:
+        try:
+            plan = tsm.Plan("tsmttsm", "d", M, N, 0, config=gi.to_tsm_config("tsmttsm", c, 3, 1))
+        except tsm.TsmError as e:
+            if e.status != 2:
+                raise
+            continue
+        assert plan.config()["kernel"] & 4096 and "l-blocks" in plan.describe(1000)["kernel"]
+        ran += 1
+        for K in (1, 7, 4099, 65537):
+            A = ti.matrix(K, M, "A", seed=K + 81)
+            B = ti.matrix(K, N, "B", seed=K + 82)
+            got = tsm.tsmttsm(torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda(), plan=plan)
+            torch.cuda.synchronize()
+            ref, bound = oracle.tsmttsm(A, B)
+            r, wi, _ = oracle.max_err_ratio(got.cpu().numpy(), ref, bound)
+            assert r <= 1e-12, (M, N, key, c, K, r, wi)
+        Ai = ti.matrix(30001, M, "A", mode="int")
+        Bi = ti.matrix(30001, N, "B", mode="int")
+        got = tsm.tsmttsm(torch.from_numpy(Ai).cuda(), torch.from_numpy(Bi).cuda(), plan=plan)
+        torch.cuda.synchronize()
+        assert np.array_equal(got.cpu().numpy(), oracle.tsmttsm(Ai, Bi)[0]), (key, c)
+    assert ran

@@ -182,6 +182,29 @@ def edge_candidates(M: int, N: int, z: bool) -> list:
     return out
 
 
+def lblock_candidates(M: int, N: int, z: bool) -> list:
+    """LB=1 (D): the core tilings of the inline-edge search with the edge
+    strips on L-blocks (tsm_kernels.cuh LB) -- only where they need fewer MMA
+    blocks than the padded tiling."""
+    if z or M < 8 or N < 8 or not (1 <= M % 8 <= 6 and 1 <= N % 8 <= 6):
+        return []
+    MR, NR = M % 8, N % 8
+    MC, NC = M - MR, N - NR
+    nl = max(cdiv(MC, 8 - MR), cdiv(NC, 8 - NR))
+    if (MC // 8) * (NC // 8) + nl >= cdiv(M, 8) * cdiv(N, 8):
+        return []
+    out, seen = [], set()
+    for c in inline_edge_candidates(M, N, z):
+        c = dict(c)
+        c.pop("EI", None)
+        c["LB"] = 1
+        k = tuple(sorted(c.items()))
+        if k not in seen:
+            seen.add(k)
+            out.append(c)
+    return out
+
+
 def inline_edge_candidates(M: int, N: int, z: bool) -> list:
     """EI=1: the edge candidates without edge warps -- the consumer warps
     compute the edge strips between their DMMAs (<= 16 strip accumulators
@@ -382,7 +405,8 @@ def cfg_type(op, dt, M, N, c) -> str:
         pair = "true" if c.get("PAIR", 0) else "false"
         return (f"tsm::TsmttsmMmaCfg<{M}, {N}, {z}, {c['MT']}, {c['NTL']}, {c['NT'] // 32 - 1 - edge}, "
                 f"{c['R']}, {c.get('AP', M)}, {c.get('BP', N)}, {tma}, {edge}, {pair}, {zr}, "
-                f"{'true' if c.get('G3', 0) else 'false'}, {'true' if c.get('EI', 0) else 'false'}>")
+                f"{'true' if c.get('G3', 0) else 'false'}, {'true' if c.get('EI', 0) else 'false'}, "
+                f"{'true' if c.get('LB', 0) else 'false'}>")
     if op == "tsmttsm":
         return f"tsm::TsmttsmCfg<{M}, {N}, {z}, {c['MT']}, {c['NTL']}, {c['NT']}, {c['R']}>"
     if c.get("impl", 0) == 4:
@@ -421,11 +445,13 @@ def flags(c: dict) -> int:
     paired 16-byte fragment loads, bits 2-3 edge warps - 1 (EDGE = edge warp count),
     bit 4 complex-as-real (ZR), bit 5 3M / Gauss complex products (G3), bit 6
     plain consumer-warp order (PLAIN; a launch argument of the DMMA kernels),
-    bit 7 inline edge (EI: consumer warps compute the edge strips)."""
+    bit 7 inline edge (EI: consumer warps compute the edge strips), bit 8
+    L-blocks (LB: edge strips by MMA blocks pairing edge rows with core
+    columns and core rows with edge columns)."""
     e = c.get("EDGE", 0)
     return ((1 if e else 0) | (c.get("PAIR", 0) << 1) | (((e - 1) & 3) << 2 if e else 0)
             | (c.get("ZR", 0) << 4) | (c.get("G3", 0) << 5) | (c.get("PLAIN", 0) << 6)
-            | (c.get("EI", 0) << 7))
+            | (c.get("EI", 0) << 7) | (c.get("LB", 0) << 8))
 
 
 def params4(op: str, M: int, N: int, c: dict) -> tuple:
@@ -622,6 +648,7 @@ def candidates(op: str, M: int, N: int, z: bool) -> list:
                                             AP=M, BP=N))
             out.extend(edge_candidates(M, N, z))
             out.extend(inline_edge_candidates(M, N, z))
+            out.extend(lblock_candidates(M, N, z))
             out.extend(pair_candidates(M, N, z))
     else:
         acc_max = 16 if z else 32
