@@ -84,6 +84,7 @@ def run_one(plan, op, z, M, N, K, conj=False, update=None, strided=False):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--quick", action="store_true", help="first 6 families only")
+    ap.add_argument("--match", default="", help="comma list of kernel-name substrings: only those families")
     a = ap.parse_args()
     fams = {}
     shapes = [(w, w) for w in range(1, 65)] + [(1, 64), (64, 1), (16, 48), (48, 16)]
@@ -94,12 +95,18 @@ def main():
                 d = p.describe(4099)
                 key = (op, dt, d["kernel"], p.config()["kernel"] & 15)
                 fams.setdefault(key, ("default", p, M, N))
-    # explicit families the tuned table may not pick (autotuner search space)
+    # explicit families the tuned table may not pick (autotuner search space);
+    # only the first candidate of each (impl, flags) class is compiled
     import gen_instances as gi
+    seen = set()
     for op in ("tsmttsm", "tsmm"):
         for dt in ("d", "z"):
-            for (M, N) in [(64, 64), (33, 17), (24, 24), (3, 5)]:
+            for (M, N) in [(64, 64), (33, 17), (24, 24), (3, 5), (57, 57), (41, 41)]:
                 for c in gi.candidates(op, M, N, dt == "z"):
+                    cls = (op, dt, c.get("impl", 0), gi.flags(c) & ~64, c.get("WR", 1) % 2)
+                    if cls in seen:
+                        continue
+                    seen.add(cls)
                     try:
                         p = tsm.Plan(op, dt, M, N, 0, config=gi.to_tsm_config(op, c, 3, 2))
                     except tsm.TsmError:
@@ -107,6 +114,8 @@ def main():
                     key = (op, dt, p.describe(4099)["kernel"], p.config()["kernel"] & 15)
                     fams.setdefault(key, ("explicit", p, M, N))
     items = sorted(fams.items(), key=lambda kv: kv[0])
+    if a.match:
+        items = [it for it in items if any(m in it[0][2] for m in a.match.split(","))]
     if a.quick:
         items = items[:6]
     n = 0
@@ -134,9 +143,11 @@ def main():
                 run_one(p, op, True, M, N, K, update=(1.0, 0.0), conj=True)
             n += 1
         print(f"conj     z {op} M={M} N={N}: ok", flush=True)
-    for (op, dt, M, N) in [("tsmttsm", "d", 32, 32), ("tsmm", "d", 16, 48), ("tsmttsm", "z", 8, 8),
-                           ("tsmm", "z", 40, 40)]:
-        p = tsm.get_plan(op, dt, M, N, 0, strided=True)
+    for (op, dt, M, N, g) in [("tsmttsm", "d", 32, 32, False), ("tsmm", "d", 16, 48, False),
+                              ("tsmttsm", "z", 8, 8, False), ("tsmm", "z", 40, 40, False),
+                              ("tsmttsm", "d", 33, 7, True), ("tsmm", "d", 57, 57, True),
+                              ("tsmm", "z", 5, 3, True)]:
+        p = tsm.get_plan(op, dt, M, N, 0, strided=not g, gather=g)
         for K in KS:
             run_one(p, op, dt == "z", M, N, K, strided=True)
             n += 1
