@@ -797,7 +797,8 @@ struct TsmttsmMmaCfg {
   static constexpr bool Z = Z_, TMA = TMA_, EDGE = EDGE_ > 0 || EI_ || LB_, PAIR = PAIR_, ZR = ZR_, G3 = G3_;
   static constexpr bool DEDGE = EDGE_ > 0 || EI_;  // DFMA edge strips (edge warps or inline)
   static_assert(!(EI_ && EDGE_ > 0), "inline edge excludes edge warps");
-  static_assert(!LB_ || (!Z_ && !ZR_ && !G3_ && !EI_ && EDGE_ == 0), "L-blocks: real kernel, no DFMA edges");
+  // (complex-as-real runs the real kernel on 2M x 2N: L-blocks apply to that product)
+  static_assert(!LB_ || (!Z_ && !G3_ && !EI_ && EDGE_ == 0), "L-blocks: real kernel, no DFMA edges");
   static_assert(!G3 || Z_, "3M (Gauss) products: complex kernel");
   static_assert(!ZR || (!Z_ && M_ % 2 == 0 && N_ % 2 == 0), "complex-as-real: real kernel on 2M x 2N");
   static_assert(!PAIR || (!Z_ && WM_ % 2 == 0 && WN_ % 2 == 0), "pairs: real, even tiles");
