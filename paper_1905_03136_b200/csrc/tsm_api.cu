@@ -356,6 +356,8 @@ static tsm_status validate_config_real(const KernelEntry& e) {
   } else if (e.edge & 12) {
     return bad("edge warp count bits (kernel bits 6-7) need the edge flag (kernel | 16)");
   }
+  if (ga_flag(e.edge) && !((e.op == KIND_TSMTTSM && e.impl == 1) || (e.op == KIND_TSMM && e.impl == 4)))
+    return bad("the gather flag (kernel | 8192) applies to TSMTTSM kernel 1 and TSMM kernel 4");
   if (lb_flag(e.edge)) {  // L-blocks (tsm_kernels.cuh LB)
     if (e.op != KIND_TSMTTSM || (e.impl != 1 && e.impl != 2) || e.dt != TSM_D)
       return bad("L-blocks (kernel | 4096) apply to the real DMMA TSMTTSM kernels 1 and 2");
@@ -549,7 +551,7 @@ tsm_status tsm_plan_create_config(tsm_plan* out, tsm_op op, tsm_dtype dtype, int
   e.p0 = cfg->p0;
   e.p1 = cfg->p1;
   e.impl = cfg->kernel & 15;
-  e.edge = (cfg->kernel >> 4) & 511;
+  e.edge = (cfg->kernel >> 4) & 1023;
   e.p2 = (op == TSM_OP_TSMTTSM && e.impl == 0) ? 0 : cfg->p2;
   e.p3 = (op == TSM_OP_TSMTTSM && e.impl >= 1) ? cfg->p3 : 0;
   e.stages = cfg->stages;
@@ -593,7 +595,7 @@ tsm_status tsm_plan_create_ex(tsm_plan* out, tsm_op op, tsm_dtype dtype, int M, 
   if (st == TSM_SUCCESS && (flags & TSM_FLAG_GATHER) && !gather_capable(*(*out)->k)) {
     tsm_plan_destroy(*out);
     *out = nullptr;
-    return fail(TSM_ERR_INVALID_VALUE, "TSM_FLAG_GATHER needs kernel 1 (TSMTTSM) or 4 (TSMM)");
+    return fail(TSM_ERR_INVALID_VALUE, "TSM_FLAG_GATHER needs the gather-capable kernel 1 (TSMTTSM) or 4 (TSMM), kernel | 8192");
   }
   if (st == TSM_SUCCESS) (*out)->flags = flags;
   return st;
@@ -614,7 +616,7 @@ tsm_status tsm_jit_precompile(tsm_op op, tsm_dtype dtype, int M, int N, const ts
     e.p0 = cfg->p0;
     e.p1 = cfg->p1;
     e.impl = cfg->kernel & 15;
-    e.edge = (cfg->kernel >> 4) & 511;
+    e.edge = (cfg->kernel >> 4) & 1023;
     e.p2 = (op == TSM_OP_TSMTTSM && e.impl == 0) ? 0 : cfg->p2;
     e.p3 = (op == TSM_OP_TSMTTSM && e.impl >= 1) ? cfg->p3 : 0;
     e.stages = cfg->stages;
@@ -735,7 +737,9 @@ static bool strided_overlap(const void* x, long long ldx, int wx, const void* y,
 static bool tma_kernel(const KernelEntry& k) {
   return k.op == KIND_TSMTTSM ? k.impl == 2 : (k.impl == 2 || k.impl == 3);
 }
-bool gather_capable(const KernelEntry& k) { return k.op == KIND_TSMTTSM ? k.impl == 1 : k.impl == 4; }
+bool gather_capable(const KernelEntry& k) {
+  return ga_flag(k.edge) && (k.op == KIND_TSMTTSM ? k.impl == 1 : k.impl == 4);
+}
 bool strided_capable(const KernelEntry& k) { return tma_kernel(k) || gather_capable(k); }
 
 // Row strides (elements) of a call: 0 = dense.  Strided views (NEXT N4) need a
@@ -980,6 +984,7 @@ tsm_status tsm_plan_describe(tsm_plan p, int64_t K, char* buf, size_t len) {
   if (g3_flag(k->edge)) kname += "+3m";
   if (ei_flag(k->edge)) kname += "+inline-edge";
   if (lb_flag(k->edge)) kname += "+l-blocks";
+  if (ga_flag(k->edge)) kname += "+gather";
   if (p->order) kname += "+plain-warp-order";
   if (p->op == TSM_OP_TSMTTSM && k->impl >= 1)
     snprintf(tmp, sizeof tmp,

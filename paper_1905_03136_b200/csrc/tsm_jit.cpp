@@ -48,13 +48,15 @@ std::string cfg_type(const KernelEntry& ein) {
        << ", " << (e.NT / 32 - 1 - edge_warps(e.edge)) << ", " << e.R << ", " << e.p2 << ", " << e.p3 << ", "
        << (e.impl == 2 ? "true" : "false") << ", " << edge_warps(e.edge) << ", "
        << ((e.edge & 2) ? "true" : "false") << ", " << zr << ", " << (g3_flag(e.edge) ? "true" : "false") << ", "
-       << (ei_flag(e.edge) ? "true" : "false") << ", " << (lb_flag(e.edge) ? "true" : "false") << ">";
+       << (ei_flag(e.edge) ? "true" : "false") << ", " << (lb_flag(e.edge) ? "true" : "false") << ", "
+       << (ga_flag(e.edge) ? "true" : "false") << ">";
   else if (e.op == KIND_TSMTTSM)
     os << "tsm::TsmttsmCfg<" << e.M << ", " << e.N << ", " << z << ", " << e.p0 << ", " << e.p1
        << ", " << e.NT << ", " << e.R << ">";
   else if (e.impl == 4)
     os << "tsm::TsmmCstbCfg<" << e.M << ", " << e.N << ", " << z << ", " << e.p0 << ", " << e.p1
-       << ", " << (e.NT / 32 - 1) << ", " << e.R << ", " << ((e.edge & 1) ? e.N % 8 : 0) << ">";
+       << ", " << (e.NT / 32 - 1) << ", " << e.R << ", " << ((e.edge & 1) ? e.N % 8 : 0) << ", "
+       << (ga_flag(e.edge) ? "true" : "false") << ">";
   else if (e.impl == 3)
     os << "tsm::TsmmCstCfg<" << e.M << ", " << e.N << ", " << z << ", " << e.p0 << ", " << e.p1
        << ", " << (e.NT / 32 - 1) << ", " << e.R << ", " << zr << ", " << ((e.edge & 1) ? e.N % 8 : 0) << ", "

@@ -787,13 +787,19 @@ constexpr int pick_kdist(int ap, int bp, bool z, bool pair, int r) {
 // instructions of one LDS.64 per fragment).
 template <int M_, int N_, bool Z_, int WM_, int WN_, int NW_, int R_, int AP_ = M_, int BP_ = N_,
           bool TMA_ = false, int EDGE_ = 0, bool PAIR_ = false, bool ZR_ = false, bool G3_ = false,
-          bool EI_ = false, bool LB_ = false>
+          bool EI_ = false, bool LB_ = false, bool GA_ = false>
 struct TsmttsmMmaCfg {
   static constexpr int M = M_, N = N_, WM = WM_, WN = WN_, NW = NW_, R = R_;
   // EI ("inline edge", kernel | 2048): the edge cells are computed by the
   // consumer warps themselves, interleaved with their DMMAs (no edge warps)
   static constexpr bool EI = EI_;
   static constexpr bool LB = LB_;
+  // GA (kernel | 8192): the gather-capable instantiation (strided views, NEXT N4).
+  // A separate instantiation: the gather producer code in every kernel made
+  // NVRTC's ptxas allocate fewer registers and spill in the edge-warp / inline-
+  // edge kernels (D 49 edge warps 96 -> 72 registers + 24 B stack, +15 % time).
+  static constexpr bool GA = GA_;
+  static_assert(!GA_ || !TMA_, "gather mode: the bulk-copy kernel");
   static constexpr bool Z = Z_, TMA = TMA_, EDGE = EDGE_ > 0 || EI_ || LB_, PAIR = PAIR_, ZR = ZR_, G3 = G3_;
   static constexpr bool DEDGE = EDGE_ > 0 || EI_;  // DFMA edge strips (edge warps or inline)
   static_assert(!(EI_ && EDGE_ > 0), "inline edge excludes edge warps");
@@ -868,7 +874,7 @@ __global__ void __launch_bounds__(Cfg::NT) tsmttsm_mma_kernel(const __grid_const
 
   if (tid == 0) {
     for (int s = 0; s < stages; s++) {
-      mbar_init(&full[s], p.gather ? 32 : 1);  // gather: one noinc arrival per producer lane
+      mbar_init(&full[s], (Cfg::GA && p.gather) ? 32 : 1);  // gather: one noinc arrival per producer lane
       mbar_init(&empty[s], NW + Cfg::NE);  // consumer + edge warps release a stage
     }
     fence_mbar_init();
@@ -1197,11 +1203,13 @@ __global__ void __launch_bounds__(Cfg::NT) tsmttsm_mma_kernel(const __grid_const
           for (int b = 0; b < Cfg::NBB; b++)
             tma_load_2d(dB + b * R * 16, &p.tmB, b * 16, static_cast<int>(r0), &full[s], pol);
         }
-      } else if (p.gather) {  // strided rows (N4): element copies, any row stride
-        const int rows = static_cast<int>((K_even - r0 < R) ? (K_even - r0) : R);
-        gather_rows<M, S>(dA, AP, p.A, r0, p.lda, rows, lane);
-        gather_rows<N, S>(dB, BP, p.B, r0, p.ldb, rows, lane);
-        cp_async_mbar_arrive_noinc(&full[s]);
+      } else if (Cfg::GA && p.gather) {  // strided rows (N4): element copies, any row stride
+        if constexpr (Cfg::GA) {
+          const int rows = static_cast<int>((K_even - r0 < R) ? (K_even - r0) : R);
+          gather_rows<M, S>(dA, AP, p.A, r0, p.lda, rows, lane);
+          gather_rows<N, S>(dB, BP, p.B, r0, p.ldb, rows, lane);
+          cp_async_mbar_arrive_noinc(&full[s]);
+        }
       } else {
         const int rows = static_cast<int>((K_even - r0 < R) ? (K_even - r0) : R);
         if (lane == 0) mbar_arrive_expect_tx(&full[s], static_cast<u32>(rows * (M + N) * S * 8));
@@ -2343,9 +2351,10 @@ constexpr int cstb_pick_rho(int M, int N, bool z) {
 // warps of the last column group (as kernel 3's edge columns) instead of a
 // padded 8-column DMMA block: D 57 costs 57 x 60 lane-FMAs per row instead of
 // 64 x 60 on the shared FP64 pipe.
-template <int M_, int N_, bool Z_, int NBW_, int WR_, int NW_, int R_, int EC_ = 0>
+template <int M_, int N_, bool Z_, int NBW_, int WR_, int NW_, int R_, int EC_ = 0, bool GA_ = false>
 struct TsmmCstbCfg {
   static constexpr int M = M_, N = N_, NBW = NBW_, WR = WR_, NW = NW_, R = R_, EC = EC_;
+  static constexpr bool GA = GA_;  // gather-capable instantiation (kernel | 8192, see TsmttsmMmaCfg)
   static constexpr bool Z = Z_;
   static_assert(EC == 0 || (EC == N % 8 && N >= 8), "edge columns: EC = N mod 8, N >= 8");
   static constexpr int S = Z ? 2 : 1;
@@ -2386,7 +2395,7 @@ __global__ void __launch_bounds__(Cfg::NT) tsmm_cstb_kernel(const __grid_constan
 
   if (tid == 0) {
     for (int s = 0; s < stages; s++) {
-      mbar_init(&full[s], p.gather ? 32 : 1);  // gather: one noinc arrival per producer lane
+      mbar_init(&full[s], (Cfg::GA && p.gather) ? 32 : 1);  // gather: one noinc arrival per producer lane
       mbar_init(&empty[s], NW);
     }
     fence_mbar_init();
@@ -2409,7 +2418,8 @@ __global__ void __launch_bounds__(Cfg::NT) tsmm_cstb_kernel(const __grid_constan
 
   if (warp == NW) {
     // ---------------- producer warp: one bulk copy per chunk of A ----------------
-    if (p.gather) {  // strided rows of A (N4): element copies by the 32 lanes, any row stride
+    if (Cfg::GA && p.gather) {  // strided rows of A (N4): element copies by the 32 lanes, any row stride
+      if constexpr (Cfg::GA) {
       Ring ring_it;
       for (long long c = blockIdx.x; c < p.nchunks; c += G, ring_it.next(stages)) {
         const int s = ring_it.s;
@@ -2418,6 +2428,7 @@ __global__ void __launch_bounds__(Cfg::NT) tsmm_cstb_kernel(const __grid_constan
         const int rows = static_cast<int>((K_even - r0 < R) ? (K_even - r0) : R);
         gather_rows<M, S>(ring + static_cast<long long>(s) * Cfg::STAGE_DOUBLES, M, p.A, r0, p.lda, rows, lane);
         cp_async_mbar_arrive_noinc(&full[s]);
+      }
       }
     } else if (lane == 0) {
       const u64 pol = policy_evict_first();
@@ -2574,7 +2585,7 @@ __global__ void __launch_bounds__(Cfg::NT) tsmm_cstb_kernel(const __grid_constan
           // the warp from the issuer-only wait.
           __syncwarp();
           asm volatile("barrier.sync %0, %1;" ::"r"(1 + rg), "r"(NG * 32) : "memory");
-          if (p.gather) {
+          if (Cfg::GA && p.gather) {
             // strided B (N4): the NG warps of the row group store the staged rows
             // element-wise (each element by one thread; update mode: B += value).
             // A buffer is rewritten two passes later, after the next pass's

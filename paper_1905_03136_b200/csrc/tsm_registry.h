@@ -23,7 +23,7 @@ struct KernelEntry {
                      // 8-aligned core, bit 1 = paired 16-byte fragment loads, bits 2-3 =
                      // edge warps - 1, bit 4 = complex-as-real, bit 5 = 3M (Gauss) complex
                      // products, bit 6 = plain warp order (launch argument), bit 7 = inline
-                     // edge, bit 8 = L-blocks (tsm_config.kernel bits 4..12)
+                     // edge, bit 8 = L-blocks, bit 9 = gather-capable (tsm_config.kernel bits 4..13)
 };
 
 // number of DFMA edge warps encoded in KernelEntry::edge
@@ -46,6 +46,10 @@ inline bool ei_flag(int flags) { return (flags & 128) != 0; }
 // MMA blocks pairing edge rows with core columns and core rows with edge
 // columns (tsm_kernels.cuh LB), instead of padded blocks
 inline bool lb_flag(int flags) { return (flags & 256) != 0; }
+
+// bit 9: the gather-capable instantiation (strided views of any row stride,
+// NEXT N4) of TSMTTSM kernel 1 / TSMM kernel 4
+inline bool ga_flag(int flags) { return (flags & 512) != 0; }
 
 // the real problem a complex-as-real entry runs (identity otherwise)
 inline KernelEntry real_view(const KernelEntry& k) {

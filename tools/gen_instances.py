@@ -406,12 +406,13 @@ def cfg_type(op, dt, M, N, c) -> str:
         return (f"tsm::TsmttsmMmaCfg<{M}, {N}, {z}, {c['MT']}, {c['NTL']}, {c['NT'] // 32 - 1 - edge}, "
                 f"{c['R']}, {c.get('AP', M)}, {c.get('BP', N)}, {tma}, {edge}, {pair}, {zr}, "
                 f"{'true' if c.get('G3', 0) else 'false'}, {'true' if c.get('EI', 0) else 'false'}, "
-                f"{'true' if c.get('LB', 0) else 'false'}>")
+                f"{'true' if c.get('LB', 0) else 'false'}, {'true' if c.get('GA', 0) else 'false'}>")
     if op == "tsmttsm":
         return f"tsm::TsmttsmCfg<{M}, {N}, {z}, {c['MT']}, {c['NTL']}, {c['NT']}, {c['R']}>"
     if c.get("impl", 0) == 4:
         ec = N % 8 if c.get("EDGE", 0) else 0
-        return f"tsm::TsmmCstbCfg<{M}, {N}, {z}, {c['NBW']}, {c['WR']}, {c['NT'] // 32 - 1}, {c['R']}, {ec}>"
+        return (f"tsm::TsmmCstbCfg<{M}, {N}, {z}, {c['NBW']}, {c['WR']}, {c['NT'] // 32 - 1}, {c['R']}, {ec}, "
+                f"{'true' if c.get('GA', 0) else 'false'}>")
     if c.get("impl", 0) == 3:
         ec = N % 8 if c.get("EDGE", 0) else 0
         return (f"tsm::TsmmCstCfg<{M}, {N}, {z}, {c['NBW']}, {c['WR']}, {c['NT'] // 32 - 1}, {c['R']}, {zr}, "
@@ -447,11 +448,12 @@ def flags(c: dict) -> int:
     plain consumer-warp order (PLAIN; a launch argument of the DMMA kernels),
     bit 7 inline edge (EI: consumer warps compute the edge strips), bit 8
     L-blocks (LB: edge strips by MMA blocks pairing edge rows with core
-    columns and core rows with edge columns)."""
+    columns and core rows with edge columns), bit 9 gather-capable
+    instantiation (GA, strided views)."""
     e = c.get("EDGE", 0)
     return ((1 if e else 0) | (c.get("PAIR", 0) << 1) | (((e - 1) & 3) << 2 if e else 0)
             | (c.get("ZR", 0) << 4) | (c.get("G3", 0) << 5) | (c.get("PLAIN", 0) << 6)
-            | (c.get("EI", 0) << 7) | (c.get("LB", 0) << 8))
+            | (c.get("EI", 0) << 7) | (c.get("LB", 0) << 8) | (c.get("GA", 0) << 9))
 
 
 def params4(op: str, M: int, N: int, c: dict) -> tuple:
@@ -713,7 +715,7 @@ def strided_capable(op: str, c: dict) -> bool:
 
 def gather_capable(op: str, c: dict) -> bool:
     """Kernels with the element-wise (cp.async) gather producer: any row stride."""
-    return c.get("impl", 0) == 1 if op == "tsmttsm" else c.get("impl", 0) == 4
+    return bool(c.get("GA")) and (c.get("impl", 0) == 1 if op == "tsmttsm" else c.get("impl", 0) == 4)
 
 
 def gather_default(op: str, M: int, N: int, z: bool, tuned: dict | None) -> dict:
@@ -721,10 +723,10 @@ def gather_default(op: str, M: int, N: int, z: bool, tuned: dict | None) -> dict
     the tuned configuration when it is gather-capable, else TSMTTSM kernel 1
     with the DMMA default tiles / TSMM kernel 4 (C-stationary, bulk)."""
     c = resolve(op, M, N, z, tuned)
-    if gather_capable(op, c):
-        return c
+    if (c.get("impl", 0) == 1 if op == "tsmttsm" else c.get("impl", 0) == 4):
+        return dict(c, GA=1)  # the tuned configuration, gather-capable instantiation
     if op == "tsmttsm":
-        d = dict(tsmttsm_mma_default(M, N, z))
+        d = dict(tsmttsm_mma_default(M, N, z), GA=1)
         if d["impl"] != 1:  # the TMA branch: same tiles, dense-stride stages
             S = 2 if z else 1
             WT = cdiv(cdiv(M, 8), d["MT"]) * cdiv(cdiv(N, 8), d["NTL"])
@@ -736,11 +738,11 @@ def gather_default(op: str, M: int, N: int, z: bool, tuned: dict | None) -> dict
     cands = tsmm_cstb_configs(M, N, z)
     if cands:
         pick = [x for x in cands if x["WR"] == 2] or cands
-        return dict(pick[0], stages=3, ctas=1)
+        return dict(pick[0], stages=3, ctas=1, GA=1)
     # N = 1: one 8-column block (7 padded columns), two row groups of one warp
     S = 2 if z else 1
     R = 32 * max(1, round(16384 / (32 * M * S * 8)))
-    return dict(NBW=1, WR=2, NT=3 * 32, R=R, impl=4, stages=3, ctas=1)
+    return dict(NBW=1, WR=2, NT=3 * 32, R=R, impl=4, stages=3, ctas=1, GA=1)
 
 
 def strided_default(op: str, M: int, N: int, z: bool, tuned: dict | None):
