@@ -359,9 +359,9 @@ static tsm_status validate_config_real(const KernelEntry& e) {
   if (ga_flag(e.edge) && !((e.op == KIND_TSMTTSM && e.impl == 1) || (e.op == KIND_TSMM && e.impl == 4)))
     return bad("the gather flag (kernel | 8192) applies to TSMTTSM kernel 1 and TSMM kernel 4");
   if (lb_flag(e.edge)) {  // L-blocks (tsm_kernels.cuh LB)
-    if (e.op != KIND_TSMTTSM || (e.impl != 1 && e.impl != 2) || e.dt != TSM_D)
-      return bad("L-blocks (kernel | 4096) apply to the real DMMA TSMTTSM kernels 1 and 2");
-    if (e.edge & (1 | 12 | 16 | 32 | 128)) return bad("L-blocks exclude edge warps, complex-as-real, 3M and inline edge");
+    if (e.op != KIND_TSMTTSM || (e.impl != 1 && e.impl != 2))
+      return bad("L-blocks (kernel | 4096) apply to the DMMA TSMTTSM kernels 1 and 2");
+    if (e.edge & (1 | 12 | 128)) return bad("L-blocks exclude edge warps and inline edge");
     const int MR = e.M % 8, NR = e.N % 8;
     if (e.M < 8 || e.N < 8 || MR < 1 || MR > 6 || NR < 1 || NR > 6)
       return bad("L-blocks need M, N >= 8 with 1..6 edge rows and columns (M, N mod 8)");

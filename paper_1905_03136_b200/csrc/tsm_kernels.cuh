@@ -804,7 +804,7 @@ struct TsmttsmMmaCfg {
   static constexpr bool DEDGE = EDGE_ > 0 || EI_;  // DFMA edge strips (edge warps or inline)
   static_assert(!(EI_ && EDGE_ > 0), "inline edge excludes edge warps");
   // (complex-as-real runs the real kernel on 2M x 2N: L-blocks apply to that product)
-  static_assert(!LB_ || (!Z_ && !G3_ && !EI_ && EDGE_ == 0), "L-blocks: real kernel, no DFMA edges");
+  static_assert(!LB_ || (!EI_ && EDGE_ == 0), "L-blocks exclude the DFMA edges");
   static_assert(!G3 || Z_, "3M (Gauss) products: complex kernel");
   static_assert(!ZR || (!Z_ && M_ % 2 == 0 && N_ % 2 == 0), "complex-as-real: real kernel on 2M x 2N");
   static_assert(!PAIR || (!Z_ && WM_ % 2 == 0 && WN_ % 2 == 0), "pairs: real, even tiles");
@@ -1163,9 +1163,11 @@ __global__ void __launch_bounds__(Cfg::NT) tsmttsm_mma_kernel(const __grid_const
   // LB: the L-blocks l = wt, wt + WT, ... of this warp's tile (one DMMA each per
   // k-step, A and B fragments gathered from the block's row / column lists)
   constexpr int NLW = Cfg::LB ? (Cfg::NL + Cfg::WT - 1) / Cfg::WT : 1;
-  double lacc[NLW][2];
+  double lacc[NLW][NA][2];  // (Z: re, im; 3M: T1, T2, T3 -- as the core blocks)
 #pragma unroll
-  for (int t = 0; t < NLW; t++) lacc[t][0] = lacc[t][1] = 0.0;
+  for (int t = 0; t < NLW; t++)
+#pragma unroll
+    for (int z = 0; z < NA; z++) lacc[t][z][0] = lacc[t][z][1] = 0.0;
   auto lstep = [&](const double* __restrict__ sA, const double* __restrict__ sB, int k0, int rows, int ap,
                    int bp) {
     constexpr int KD = Cfg::KD;
@@ -1177,9 +1179,26 @@ __global__ void __launch_bounds__(Cfg::NT) tsmttsm_mma_kernel(const __grid_const
       if (l >= Cfg::NL) break;  // (warp-uniform)
       const int mr = g < MR ? Cfg::MC + g : l * (8 - MR) + (g - MR);  // MMA row g -> m
       const int nc = g < NR ? Cfg::NC + g : l * (8 - NR) + (g - NR);  // MMA column g -> n
-      const double a = (rv && (g < MR || mr < Cfg::MC)) ? sA[off(kr, mr, ap)] : 0.0;
-      const double b = (rv && (g < NR || nc < Cfg::NC)) ? sB[off(kr, nc, bp)] : 0.0;
-      dmma(lacc[t][0], lacc[t][1], a, b);
+      const bool av = rv && (g < MR || mr < Cfg::MC), bv = rv && (g < NR || nc < Cfg::NC);
+      if constexpr (!Cfg::Z) {
+        const double a = av ? sA[off(kr, mr, ap)] : 0.0;
+        const double b = bv ? sB[off(kr, nc, bp)] : 0.0;
+        dmma(lacc[t][0][0], lacc[t][0][1], a, b);
+      } else {
+        double2 a = av ? *reinterpret_cast<const double2*>(sA + off(kr, mr, ap)) : make_double2(0.0, 0.0);
+        const double2 b = bv ? *reinterpret_cast<const double2*>(sB + off(kr, nc, bp)) : make_double2(0.0, 0.0);
+        a.y = flip_sign(a.y, p.conj);  // A^H B (N2)
+        if constexpr (Cfg::G3) {
+          dmma(lacc[t][0][0], lacc[t][0][1], a.x, b.x);              // T1 += ar br
+          dmma(lacc[t][1][0], lacc[t][1][1], a.y, b.y);              // T2 += ai bi
+          dmma(lacc[t][2][0], lacc[t][2][1], a.x + a.y, b.x + b.y);  // T3 += (ar+ai)(br+bi)
+        } else {
+          dmma(lacc[t][0][0], lacc[t][0][1], a.x, b.x);   // re += ar br
+          dmma(lacc[t][0][0], lacc[t][0][1], -a.y, b.y);  // re -= ai bi
+          dmma(lacc[t][1][0], lacc[t][1][1], a.x, b.y);   // im += ar bi
+          dmma(lacc[t][1][0], lacc[t][1][1], a.y, b.x);   // im += ai br
+        }
+      }
     }
   };
 
@@ -1382,8 +1401,19 @@ __global__ void __launch_bounds__(Cfg::NT) tsmttsm_mma_kernel(const __grid_const
               n = m < Cfg::MC ? Cfg::NC + j : -1;
             }
             if (n >= 0) {
-              const int idx = m * N + n;
-              sP[idx] = (sl == 0) ? lacc[t][e] : sP[idx] + lacc[t][e];
+              double v[S];
+              if constexpr (Cfg::G3) {  // re = T1 - T2, im = T3 - T1 - T2
+                v[0] = lacc[t][0][e] - lacc[t][1][e];
+                v[S - 1] = lacc[t][2][e] - lacc[t][0][e] - lacc[t][1][e];
+              } else {
+#pragma unroll
+                for (int z = 0; z < S; z++) v[z] = lacc[t][z][e];
+              }
+#pragma unroll
+              for (int z = 0; z < S; z++) {
+                const int idx = (m * N + n) * S + z;
+                sP[idx] = (sl == 0) ? v[z] : sP[idx] + v[z];
+              }
             }
           }
         }

@@ -576,3 +576,41 @@ def test_tsmttsm_zr_lblocks(tsm, M, N, conj):
         torch.cuda.synchronize()
         assert np.array_equal(got.cpu().numpy(), oracle.tsmttsm(Ai, Bi, conj=conj)[0]), (key, c)
     assert ran
+
+
+@pytest.mark.parametrize("conj", [False, True], ids=["T", "H"])
+@pytest.mark.parametrize("M,N", [(17, 17), (33, 33), (57, 57), (9, 9), (25, 41)])
+def test_tsmttsm_z_lblocks(tsm, M, N, conj):
+    """Native complex TSMTTSM with L-blocks (kernel | 4096): the 4-DMMA and
+    the 3M (kernel | 512) forms, bulk / TMA, plain and conjugate, ragged K
+    within the 1e-12 |A|^T|B| tolerance, integer inputs bit-exact."""
+    base = [c for c in gi.candidates("tsmttsm", M, N, True) if c.get("LB") and not c.get("ZR")]
+    if not base:
+        pytest.skip("no native complex L-block candidate")
+    picked = {}
+    for c in base:
+        picked.setdefault((c.get("impl"), c.get("G3", 0)), c)
+    ran = 0
+    for key, c in sorted(picked.items()):
+        try:
+            plan = tsm.Plan("tsmttsm", "z", M, N, 0, config=gi.to_tsm_config("tsmttsm", c, 3, 1), conj=conj)
+        except tsm.TsmError as e:
+            if e.status != 2:
+                raise
+            continue
+        assert "l-blocks" in plan.describe(1000)["kernel"]
+        ran += 1
+        for K in (1, 7, 4099, 65537):
+            A = ti.matrix(K, M, "A", complex_=True, seed=K + 95)
+            B = ti.matrix(K, N, "B", complex_=True, seed=K + 96)
+            got = tsm.tsmttsm(torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda(), plan=plan, conj=conj)
+            torch.cuda.synchronize()
+            ref, bound = oracle.tsmttsm(A, B, conj=conj)
+            r, wi, _ = oracle.max_err_ratio(got.cpu().numpy(), ref, bound)
+            assert r <= 1e-12, (M, N, key, c, K, r, wi)
+        Ai = ti.matrix(30001, M, "A", complex_=True, mode="int")
+        Bi = ti.matrix(30001, N, "B", complex_=True, mode="int")
+        got = tsm.tsmttsm(torch.from_numpy(Ai).cuda(), torch.from_numpy(Bi).cuda(), plan=plan, conj=conj)
+        torch.cuda.synchronize()
+        assert np.array_equal(got.cpu().numpy(), oracle.tsmttsm(Ai, Bi, conj=conj)[0]), (key, c)
+    assert ran

@@ -183,10 +183,10 @@ def edge_candidates(M: int, N: int, z: bool) -> list:
 
 
 def lblock_candidates(M: int, N: int, z: bool) -> list:
-    """LB=1 (D): the core tilings of the inline-edge search with the edge
+    """LB=1: the core tilings of the inline-edge search with the edge
     strips on L-blocks (tsm_kernels.cuh LB) -- only where they need fewer MMA
     blocks than the padded tiling."""
-    if z or M < 8 or N < 8 or not (1 <= M % 8 <= 6 and 1 <= N % 8 <= 6):
+    if M < 8 or N < 8 or not (1 <= M % 8 <= 6 and 1 <= N % 8 <= 6):
         return []
     MR, NR = M % 8, N % 8
     MC, NC = M - MR, N - NR
