@@ -490,9 +490,22 @@ static tsm_status make_plan(tsm_plan* out, const KernelEntry& want, int device, 
   size_t smem = smem_bytes(*k, stages);
   while (smem > di.smem_optin && stages > 2) smem = smem_bytes(*k, --stages);
   if (smem > di.smem_optin) return fail(TSM_ERR_UNSUPPORTED, "shared memory request too large");
-  cudaError_t e = cudaFuncSetAttribute(k->func, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(smem));
-  if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(MaxDynamicSharedMemorySize)");
+  // The attribute belongs to the kernel function, which plans with other run-time
+  // parameters (stages) share: only ever raise it.  Setting it per plan let a
+  // later plan with fewer stages lower the limit under an earlier one, whose
+  // launches then failed with "invalid argument" (GPU suite, run 12).
+  cudaError_t e;
+  {
+    static std::mutex mu;
+    std::lock_guard<std::mutex> lk(mu);
+    cudaFuncAttributes fa{};
+    e = cudaFuncGetAttributes(&fa, k->func);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaFuncGetAttributes");
+    if (static_cast<size_t>(fa.maxDynamicSharedSizeBytes) < smem) {
+      e = cudaFuncSetAttribute(k->func, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+      if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(MaxDynamicSharedMemorySize)");
+    }
+  }
   int occ = 0;
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k->func, k->NT, smem);
   if (e != cudaSuccess) return cuda_fail(e, "cudaOccupancyMaxActiveBlocksPerMultiprocessor");

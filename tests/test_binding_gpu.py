@@ -70,3 +70,26 @@ def test_update_and_cgs_reject_mismatches(tsm):
         tsm.cgs_step(A, B, p_tt=tsm.get_plan("tsmttsm", "d", 8, 8, 0))
     with pytest.raises(ValueError, match="plan"):
         tsm.cgs_step(A, B, p_mm=tsm.get_plan("tsmttsm", "d", 8, 5, 0))
+
+
+def test_shared_kernel_smem_attribute_only_grows():
+    """Plans with the same kernel function but different run-time stages share
+    the function's max-dynamic-shared-memory attribute: a later plan with
+    fewer stages must not lower it under an earlier plan (GPU suite run 12:
+    'cudaLaunchKernel: invalid argument' on the earlier plan)."""
+    import numpy as np
+    import oracle
+    import tsminputs as ti
+    from paper_1905_03136_b200 import binding as tsm
+    cfg = dict(threads=288, rows_per_chunk=64, p0=2, p1=2, p2=24, p3=24, stages=6, ctas_per_sm=1, kernel=1, p3_=0)
+    cfg.pop("p3_")
+    big = tsm.Plan("tsmttsm", "d", 24, 24, 0, config=cfg)
+    small = tsm.Plan("tsmttsm", "d", 24, 24, 0, config=dict(cfg, stages=2))
+    assert big.config()["stages"] > small.config()["stages"]
+    A = ti.matrix(100003, 24, "A")
+    B = ti.matrix(100003, 24, "B")
+    for plan in (big, small, big):
+        got = tsm.tsmttsm(torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda(), plan=plan).cpu().numpy()
+        ref, bound = oracle.tsmttsm(A, B)
+        assert oracle.max_err_ratio(got, ref, bound)[0] <= 1e-12
+    assert np.isfinite(got).all()
