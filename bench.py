@@ -406,7 +406,7 @@ class Ctx:
             pk["fp64_tflops"] = probe / 1e12
             pk["fp64_source"] = "probe"
 
-    def row(self, op, z, M, N, K, ms, kname=""):
+    def row(self, op, z, M, N, K, ms, kname="", mhz=None):
         """Per-kernel roofline row: % of min(b_s * I, P_fp64)."""
         pk = self.peaks
         b, f = sizes(op, M, N, K, z)
@@ -418,6 +418,11 @@ class Ctx:
         r = {"op": op, "dtype": "z" if z else "d", "M": M, "N": N, "K": K, "ms": ms, "gbs": b / t / 1e9,
              "gflops": f / t / 1e9, "bound": "hbm" if t_hbm >= t_fp else "fp64", "frac": roof / t,
              "kernel": kname}
+        if mhz:  # the FP64 roof at the clock measured right after this kernel (sweep rows)
+            Pk = min(pk["dmma_tflops"] * 1e12, SMS * FMA_PER_CLK_SM * 2 * mhz * 1e6)
+            fexec = f * (0.75 if (z and "3m" in kname) else 1.0)
+            r["frac_at_kernel_clock"] = max(t_hbm, fexec / Pk) / t
+            r["sm_mhz_after"] = mhz
         if z and "3m" in kname:  # 3M / Gauss: 6 executed real flops per complex MAC (R12)
             r["frac_exec"] = max(t_hbm, 0.75 * t_fp) / t
             r["bound_exec"] = "hbm" if t_hbm >= 0.75 * t_fp else "fp64"
@@ -428,7 +433,10 @@ def summarize(rows):
     fr = [r.get("frac_exec", r["frac"]) for r in rows]
     fp = [r["frac"] for r in rows]
     worst = min(rows, key=lambda r: r.get("frac_exec", r["frac"]))
-    return {"shapes": len(rows), "mean_frac": sum(fr) / len(fr), "min_frac": min(fr),
+    fc = [r["frac_at_kernel_clock"] for r in rows if "frac_at_kernel_clock" in r]
+    extra = {"mean_frac_at_kernel_clock": sum(fc) / len(fc), "min_frac_at_kernel_clock": min(fc),
+             "sm_mhz_after_kernels_min": min(r["sm_mhz_after"] for r in rows if "sm_mhz_after" in r)} if fc else {}
+    return {**extra, "shapes": len(rows), "mean_frac": sum(fr) / len(fr), "min_frac": min(fr),
             "n_ge_90": sum(1 for x in fr if x >= 0.9),
             "mean_frac_paper_flops": sum(fp) / len(fp), "min_frac_paper_flops": min(fp),
             "worst": f"{worst['op']}_{worst['dtype']} {worst['M']}x{worst['N']} K={worst['K']} "
@@ -456,8 +464,18 @@ def sweep(ctx, raw, z, widths, K, steps, warmup):
         else:
             calls.append(lambda a=a, M=M: ctx.launch("tsmm", z, M, M, K, a, ctx.view(O, z, K, M), Cs[M]))
     per, step_ms = ctx.timed(calls, steps, warmup)
-    rows = [ctx.row(op, z, M, N, K, ms, ctx.plan(op, dt, M, N).describe(K).get("kernel", ""))
-            for (op, _, M, N, _), ms in zip(items, per)]
+    # untimed pass: the SM clock right after every kernel of the step (a 1-thread
+    # probe counting cycles over 2 us of globaltimer) -- the clock the FP64-bound
+    # kernels actually ran at under the power cap
+    for _ in range(2):
+        clk = ctx.torch.zeros(2 * len(calls), dtype=ctx.torch.float64, device=ctx.dev)
+        for i, c in enumerate(calls):
+            c()
+            ctx.tsm.probe("clock", clk[2 * i:].data_ptr(), 16, 2000, ctx.s_ptr)
+        ctx.torch.cuda.synchronize()
+    mhzs = clk[0::2].cpu().tolist()
+    rows = [ctx.row(op, z, M, N, K, ms, ctx.plan(op, dt, M, N).describe(K).get("kernel", ""), mhz)
+            for (op, _, M, N, _), ms, mhz in zip(items, per, mhzs)]
     byts = sum(sizes(op, M, N, K, z)[0] for (op, _, M, N, _) in items)
     return rows, step_ms, byts, Cs
 
@@ -714,7 +732,7 @@ def main():
     clk = clocks.stop()
     ctx.set_fp64_peak(clk.get("sm_mhz"))
     # rows were computed before the clock was known: recompute with the final peak
-    rows = [ctx.row(r["op"], z, r["M"], r["N"], r["K"], r["ms"], r["kernel"]) for r in rows]
+    rows = [ctx.row(r["op"], z, r["M"], r["N"], r["K"], r["ms"], r["kernel"], r.get("sm_mhz_after")) for r in rows]
     tot_k = sum(r["ms"] for r in rows)
     for r in rows:
         r["share"] = r["ms"] / tot_k

@@ -344,6 +344,7 @@ tsm_status tsm_l2_flush(void *scratch, size_t bytes, tsm_stream stream);
 #define TSM_PROBE_READ 0
 #define TSM_PROBE_COPY 1
 #define TSM_PROBE_DMMA 2
+#define TSM_PROBE_CLOCK 3 /* one thread: SM cycles over `iters` ns of globaltimer -> MHz in buf[0] */
 tsm_status tsm_probe(int kind, void *buf, size_t bytes, int64_t iters, tsm_stream stream, double *work);
 
 /* ------------------------------------------------------------------------ */

@@ -237,7 +237,7 @@ def tsm_l2_flush(scratch, nbytes, stream):
     check(lib.tsm_l2_flush(scratch, nbytes, stream), "tsm_l2_flush")
 
 
-PROBE = {"read": 0, "copy": 1, "dmma": 2}
+PROBE = {"read": 0, "copy": 1, "dmma": 2, "clock": 3}
 
 
 def probe(kind: str, buf, nbytes: int, iters: int, stream) -> float:

@@ -258,6 +258,19 @@ __global__ void probe_dmma_kernel(double* sink, long long iters) {
   if (s == 1.2345678e300) sink[0] = s;
 }
 
+// SM clock right now: one thread counts SM cycles (clock64) over ~window_ns of
+// wall time (globaltimer) and writes the rate in MHz to out[0].
+__global__ void probe_clock_kernel(double* out, long long window_ns) {
+  unsigned long long t0, t1;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  const long long c0 = clock64();
+  do {
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+  } while (static_cast<long long>(t1 - t0) < window_ns);
+  const long long c1 = clock64();
+  out[0] = 1e3 * static_cast<double>(c1 - c0) / static_cast<double>(t1 - t0);
+}
+
 }  // namespace tsm
 
 using namespace tsm;
@@ -1138,6 +1151,11 @@ tsm_status tsm_probe(int kind, void* buf, size_t bytes, int64_t iters, tsm_strea
       probe_dmma_kernel<<<di.sms * 8, 128, 0, s>>>(static_cast<double*>(buf), iters);
       // 8 mma per iteration per warp, 8x8x4 FMAs = 256 FMA = 512 flops each
       *work = static_cast<double>(di.sms) * 8 * 4 * static_cast<double>(iters) * 8 * 512.0;
+      break;
+    case TSM_PROBE_CLOCK:
+      if (iters < 1) return fail(TSM_ERR_INVALID_VALUE, "iters (window in ns) must be >= 1");
+      probe_clock_kernel<<<1, 1, 0, s>>>(static_cast<double*>(buf), iters);
+      *work = static_cast<double>(iters);
       break;
     default:
       return fail(TSM_ERR_INVALID_VALUE, "unknown probe kind");
