@@ -295,3 +295,62 @@ def test_flag_encoding_and_new_candidates():
     assert not [c for c in gi.candidates("tsmttsm", 32, 32, False) if c.get("G3")]
     assert [c for c in gi.candidates("tsmttsm", 32, 32, True) if c.get("G3")]
     assert [c for c in gi.candidates("tsmm", 32, 32, True) if c.get("G3")]
+
+
+def _lblock_cells(M, N, WT=1):
+    """Mirror of tsm_kernels.cuh L-blocks: the cells each L-block's epilogue
+    writes (MMA row g, columns 2q + e) and the A / B columns its fragments read."""
+    MR, NR = M % 8, N % 8
+    MC, NC = M - MR, N - NR
+    NL = max(-(-MC // (8 - MR)), -(-NC // (8 - NR)))
+    writes = []
+    for l in range(NL):
+        for g in range(8):
+            for j in range(8):
+                if g < MR:
+                    m = MC + g
+                    n = (NC + j if l == 0 else -1) if j < NR else l * (8 - NR) + (j - NR)
+                    if n >= NC and j >= NR:
+                        n = -1
+                elif j < NR:
+                    m = l * (8 - MR) + (g - MR)
+                    n = NC + j if m < MC else -1
+                else:
+                    n = -1
+                if n >= 0:
+                    writes.append((m, n))
+    return NL, writes
+
+
+def test_lblock_mapping_covers_every_edge_cell_once():
+    """L-blocks (kernel | 4096): for every M, N >= 8 with 1..6 edge rows and
+    columns, the blocks' epilogues write every cell outside the 8-aligned core
+    exactly once and no core cell; the block count matches the kernel's NL and
+    the generator only offers them where they need fewer MMA blocks than
+    padding."""
+    for M in range(9, 65):
+        for N in range(9, 65):
+            MR, NR = M % 8, N % 8
+            if not (1 <= MR <= 6 and 1 <= NR <= 6):
+                continue
+            NL, writes = _lblock_cells(M, N)
+            MC, NC = M - MR, N - NR
+            edge = {(m, n) for m in range(M) for n in range(N) if m >= MC or n >= NC}
+            assert len(writes) == len(set(writes)), (M, N)
+            assert set(writes) == edge, (M, N)
+            pays = (MC // 8) * (NC // 8) + NL < -(-M // 8) * -(-N // 8)
+            offered = bool([c for c in gi.lblock_candidates(M, N, False)])
+            assert offered == (pays and bool(gi.inline_edge_candidates(M, N, False))), (M, N)
+
+
+def test_gather_defaults_exist_for_every_shape():
+    """TSM_FLAG_GATHER: every (op, dtype, M, N) has a gather-capable default
+    (TSMTTSM kernel 1 / TSMM kernel 4 with the GA flag), and TSM_FLAG_STRIDED
+    falls back to it wherever the shape has no TMA kernel."""
+    for op in ("tsmttsm", "tsmm"):
+        for z in (False, True):
+            for (M, N) in [(1, 1), (1, 64), (64, 1), (3, 5), (7, 9), (33, 33), (57, 57), (64, 64), (16, 48)]:
+                c = gi.gather_default(op, M, N, z, None)
+                assert c.get("GA") == 1 and gi.gather_capable(op, c), (op, z, M, N, c)
+                s = gi.strided_default(op, M, N, z, None)
+                assert s is not None and (gi.strided_capable(op, s) or gi.gather_capable(op, s)), (op, z, M, N)
