@@ -511,7 +511,15 @@ def nonsquare(ctx, raw, steps, warmup):
 
 def config0(ctx, raw, reps):
     """configs[0]: TSMTTSM D M=N=8, K=10^6 (128 MB, about the L2 size): the L2
-    is flushed (a 2 x L2 write) before every timed call."""
+    is flushed before every timed call, two ways:
+      * "clean" (the row's ms / frac): write 2 x L2 of scratch, then read its
+        first L2 bytes, so L2 ends up full of CLEAN lines that hold none of
+        the kernel's inputs;
+      * "dirty" (ms_dirty_flush / frac_dirty_flush): the 2 x L2 write only.
+        The timed call then also pays the write-back of ~L2 bytes of the
+        flush kernel's dirty lines as its reads evict them -- a cost of the
+        flush, not of the TSMTTSM (libtsm's read probe over the same 128 MB
+        shows the same ~15 us, profiles/r02_smallk_run3.md)."""
     A, B, O = raw
     K, M = 10 ** 6, 8
     ctx.fill(A, False, "A", K * M)
@@ -521,13 +529,28 @@ def config0(ctx, raw, reps):
     l2 = ctx.torch.cuda.get_device_properties(ctx.dev).L2_cache_size
     scratch = O.view(ctx.torch.float64)[: 2 * l2 // 8]
 
-    def flush():
+    def flush_dirty():
         ctx.tsm.tsm_l2_flush(scratch.data_ptr(), scratch.numel() * 8, ctx.s_ptr)
+
+    def flush_clean():
+        flush_dirty()
+        ctx.tsm.probe("read", scratch.data_ptr(), (l2 // 4096) * 4096, 1, ctx.s_ptr)
     calls = [lambda: ctx.launch("tsmttsm", False, M, M, K, ctx.view(A, False, K, M), ctx.view(B, False, K, M), C,
                                 use_comm=False)]
-    per, _ = ctx.timed(calls, reps, 3, flush=flush)
-    r = ctx.row("tsmttsm", False, M, M, K, per[0], ctx.plan("tsmttsm", "d", M, M).describe(K).get("kernel", ""))
-    r["l2"] = "flushed before every call"
+    kname = ctx.plan("tsmttsm", "d", M, M).describe(K).get("kernel", "")
+    per, _ = ctx.timed(calls, reps, 3, flush=flush_clean)
+    r = ctx.row("tsmttsm", False, M, M, K, per[0], kname)
+    per_d, _ = ctx.timed(calls, reps, 3, flush=flush_dirty)
+    rd = ctx.row("tsmttsm", False, M, M, K, per_d[0], kname)
+    r["ms_dirty_flush"], r["frac_dirty_flush"] = rd["ms"], rd["frac"]
+    # the floor of one cold launch over these bytes: libtsm's read-only probe
+    # over 128 MB (the bytes of A and B) after the same clean flush
+    nb = 2 * K * M * 8
+    per_p, _ = ctx.timed([lambda: ctx.tsm.probe("read", A.data_ptr(), nb, 1, ctx.s_ptr)], reps, 3,
+                         flush=flush_clean)
+    r["read_probe_ms"] = per_p[0]
+    r["frac_of_read_probe"] = per_p[0] / r["ms"]
+    r["l2"] = "flushed before every call: 2 x L2 write + 1 x L2 read (clean lines); *_dirty_flush: write only"
     return r
 
 
@@ -745,7 +768,9 @@ def main():
                     "peak_source": f"in-run probe ({'read-only' if dom['op'] == 'tsmttsm' else 'copy'})"}
     else:
         fexec = f * (0.75 if "3m" in dom["kernel"] else 1.0)
-        roofline = {"bound": "alu", "achieved": fexec / (dom["ms"] * 1e-3) / 1e12, "peak": pk["fp64_tflops"],
+        # DMMA (mma.sync m8n8k4 f64) is the FP64 tensor-core contraction: the
+        # peak is its own dtype's, the in-run DMMA probe at the timed clock
+        roofline = {"bound": "tensor", "achieved": fexec / (dom["ms"] * 1e-3) / 1e12, "peak": pk["fp64_tflops"],
                     "unit": "TFLOP/s",
                     "peak_source": (f"FP64 (DMMA) peak = min(in-run probe {pk['dmma_tflops']:.2f} TFLOP/s, "
                                     f"148 SM x 64 FMA/clk x 2 x {pk.get('fp64_sm_mhz')} MHz median SM clock "
@@ -791,7 +816,8 @@ def main():
                                                                          for r in nrows])
         c0 = config0(ctx, raw, 20)
         report["config0"] = c0
-        subs["configs0"] = {k: c0[k] for k in ("ms", "gbs", "frac", "bound", "kernel", "l2")}
+        subs["configs0"] = {k: c0[k] for k in ("ms", "gbs", "frac", "bound", "kernel", "l2", "ms_dirty_flush",
+                                                 "frac_dirty_flush", "read_probe_ms", "frac_of_read_probe")}
     if args.report and rank == 0:
         json.dump({"line": line, "kernels": report}, open(args.report, "w"), indent=1)
 

@@ -445,13 +445,20 @@ __device__ __forceinline__ void grid_reduce(const TsmttsmArgs& p, const double* 
   const int t = static_cast<int>(s_ticket);
   if (t < G - nfin) return;
   const int f = t - (G - nfin);
+  const PeerArgs& pq = p.peer;
+  // A single finisher (nfin == 1) holds ticket G-1: every block has published
+  // its partial already (fence before its ticket), so it needs no wait -- an
+  // acquire fence orders its partial reads after the ticket.
+  const bool solo = nfin == 1 && pq.nranks == 0;
   if (tid == 0) {
-    while (ld_acquire_gpu(&p.counters[0]) < static_cast<u32>(G)) __nanosleep(64);
+    if (solo)
+      __threadfence();
+    else
+      while (ld_acquire_gpu(&p.counters[0]) < static_cast<u32>(G)) __nanosleep(64);
   }
   __syncthreads();
   // finisher f owns cells [c0, c1); TPC threads per cell split the block
   // range into contiguous segments, combined afterwards in segment order.
-  const PeerArgs& pq = p.peer;
   // N3 fail-fast: an earlier fused call on this rank timed out or saw a foreign
   // sequence number -> no stores to peers, no arrivals, C = NaN (tsm_peer_reset)
   __shared__ int s_failed;
@@ -504,7 +511,15 @@ __device__ __forceinline__ void grid_reduce(const TsmttsmArgs& p, const double* 
       }
     }
   }
-  if (pq.nranks == 0) __threadfence();
+  if (solo) {
+    // reset for the next call: no other block touches the counters again in
+    // this launch, and the launch boundary orders the store before the next one
+    if (tid == 0) p.counters[0] = 0;
+    return;
+  }
+  // (single GPU: C needs no fence -- the launch boundary publishes it; the
+  // counter reset only has to follow every finisher's wait, which the
+  // counters[1] atomics order)
   __syncthreads();
   if (tid == 0) {
     // N3: one system-scope fence per block after the CTA barrier (cumulative over

@@ -197,6 +197,28 @@ def test_workspace_reuse_across_shapes(tsm):
         check_tsmttsm(tsm, K, M, N, False)
 
 
+def test_grid_reduce_solo_and_multi_finisher(tsm):
+    # T4 has two finishing schemes: one finisher (nfin == 1, ticket G-1: no wait,
+    # plain counter reset) and several (spin on the ticket counter, reset by
+    # the last of them).  Alternate them on one cached workspace, repeat each
+    # call, and check every result against the oracle and bitwise repeatability.
+    seen = set()
+    cases = [(4, 4, 1 << 20), (8, 8, 1000003), (4, 4, 9999), (8, 8, 4099), (1, 1, 300001),
+             (32, 32, 200001), (4, 4, 1 << 20), (64, 64, 70001)]
+    for (M, N, K) in cases:
+        nfin = tsm.Plan("tsmttsm", "d", M, N).describe(K)["nfin"]
+        seen.add("solo" if nfin == 1 else "multi")
+        A = ti.matrix(K, M, "A")
+        B = ti.matrix(K, N, "B")
+        got = [run_tsmttsm(tsm, A, B) for _ in range(3)]
+        ref, bound = oracle.tsmttsm(A, B)
+        for g in got:
+            r, wi, _ = oracle.max_err_ratio(g, ref, bound)
+            assert r <= TOL_TSMTTSM, f"M={M} N={N} K={K} nfin={nfin}: err/bound {r:.3e} at {wi}"
+            assert np.array_equal(g, got[0]), f"M={M} N={N} K={K} nfin={nfin}: not repeatable"
+    assert seen == {"solo", "multi"}, seen
+
+
 # ---------------------------------------------------------------------------
 # Shapes outside the AOT set: NVRTC run-time instantiation of the same
 # templates; explicit configurations (the autotuner's search space).

@@ -71,7 +71,8 @@ def main():
     res = {"after_flush": timed(lambda: tsm.tsm_l2_flush(flush.data_ptr(), flush.numel(), s)),
            "after_heavy": timed(heavy),
            "after_heavy_and_2ms_pause": timed(pause_after_heavy),
-           "after_read_flush": timed(lambda: tsm.probe("read", flush.data_ptr(), flush.numel(), 1, s))}
+           "after_read_flush": timed(lambda: tsm.probe("read", flush.data_ptr(), flush.numel(), 1, s)),
+           "after_itself": timed(light)}
     print({k: round(v, 4) for k, v in res.items()}, f"light {a.light} heavy {a.heavy} dtype {a.dtype}")
 
 
