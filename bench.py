@@ -423,10 +423,41 @@ class Ctx:
             fexec = f * (0.75 if (z and "3m" in kname) else 1.0)
             r["frac_at_kernel_clock"] = max(t_hbm, fexec / Pk) / t
             r["sm_mhz_after"] = mhz
+            # the same roofline with the work the kernel executes (tile padding
+            # included): how close the kernel runs to what its tiling allows
+            tw = tile_work(op, M, N, z, kname)
+            r["tile_work"] = tw
+            r["frac_of_executed"] = max(t_hbm, tw * fexec / Pk) / t
         if z and "3m" in kname:  # 3M / Gauss: 6 executed real flops per complex MAC (R12)
             r["frac_exec"] = max(t_hbm, 0.75 * t_fp) / t
             r["bound_exec"] = "hbm" if t_hbm >= 0.75 * t_fp else "fp64"
         return r
+
+
+def tile_work(op, M, N, z, kname):
+    """Multiply-adds the kernel executes per row, padding included, over the
+    useful M*N (the 'tile ceiling' of DESIGN.md §5b: DMMA works on 8 x 8 blocks
+    of C (TSMTTSM) / 4-deep k-steps x 8-column blocks (TSMM); the DFMA edge
+    cells are useful work on the same FP64 pipe).  1.0 for the DFMA kernels."""
+    if "dmma" not in kname:
+        return 1.0
+    if "complex-as-real" in kname:
+        M, N = 2 * M, 2 * N  # the real kernel on the interleaved view (4 real MACs per complex one)
+    cd = lambda a, b: -(-a // b)  # noqa: E731
+    if op == "tsmttsm":
+        MC, NC = 8 * (M // 8), 8 * (N // 8)
+        if "l-blocks" in kname:
+            er, ec = M - MC, N - NC
+            nl = max(cd(MC, 8 - er), cd(NC, 8 - ec))
+            work = 64 * ((MC // 8) * (NC // 8) + nl)
+        elif "edge" in kname:  # DFMA edge warps / inline edge: the edge cells unpadded
+            work = MC * NC + (M * N - MC * NC)
+        else:
+            work = 64 * cd(M, 8) * cd(N, 8)
+    else:
+        ec = N % 8 if "edge-columns" in kname else 0
+        work = 4 * cd(M, 4) * 8 * cd(N - ec, 8) + M * ec
+    return work / (M * N)
 
 
 def summarize(rows):
@@ -434,7 +465,9 @@ def summarize(rows):
     fp = [r["frac"] for r in rows]
     worst = min(rows, key=lambda r: r.get("frac_exec", r["frac"]))
     fc = [r["frac_at_kernel_clock"] for r in rows if "frac_at_kernel_clock" in r]
+    fe = [r["frac_of_executed"] for r in rows if "frac_of_executed" in r]
     extra = {"mean_frac_at_kernel_clock": sum(fc) / len(fc), "min_frac_at_kernel_clock": min(fc),
+             "mean_frac_of_executed": sum(fe) / len(fe), "min_frac_of_executed": min(fe),
              "sm_mhz_after_kernels_min": min(r["sm_mhz_after"] for r in rows if "sm_mhz_after" in r)} if fc else {}
     return {**extra, "shapes": len(rows), "mean_frac": sum(fr) / len(fr), "min_frac": min(fr),
             "n_ge_90": sum(1 for x in fr if x >= 0.9),

@@ -9,15 +9,17 @@ import sys
 
 def table(rows, title):
     out = [f"## {title}", "", "| op | dtype | M | N | K | ms | GB/s | GFLOP/s | bound | % roofline | "
-           "% exec. roofline | SM MHz after | % at that clock | kernel |",
-           "|---|---|---|---|---|---|---|---|---|---|---|---|---|---|"]
+           "% exec. roofline | SM MHz after | % at that clock | tile work | % of executed | kernel |",
+           "|---|---|---|---|---|---|---|---|---|---|---|---|---|---|---|---|"]
     for r in rows:
         fe = r.get("frac_exec")
         mz, fk = r.get("sm_mhz_after"), r.get("frac_at_kernel_clock")
+        tw, fx = r.get("tile_work"), r.get("frac_of_executed")
         out.append(f"| {r['op']} | {r['dtype'].upper()} | {r['M']} | {r['N']} | 2^{int(r['K']).bit_length() - 1} "
                    f"| {r['ms']:.3f} | {r['gbs']:.0f} | {r['gflops']:.0f} | {r['bound']} | {100 * r['frac']:.1f} | "
                    f"{'' if fe is None else f'{100 * fe:.1f}'} | {'' if mz is None else f'{mz:.0f}'} | "
-                   f"{'' if fk is None else f'{100 * fk:.1f}'} | {r['kernel']} |")
+                   f"{'' if fk is None else f'{100 * fk:.1f}'} | {'' if tw is None else f'{tw:.3f}'} | "
+                   f"{'' if fx is None else f'{100 * fx:.1f}'} | {r['kernel']} |")
     return out
 
 
@@ -54,7 +56,9 @@ def main():
            "Per-kernel times are the median over the timed steps of back-to-back kernels (no flush between "
            "kernels; configs[0] flushed). 'SM MHz after': the clock a 1-thread probe measured right after the "
            "kernel in an untimed pass of the same sequence; '% at that clock': the roofline with the FP64 peak "
-           "at that clock.", "", "band minimum / mean (% of roofline; 3M: executed):", ""]
+           "at that clock; 'tile work': multiply-adds executed per useful one (8 x 8 DMMA blocks / 4-deep k-steps, "
+           "padding included; bench.py tile_work); '% of executed': the roofline at that clock with the executed "
+           "work -- how close the kernel runs to what its tiling allows.", "", "band minimum / mean (% of roofline; 3M: executed):", ""]
     allrows = list(k.get("sweep", [])) + list(k.get("z_sweep", []))
     body = bands(allrows) + [""]
     body += table(k.get("sweep", []), "D sweep (headline step)") + [""]
