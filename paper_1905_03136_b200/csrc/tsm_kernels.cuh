@@ -727,6 +727,13 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
                : "+d"(d0), "+d"(d1)
                : "d"(a), "d"(b));
 }
+// a + b evaluated where it stands (volatile asm: the compiler neither hoists it
+// out of a loop nor keeps it live across iterations)
+__device__ __forceinline__ double dadd_here(double a, double b) {
+  double r;
+  asm volatile("add.rn.f64 %0, %1, %2;" : "=d"(r) : "d"(a), "d"(b));
+  return r;
+}
 __device__ __forceinline__ void mbar_arrive(u64* bar) {
   asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar))
                : "memory");
@@ -2064,6 +2071,18 @@ struct TsmmCstCfg {
   static constexpr int NBL = NB - (NG - 1) * NBW;   // DMMA blocks of the last column group
   static constexpr int OBL = ((8 * NBL + EC) * S + 15) / 16;  // its boxes (incl. edge columns)
   static constexpr int NT = (NW + 1) * 32;
+  // 3M C slices: Re c, Im c and Re c + Im c are MK x NBW x 3 doubles per lane.
+  // When they and the accumulators do not fit the registers ptxas grants a
+  // thread under __launch_bounds__(NT) (65536 over NT rounded up to 128
+  // threads, in steps of 8: 96 at NT = 544), the sum is recomputed per k-step
+  // (one DADD per block, FP64 pipe) instead of kept: ptxas otherwise spills the
+  // slice to local memory inside the k-loop (Z 64, NW 16: 192 -> 32 B of
+  // spill stores, Z 57 WR 2: 276 -> 168 B; long_sb 12 % of the stall
+  // samples of Z 64, ncu run 13).
+  static constexpr int CF_REGS = MK * NBW * 3 * 2, ACC_REGS = WR * NBW * 3 * 4;
+  static constexpr int REG_BUDGET = (65536 / (((NT + 127) / 128) * 128)) & ~7;
+  static constexpr bool G3R = G3 && CF_REGS + ACC_REGS + 40 > REG_BUDGET;
+  static constexpr int NCF = G3 ? (G3R ? 2 : 3) : S;  // C fragments held per block
   static constexpr int STAGE_DOUBLES = R * NBA * 16;
   static constexpr int OUT_DOUBLES = (OB > OBL ? OB : OBL) * RW * 16;  // per warp
   static constexpr int CE_DOUBLES = ((MK * 4 * EC * S + 127) / 128) * 128;  // edge C' in smem
@@ -2150,7 +2169,7 @@ __global__ void __launch_bounds__(Cfg::NT) tsmm_cst_kernel(const __grid_constant
     double* stg = sOut + warp * Cfg::OUT_DOUBLES;
     // this warp's C slice as MMA-B fragments: lane holds C[4ks+q][8(nb0+j)+g]
     // (3M: Re c, Im c, Re c + Im c)
-    double cf[MK][NBW][NA];
+    double cf[MK][NBW][Cfg::NCF];
 #pragma unroll
     for (int ks = 0; ks < MK; ks++)
 #pragma unroll
@@ -2172,7 +2191,7 @@ __global__ void __launch_bounds__(Cfg::NT) tsmm_cst_kernel(const __grid_constant
           for (int z = 0; z < S; z++) cf[ks][j][z] = (m < M && n < N) ? __ldg(&p.C[(m * N + n) * S + z]) : 0.0;
           if constexpr (Cfg::Z) {
             c_prime(p, cf[ks][j][0], cf[ks][j][1]);
-            if constexpr (Cfg::G3) cf[ks][j][NA - 1] = cf[ks][j][0] + cf[ks][j][1];
+            if constexpr (Cfg::G3 && !Cfg::G3R) cf[ks][j][2] = cf[ks][j][0] + cf[ks][j][1];
           } else {
             cf[ks][j][0] *= p.alpha_re;
           }
@@ -2236,7 +2255,10 @@ __global__ void __launch_bounds__(Cfg::NT) tsmm_cst_kernel(const __grid_constant
                   for (int j = 0; j < NBV; j++) {
                     dmma(acc[i][j][0][0], acc[i][j][0][1], a.x, cf[ks][j][0]);
                     dmma(acc[i][j][1][0], acc[i][j][1][1], a.y, cf[ks][j][1]);
-                    dmma(acc[i][j][2][0], acc[i][j][2][1], sa, cf[ks][j][2]);
+                    if constexpr (Cfg::G3R)  // (volatile: not hoisted out of the loops)
+                      dmma(acc[i][j][2][0], acc[i][j][2][1], sa, dadd_here(cf[ks][j][0], cf[ks][j][1]));
+                    else
+                      dmma(acc[i][j][2][0], acc[i][j][2][1], sa, cf[ks][j][2]);
                   }
                 } else {
                 const double nai = -a.y;

@@ -288,6 +288,41 @@ def test_tsmttsm_inline_edge(tsm, dt, M, N):
     assert ran
 
 
+@pytest.mark.parametrize("M,N,cfg", [
+    (64, 64, {"G3": 1, "NBW": 1, "NT": 544, "R": 32, "WR": 1, "impl": 3}),
+    (57, 57, {"G3": 1, "NBW": 1, "NT": 544, "R": 32, "WR": 2, "impl": 3}),
+    (49, 49, {"EDGE": 1, "G3": 1, "NBW": 1, "NT": 416, "R": 16, "WR": 1, "impl": 3}),
+])
+def test_tsmm_3m_recomputed_sums(tsm, M, N, cfg):
+    """3M C-stationary configurations whose C slice (Re c, Im c, Re c + Im c)
+    exceeds the register budget: the kernel keeps Re c, Im c and recomputes
+    the sum per k-step (TsmmCstCfg::G3R).  Tolerance on ragged K, plain and
+    conjugate; integer-valued inputs bit-exact."""
+    for conj in (False, True):
+        plan = tsm.Plan("tsmm", "z", M, N, 0, config=gi.to_tsm_config("tsmm", cfg, 4, 1), conj=conj)
+        assert plan.config()["kernel"] & 512
+        for K in (1, 33, 4099, 100003):
+            A = ti.matrix(K, M, "A", complex_=True, seed=K + 41)
+            Cm = ti.matrix(M, N, "C", complex_=True, seed=K + 42)
+            B0 = np.zeros((K, N), dtype=np.complex128)
+            got = torch.from_numpy(B0).cuda()
+            tsm.tsmm_update(torch.from_numpy(A).cuda(), torch.from_numpy(Cm).cuda(), got, 1.0, 0.0,
+                            plan=plan, conj=conj)
+            torch.cuda.synchronize()
+            ref, bound = oracle.tsmm_update(A, Cm, B0, 1.0, 0.0, conj=conj)
+            r, wi, _ = oracle.max_err_ratio(got.cpu().numpy(), ref, bound)
+            assert r <= 1e-13, (M, N, cfg, conj, K, r, wi)
+        Ai = ti.matrix(20001, M, "A", complex_=True, mode="int")
+        Ci = ti.matrix(M, N, "C", complex_=True, mode="int")
+        B0 = np.zeros((20001, N), dtype=np.complex128)
+        got = torch.from_numpy(B0).cuda()
+        tsm.tsmm_update(torch.from_numpy(Ai).cuda(), torch.from_numpy(Ci).cuda(), got, 1.0, 0.0,
+                        plan=plan, conj=conj)
+        torch.cuda.synchronize()
+        ref = oracle.tsmm_update(Ai, Ci, B0, 1.0, 0.0, conj=conj)[0]
+        assert np.array_equal(got.cpu().numpy(), ref), (M, N, cfg, conj)
+
+
 @pytest.mark.parametrize("conj", [False, True], ids=["C", "conjC"])
 @pytest.mark.parametrize("M,N", [(32, 32), (17, 17), (24, 40), (64, 64), (9, 8), (50, 13)])
 def test_tsmm_3m(tsm, M, N, conj):
