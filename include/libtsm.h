@@ -243,7 +243,9 @@ const char *tsm_last_error_detail(void);
 /*   indefinitely -- e.g. a persistent kernel, or an NCCL kernel waiting for */
 /*   a peer that itself waits on this call -- can stall it.  Concurrent      */
 /*   kernels that finish on their own (any libtsm call, NCCL collectives     */
-/*   whose peers progress independently) only delay it.                      */
+/*   whose peers progress independently) only delay it.  With nfin = 1     */
+/*   (tsm_plan_describe) the single finisher is the block holding the last  */
+/*   ticket: it never waits, so that case needs no co-residency at all.      */
 /* ------------------------------------------------------------------------ */
 tsm_status tsmttsm_d(tsm_plan p, int64_t K, const double *A, const double *B, double *C,
                      void *ws, size_t ws_bytes, tsm_stream stream);
