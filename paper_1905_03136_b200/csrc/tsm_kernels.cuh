@@ -2235,6 +2235,16 @@ __global__ void __launch_bounds__(Cfg::NT) tsmm_cst_kernel(const __grid_constant
           for (int ks = 0; ks < MK; ks++) {
             const int m = 4 * ks + q;
             const bool mv = (4 * ks + 4 <= M) || (m < M);
+            // G3R: Re c + Im c of this k-step, once for all WR > 1 row blocks
+            // (volatile: recomputed every k-step, never kept live; with WR = 1
+            // it stays next to its DMMA, which ptxas allocates better: Z 64
+            // NT 544 32 B of spill stores instead of 72)
+            constexpr bool HOIST = Cfg::G3R && WR > 1;
+            double csum[HOIST ? NBV : 1];
+            if constexpr (HOIST) {
+  #pragma unroll
+              for (int j = 0; j < NBV; j++) csum[j] = dadd_here(cf[ks][j][0], cf[ks][j][1]);
+            }
   #pragma unroll
             for (int i = 0; i < WR; i++) {
               const int r = wr0 + 8 * i + rho;
@@ -2255,7 +2265,9 @@ __global__ void __launch_bounds__(Cfg::NT) tsmm_cst_kernel(const __grid_constant
                   for (int j = 0; j < NBV; j++) {
                     dmma(acc[i][j][0][0], acc[i][j][0][1], a.x, cf[ks][j][0]);
                     dmma(acc[i][j][1][0], acc[i][j][1][1], a.y, cf[ks][j][1]);
-                    if constexpr (Cfg::G3R)  // (volatile: not hoisted out of the loops)
+                    if constexpr (HOIST)
+                      dmma(acc[i][j][2][0], acc[i][j][2][1], sa, csum[j]);
+                    else if constexpr (Cfg::G3R)
                       dmma(acc[i][j][2][0], acc[i][j][2][1], sa, dadd_here(cf[ks][j][0], cf[ks][j][1]));
                     else
                       dmma(acc[i][j][2][0], acc[i][j][2][1], sa, cf[ks][j][2]);
