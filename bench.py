@@ -76,7 +76,8 @@ def bench_config(args, widths, world):
     return {"workload": f"configs[1] sweep: {'Z' if z else 'D'} M=N {widths[0]}..{widths[-1]}, "
                         "tsmttsm then tsmm per step",
             "K_per_gpu": args.K, "widths": f"{widths[0]}..{widths[-1]}",
-            "l2": "inputs > L2 (>=268 MB per kernel), no flush",
+            "l2": "inputs > L2 (>=268 MB per kernel), no flush between kernels; one L2 drain (a read of "
+                  "2 x L2 of clean memory) at the end of each step, timed inside the step",
             "parallelism": f"K-sharded x{world}" if world > 1 else "single GPU",
             "collectives": ("fused peer-memory reduction (tsmttsm_peer)" if getattr(args, "peer", False)
                             else "allgather+rank-order sum" if args.deterministic else "nccl allreduce")
@@ -496,7 +497,21 @@ def sweep(ctx, raw, z, widths, K, steps, warmup):
             calls.append(lambda a=a, M=M: ctx.launch("tsmttsm", z, M, M, K, a, ctx.view(B, z, K, M), Cs[M]))
         else:
             calls.append(lambda a=a, M=M: ctx.launch("tsmm", z, M, M, K, a, ctx.view(O, z, K, M), Cs[M]))
+    # L2 drain at the end of the step (timed inside the step, not a kernel row):
+    # the last TSMM leaves ~L2-size of dirty B lines, whose write-back the next
+    # step's first TSMTTSMs would otherwise pay (order probe run 23: TSMTTSM D 1 /
+    # 2 / 4 take 6-16 us longer right after TSMM D 64 than after a clean L2).
+    # A read of 2 x L2 of clean memory (the tail of the A buffer, which the first
+    # kernels of the next step do not read) absorbs it, so each kernel row
+    # carries its own cost; the step time still includes it.
+    l2 = ctx.torch.cuda.get_device_properties(ctx.dev).L2_cache_size
+    nb = ((2 * l2) // 4096) * 4096
+    drain_ptr = A.data_ptr() + A.numel() - nb
+    assert A.numel() - nb >= K * min(widths) * (16 if z else 8) * 4, "drain overlaps the first kernels' inputs"
+    calls.append(lambda: ctx.tsm.probe("read", drain_ptr, nb, 1, ctx.s_ptr))
     per, step_ms = ctx.timed(calls, steps, warmup)
+    drain_ms = per.pop()
+    calls.pop()
     # untimed pass: the SM clock right after every kernel of the step (a 1-thread
     # probe counting cycles over 2 us of globaltimer) -- the clock the FP64-bound
     # kernels actually ran at under the power cap
@@ -510,6 +525,7 @@ def sweep(ctx, raw, z, widths, K, steps, warmup):
     rows = [ctx.row(op, z, M, N, K, ms, ctx.plan(op, dt, M, N).describe(K).get("kernel", ""), mhz)
             for (op, _, M, N, _), ms, mhz in zip(items, per, mhzs)]
     byts = sum(sizes(op, M, N, K, z)[0] for (op, _, M, N, _) in items)
+    ctx.l2_drain_ms = drain_ms
     return rows, step_ms, byts, Cs
 
 
@@ -829,7 +845,8 @@ def main():
             "roofline": roofline,
             "roofline_step": dict(summarize(rows), frac=sum(r["ms"] * r["frac"] for r in rows) / tot_k),
             "peaks": dict(pk, measured_peaks_json_hbm_gbs=measured_peaks_file()),
-            "gpu_launches": len(rows) * args.steps, "clocks": clk}
+            "gpu_launches": (len(rows) + 1) * args.steps, "clocks": clk,
+            "l2_drain_ms_per_step": getattr(ctx, "l2_drain_ms", None)}
     report = {"sweep": rows}
 
     # ---------------- sub-results (single GPU) ----------------
