@@ -686,9 +686,14 @@ def candidates(op: str, M: int, N: int, z: bool) -> list:
         d = tsmm_mma_default(M, N, z)
         S_ = 2 if z else 1
         NB = cdiv(N, 8)
-        for NW in (4, 8):
+        for NW in (4, 8, 12, 16):
             for WR in (1, 2, 4):
                 if WR * NB * 2 * S_ > 64:
+                    continue
+                # 12 / 16 consumer warps (3-4 per SMSP; ncu run 23: 2 per SMSP
+                # leave the tensor pipe at 88 % on TSMM D 63): only with the
+                # accumulators of one row block (ptxas grants 128 / 96 registers)
+                if NW > 8 and WR * NB * S_ > 8:
                     continue
                 rpp = 8 * WR * NW
                 for tgt in (12288, 24576):
