@@ -826,6 +826,11 @@ def main():
                                     f"in the timed region = {pk.get('fp64_at_clock_tflops', 0):.2f}) -> "
                                     f"{pk['fp64_source']}")}
     roofline["frac"] = roofline["achieved"] / roofline["peak"]
+    # context: the executed work of that kernel's tiling (8 x 8 DMMA blocks,
+    # bench.tile_work) and its fraction of that work's roofline at its own clock
+    if "tile_work" in dom:
+        roofline["tile_work"] = dom["tile_work"]
+        roofline["frac_of_executed_at_kernel_clock"] = dom["frac_of_executed"]
     roofline["kernel"] = f"{dom['op']}_{args.dtype} M=N={dom['M']} ({dom['kernel']})"
     roofline["share_of_step"] = dom["share"]
     roofline["traffic"] = None
